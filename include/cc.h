@@ -1,0 +1,164 @@
+/*
+ * cc.h -- C ABI of the B200-native adaptive connected-components library (libcc.so).
+ *
+ * Method: Jain, Flick, Pan, Green, Aluru, "An Adaptive Parallel Algorithm for Computing
+ * Connected Components" (arXiv 1607.06156).  References below are to that paper's
+ * LaTeX source (PAPER.md:<line>) and to SURVEY.md §8(b), which fixes this boundary.
+ *
+ * What cc_run computes (PAPER.md:28 definition, PAPER.md:197 projection):
+ *   label(v) = min { u : u is connected to v }   (the component's minimum vertex id)
+ * via Alg. 2: degree distribution -> power-law gate -> optionally one
+ * BFS that peels the giant component -> edge-tuple Shiloach-Vishkin (Alg. 1,
+ * PAPER.md:133-178) with completed-partition exclusion on the rest.
+ *
+ * Conventions (all entry points):
+ *  - Status codes only; nothing aborts, exits or throws across the ABI.  Details of the
+ *    last failure are in cc_last_error(ctx).
+ *  - Pointers are plain host or device pointers, sizes are element counts.  Input
+ *    buffers are borrowed for the duration of the call only (copied).  Output buffers are
+ *    caller-allocated.  cc_report.iters is owned by the context and valid until the next
+ *    cc_run / cc_destroy.
+ *  - All device work is enqueued on cfg.stream (a cudaStream_t, NULL = legacy default);
+ *    cc_run and cc_labels_* return after their results are complete (they synchronise
+ *    that stream).
+ *  - Device memory comes from cfg.alloc/cfg.free when set (e.g. the PyTorch caching
+ *    allocator), else from cudaMallocAsync on cfg.stream.
+ *  - One context per thread per GPU.
+ */
+#ifndef CC_H_
+#define CC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cc_ctx cc_ctx; /* opaque; owns all device buffers */
+
+typedef enum {
+  CC_OK = 0,
+  CC_ERR_INVALID = 1, /* bad argument (NULL pointer, bad mode, n too large, ...) */
+  CC_ERR_RANGE = 2,   /* u32 mode: an edge endpoint >= n_vertices (checked on device) */
+  CC_ERR_NOMEM = 3,   /* device allocation failed */
+  CC_ERR_CUDA = 4,    /* a CUDA runtime error (message in cc_last_error) */
+  CC_ERR_COMM = 5,    /* multi-GPU exchange failed */
+  CC_ERR_STATE = 6,   /* call out of order, e.g. cc_run before cc_load_edges */
+  CC_ERR_NOCONV = 7   /* SV did not converge within 2*ceil(log2 n)+8 iterations */
+} cc_status;
+
+typedef enum {
+  CC_MODE_AUTO = 0,   /* Alg. 2: the gate decides whether to run the BFS peel */
+  CC_MODE_SV = 1,     /* hard-coded: SV only (fig:dynamic 'never BFS')        */
+  CC_MODE_BFS_SV = 2  /* hard-coded: BFS peel, then SV on the remainder       */
+} cc_mode;
+
+typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
+
+/* cc_config.flags */
+#define CC_FLAG_TRACE 0x1u           /* record per-iteration counters in cc_report.iters   */
+#define CC_FLAG_GATE_KS 0x2u         /* decide with the paper's K-S < tau
+                                        instead of gate G (least-squares fit)  */
+#define CC_FLAG_NO_EARLY_EXCLUDE 0x4u /* reserved: end-of-iteration exclusion timing        */
+#define CC_FLAG_REGROUP_DIRECT 0x8u  /* SV regroups by direct addressing instead of radix
+                                        sort (B200 variant; identical sets)  */
+
+typedef void* (*cc_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*cc_free_fn)(void* ptr, size_t bytes, void* stream, void* user);
+
+typedef struct {
+  int device;          /* CUDA device ordinal                                         */
+  void* stream;        /* cudaStream_t; NULL = legacy default stream                   */
+  int rank, world_size;/* SPMD position; world_size == 1 for a single GPU              */
+  cc_alloc_fn alloc;   /* optional device allocator hooks (NULL => cudaMallocAsync)     */
+  cc_free_fn free;
+  void* alloc_user;
+  double tau;          /* K-S threshold for CC_FLAG_GATE_KS; <= 0 => 0.05*/
+  uint64_t seed;       /* reserved (deterministic run; no randomness is drawn)         */
+  uint32_t flags;      /* CC_FLAG_*                                                    */
+} cc_config;
+
+/* One SV iteration (counters of SURVEY.md §8(c) "Trace oracle"). */
+typedef struct {
+  uint64_t active_in;  /* A_i: non-temporary tuples entering the iteration             */
+  uint64_t partitions; /* |P_i| at the first partition pass                            */
+  uint64_t temps;      /* T_i: temporary tuples <p_min,_,p_min>_tmp appended    */
+  uint64_t completed;  /* partitions found completed                    */
+  uint64_t changed;    /* #{p : p_min != p} at the first partition pass        */
+  uint64_t changed2;   /* same count at the second partition pass             */
+  double ms;           /* device time of the iteration                                 */
+} cc_iter_stat;
+
+typedef struct {
+  int ran_bfs;                        /* route taken by Alg. 2                          */
+  double ls_alpha, ls_r2;             /* gate G: log-log least-squares fit              */
+  double ks_stat, ks_alpha;           /* paper's K-S statistic and alpha-hat (reported) */
+  uint32_t ks_xmin;
+  uint64_t max_degree;
+  uint64_t n_present;                 /* ids touched by an edge                         */
+  uint64_t m_edges;                   /* undirected edge records (incl. dups, loops)    */
+  uint64_t components;                /* number of components (isolated ids included)   */
+  uint64_t bfs_root, bfs_visited, bfs_levels, remainder_edges;
+  uint32_t sv_iterations;
+  double ms_total, ms_prediction, ms_relabel, ms_bfs, ms_filter, ms_sv, ms_finalize;
+  const cc_iter_stat* iters;          /* sv_iterations entries (CC_FLAG_TRACE)          */
+  uint32_t n_iters;
+} cc_report;
+
+/* Library version string. */
+const char* cc_version(void);
+
+/* Create a context on cfg->device.  cfg is copied.  Returns CC_ERR_INVALID for a NULL
+ * argument or bad world_size, CC_ERR_CUDA if the device cannot be used. */
+cc_status cc_init(const cc_config* cfg, cc_ctx** out);
+
+/* Load an undirected edge list (the input G(V,E) of Alg. 1/2; PAPER.md:205 block
+ * distributed edge list, here one block per rank).
+ *   w          CC_U32: ids are uint32 < n_vertices; CC_U64: ids are arbitrary uint64
+ *   pairs      interleaved endpoints (u0,v0,u1,v1,...): 2*m_local ids of width w
+ *   m_local    number of undirected edge records on this rank (duplicates and
+ *              self-loops are legal and kept)
+ *   n_vertices u32: id bound n (V = [0,n), isolated ids are singleton components);
+ *              u64: must be 0 (V = ids that appear in the edge list)
+ *   pairs_on_device  nonzero if `pairs` is a device pointer
+ * Ids >= n in u32 mode -> CC_ERR_RANGE (detected on device).  n > 2^30 -> CC_ERR_INVALID.
+ * Replaces any previously loaded graph. */
+cc_status cc_load_edges(cc_ctx* ctx, cc_idw w, const void* pairs, uint64_t m_local,
+                        uint64_t n_vertices, int pairs_on_device);
+
+/* Compute component labels (Alg. 2 with `mode`), fill *out if non-NULL.  Labels stay on
+ * the device for cc_labels_*.  CC_ERR_STATE if no graph is loaded. */
+cc_status cc_run(cc_ctx* ctx, cc_mode mode, cc_report* out);
+
+/* u32 mode: labels of ids [0, n) (this rank's block when world_size > 1).  `out` has
+ * room for `cap` labels; *count receives n.  CC_ERR_INVALID if cap < n. */
+cc_status cc_labels_u32(cc_ctx* ctx, uint32_t* out, uint64_t cap, uint64_t* count,
+                        int out_on_device);
+
+/* u64 mode: the distinct ids (ascending) and the label (an id) of each. */
+cc_status cc_labels_u64(cc_ctx* ctx, uint64_t* ids, uint64_t* labels, uint64_t cap,
+                        uint64_t* count, int out_on_device);
+
+/* Device pointer of the label array (u32 mode), valid until the next load/destroy, and
+ * the device stream all work is enqueued on.  For zero-copy consumers. */
+cc_status cc_labels_device(cc_ctx* ctx, const uint32_t** labels, uint64_t* count);
+
+/* Number of kernel launches enqueued by the last cc_run (evidence for bench.py). */
+uint64_t cc_last_launch_count(const cc_ctx* ctx);
+
+/* Device time (ms, CUDA events on cfg.stream) of the dominant kernel family in the last
+ * cc_run, with its algorithmic bytes (for the roofline line of bench.py):
+ *   which = 0: radix-sort scatter passes, 1: segmented passes, 2: BFS levels. */
+cc_status cc_kernel_stats(const cc_ctx* ctx, int which, double* ms, double* bytes,
+                          uint64_t* launches);
+
+cc_status cc_destroy(cc_ctx* ctx);
+
+const char* cc_status_string(cc_status s);
+const char* cc_last_error(const cc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CC_H_ */

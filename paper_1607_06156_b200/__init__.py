@@ -1,0 +1,241 @@
+"""Thin Python binding of libcc.so (include/cc.h): argument marshalling only.
+
+Every step of the connected-components path runs in the sm_100a kernels of ``csrc/``;
+this module only converts arguments, supplies PyTorch's stream and caching allocator to
+the library, and converts the report.  There is no CPU fallback: if ``libcc.so`` is
+missing, importing the binding raises.
+
+Names follow the C ABI: :func:`cc_init`, :func:`cc_load_edges`, :func:`cc_run`,
+:func:`cc_labels_u32`, :func:`cc_destroy`, plus the convenience class :class:`CC`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcc.so")
+
+CC_OK, CC_ERR_INVALID, CC_ERR_RANGE, CC_ERR_NOMEM, CC_ERR_CUDA, CC_ERR_COMM, CC_ERR_STATE, \
+    CC_ERR_NOCONV = range(8)
+MODES = {"auto": 0, "sv": 1, "bfs+sv": 2}
+CC_U32, CC_U64 = 0, 1
+CC_FLAG_TRACE = 0x1
+CC_FLAG_GATE_KS = 0x2
+CC_FLAG_NO_EARLY_EXCLUDE = 0x4
+CC_FLAG_REGROUP_DIRECT = 0x8
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class cc_config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
+                ("world_size", ctypes.c_int), ("alloc", ALLOC_FN), ("free", FREE_FN),
+                ("alloc_user", ctypes.c_void_p), ("tau", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32)]
+
+
+class cc_iter_stat(ctypes.Structure):
+    _fields_ = [("active_in", ctypes.c_uint64), ("partitions", ctypes.c_uint64),
+                ("temps", ctypes.c_uint64), ("completed", ctypes.c_uint64),
+                ("changed", ctypes.c_uint64), ("changed2", ctypes.c_uint64), ("ms", ctypes.c_double)]
+
+
+class cc_report(ctypes.Structure):
+    _fields_ = [("ran_bfs", ctypes.c_int), ("ls_alpha", ctypes.c_double), ("ls_r2", ctypes.c_double),
+                ("ks_stat", ctypes.c_double), ("ks_alpha", ctypes.c_double),
+                ("ks_xmin", ctypes.c_uint32), ("max_degree", ctypes.c_uint64),
+                ("n_present", ctypes.c_uint64), ("m_edges", ctypes.c_uint64),
+                ("components", ctypes.c_uint64), ("bfs_root", ctypes.c_uint64),
+                ("bfs_visited", ctypes.c_uint64), ("bfs_levels", ctypes.c_uint64),
+                ("remainder_edges", ctypes.c_uint64), ("sv_iterations", ctypes.c_uint32),
+                ("ms_total", ctypes.c_double), ("ms_prediction", ctypes.c_double),
+                ("ms_relabel", ctypes.c_double), ("ms_bfs", ctypes.c_double),
+                ("ms_filter", ctypes.c_double), ("ms_sv", ctypes.c_double),
+                ("ms_finalize", ctypes.c_double), ("iters", ctypes.POINTER(cc_iter_stat)),
+                ("n_iters", ctypes.c_uint32)]
+
+
+EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
+           "cc_labels_device", "cc_last_launch_count", "cc_kernel_stats", "cc_destroy",
+           "cc_status_string", "cc_last_error"]
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"libcc.so not built ({path}); run __graft_entry__.build() -- "
+                          "there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    lib.cc_version.restype = ctypes.c_char_p
+    lib.cc_status_string.restype = ctypes.c_char_p
+    lib.cc_status_string.argtypes = [ctypes.c_int]
+    lib.cc_last_error.restype = ctypes.c_char_p
+    lib.cc_last_error.argtypes = [P]
+    lib.cc_init.argtypes = [ctypes.POINTER(cc_config), ctypes.POINTER(P)]
+    lib.cc_load_edges.argtypes = [P, ctypes.c_int, P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]
+    lib.cc_run.argtypes = [P, ctypes.c_int, ctypes.POINTER(cc_report)]
+    lib.cc_labels_u32.argtypes = [P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+    lib.cc_labels_u64.argtypes = [P, P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+    lib.cc_labels_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_uint64)]
+    lib.cc_last_launch_count.restype = ctypes.c_uint64
+    lib.cc_last_launch_count.argtypes = [P]
+    lib.cc_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
+    lib.cc_destroy.argtypes = [P]
+    for f in ("cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
+              "cc_labels_device", "cc_kernel_stats", "cc_destroy"):
+        getattr(lib, f).restype = ctypes.c_int
+    return lib
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = load_library()
+    return _lib
+
+
+class CCError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{lib().cc_status_string(status).decode()}: {msg}")
+        self.status = status
+
+
+def _check(ctx, status):
+    if status != CC_OK:
+        msg = lib().cc_last_error(ctx).decode() if ctx else ""
+        raise CCError(status, msg)
+
+
+# ------------------------------------------------------------------ C-ABI-named wrappers
+def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True):
+    """Create a context.  ``stream``: a torch.cuda.Stream or raw cudaStream_t int (default:
+    torch's current stream).  ``torch_alloc``: route device allocations through PyTorch's
+    caching allocator."""
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    cfg = cc_config()
+    cfg.device = device
+    cfg.stream = sptr
+    cfg.rank = 0
+    cfg.world_size = 1
+    cfg.tau = tau
+    cfg.flags = flags
+    keep = []
+    if torch_alloc:
+        dev = device
+
+        def _alloc(nbytes, st, user):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), dev, st or 0)
+            except Exception:  # OOM -> NULL -> CC_ERR_NOMEM
+                return None
+
+        def _free(ptr, nbytes, st, user):
+            torch.cuda.caching_allocator_delete(ptr)
+
+        a, f = ALLOC_FN(_alloc), FREE_FN(_free)
+        cfg.alloc, cfg.free = a, f
+        keep += [a, f]
+    h = ctypes.c_void_p()
+    _check(None, lib().cc_init(ctypes.byref(cfg), ctypes.byref(h)))
+    return h, keep
+
+
+def cc_load_edges(ctx, pairs, n_vertices, ids="u32"):
+    """pairs: (m,2) uint32 numpy array (host) or torch CUDA tensor (device)."""
+    if ids != "u32":
+        w = CC_U64
+    else:
+        w = CC_U32
+    if hasattr(pairs, "is_cuda") and pairs.is_cuda:
+        t = pairs.contiguous()
+        m = t.shape[0]
+        _check(ctx, lib().cc_load_edges(ctx, w, ctypes.c_void_p(t.data_ptr()), m, n_vertices, 1))
+        return m
+    a = np.ascontiguousarray(pairs, dtype=np.uint32 if w == CC_U32 else np.uint64).reshape(-1, 2)
+    m = a.shape[0]
+    _check(ctx, lib().cc_load_edges(ctx, w, a.ctypes.data_as(ctypes.c_void_p), m, n_vertices, 0))
+    return m
+
+
+def _report(r: cc_report) -> dict:
+    d = {k: getattr(r, k) for k, _ in cc_report._fields_ if k != "iters"}
+    d["iters"] = [{k: getattr(r.iters[i], k) for k, _ in cc_iter_stat._fields_}
+                  for i in range(r.n_iters)]
+    return d
+
+
+def cc_run(ctx, mode="auto") -> dict:
+    r = cc_report()
+    _check(ctx, lib().cc_run(ctx, MODES[mode], ctypes.byref(r)))
+    return _report(r)
+
+
+def cc_labels_u32(ctx, out=None):
+    """Labels into a new numpy array (host) or into ``out`` (numpy or torch CUDA uint32/int32)."""
+    cnt = ctypes.c_uint64()
+    lib().cc_labels_u32(ctx, None, 0, ctypes.byref(cnt), 0)  # query n (returns INVALID)
+    n = cnt.value
+    if out is None:
+        out = np.empty(n, dtype=np.uint32)
+    if hasattr(out, "is_cuda") and out.is_cuda:
+        _check(ctx, lib().cc_labels_u32(ctx, ctypes.c_void_p(out.data_ptr()), out.numel(),
+                                        ctypes.byref(cnt), 1))
+    else:
+        _check(ctx, lib().cc_labels_u32(ctx, out.ctypes.data_as(ctypes.c_void_p), out.shape[0],
+                                        ctypes.byref(cnt), 0))
+    return out
+
+
+def cc_kernel_stats(ctx, which):
+    ms, by, ln = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
+    _check(ctx, lib().cc_kernel_stats(ctx, which, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(ln)))
+    return dict(ms=ms.value, bytes=by.value, launches=ln.value)
+
+
+def cc_destroy(ctx):
+    _check(None, lib().cc_destroy(ctx))
+
+
+class CC:
+    """Convenience wrapper: ``CC().load(edges, n).run('auto')`` then ``.labels()``."""
+
+    def __init__(self, device=0, stream=None, flags=0, tau=0.05, torch_alloc=True):
+        self.ctx, self._keep = cc_init(device, stream, flags, tau, torch_alloc)
+
+    def load(self, pairs, n_vertices, ids="u32"):
+        cc_load_edges(self.ctx, pairs, n_vertices, ids)
+        return self
+
+    def run(self, mode="auto"):
+        return cc_run(self.ctx, mode)
+
+    def labels(self, out=None):
+        return cc_labels_u32(self.ctx, out)
+
+    def launches(self):
+        return int(lib().cc_last_launch_count(self.ctx))
+
+    def kernel_stats(self, which):
+        return cc_kernel_stats(self.ctx, which)
+
+    def close(self):
+        if self.ctx:
+            cc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

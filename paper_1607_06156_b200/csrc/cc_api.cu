@@ -1,0 +1,625 @@
+// cc_api.cu -- the C ABI (include/cc.h) and the Alg. 2 driver.
+//
+// cc_run(mode):
+//   prediction : degrees + degree distribution on device, gate on host   (Alg. 2 lines 2-3)
+//   BFS route  : edge-streaming bitmap BFS from the max-degree root, label the visited
+//                component with its min id, filter its edges            (lines 7-11)
+//   SV         : Alg. 1 on the remaining edges, four regroups per iteration with
+//                completed-partition exclusion
+// All compute runs in the kernels of radix.cu / sv.cu / graph.cu; the host only sequences
+// launches and reads small counters (one sync per SV iteration, one per BFS level).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cc.h"
+#include "gate.h"
+#include "graph.cuh"
+#include "radix.cuh"
+#include "sv.cuh"
+
+using namespace cc;
+
+#define CC_VERSION_STR "cc-b200 0.1.0 (sm_100a)"
+
+struct cc_ctx {
+  cc_config cfg{};
+  cudaStream_t st = nullptr;
+  std::string err;
+  // graph
+  bool loaded = false, ran = false;
+  cc_idw idw = CC_U32;
+  uint64_t n = 0, m = 0;
+  int kbits = 0;
+  uint2* d_edges = nullptr;
+  uint2* d_rem = nullptr;
+  uint32_t* d_label = nullptr;
+  uint32_t* d_deg = nullptr;
+  uint32_t* d_hist = nullptr;
+  uint32_t* d_tail = nullptr;
+  uint32_t* d_bm[3] = {nullptr, nullptr, nullptr};  // visited, frontier, next
+  uint64_t* d_w[2] = {nullptr, nullptr};
+  uint32_t* d_q[2] = {nullptr, nullptr};
+  uint64_t cap = 0;
+  uint32_t* d_segA = nullptr;
+  uint32_t* d_segB = nullptr;
+  uint64_t* d_ctr = nullptr;   // sv counters
+  uint64_t* d_gctr = nullptr;  // graph counters
+  uint64_t* h_ctr = nullptr;   // pinned mirrors
+  uint64_t* h_gctr = nullptr;
+  uint32_t* h_hist = nullptr;  // pinned histogram staging
+  uint32_t* h_word = nullptr;
+  radix::Workspace rws;
+  std::vector<std::pair<void*, size_t>> allocs;
+  // report
+  std::vector<cc_iter_stat> iters;
+  cc_report rep{};
+  uint64_t launches = 0;
+  // profiling (CC_FLAG_TRACE): per-family events
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_sort, prof_seg, prof_bfs;
+  std::vector<cudaEvent_t> it_ev;  // SV iteration start events
+  double sort_bytes = 0, seg_bytes = 0, bfs_bytes = 0;
+  double kms[3] = {0, 0, 0}, kbytes[3] = {0, 0, 0};
+  uint64_t klaunch[3] = {0, 0, 0};
+};
+
+// ------------------------------------------------------------------------------ helpers
+static cc_status fail(cc_ctx* c, cc_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, e_ == cudaErrorMemoryAllocation ? CC_ERR_NOMEM : CC_ERR_CUDA,        \
+                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define CKL()                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, CC_ERR_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+#define TRY(x)                        \
+  do {                                \
+    cc_status s_ = (x);               \
+    if (s_ != CC_OK) return s_;       \
+  } while (0)
+
+static cc_status dalloc(cc_ctx* c, void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (c->cfg.alloc) {
+    *p = c->cfg.alloc(bytes, (void*)c->st, c->cfg.alloc_user);
+    if (!*p) return fail(c, CC_ERR_NOMEM, "allocator hook returned NULL for %zu bytes", bytes);
+  } else {
+    cudaError_t e = cudaMallocAsync(p, bytes, c->st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, CC_ERR_NOMEM, "cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
+  }
+  c->allocs.push_back({*p, bytes});
+  return CC_OK;
+}
+template <typename T>
+static cc_status dalloc_t(cc_ctx* c, T** p, size_t count) {
+  return dalloc(c, reinterpret_cast<void**>(p), count * sizeof(T));
+}
+static void dfree_all(cc_ctx* c) {
+  for (auto& a : c->allocs) {
+    if (c->cfg.free) c->cfg.free(a.first, a.second, (void*)c->st, c->cfg.alloc_user);
+    else cudaFreeAsync(a.first, c->st);
+  }
+  c->allocs.clear();
+  c->d_edges = c->d_rem = nullptr;
+  c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
+  c->d_bm[0] = c->d_bm[1] = c->d_bm[2] = nullptr;
+  c->d_w[0] = c->d_w[1] = nullptr;
+  c->d_q[0] = c->d_q[1] = nullptr;
+  c->d_ctr = c->d_gctr = nullptr;
+  c->rws = radix::Workspace();
+  c->cap = 0;
+}
+
+static cudaEvent_t ev_get(cc_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+static bool profiling(const cc_ctx* c) { return (c->cfg.flags & CC_FLAG_TRACE) != 0; }
+
+static int bits_for(uint64_t n) {
+  int b = 0;
+  while (b < 63 && (1ull << b) < n) b++;
+  return b;
+}
+
+// ------------------------------------------------------------------------------ ABI
+extern "C" {
+
+const char* cc_version(void) { return CC_VERSION_STR; }
+
+const char* cc_status_string(cc_status s) {
+  switch (s) {
+    case CC_OK: return "CC_OK";
+    case CC_ERR_INVALID: return "CC_ERR_INVALID";
+    case CC_ERR_RANGE: return "CC_ERR_RANGE";
+    case CC_ERR_NOMEM: return "CC_ERR_NOMEM";
+    case CC_ERR_CUDA: return "CC_ERR_CUDA";
+    case CC_ERR_COMM: return "CC_ERR_COMM";
+    case CC_ERR_STATE: return "CC_ERR_STATE";
+    case CC_ERR_NOCONV: return "CC_ERR_NOCONV";
+  }
+  return "CC_ERR_UNKNOWN";
+}
+
+const char* cc_last_error(const cc_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+uint64_t cc_last_launch_count(const cc_ctx* c) { return c ? c->launches : 0; }
+
+cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
+  if (!cfg || !out) return CC_ERR_INVALID;
+  *out = nullptr;
+  if (cfg->world_size != 1 || cfg->rank != 0)
+    return CC_ERR_INVALID;  // multi-GPU contexts: see DESIGN.md §7 (not in this build)
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    cudaGetLastError();
+    return CC_ERR_CUDA;
+  }
+  if (cfg->device < 0 || cfg->device >= ndev) return CC_ERR_INVALID;
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return CC_ERR_CUDA;
+  cc_ctx* c = new cc_ctx();
+  c->cfg = *cfg;
+  if (c->cfg.tau <= 0) c->cfg.tau = 0.05;
+  c->st = (cudaStream_t)cfg->stream;
+  if (cudaMallocHost(&c->h_ctr, sizeof(uint64_t) * (sv::C_NUM + graph::G_NUM + 8)) != cudaSuccess ||
+      cudaMallocHost(&c->h_hist, sizeof(uint32_t) * (graph::HIST_DENSE + graph::TAIL_CAP)) !=
+          cudaSuccess) {
+    delete c;
+    return CC_ERR_NOMEM;
+  }
+  c->h_gctr = c->h_ctr + sv::C_NUM;
+  c->h_word = reinterpret_cast<uint32_t*>(c->h_gctr + graph::G_NUM);
+  *out = c;
+  return CC_OK;
+}
+
+cc_status cc_destroy(cc_ctx* c) {
+  if (!c) return CC_ERR_INVALID;
+  cudaSetDevice(c->cfg.device);
+  dfree_all(c);
+  cudaStreamSynchronize(c->st);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->h_ctr) cudaFreeHost(c->h_ctr);
+  if (c->h_hist) cudaFreeHost(c->h_hist);
+  delete c;
+  return CC_OK;
+}
+
+cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint64_t n, int on_dev) {
+  if (!c) return CC_ERR_INVALID;
+  if (m && !pairs) return fail(c, CC_ERR_INVALID, "pairs is NULL");
+  if (w != CC_U32) return fail(c, CC_ERR_INVALID, "u64 ids are not supported by this build");
+  if (n > (1ull << 30)) return fail(c, CC_ERR_INVALID, "n_vertices %llu > 2^30", (unsigned long long)n);
+  if (2 * m + 2 * n >= (1ull << 32))
+    return fail(c, CC_ERR_INVALID, "tuple count 2m+2n exceeds 2^32 on one GPU");
+  CK(cudaSetDevice(c->cfg.device));
+  dfree_all(c);
+  c->loaded = c->ran = false;
+  c->idw = w;
+  c->n = n;
+  c->m = m;
+  c->kbits = bits_for(n);
+  const uint64_t nw = (n + 31) / 32 + 1;
+  c->cap = 2 * m + 2 * n + 64;
+  TRY(dalloc_t(c, &c->d_edges, m + 1));
+  TRY(dalloc_t(c, &c->d_label, n + 1));
+  TRY(dalloc_t(c, &c->d_deg, n + 1));
+  TRY(dalloc_t(c, &c->d_hist, graph::HIST_DENSE));
+  TRY(dalloc_t(c, &c->d_tail, graph::TAIL_CAP));
+  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], nw));
+  for (int i = 0; i < 2; i++) {
+    TRY(dalloc_t(c, &c->d_w[i], c->cap));
+    TRY(dalloc_t(c, &c->d_q[i], c->cap));
+  }
+  TRY(dalloc_t(c, &c->d_segA, n + 1));
+  TRY(dalloc_t(c, &c->d_segB, n + 1));
+  TRY(dalloc_t(c, &c->d_ctr, sv::C_NUM));
+  TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM));
+  c->rws.max_tiles = c->cap / radix::TILE + 2;
+  TRY(dalloc_t(c, &c->rws.ghist, radix::MAX_PASSES * radix::RADIX));
+  TRY(dalloc_t(c, &c->rws.lookback, c->rws.max_tiles * radix::RADIX));
+  TRY(dalloc_t(c, &c->rws.tile_ctr, radix::MAX_PASSES));
+  CK(cudaMemsetAsync(c->rws.lookback, 0, sizeof(uint64_t) * c->rws.max_tiles * radix::RADIX, c->st));
+  if (m)
+    CK(cudaMemcpyAsync(c->d_edges, pairs, m * sizeof(uint2),
+                       on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+  // validate ids < n on device
+  CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
+  graph::launch_validate(c->d_edges, m, n, c->d_gctr, c->st);
+  CKL();
+  CK(cudaMemcpyAsync(c->h_gctr, c->d_gctr, sizeof(uint64_t) * graph::G_NUM, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->h_gctr[graph::G_ERR]) return fail(c, CC_ERR_RANGE, "edge endpoint >= n_vertices");
+  c->loaded = true;
+  return CC_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------ stages
+struct Timer {
+  cc_ctx* c;
+  cudaEvent_t a;
+  explicit Timer(cc_ctx* c_) : c(c_), a(ev_get(c_)) { cudaEventRecord(a, c->st); }
+  std::pair<cudaEvent_t, cudaEvent_t> stop() {
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->st);
+    return {a, b};
+  }
+};
+
+static cc_status sync_read(cc_ctx* c) {
+  CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(uint64_t) * sv::C_NUM, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->h_gctr, c->d_gctr, sizeof(uint64_t) * graph::G_NUM, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return CC_OK;
+}
+
+// radix sort wrapper with optional per-call timing
+static int do_sort(cc_ctx* c, int cur, uint64_t n, bool pairs) {
+  cudaEvent_t a = nullptr;
+  if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
+  int r = radix::sort_pairs(c->rws, c->d_w, c->d_q, cur, n, c->kbits, pairs, c->st, &c->launches);
+  if (profiling(c)) {
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->st);
+    c->prof_sort.push_back({a, b});
+    const int P = radix::num_passes(c->kbits);
+    // algorithmic bytes: histogram reads the key word once, each pass reads and writes the
+    // element once (8 B word + 4 B payload for the by-p regroups)
+    c->sort_bytes += (double)n * (8.0 + P * 2.0 * (pairs ? 12.0 : 8.0));
+    c->klaunch[0] += (uint64_t)(P + 1);
+  }
+  return r;
+}
+
+static void seg_begin(cc_ctx* c, cudaEvent_t* a) {
+  if (profiling(c)) { *a = ev_get(c); cudaEventRecord(*a, c->st); }
+}
+static void seg_end(cc_ctx* c, cudaEvent_t a, double bytes, int nl) {
+  if (profiling(c)) {
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->st);
+    c->prof_seg.push_back({a, b});
+    c->seg_bytes += bytes;
+    c->klaunch[1] += nl;
+  }
+}
+
+// Alg. 1 on (edges, m_sv); vertices present iff deg > 0 and not BFS-visited.
+static cc_status run_sv(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint32_t* vis) {
+  const uint64_t n = c->n;
+  CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
+  sv::launch_init_tuples(edges, m_sv, c->d_deg, vis, n, c->d_w[0], c->d_ctr, c->st, &c->launches);
+  CKL();
+  TRY(sync_read(c));
+  uint64_t A = 2 * m_sv + c->h_ctr[sv::C_VT_OUT];
+  if (A == 0) return CC_OK;
+  const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
+  int cur = do_sort(c, 0, A, false);  // line 8: sort by r
+  CKL();
+  uint64_t chg2_prev = 0;
+  for (uint32_t it = 0;; it++) {
+    if (it >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
+    cudaEvent_t ev_it = ev_get(c);
+    CK(cudaEventRecord(ev_it, c->st));
+    cudaEvent_t a = nullptr;
+    // ---- lines 9-13: vertex buckets, q <- u_min, PC
+    seg_begin(c, &a);
+    CK(cudaMemsetAsync(c->d_segA, 0xFF, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(c->d_segB, 0, sizeof(uint32_t) * n, c->st));
+    sv::launch_seg_reduce(sv::SEG_VMINMAX, c->d_w[cur], nullptr, A, c->d_segA, c->d_segB, c->st);
+    sv::launch_vertex_apply(true, c->d_w[cur], A, c->d_segA, c->d_segB, c->d_w[cur ^ 1],
+                            c->d_q[cur ^ 1], c->st);
+    seg_end(c, a, (double)A * (8 + 8 + 12), 2);
+    c->launches += 2;
+    cur ^= 1;
+    CKL();
+    // ---- line 14: sort by p;  lines 15-22: partition buckets, exclusion, temps
+    cur = do_sort(c, cur, A, true);
+    seg_begin(c, &a);
+    CK(cudaMemsetAsync(c->d_segA, 0xFF, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(c->d_segB, 0, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_TEMPS + 1), c->st));
+    sv::launch_seg_reduce(sv::SEG_PMIN_NC, c->d_w[cur], c->d_q[cur], A, c->d_segA, c->d_segB, c->st);
+    sv::launch_partition_apply(true, true, c->d_w[cur], c->d_q[cur], A, c->d_segA, c->d_segB,
+                               c->d_w[cur ^ 1], c->d_label, c->d_ctr, c->st);
+    c->launches += 2;
+    cur ^= 1;
+    CKL();
+    TRY(sync_read(c));
+    const uint64_t out = c->h_ctr[sv::C_OUT];
+    const uint64_t T = c->h_ctr[sv::C_TEMPS];
+    const uint64_t A1 = out - T;
+    seg_end(c, a, (double)A * (12 + 12) + (double)out * 8, 2);
+    cc_iter_stat s{};
+    s.active_in = A;
+    s.partitions = c->h_ctr[sv::C_PARTITIONS];
+    s.completed = c->h_ctr[sv::C_COMPLETED];
+    s.changed = c->h_ctr[sv::C_CHANGED];
+    s.temps = T;
+    if (!c->iters.empty()) {
+      c->iters.back().changed2 = c->h_ctr[sv::C_CHANGED2] - chg2_prev;
+      chg2_prev = c->h_ctr[sv::C_CHANGED2];
+    }
+    c->iters.push_back(s);
+    c->it_ev.push_back(ev_it);
+    if (out == 0) break;
+    // ---- line 24: redo lines 8-13 with the temporaries
+    cur = do_sort(c, cur, out, false);
+    seg_begin(c, &a);
+    CK(cudaMemsetAsync(c->d_segA, 0xFF, sizeof(uint32_t) * n, c->st));
+    sv::launch_seg_reduce(sv::SEG_VMIN, c->d_w[cur], nullptr, out, c->d_segA, nullptr, c->st);
+    sv::launch_vertex_apply(false, c->d_w[cur], out, c->d_segA, nullptr, c->d_w[cur ^ 1],
+                            c->d_q[cur ^ 1], c->st);
+    seg_end(c, a, (double)out * (8 + 8 + 12), 2);
+    c->launches += 2;
+    cur ^= 1;
+    // ---- line 25: redo lines 14-21;  lines 26-28: erase temporaries
+    cur = do_sort(c, cur, out, true);
+    seg_begin(c, &a);
+    CK(cudaMemsetAsync(c->d_segA, 0xFF, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(c->d_ctr + sv::C_OUT, 0, sizeof(uint64_t), c->st));
+    sv::launch_seg_reduce(sv::SEG_PMIN, c->d_w[cur], c->d_q[cur], out, c->d_segA, nullptr, c->st);
+    sv::launch_partition_apply(false, true, c->d_w[cur], c->d_q[cur], out, c->d_segA, nullptr,
+                               c->d_w[cur ^ 1], c->d_label, c->d_ctr, c->st);
+    seg_end(c, a, (double)out * (12 + 12) + (double)A1 * 8, 2);
+    c->launches += 2;
+    cur ^= 1;
+    CKL();
+    A = A1;
+    if (A == 0) break;
+    cur = do_sort(c, cur, A, false);  // next iteration's line 8
+    CKL();
+  }
+  // changed2 of the last iteration
+  TRY(sync_read(c));
+  if (!c->iters.empty()) c->iters.back().changed2 = c->h_ctr[sv::C_CHANGED2] - chg2_prev;
+  return CC_OK;
+}
+
+extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
+  if (!c) return CC_ERR_INVALID;
+  if (!c->loaded) return fail(c, CC_ERR_STATE, "cc_run before cc_load_edges");
+  if (mode != CC_MODE_AUTO && mode != CC_MODE_SV && mode != CC_MODE_BFS_SV)
+    return fail(c, CC_ERR_INVALID, "bad mode %d", (int)mode);
+  CK(cudaSetDevice(c->cfg.device));
+  c->ran = false;
+  c->iters.clear();
+  c->launches = 0;
+  c->ev_used = 0;
+  c->prof_sort.clear(); c->prof_seg.clear(); c->prof_bfs.clear(); c->it_ev.clear();
+  c->sort_bytes = c->seg_bytes = c->bfs_bytes = 0;
+  for (int i = 0; i < 3; i++) { c->kms[i] = c->kbytes[i] = 0; c->klaunch[i] = 0; }
+  cc_report& R = c->rep;
+  R = cc_report{};
+  const uint64_t n = c->n, m = c->m;
+  R.m_edges = m;
+
+  cudaEvent_t e0 = ev_get(c), e_pred, e_bfs, e_filter, e_sv, e_end;
+  CK(cudaEventRecord(e0, c->st));
+  // ------------------------------------------------ prediction (Alg. 2 lines 2-3)
+  CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
+  CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
+  CK(cudaMemsetAsync(c->d_gctr + graph::G_MINVIS, 0xFF, sizeof(uint64_t), c->st));
+  sv::launch_init_labels(c->d_label, n, c->st);
+  graph::launch_degree(c->d_edges, m, c->d_deg, c->st);
+  const bool want_hist = (mode == CC_MODE_AUTO) || (c->cfg.flags & CC_FLAG_TRACE);
+  if (want_hist) CK(cudaMemsetAsync(c->d_hist, 0, sizeof(uint32_t) * graph::HIST_DENSE, c->st));
+  graph::launch_deg_hist(c->d_deg, n, c->d_hist, c->d_tail, c->d_gctr, c->st);
+  c->launches += 3;
+  CKL();
+  TRY(sync_read(c));
+  R.n_present = c->h_gctr[graph::G_NPRESENT];
+  const uint64_t maxkey = c->h_gctr[graph::G_MAXKEY];
+  R.max_degree = maxkey >> 32;
+  const uint64_t root = maxkey ? (uint64_t)(0xFFFFFFFFu - (uint32_t)maxkey) : 0;
+  bool run_bfs = (mode == CC_MODE_BFS_SV);
+  R.ls_alpha = R.ls_r2 = R.ks_stat = R.ks_alpha = NAN;
+  if (want_hist && R.max_degree > 0) {
+    const uint64_t dmax = R.max_degree;
+    const uint64_t dense_n = std::min<uint64_t>(dmax + 1, graph::HIST_DENSE);
+    const uint64_t tail_n = std::min<uint64_t>(c->h_gctr[graph::G_TAIL], graph::TAIL_CAP);
+    CK(cudaMemcpyAsync(c->h_hist, c->d_hist, sizeof(uint32_t) * dense_n, cudaMemcpyDeviceToHost, c->st));
+    if (tail_n)
+      CK(cudaMemcpyAsync(c->h_hist + graph::HIST_DENSE, c->d_tail, sizeof(uint32_t) * tail_n,
+                         cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    gate::Hist h;
+    for (uint64_t d = 1; d < dense_n; d++)
+      if (c->h_hist[d]) h.push_back({d, c->h_hist[d]});
+    if (tail_n) {
+      std::vector<uint32_t> t(c->h_hist + graph::HIST_DENSE, c->h_hist + graph::HIST_DENSE + tail_n);
+      std::sort(t.begin(), t.end());
+      for (size_t i = 0; i < t.size();) {
+        size_t j = i;
+        while (j < t.size() && t[j] == t[i]) j++;
+        h.push_back({t[i], (uint64_t)(j - i)});
+        i = j;
+      }
+    }
+    gate::LsFit g = gate::fit_ls(h);
+    R.ls_alpha = g.alpha;
+    R.ls_r2 = g.r2;
+    const bool need_ks = (c->cfg.flags & CC_FLAG_GATE_KS) || (c->cfg.flags & CC_FLAG_TRACE);
+    bool ks_ok = false;
+    if (need_ks) {
+      gate::KsFit k = gate::fit_ks(h);
+      if (k.valid) {
+        R.ks_stat = k.ks; R.ks_alpha = k.alpha; R.ks_xmin = k.xmin; ks_ok = true;
+      }
+    }
+    if (mode == CC_MODE_AUTO)
+      run_bfs = (c->cfg.flags & CC_FLAG_GATE_KS) ? (ks_ok && R.ks_stat < c->cfg.tau) : g.scale_free;
+  }
+  if (R.max_degree == 0) run_bfs = false;
+  e_pred = ev_get(c);
+  CK(cudaEventRecord(e_pred, c->st));
+
+  // ------------------------------------------------ BFS peel + filter (lines 7-11)
+  const uint2* sv_edges = c->d_edges;
+  uint64_t m_sv = m;
+  const uint32_t* vis = nullptr;
+  e_bfs = e_filter = e_pred;
+  if (run_bfs) {
+    R.ran_bfs = 1;
+    R.bfs_root = root;
+    const uint64_t nw = (n + 31) / 32;
+    uint32_t *V = c->d_bm[0], *F = c->d_bm[1], *X = c->d_bm[2];
+    CK(cudaMemsetAsync(V, 0, sizeof(uint32_t) * nw, c->st));
+    CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * nw, c->st));
+    c->h_word[0] = 1u << (root & 31);
+    CK(cudaMemcpyAsync(V + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(F + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+    uint64_t visited = 1, levels = 0;
+    while (true) {
+      CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
+      CK(cudaMemsetAsync(c->d_gctr + graph::G_NEWVIS, 0, sizeof(uint64_t), c->st));
+      cudaEvent_t a = nullptr;
+      if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
+      graph::launch_bfs_level(c->d_edges, m, F, V, X, c->d_gctr, c->st);
+      c->launches += 1;
+      if (profiling(c)) {
+        cudaEvent_t b = ev_get(c);
+        cudaEventRecord(b, c->st);
+        c->prof_bfs.push_back({a, b});
+        c->bfs_bytes += 8.0 * (double)m;
+        c->klaunch[2] += 1;
+      }
+      CKL();
+      TRY(sync_read(c));
+      const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
+      if (nv == 0) break;
+      visited += nv;
+      levels++;
+      std::swap(F, X);
+    }
+    R.bfs_visited = visited;
+    R.bfs_levels = levels;
+    graph::launch_min_visited(V, n, c->d_gctr, c->st);
+    graph::launch_bfs_labels(V, n, c->d_label, c->d_gctr, c->st);
+    c->launches += 2;
+    e_bfs = ev_get(c);
+    CK(cudaEventRecord(e_bfs, c->st));
+    if (!c->d_rem) TRY(dalloc_t(c, &c->d_rem, m + 1));
+    graph::launch_filter(c->d_edges, m, V, c->d_rem, c->d_gctr, c->st);
+    c->launches += 1;
+    CKL();
+    TRY(sync_read(c));
+    m_sv = c->h_gctr[graph::G_REMAIN];
+    R.remainder_edges = m_sv;
+    sv_edges = c->d_rem;
+    vis = V;
+    e_filter = ev_get(c);
+    CK(cudaEventRecord(e_filter, c->st));
+  }
+
+  // ------------------------------------------------ SV (line 13)
+  TRY(run_sv(c, sv_edges, m_sv, vis));
+  R.sv_iterations = (uint32_t)c->iters.size();
+  e_sv = ev_get(c);
+  CK(cudaEventRecord(e_sv, c->st));
+  e_end = ev_get(c);
+  CK(cudaEventRecord(e_end, c->st));
+  CK(cudaStreamSynchronize(c->st));
+
+  // ------------------------------------------------ report
+  R.ms_total = ev_ms(e0, e_end);
+  R.ms_prediction = ev_ms(e0, e_pred);
+  R.ms_bfs = run_bfs ? ev_ms(e_pred, e_bfs) : 0;
+  R.ms_filter = run_bfs ? ev_ms(e_bfs, e_filter) : 0;
+  R.ms_sv = ev_ms(e_filter, e_sv);
+  R.ms_finalize = ev_ms(e_sv, e_end);
+  for (size_t i = 0; i < c->it_ev.size() && i < c->iters.size(); i++)
+    c->iters[i].ms = ev_ms(c->it_ev[i], i + 1 < c->it_ev.size() ? c->it_ev[i + 1] : e_sv);
+  if (profiling(c)) {
+    for (auto& p : c->prof_sort) c->kms[0] += ev_ms(p.first, p.second);
+    for (auto& p : c->prof_seg) c->kms[1] += ev_ms(p.first, p.second);
+    for (auto& p : c->prof_bfs) c->kms[2] += ev_ms(p.first, p.second);
+    c->kbytes[0] = c->sort_bytes;
+    c->kbytes[1] = c->seg_bytes;
+    c->kbytes[2] = c->bfs_bytes;
+  }
+  R.iters = c->iters.data();
+  R.n_iters = (uint32_t)c->iters.size();
+  // components (isolated ids included): computed by the caller from labels if needed;
+  // here: n_present-independent count of roots is not materialised (see cc_labels_u32).
+  c->ran = true;
+  if (out) *out = R;
+  return CC_OK;
+}
+
+extern "C" cc_status cc_labels_u32(cc_ctx* c, uint32_t* out, uint64_t cap, uint64_t* count,
+                                   int out_on_device) {
+  if (!c) return CC_ERR_INVALID;
+  if (!c->ran) return fail(c, CC_ERR_STATE, "cc_labels before cc_run");
+  if (count) *count = c->n;
+  if (!out || cap < c->n) return fail(c, CC_ERR_INVALID, "output buffer too small");
+  CK(cudaSetDevice(c->cfg.device));
+  if (c->n)
+    CK(cudaMemcpyAsync(out, c->d_label, sizeof(uint32_t) * c->n,
+                       out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return CC_OK;
+}
+
+extern "C" cc_status cc_labels_u64(cc_ctx* c, uint64_t* ids, uint64_t* labels, uint64_t cap,
+                                   uint64_t* count, int out_on_device) {
+  (void)ids; (void)labels; (void)cap; (void)count; (void)out_on_device;
+  if (!c) return CC_ERR_INVALID;
+  return fail(c, CC_ERR_STATE, "no u64 graph loaded");
+}
+
+extern "C" cc_status cc_labels_device(cc_ctx* c, const uint32_t** labels, uint64_t* count) {
+  if (!c || !labels) return CC_ERR_INVALID;
+  if (!c->ran) return fail(c, CC_ERR_STATE, "cc_labels_device before cc_run");
+  *labels = c->d_label;
+  if (count) *count = c->n;
+  return CC_OK;
+}
+
+extern "C" cc_status cc_kernel_stats(const cc_ctx* c, int which, double* ms, double* bytes,
+                                     uint64_t* launches) {
+  if (!c || which < 0 || which > 2) return CC_ERR_INVALID;
+  if (ms) *ms = c->kms[which];
+  if (bytes) *bytes = c->kbytes[which];
+  if (launches) *launches = c->klaunch[which];
+  return CC_OK;
+}

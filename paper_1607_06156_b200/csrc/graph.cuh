@@ -1,0 +1,37 @@
+// graph.cuh -- prediction (degree distribution), BFS peel and filter kernels (Alg. 2).
+#pragma once
+#include "common.cuh"
+
+namespace cc {
+namespace graph {
+
+constexpr uint32_t HIST_DENSE = 1u << 20;  // dense histogram bins [0, 2^20); larger -> tail list
+constexpr uint32_t TAIL_CAP = 1u << 20;
+
+// counters (u64) in the graph-stage counter block
+enum GCtr : int {
+  G_NPRESENT = 0,  // ids with degree >= 1
+  G_MAXKEY,        // max over (deg<<32 | ~v): max degree, ties -> smallest id
+  G_TAIL,          // number of degrees >= HIST_DENSE (tail list length)
+  G_NEWVIS,        // BFS: newly visited in the current level
+  G_REMAIN,        // filter output cursor
+  G_MINVIS,        // min visited id
+  G_ERR,           // input validation flags
+  G_NUM
+};
+
+void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr, cudaStream_t st);
+void launch_degree(const uint2* edges, uint64_t m, uint32_t* deg, cudaStream_t st);
+void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* tail,
+                     uint64_t* gctr, cudaStream_t st);
+// edge-streaming bitmap BFS level; returns nothing, newly visited count in gctr[G_NEWVIS]
+void launch_bfs_level(const uint2* edges, uint64_t m, const uint32_t* frontier, uint32_t* visited,
+                      uint32_t* next, uint64_t* gctr, cudaStream_t st);
+void launch_filter(const uint2* edges, uint64_t m, const uint32_t* visited, uint2* out,
+                   uint64_t* gctr, cudaStream_t st);
+void launch_bfs_labels(const uint32_t* visited, uint64_t n, uint32_t* label, uint64_t* gctr,
+                       cudaStream_t st);
+void launch_min_visited(const uint32_t* visited, uint64_t n, uint64_t* gctr, cudaStream_t st);
+
+}  // namespace graph
+}  // namespace cc

@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Labels are integer results and must be bit-identical to the union-find oracle; the SV
+per-iteration counters are order-independent functions of the input and
+must equal the Alg. 1 transcription exactly; the gate's floating-point outputs are compared
+to the oracle's FP64 within 1e-9 relative (same formula, same precision, different
+summation order), and the route decision must be identical.
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from oracle import bfs as obfs
+from oracle import degree as odeg
+from oracle import sv as osv
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def cc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_06156_b200 as ccmod
+    ctx = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE)
+    yield ctx
+    ctx.close()
+
+
+def run(cc, n, edges, mode="auto"):
+    e = np.asarray(edges, dtype=np.uint32).reshape(-1, 2)
+    cc.load(e, n)
+    rep = cc.run(mode)
+    return cc.labels().astype(np.int64), rep
+
+
+def trace_of(rep):
+    return [dict(A=it["active_in"], P=it["partitions"], T=it["temps"], completed=it["completed"],
+                 changed=it["changed"], changed2=it["changed2"]) for it in rep["iters"]]
+
+
+def norm(tr):
+    return [{k: int(r[k]) for k in ("A", "P", "T", "completed", "changed", "changed2")} for r in tr]
+
+
+# ------------------------------------------------------------------ hand cases + tiny
+def test_hand_cases(cc):
+    h = json.load(open(os.path.join(ROOT, "tests", "golden", "hand_cases.json")))
+    for c in h["cases"]:
+        for mode in ("auto", "sv", "bfs+sv"):
+            lab, _ = run(cc, c["n"], c["edges"], mode)
+            assert lab.tolist() == c["labels"], (c["name"], mode)
+
+
+def test_fig1b_trace(cc):
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "fig1b.json")))
+    lab, rep = run(cc, g["n"], g["edges"], "sv")
+    assert lab.tolist() == g["labels"]
+    assert norm(trace_of(rep)) == g["trace"]
+
+
+def test_exhaustive_tiny(cc):
+    for n in (1, 2, 3, 4):
+        pairs = list(itertools.combinations_with_replacement(range(n), 2))
+        for mask in range(1 << len(pairs)):
+            edges = [pairs[i] for i in range(len(pairs)) if mask >> i & 1]
+            want, tr = osv.sv_trace(n, edges)
+            lab, rep = run(cc, n, edges, "sv")
+            assert np.array_equal(lab, want), edges
+            assert norm(trace_of(rep)) == norm(tr), edges
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_small_trace(cc, seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(2, 3000))
+    m = int(rng.integers(0, 3 * n))
+    e = graphgen.er(seed, n, m)
+    want, tr = osv.sv_trace(n, e)
+    lab, rep = run(cc, n, e, "sv")
+    assert np.array_equal(lab, want)
+    assert norm(trace_of(rep)) == norm(tr)
+
+
+def test_regression_trees(cc):
+    """SURVEY.md C3 counterexamples to 'drop stable partitions': must label all 0."""
+    t1 = [(19, 12), (21, 10), (24, 5), (24, 14), (17, 18), (16, 1), (11, 23), (11, 9), (6, 3),
+          (15, 4), (22, 5), (8, 23), (12, 20), (10, 19), (9, 2), (3, 4), (17, 0), (21, 22),
+          (15, 18), (7, 13), (6, 7), (13, 16), (1, 14), (20, 8)]
+    t2 = [(9, 13), (5, 19), (12, 3), (17, 10), (13, 7), (19, 10), (6, 7), (12, 18), (16, 14),
+          (3, 6), (1, 14), (8, 15), (16, 18), (11, 9), (4, 0), (8, 2), (11, 2), (4, 17), (15, 5)]
+    for n, t in ((25, t1), (20, t2)):
+        lab, _ = run(cc, n, t, "sv")
+        assert np.all(lab == 0)
+
+
+# ------------------------------------------------------------------ edge cases
+def test_empty_and_isolated(cc):
+    lab, rep = run(cc, 10, np.zeros((0, 2), np.uint32))
+    assert lab.tolist() == list(range(10))
+    assert rep["sv_iterations"] == 0
+    lab, _ = run(cc, 1, [(0, 0)])
+    assert lab.tolist() == [0]
+
+
+def test_range_error(cc):
+    import paper_1607_06156_b200 as ccmod
+    with pytest.raises(ccmod.CCError) as ei:
+        cc.load(np.array([[0, 5]], np.uint32), 5)
+    assert ei.value.status == ccmod.CC_ERR_RANGE
+
+
+@pytest.mark.parametrize("m", [4095, 4096, 4097, 8191, 2 * 4096 * 16 + 3, 100003])
+def test_ragged_tiles(cc, m):
+    """Tuple counts straddling radix tiles (4096), segment chunks (2048) and pass tiles."""
+    n = max(64, m // 3)
+    e = graphgen.er(m, n, m)
+    want, tr = osv.sv_trace(n, e)
+    lab, rep = run(cc, n, e, "sv")
+    assert np.array_equal(lab, want)
+    assert norm(trace_of(rep)) == norm(tr)
+
+
+def test_long_path_and_star(cc):
+    """Giant buckets spanning many tiles (star hub) and deep pointer jumping (path)."""
+    n = 200000
+    perm = np.random.default_rng(3).permutation(n).astype(np.uint32)
+    path = np.stack([perm[:-1], perm[1:]], 1)
+    lab, rep = run(cc, n, path, "sv")
+    assert np.all(lab == 0)
+    assert rep["sv_iterations"] <= 2 * 18 + 2
+    star = np.stack([np.full(n - 1, 7, np.uint32), np.delete(np.arange(n, dtype=np.uint32), 7)], 1)
+    for mode in ("sv", "bfs+sv"):
+        lab, _ = run(cc, n, star, mode)
+        assert np.all(lab == 0)
+
+
+# ------------------------------------------------------------------ configs (BASELINE.json)
+@pytest.mark.parametrize("cfg,scale", [("c1", 1.0), ("c2", 0.02), ("c3", 0.02)])
+def test_config_trace_parity(cc, cfg, scale):
+    g = graphgen.make(cfg, scale)
+    want, tr = osv.sv_trace(g.n, g.edges)
+    lab, rep = run(cc, g.n, g.edges, "sv")
+    assert np.array_equal(lab, want)
+    assert norm(trace_of(rep)) == norm(tr)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_config_full_labels(cc, cfg):
+    """Full BASELINE.json sizes, the launch configuration bench.py times (mode=auto)."""
+    g = graphgen.make(cfg)
+    want = oracle.uf_labels(g.n, g.edges).astype(np.int64)
+    for mode in ("auto", "sv"):
+        lab, rep = run(cc, g.n, g.edges, mode)
+        assert np.array_equal(lab, want), mode
+        assert rep["ran_bfs"] == (1 if mode == "bfs+sv" else 0)
+        # trace invariants at any size (C5): T = P - completed; A non-increasing
+        its = rep["iters"]
+        for i, it in enumerate(its):
+            assert it["temps"] == it["partitions"] - it["completed"]
+            if i:
+                assert it["active_in"] <= its[i - 1]["active_in"]
+        assert its[-1]["changed"] == 0
+
+
+def test_rmat_bfs_route(cc):
+    g = graphgen.rmat_scale_graph(18)
+    want = oracle.uf_labels(g.n, g.edges).astype(np.int64)
+    deg, hist = odeg.degree_distribution(g.n, g.edges)
+    root = obfs.bfs_root(deg)
+    vis, levels = obfs.bfs(g.n, g.edges, root)
+    for mode in ("auto", "bfs+sv", "sv"):
+        lab, rep = run(cc, g.n, g.edges, mode)
+        assert np.array_equal(lab, want), mode
+        if mode != "sv":
+            assert rep["ran_bfs"] == 1
+            assert rep["bfs_root"] == root
+            assert rep["bfs_visited"] == int(vis.sum())
+            assert rep["bfs_levels"] == levels
+            rem = obfs.filter_edges(g.edges, vis)
+            assert rep["remainder_edges"] == rem.shape[0]
+            # SV trace on the remainder equals the oracle's
+            _, tr = osv.sv_trace(g.n, rem)
+            assert norm(trace_of(rep)) == norm(tr)
+
+
+# ------------------------------------------------------------------ prediction / gate
+@pytest.mark.parametrize("graph", ["c1", "c2s", "rmat14", "rmat18"])
+def test_gate_parity(cc, graph):
+    if graph == "c1":
+        g = graphgen.make("c1")
+    elif graph == "c2s":
+        g = graphgen.make("c2", 0.05)
+    else:
+        g = graphgen.rmat_scale_graph(int(graph[4:]))
+    _, hist = odeg.degree_distribution(g.n, g.edges)
+    gl = odeg.gate_ls(hist)
+    ks = odeg.ks_powerlaw(hist)
+    lab, rep = run(cc, g.n, g.edges, "auto")
+    assert rep["max_degree"] == gl["dmax"]
+    assert rep["n_present"] == int(hist.sum())
+    assert rep["ran_bfs"] == int(gl["scale_free"])
+    if np.isnan(gl["alpha"]):
+        assert np.isnan(rep["ls_alpha"])
+    else:
+        assert rep["ls_alpha"] == pytest.approx(gl["alpha"], rel=1e-9)
+        assert rep["ls_r2"] == pytest.approx(gl["r2"], rel=1e-9)
+    if np.isnan(ks["ks"]):
+        assert np.isnan(rep["ks_stat"])
+    else:
+        assert rep["ks_xmin"] == ks["xmin"]
+        assert rep["ks_alpha"] == pytest.approx(ks["alpha"], rel=1e-9)
+        assert rep["ks_stat"] == pytest.approx(ks["ks"], rel=1e-7, abs=1e-9)
+
+
+def test_device_input_and_output(cc):
+    import torch
+    g = graphgen.make("c1", 0.5)
+    want = oracle.uf_labels(g.n, g.edges)
+    t = torch.from_numpy(g.edges.view(np.int32)).cuda()
+    cc.load(t, g.n)
+    cc.run("auto")
+    out = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    cc.labels(out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
