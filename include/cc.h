@@ -57,12 +57,13 @@ typedef enum {
 typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
 
 /* cc_config.flags */
-#define CC_FLAG_TRACE 0x1u           /* record per-iteration counters in cc_report.iters   */
+#define CC_FLAG_TRACE 0x1u           /* also fit the histogram + K-S in forced modes        */
 #define CC_FLAG_GATE_KS 0x2u         /* decide with the paper's K-S < tau
                                         instead of gate G (least-squares fit)  */
 #define CC_FLAG_NO_EARLY_EXCLUDE 0x4u /* reserved: end-of-iteration exclusion timing        */
 #define CC_FLAG_REGROUP_DIRECT 0x8u  /* SV regroups by direct addressing instead of radix
                                         sort (B200 variant; identical sets)  */
+#define CC_FLAG_PROFILE 0x10u        /* CUDA-event timing of kernel families (cc_kernel_stats) */
 
 typedef void* (*cc_alloc_fn)(size_t bytes, void* stream, void* user);
 typedef void (*cc_free_fn)(void* ptr, size_t bytes, void* stream, void* user);
@@ -147,8 +148,8 @@ cc_status cc_labels_device(cc_ctx* ctx, const uint32_t** labels, uint64_t* count
 /* Number of kernel launches enqueued by the last cc_run (evidence for bench.py). */
 uint64_t cc_last_launch_count(const cc_ctx* ctx);
 
-/* Device time (ms, CUDA events on cfg.stream) of the dominant kernel family in the last
- * cc_run, with its algorithmic bytes (for the roofline line of bench.py):
+/* Device time (ms, CUDA events on cfg.stream) of a kernel family in the last cc_run
+ * (recorded only under CC_FLAG_PROFILE), with its algorithmic bytes (bench.py roofline):
  *   which = 0: radix-sort scatter passes, 1: segmented passes, 2: BFS levels. */
 cc_status cc_kernel_stats(const cc_ctx* ctx, int which, double* ms, double* bytes,
                           uint64_t* launches);

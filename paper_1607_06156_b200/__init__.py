@@ -26,6 +26,7 @@ CC_FLAG_TRACE = 0x1
 CC_FLAG_GATE_KS = 0x2
 CC_FLAG_NO_EARLY_EXCLUDE = 0x4
 CC_FLAG_REGROUP_DIRECT = 0x8
+CC_FLAG_PROFILE = 0x10
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)

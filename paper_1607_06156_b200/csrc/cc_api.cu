@@ -44,6 +44,7 @@ struct cc_ctx {
   uint32_t* d_hist = nullptr;
   uint32_t* d_tail = nullptr;
   uint32_t* d_bm[3] = {nullptr, nullptr, nullptr};  // visited, frontier, next
+  uint32_t* d_sbm[3] = {nullptr, nullptr, nullptr}; // direct SV: notpc, ncp, head
   uint64_t* d_w[2] = {nullptr, nullptr};
   uint32_t* d_q[2] = {nullptr, nullptr};
   uint64_t cap = 0;
@@ -130,6 +131,7 @@ static void dfree_all(cc_ctx* c) {
   c->d_edges = c->d_rem = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
   c->d_bm[0] = c->d_bm[1] = c->d_bm[2] = nullptr;
+  c->d_sbm[0] = c->d_sbm[1] = c->d_sbm[2] = nullptr;
   c->d_w[0] = c->d_w[1] = nullptr;
   c->d_q[0] = c->d_q[1] = nullptr;
   c->d_ctr = c->d_gctr = nullptr;
@@ -150,7 +152,7 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   cudaEventElapsedTime(&ms, a, b);
   return ms;
 }
-static bool profiling(const cc_ctx* c) { return (c->cfg.flags & CC_FLAG_TRACE) != 0; }
+static bool profiling(const cc_ctx* c) { return (c->cfg.flags & CC_FLAG_PROFILE) != 0; }
 
 static int bits_for(uint64_t n) {
   int b = 0;
@@ -243,6 +245,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->d_hist, graph::HIST_DENSE));
   TRY(dalloc_t(c, &c->d_tail, graph::TAIL_CAP));
   for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], nw));
+  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_sbm[i], nw));
   for (int i = 0; i < 2; i++) {
     TRY(dalloc_t(c, &c->d_w[i], c->cap));
     TRY(dalloc_t(c, &c->d_q[i], c->cap));
@@ -323,6 +326,79 @@ static void seg_end(cc_ctx* c, cudaEvent_t a, double bytes, int nl) {
   }
 }
 
+// Alg. 1 with direct-addressed buckets (sv_direct.cu): same passes, no tuple movement
+// except the compaction of the partition passes.
+static cc_status run_sv_direct(cc_ctx* c, uint64_t A, int cur) {
+  const uint64_t n = c->n;
+  const uint64_t nw = (n + 31) / 32;
+  uint32_t *umin = c->d_segA, *pmin = c->d_segB;
+  uint32_t *notpc = c->d_sbm[0], *ncp = c->d_sbm[1], *head = c->d_sbm[2];
+  const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
+  uint64_t chg2_prev = 0;
+  for (uint32_t it = 0;; it++) {
+    if (it >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
+    cudaEvent_t ev_it = ev_get(c);
+    CK(cudaEventRecord(ev_it, c->st));
+    cudaEvent_t a = nullptr;
+    seg_begin(c, &a);
+    // ---- lines 8-13: u_min per vertex bucket, 'potentially completed'
+    CK(cudaMemsetAsync(umin, 0xFF, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(notpc, 0, sizeof(uint32_t) * nw, c->st));
+    sv::launch_direct_vmin(c->d_w[cur], A, umin, c->st);
+    sv::launch_direct_vpc(c->d_w[cur], A, umin, notpc, c->st);
+    // ---- lines 14-22: p_min per partition bucket, completion, exclusion, temporaries
+    CK(cudaMemsetAsync(pmin, 0xFF, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(ncp, 0, sizeof(uint32_t) * nw, c->st));
+    CK(cudaMemsetAsync(head, 0, sizeof(uint32_t) * nw, c->st));
+    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_TEMPS + 1), c->st));
+    sv::launch_direct_pmin(true, c->d_w[cur], A, umin, notpc, pmin, ncp, c->st);
+    sv::launch_direct_papply(true, c->d_w[cur], A, pmin, ncp, head, c->d_w[cur ^ 1], c->d_label,
+                             c->d_ctr, c->st);
+    c->launches += 4;
+    cur ^= 1;
+    CKL();
+    TRY(sync_read(c));
+    const uint64_t out = c->h_ctr[sv::C_OUT];
+    const uint64_t T = c->h_ctr[sv::C_TEMPS];
+    const uint64_t A1 = out - T;
+    cc_iter_stat s{};
+    s.active_in = A;
+    s.partitions = c->h_ctr[sv::C_PARTITIONS];
+    s.completed = c->h_ctr[sv::C_COMPLETED];
+    s.changed = c->h_ctr[sv::C_CHANGED];
+    s.temps = T;
+    if (!c->iters.empty()) {
+      c->iters.back().changed2 = c->h_ctr[sv::C_CHANGED2] - chg2_prev;
+      chg2_prev = c->h_ctr[sv::C_CHANGED2];
+    }
+    c->iters.push_back(s);
+    c->it_ev.push_back(ev_it);
+    if (out == 0) {
+      seg_end(c, a, (double)A * 32, 4);
+      break;
+    }
+    // ---- line 24 (redo 8-13 with temporaries) and line 25 (redo 14-21), lines 26-28
+    CK(cudaMemsetAsync(umin, 0xFF, sizeof(uint32_t) * n, c->st));
+    sv::launch_direct_vmin(c->d_w[cur], out, umin, c->st);
+    CK(cudaMemsetAsync(pmin, 0xFF, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(head, 0, sizeof(uint32_t) * nw, c->st));
+    CK(cudaMemsetAsync(c->d_ctr + sv::C_OUT, 0, sizeof(uint64_t), c->st));
+    sv::launch_direct_pmin(false, c->d_w[cur], out, umin, nullptr, pmin, nullptr, c->st);
+    sv::launch_direct_papply(false, c->d_w[cur], out, pmin, nullptr, head, c->d_w[cur ^ 1],
+                             c->d_label, c->d_ctr, c->st);
+    c->launches += 3;
+    cur ^= 1;
+    CKL();
+    // algorithmic bytes of the streamed tuple words (8 B per read / write)
+    seg_end(c, a, (double)A * 32 + (double)out * (8 + 24) + (double)A1 * 8, 7);
+    A = A1;
+    if (A == 0) break;
+  }
+  TRY(sync_read(c));
+  if (!c->iters.empty()) c->iters.back().changed2 = c->h_ctr[sv::C_CHANGED2] - chg2_prev;
+  return CC_OK;
+}
+
 // Alg. 1 on (edges, m_sv); vertices present iff deg > 0 and not BFS-visited.
 static cc_status run_sv(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint32_t* vis) {
   const uint64_t n = c->n;
@@ -332,6 +408,7 @@ static cc_status run_sv(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint
   TRY(sync_read(c));
   uint64_t A = 2 * m_sv + c->h_ctr[sv::C_VT_OUT];
   if (A == 0) return CC_OK;
+  if (c->cfg.flags & CC_FLAG_REGROUP_DIRECT) return run_sv_direct(c, A, 0);
   const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
   int cur = do_sort(c, 0, A, false);  // line 8: sort by r
   CKL();

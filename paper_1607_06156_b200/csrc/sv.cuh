@@ -34,5 +34,15 @@ void launch_partition_apply(bool first, bool sorted, const uint64_t* win, const 
                             uint64_t n, const uint32_t* segA, const uint32_t* segB,
                             uint64_t* wout, uint32_t* label, uint64_t* ctr, cudaStream_t st);
 
+// direct-addressed bucket passes (sv_direct.cu)
+void launch_direct_vmin(const uint64_t* w, uint64_t n, uint32_t* umin, cudaStream_t st);
+void launch_direct_vpc(const uint64_t* w, uint64_t n, const uint32_t* umin, uint32_t* notpc,
+                       cudaStream_t st);
+void launch_direct_pmin(bool first, const uint64_t* w, uint64_t n, const uint32_t* umin,
+                        const uint32_t* notpc, uint32_t* pmin, uint32_t* ncp, cudaStream_t st);
+void launch_direct_papply(bool first, const uint64_t* w, uint64_t n, const uint32_t* pmin,
+                          const uint32_t* ncp, uint32_t* headbm, uint64_t* wout, uint32_t* label,
+                          uint64_t* ctr, cudaStream_t st);
+
 }  // namespace sv
 }  // namespace cc

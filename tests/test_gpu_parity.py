@@ -24,13 +24,16 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.fixture(scope="module")
-def cc():
+@pytest.fixture(scope="module", params=["sort", "direct"])
+def cc(request):
+    """Both regroup engines: radix-sorted buckets (paper's data movement) and
+    direct-addressed buckets (B200 variant); same sets, same counters."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1607_06156_b200 as ccmod
-    ctx = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE)
+    flags = ccmod.CC_FLAG_TRACE | (ccmod.CC_FLAG_REGROUP_DIRECT if request.param == "direct" else 0)
+    ctx = ccmod.CC(device=0, flags=flags)
     yield ctx
     ctx.close()
 
