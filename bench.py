@@ -181,7 +181,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="auto", choices=["auto", "sv", "bfs+sv"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--regroup", default="direct", choices=["direct", "sort"],
+    ap.add_argument("--regroup", default="csr", choices=["csr", "direct", "sort"],
                     help="SV bucket regroup engine (DESIGN.md §5.3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -203,7 +203,7 @@ def main():
 
     g = make_graph(args.config, rk)
     n, m = g.n, g.m
-    flags = cc.CC_FLAG_PROFILE | (cc.CC_FLAG_REGROUP_DIRECT if args.regroup == "direct" else 0)
+    flags = cc.CC_FLAG_PROFILE | cc.REGROUP_FLAGS[args.regroup]
     ctx = cc.CC(device=lr, stream=stream, flags=flags)
     d_edges = torch.from_numpy(g.edges.view(np.int32)).to(dev)
     ctx.load(d_edges, n)

@@ -61,8 +61,13 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
 #define CC_FLAG_GATE_KS 0x2u         /* decide with the paper's K-S < tau
                                         instead of gate G (least-squares fit)  */
 #define CC_FLAG_NO_EARLY_EXCLUDE 0x4u /* reserved: end-of-iteration exclusion timing        */
-#define CC_FLAG_REGROUP_DIRECT 0x8u  /* SV regroups by direct addressing instead of radix
-                                        sort (B200 variant; identical sets)  */
+/* SV regroup engine (all three compute identical sets and counters):
+ *   default : r-stationary -- tuples regrouped by r once (CSR build), partition buckets
+ *             addressed directly in L2-resident slots, ordered compaction
+ *   SORT    : the paper's four radix-sort regroups per iteration
+ *   DIRECT  : no regroup at all; both bucket kinds addressed directly (ablation)        */
+#define CC_FLAG_REGROUP_SORT 0x8u
+#define CC_FLAG_REGROUP_DIRECT 0x20u
 #define CC_FLAG_PROFILE 0x10u        /* CUDA-event timing of kernel families (cc_kernel_stats) */
 
 typedef void* (*cc_alloc_fn)(size_t bytes, void* stream, void* user);

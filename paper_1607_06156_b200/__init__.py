@@ -25,7 +25,9 @@ CC_U32, CC_U64 = 0, 1
 CC_FLAG_TRACE = 0x1
 CC_FLAG_GATE_KS = 0x2
 CC_FLAG_NO_EARLY_EXCLUDE = 0x4
-CC_FLAG_REGROUP_DIRECT = 0x8
+CC_FLAG_REGROUP_SORT = 0x8
+CC_FLAG_REGROUP_DIRECT = 0x20
+REGROUP_FLAGS = {"csr": 0, "sort": 0x8, "direct": 0x20}
 CC_FLAG_PROFILE = 0x10
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)

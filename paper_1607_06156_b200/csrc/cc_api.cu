@@ -23,6 +23,7 @@
 #include "graph.cuh"
 #include "radix.cuh"
 #include "sv.cuh"
+#include "csr.cuh"
 
 using namespace cc;
 
@@ -57,6 +58,7 @@ struct cc_ctx {
   uint32_t* h_hist = nullptr;  // pinned histogram staging
   uint32_t* h_word = nullptr;
   radix::Workspace rws;
+  scan::State ss;
   std::vector<std::pair<void*, size_t>> allocs;
   // report
   std::vector<cc_iter_stat> iters;
@@ -136,6 +138,7 @@ static void dfree_all(cc_ctx* c) {
   c->d_q[0] = c->d_q[1] = nullptr;
   c->d_ctr = c->d_gctr = nullptr;
   c->rws = radix::Workspace();
+  c->ss = scan::State();
   c->cap = 0;
 }
 
@@ -238,7 +241,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   c->m = m;
   c->kbits = bits_for(n);
   const uint64_t nw = (n + 31) / 32 + 1;
-  c->cap = 2 * m + 2 * n + 64;
+  c->cap = (2 * m + 2 * n + 64 + 1023) & ~1023ull;  // keeps P = R + cap 16-byte aligned
   TRY(dalloc_t(c, &c->d_edges, m + 1));
   TRY(dalloc_t(c, &c->d_label, n + 1));
   TRY(dalloc_t(c, &c->d_deg, n + 1));
@@ -258,6 +261,10 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->rws.ghist, radix::MAX_PASSES * radix::RADIX));
   TRY(dalloc_t(c, &c->rws.lookback, c->rws.max_tiles * radix::RADIX));
   TRY(dalloc_t(c, &c->rws.tile_ctr, radix::MAX_PASSES));
+  c->ss.max_tiles = (c->cap + n) / 2048 + 4;
+  TRY(dalloc_t(c, &c->ss.flags, c->ss.max_tiles));
+  TRY(dalloc_t(c, &c->ss.ticket, 4));
+  CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * c->ss.max_tiles, c->st));
   CK(cudaMemsetAsync(c->rws.lookback, 0, sizeof(uint64_t) * c->rws.max_tiles * radix::RADIX, c->st));
   if (m)
     CK(cudaMemcpyAsync(c->d_edges, pairs, m * sizeof(uint2),
@@ -399,9 +406,112 @@ static cc_status run_sv_direct(cc_ctx* c, uint64_t A, int cur) {
   return CC_OK;
 }
 
+// Alg. 1, r-stationary engine (sv_csr.cu): one counting regroup by r (CSR build), then
+// per iteration: vertex pass, partition pass, partition statistics + temporaries,
+// ordered exclusion of completed partitions; second vertex/partition pass in place.
+static cc_status scan_epoch_guard(cc_ctx* c) {
+  if (((c->ss.epoch + 4) & scan::EPOCH_MASK) < 4) {
+    CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * c->ss.max_tiles, c->st));
+    c->ss.epoch += 8;
+  }
+  return CC_OK;
+}
+
+static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint32_t* vis) {
+  const uint64_t n = c->n;
+  const uint64_t nw = (n + 31) / 32;
+  uint32_t* R[2] = {reinterpret_cast<uint32_t*>(c->d_w[0]), reinterpret_cast<uint32_t*>(c->d_w[1])};
+  uint32_t* P[2] = {R[0] + c->cap, R[1] + c->cap};
+  uint32_t *off = c->d_q[0], *cur = c->d_q[1];
+  uint32_t *U = c->d_segA, *PMIN = c->d_segB;
+  uint32_t *NP = c->d_sbm[0], *NCP = c->d_sbm[1], *TB = c->d_sbm[2];
+  CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
+  cudaEvent_t a = nullptr;
+  seg_begin(c, &a);
+  TRY(scan_epoch_guard(c));
+  csr::build(edges, m_sv, c->d_deg, vis, n, off, cur, R[0], P[0], c->ss, c->d_ctr, c->st);
+  c->launches += 1;
+  CKL();
+  TRY(sync_read(c));
+  uint64_t A = c->h_ctr[sv::C_VT_OUT];
+  if (A == 0) return CC_OK;
+  if (A > c->cap) return fail(c, CC_ERR_INVALID, "tuple count %llu exceeds capacity", (unsigned long long)A);
+  csr::fill(edges, m_sv, off, cur, n, A, R[0], P[0], c->st);
+  c->launches += 2;
+  CKL();
+  seg_end(c, a, 4.0 * n + 8.0 * m_sv + 8.0 * A + 4.0 * n, 3);
+  int cur_buf = 0;
+  const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
+  uint64_t chg2_prev = 0;
+  for (uint32_t it = 0;; it++) {
+    if (it >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
+    cudaEvent_t ev_it = ev_get(c);
+    CK(cudaEventRecord(ev_it, c->st));
+    seg_begin(c, &a);
+    uint32_t *Rc = R[cur_buf], *Pc = P[cur_buf];
+    // ---- lines 8-13: vertex buckets are CSR rows; u_min and 'potentially completed'
+    CK(cudaMemsetAsync(U, 0xFF, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(NP, 0, sizeof(uint32_t) * nw, c->st));
+    csr::vpass(true, Rc, Pc, A, U, NP, c->st);
+    // ---- lines 14-21: p_min per partition bucket; completion
+    CK(cudaMemsetAsync(PMIN, 0xFF, sizeof(uint32_t) * n, c->st));
+    CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nw, c->st));
+    CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nw, c->st));
+    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_TEMPS + 1), c->st));
+    csr::ppass(true, Rc, Pc, A, U, NP, nullptr, PMIN, NCP, c->st);
+    // ---- line 22 (temporaries) + counters; exclusion of completed partitions
+    csr::pscan(true, PMIN, NCP, n, TB, c->d_ctr, c->st);
+    TRY(scan_epoch_guard(c));
+    csr::papply1(Rc, Pc, A, PMIN, NCP, R[cur_buf ^ 1], P[cur_buf ^ 1], c->d_label, c->ss, c->d_ctr,
+                 c->st);
+    c->launches += 4;
+    cur_buf ^= 1;
+    CKL();
+    TRY(sync_read(c));
+    const uint64_t A1 = c->h_ctr[sv::C_OUT];
+    cc_iter_stat s{};
+    s.active_in = A;
+    s.partitions = c->h_ctr[sv::C_PARTITIONS];
+    s.completed = c->h_ctr[sv::C_COMPLETED];
+    s.changed = c->h_ctr[sv::C_CHANGED];
+    s.temps = c->h_ctr[sv::C_TEMPS];
+    if (!c->iters.empty()) {
+      c->iters.back().changed2 = c->h_ctr[sv::C_CHANGED2] - chg2_prev;
+      chg2_prev = c->h_ctr[sv::C_CHANGED2];
+    }
+    c->iters.push_back(s);
+    c->it_ev.push_back(ev_it);
+    if (A1 == 0) {
+      seg_end(c, a, 8.0 * A + 8.0 * A + 8.0 * A, 4);
+      break;
+    }
+    Rc = R[cur_buf];
+    Pc = P[cur_buf];
+    // ---- line 24: vertex buckets again, temporaries <u,_,u> from the TB bitmap
+    CK(cudaMemsetAsync(U, 0xFF, sizeof(uint32_t) * n, c->st));
+    csr::vpass(false, Rc, Pc, A1, U, nullptr, c->st);
+    // ---- line 25: partition buckets again (+ temporaries), p <- p_min in place
+    CK(cudaMemsetAsync(PMIN, 0xFF, sizeof(uint32_t) * n, c->st));
+    csr::ppass(false, Rc, Pc, A1, U, nullptr, TB, PMIN, nullptr, c->st);
+    csr::temps(TB, n, U, PMIN, c->st);
+    csr::pscan(false, PMIN, nullptr, n, nullptr, c->d_ctr, c->st);
+    csr::papply2(Pc, A1, PMIN, c->st);
+    c->launches += 5;
+    CKL();
+    // algorithmic bytes streamed by this iteration's tuple passes (R,P u32 each)
+    seg_end(c, a, 8.0 * A * 3 + 8.0 * A1 * 4, 9);
+    A = A1;
+  }
+  TRY(sync_read(c));
+  if (!c->iters.empty()) c->iters.back().changed2 = c->h_ctr[sv::C_CHANGED2] - chg2_prev;
+  return CC_OK;
+}
+
 // Alg. 1 on (edges, m_sv); vertices present iff deg > 0 and not BFS-visited.
 static cc_status run_sv(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint32_t* vis) {
   const uint64_t n = c->n;
+  if (!(c->cfg.flags & (CC_FLAG_REGROUP_SORT | CC_FLAG_REGROUP_DIRECT)))
+    return run_sv_csr(c, edges, m_sv, vis);
   CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
   sv::launch_init_tuples(edges, m_sv, c->d_deg, vis, n, c->d_w[0], c->d_ctr, c->st, &c->launches);
   CKL();

@@ -1,0 +1,27 @@
+// csr.cuh -- launchers of the r-stationary SV engine (sv_csr.cu).
+#pragma once
+#include "scan.cuh"
+
+namespace cc {
+namespace csr {
+
+// CSR build (counting regroup by r): off[v] / cur[v] from degrees; ctr[C_VT_OUT] = A_0.
+void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* vis, uint64_t n,
+           uint32_t* off, uint32_t* cur, uint32_t* R, uint32_t* P, scan::State& ss, uint64_t* ctr,
+           cudaStream_t st);
+void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
+          uint32_t* R, uint32_t* P, cudaStream_t st);
+void vpass(bool with_pc, const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* U, uint32_t* NP,
+           cudaStream_t st);
+void ppass(bool first, const uint32_t* R, const uint32_t* P, uint64_t A, const uint32_t* U,
+           const uint32_t* NP, const uint32_t* TB, uint32_t* PMIN, uint32_t* NCP, cudaStream_t st);
+void temps(const uint32_t* TB, uint64_t n, const uint32_t* U, uint32_t* PMIN, cudaStream_t st);
+void pscan(bool first, const uint32_t* PMIN, const uint32_t* NCP, uint64_t n, uint32_t* TB,
+           uint64_t* ctr, cudaStream_t st);
+void papply1(const uint32_t* R, const uint32_t* P, uint64_t A, const uint32_t* PMIN,
+             const uint32_t* NCP, uint32_t* R2, uint32_t* P2, uint32_t* label, scan::State& ss,
+             uint64_t* ctr, cudaStream_t st);
+void papply2(uint32_t* P, uint64_t A, const uint32_t* PMIN, cudaStream_t st);
+
+}  // namespace csr
+}  // namespace cc

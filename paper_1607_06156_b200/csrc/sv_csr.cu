@@ -1,0 +1,417 @@
+// sv_csr.cu -- r-stationary edge-tuple SV (the default engine).
+//
+// Alg. 1 regroups A_i by the third element r (line 8) and by the first element p
+// (line 14) in every pass.  r never changes ("The third
+// element r ... is not changed throughout the algorithm") and the exclusion of completed
+// partitions removes whole vertex buckets, so one stable regroup by r at the start keeps
+// every later vertex bucket VB_i(u) contiguous: the tuple array is stored in CSR order
+// (row u = VB(u) = <x,_,u> for x in N[u]) and is only ever compacted in order.  That
+// one-time regroup is a counting sort on the degrees the prediction stage already
+// computed (SURVEY.md §8(a) a4 "CSR build").  Partition buckets PB_i(p) are addressed
+// directly: the minimum over PB_i(p) lives in slot p of an n-sized array kept in L2.
+// The temporaries <p_min,_,p_min>_tmp of line 22 are a bitmap over vertices: all a temp
+// does is add its own id p_min to VB(p_min) in pass 3 and its candidate to PB(p_min) in
+// pass 4 (fig:doubling), which the pass kernels fold in from the bitmap.
+// Every set and every counter of Alg. 1 is unchanged (tests/test_gpu_parity.py).
+//
+// Arrays (SoA, u32): R[i] = r (sorted), P[i] = p.  Slots: U[u] (u_min), NP (bitmap:
+// |M(u)| > 1), PMIN[p] (p_min), NCP (bitmap: PB(p) has a tuple that is not potentially
+// completed), TB (bitmap: temporary tuple targets).
+#include <algorithm>
+
+#include "csr.cuh"
+#include "sv.cuh"
+
+namespace cc {
+namespace csr {
+
+constexpr int B = 256;
+constexpr uint32_t INF = 0xFFFFFFFFu;
+
+CC_DEVI void min_slot(uint32_t* a, uint32_t i, uint32_t v) {
+  if (v < *(volatile uint32_t*)&a[i]) atomicMin(&a[i], v);
+}
+CC_DEVI bool tbit(const uint32_t* bm, uint32_t i) { return (__ldg(&bm[i >> 5]) >> (i & 31)) & 1u; }
+CC_DEVI bool tbit_v(const uint32_t* bm, uint32_t i) {
+  return (*(volatile const uint32_t*)&bm[i >> 5] >> (i & 31)) & 1u;
+}
+CC_DEVI void set_bit(uint32_t* bm, uint32_t i) {
+  const uint32_t m = 1u << (i & 31);
+  if (!(*(volatile uint32_t*)&bm[i >> 5] & m)) atomicOr(&bm[i >> 5], m);
+}
+
+static unsigned grid(uint64_t work, unsigned per_block, unsigned cap) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, cap));
+}
+
+// ===================================================================== CSR build (a4)
+// cnt[v] = |VB_0(v)| = deg(v) + 1 for present v (the vertex tuple <v,_,v> + one tuple per
+// arc into v), 0 otherwise.  Exclusive scan -> off[v]; cur[v] = off[v] + 1 is the next
+// free slot for arcs.  Tile = B*8 vertices, single pass with decoupled look-back.
+constexpr int SITEMS = 8;
+__global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
+                                            const uint32_t* __restrict__ vis, uint64_t n,
+                                            uint32_t* __restrict__ off, uint32_t* __restrict__ cur,
+                                            uint64_t* flags, uint32_t* ticket, uint32_t epoch,
+                                            unsigned long long* total) {
+  __shared__ uint32_t s_scan[B / 32 + 1];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_pref;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t v0 = tile * (B * SITEMS) + (uint64_t)threadIdx.x * SITEMS;
+  uint32_t c[SITEMS];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < SITEMS; k++) {
+    const uint64_t v = v0 + k;
+    uint32_t x = 0;
+    if (v < n) {
+      x = deg[v];
+      if (x && vis && ((vis[v >> 5] >> (v & 31)) & 1u)) x = 0;
+      if (x) x += 1;
+    }
+    c[k] = x;
+    sum += x;
+  }
+  uint32_t tot;
+  const uint32_t excl = block_excl_scan<B>(sum, s_scan, &tot);
+  const uint64_t pref = scan::tile_prefix(flags, tile, tot, epoch, &s_pref);
+  uint32_t run = (uint32_t)pref + excl;
+#pragma unroll
+  for (int k = 0; k < SITEMS; k++) {
+    const uint64_t v = v0 + k;
+    if (v < n) {
+      off[v] = run;
+      cur[v] = run + 1;
+    }
+    run += c[k];
+  }
+  if (n > 0 && v0 <= n - 1 && n - 1 < v0 + SITEMS) {  // owner of the last vertex
+    off[n] = run;
+    *total = run;
+  }
+}
+
+// R[i] = owner row of position i (binary search once per thread, then walk); the vertex
+// tuple <r,_,r> sits at the first slot of row r.
+constexpr int FITEMS = 8;
+__global__ void __launch_bounds__(B) k_fill(const uint32_t* __restrict__ off, uint64_t n, uint64_t A,
+                                            uint32_t* __restrict__ R, uint32_t* __restrict__ P) {
+  const uint64_t i0 = (blockIdx.x * (uint64_t)B + threadIdx.x) * FITEMS;
+  if (i0 >= A) return;
+  // last v with off[v] <= i0
+  uint64_t lo = 0, hi = n;  // invariant: off[lo] <= i0 < off[hi] (off[n] = A)
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (__ldg(&off[mid]) <= i0) lo = mid; else hi = mid;
+  }
+  uint64_t r = lo;
+  uint32_t next = __ldg(&off[r + 1]);
+  for (int k = 0; k < FITEMS; k++) {
+    const uint64_t i = i0 + k;
+    if (i >= A) break;
+    while (next <= i) { r++; next = __ldg(&off[r + 1]); }
+    R[i] = (uint32_t)r;
+    if (i == __ldg(&off[r])) P[i] = (uint32_t)r;
+  }
+}
+
+// Alg. 1 line 3: <x,_,y> in VB(y) and <y,_,x> in VB(x) for every edge {x,y}.
+__global__ void __launch_bounds__(B) k_scatter(const uint2* __restrict__ e, uint64_t m,
+                                               uint32_t* cur, uint32_t* __restrict__ P) {
+  for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < m; i += (uint64_t)gridDim.x * B) {
+    const uint2 xy = e[i];
+    P[atomicAdd(&cur[xy.y], 1u)] = xy.x;
+    P[atomicAdd(&cur[xy.x], 1u)] = xy.y;
+  }
+}
+
+// ===================================================================== vertex passes
+// Lines 9-13 (WITH_PC) / line 24: per vertex bucket (a run of equal R), u_min = min p and,
+// for PC, whether max p != min p.  Warp chunks with carry (as sv.cu k_seg_reduce).
+constexpr int VSTEPS = 64;
+constexpr int VCHUNK = 32 * VSTEPS;
+template <bool WITH_PC>
+__global__ void __launch_bounds__(B) k_vpass(const uint32_t* __restrict__ R,
+                                             const uint32_t* __restrict__ P, uint64_t A,
+                                             uint32_t* __restrict__ U, uint32_t* __restrict__ NP) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)B + threadIdx.x) >> 5;
+  const uint64_t cbase = warp * VCHUNK;
+  if (cbase >= A) return;
+  uint32_t ckey = INF, cmin = INF, cmax = 0;
+  auto emit = [&](uint32_t key, uint32_t mn, uint32_t mx) {
+    atomicMin(&U[key], mn);
+    if (WITH_PC && mn != mx) atomicOr(&NP[key >> 5], 1u << (key & 31));
+  };
+  for (int k = 0; k < VSTEPS; k++) {
+    const uint64_t i = cbase + (uint64_t)k * 32 + lane;
+    uint32_t key = INF, mn = INF, mx = 0;
+    if (i < A) {
+      key = __ldg(&R[i]);
+      mn = mx = __ldg(&P[i]);
+    }
+    if (__all_sync(0xffffffffu, key == INF)) break;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ko = __shfl_down_sync(0xffffffffu, key, o);
+      const uint32_t a = __shfl_down_sync(0xffffffffu, mn, o);
+      const uint32_t b = WITH_PC ? __shfl_down_sync(0xffffffffu, mx, o) : 0u;
+      if (lane + o < 32 && ko == key) {
+        mn = min(mn, a);
+        if (WITH_PC) mx = max(mx, b);
+      }
+    }
+    const uint32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
+    const bool head = (lane == 0) || (kprev != key);
+    const uint32_t hmask = __ballot_sync(0xffffffffu, head);
+    const int last = 31 - __clz(hmask);
+    const uint32_t key0 = __shfl_sync(0xffffffffu, key, 0);
+    uint32_t mn0 = __shfl_sync(0xffffffffu, mn, 0);
+    uint32_t mx0 = __shfl_sync(0xffffffffu, mx, 0);
+    const uint32_t keyL = __shfl_sync(0xffffffffu, key, last);
+    const uint32_t mnL = __shfl_sync(0xffffffffu, mn, last);
+    const uint32_t mxL = __shfl_sync(0xffffffffu, mx, last);
+    if (key0 == ckey) {
+      mn0 = min(mn0, cmin);
+      mx0 = max(mx0, cmax);
+    } else if (lane == 0 && ckey != INF) {
+      emit(ckey, cmin, cmax);
+    }
+    if (last == 0) {
+      ckey = key0; cmin = mn0; cmax = mx0;
+    } else {
+      if (lane == 0 && key0 != INF) emit(key0, mn0, mx0);
+      if (head && lane != 0 && lane != last && key != INF) emit(key, mn, mx);
+      ckey = keyL; cmin = mnL; cmax = mxL;
+    }
+  }
+  if (lane == 0 && ckey != INF) emit(ckey, cmin, cmax);
+}
+
+// ===================================================================== partition passes
+// Line 15 (FIRST) / line 25: p_min = min over PB(p) of q = u_min(r) -> PMIN[p]; FIRST also
+// marks PB(p) 'not completed' when a tuple's vertex is not potentially completed.
+// Second pass: q includes the temporary <r,_,r> in VB(r) when TB(r).
+template <bool FIRST>
+__global__ void __launch_bounds__(B) k_ppass(const uint32_t* __restrict__ R,
+                                             const uint32_t* __restrict__ P, uint64_t A,
+                                             const uint32_t* __restrict__ U,
+                                             const uint32_t* __restrict__ NP,
+                                             const uint32_t* __restrict__ TB, uint32_t* PMIN,
+                                             uint32_t* NCP) {
+  const uint64_t nq = (A + 3) >> 2;
+  for (uint64_t t = blockIdx.x * (uint64_t)B + threadIdx.x; t < nq; t += (uint64_t)gridDim.x * B) {
+    uint32_t r[4], p[4];
+    int cnt = 4;
+    if (4 * t + 3 < A) {
+      const uint4 a = ldg_stream(reinterpret_cast<const uint4*>(R) + t);
+      const uint4 b = ldg_stream(reinterpret_cast<const uint4*>(P) + t);
+      r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+      p[0] = b.x; p[1] = b.y; p[2] = b.z; p[3] = b.w;
+    } else {
+      cnt = (int)(A - 4 * t);
+      for (int j = 0; j < 4; j++)
+        if (j < cnt) { r[j] = R[4 * t + j]; p[j] = P[4 * t + j]; }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (j >= cnt) break;
+      uint32_t q = __ldg(&U[r[j]]);
+      if (!FIRST && tbit(TB, r[j])) q = min(q, r[j]);
+      min_slot(PMIN, p[j], q);
+      if (FIRST && tbit(NP, r[j])) set_bit(NCP, p[j]);
+    }
+  }
+}
+
+// Temporaries of line 22 in pass 4: <u,_,u>_tmp in PB(u) with q = u_min'(u) = min(U[u], u).
+__global__ void k_temps(const uint32_t* __restrict__ TB, uint64_t n, const uint32_t* __restrict__ U,
+                        uint32_t* PMIN) {
+  const uint64_t nw = (n + 31) / 32;
+  for (uint64_t w = blockIdx.x * (uint64_t)B + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * B) {
+    uint32_t bits = TB[w];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint32_t u = (uint32_t)(w * 32 + b);
+      min_slot(PMIN, u, min(__ldg(&U[u]), u));
+    }
+  }
+}
+
+// Partition statistics over the slots (P_i, completed, changed, T_i; or changed2) and the
+// temporary-tuple bitmap (one temp <p_min,_,p_min> per surviving partition, line 22).
+template <bool FIRST>
+__global__ void __launch_bounds__(B) k_pscan(const uint32_t* __restrict__ PMIN,
+                                             const uint32_t* __restrict__ NCP, uint64_t n,
+                                             uint32_t* TB, unsigned long long* ctr) {
+  uint32_t np = 0, nc = 0, ch = 0, nt = 0;
+  for (uint64_t p = blockIdx.x * (uint64_t)B + threadIdx.x; p < n; p += (uint64_t)gridDim.x * B) {
+    const uint32_t pm = PMIN[p];
+    if (pm == INF) continue;
+    ch += (pm != (uint32_t)p);
+    if (FIRST) {
+      np++;
+      const bool comp = !tbit(NCP, (uint32_t)p) && pm == (uint32_t)p;
+      nc += comp;
+      if (!comp) {
+        nt++;
+        set_bit(TB, pm);
+      }
+    }
+  }
+  np = warp_sum(np); nc = warp_sum(nc); ch = warp_sum(ch); nt = warp_sum(nt);
+  if ((threadIdx.x & 31) == 0) {
+    if (FIRST) {
+      if (np) atomicAdd(&ctr[sv::C_PARTITIONS], (unsigned long long)np);
+      if (nc) atomicAdd(&ctr[sv::C_COMPLETED], (unsigned long long)nc);
+      if (ch) atomicAdd(&ctr[sv::C_CHANGED], (unsigned long long)ch);
+      if (nt) atomicAdd(&ctr[sv::C_TEMPS], (unsigned long long)nt);
+    } else if (ch) {
+      atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
+    }
+  }
+}
+
+// Lines 17-21 + sec:distSVOpt1: tuples of completed partitions leave (their vertex takes
+// label p), survivors get p <- p_min.  Ordered stream compaction (tile
+// prefix by decoupled look-back) keeps R sorted.
+constexpr int CITEMS = 8;
+constexpr int CTILE = B * CITEMS;
+__global__ void __launch_bounds__(B) k_papply1(const uint32_t* __restrict__ R,
+                                               const uint32_t* __restrict__ P, uint64_t A,
+                                               const uint32_t* __restrict__ PMIN,
+                                               const uint32_t* __restrict__ NCP,
+                                               uint32_t* __restrict__ R2, uint32_t* __restrict__ P2,
+                                               uint32_t* __restrict__ label, uint64_t* flags,
+                                               uint32_t* ticket, uint32_t epoch,
+                                               unsigned long long* ctr) {
+  __shared__ uint32_t s_scan[B / 32 + 1];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_pref;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t i0 = tile * CTILE + (uint64_t)threadIdx.x * CITEMS;
+  uint32_t r[CITEMS], p[CITEMS];
+  uint32_t keep = 0;  // bitmask of kept items
+  if (i0 + CITEMS <= A) {
+    const uint4* r4 = reinterpret_cast<const uint4*>(R + i0);
+    const uint4* p4 = reinterpret_cast<const uint4*>(P + i0);
+    uint4 a = ldg_stream(r4), b = ldg_stream(r4 + 1), c = ldg_stream(p4), d = ldg_stream(p4 + 1);
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+    p[0] = c.x; p[1] = c.y; p[2] = c.z; p[3] = c.w; p[4] = d.x; p[5] = d.y; p[6] = d.z; p[7] = d.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < CITEMS; k++) {
+      r[k] = (i0 + k < A) ? R[i0 + k] : INF;
+      p[k] = (i0 + k < A) ? P[i0 + k] : 0;
+    }
+  }
+  uint32_t prev = (i0 > 0 && i0 <= A) ? __ldg(&R[i0 - 1]) : INF;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++) {
+    if (i0 + k < A) {
+      const uint32_t pm = __ldg(&PMIN[p[k]]);
+      const bool comp = (pm == p[k]) && !tbit(NCP, p[k]);
+      if (comp) {
+        if (r[k] != prev) label[r[k]] = p[k];  // first tuple of VB(r)
+      } else {
+        keep |= 1u << k;
+        p[k] = pm;
+        cnt++;
+      }
+      prev = r[k];
+    }
+  }
+  uint32_t tot;
+  const uint32_t excl = block_excl_scan<B>(cnt, s_scan, &tot);
+  const uint64_t pref = scan::tile_prefix(flags, tile, tot, epoch, &s_pref);
+  uint64_t o = pref + excl;
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++)
+    if (keep >> k & 1u) {
+      R2[o] = r[k];
+      P2[o] = p[k];
+      o++;
+    }
+  if (i0 < A && i0 + CITEMS >= A) atomicAdd(&ctr[sv::C_OUT], (unsigned long long)(pref + excl + cnt));
+}
+
+// Line 25 update: p <- p_min of the second partition pass, in place (temporaries are
+// bitmap entries, so nothing is erased and the array stays in R order).
+__global__ void __launch_bounds__(B) k_papply2(uint32_t* __restrict__ P, uint64_t A,
+                                               const uint32_t* __restrict__ PMIN) {
+  const uint64_t nq = (A + 3) >> 2;
+  for (uint64_t t = blockIdx.x * (uint64_t)B + threadIdx.x; t < nq; t += (uint64_t)gridDim.x * B) {
+    if (4 * t + 3 < A) {
+      uint4 b = reinterpret_cast<const uint4*>(P)[t];
+      b.x = __ldg(&PMIN[b.x]); b.y = __ldg(&PMIN[b.y]); b.z = __ldg(&PMIN[b.z]); b.w = __ldg(&PMIN[b.w]);
+      reinterpret_cast<uint4*>(P)[t] = b;
+    } else {
+      for (uint64_t i = 4 * t; i < A; i++) P[i] = __ldg(&PMIN[P[i]]);
+    }
+  }
+}
+
+// ===================================================================== launchers
+void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* vis, uint64_t n,
+           uint32_t* off, uint32_t* cur, uint32_t* R, uint32_t* P, scan::State& ss, uint64_t* ctr,
+           cudaStream_t st) {
+  // ctr[C_VT_OUT] receives A_0
+  if (!n) return;
+  cudaMemsetAsync(ss.ticket, 0, sizeof(uint32_t), st);
+  const uint64_t tiles = (n + B * SITEMS - 1) / (B * SITEMS);
+  k_rows<<<(unsigned)tiles, B, 0, st>>>(deg, vis, n, off, cur, ss.flags, ss.ticket, ++ss.epoch,
+                                         reinterpret_cast<unsigned long long*>(ctr + sv::C_VT_OUT));
+}
+void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
+          uint32_t* R, uint32_t* P, cudaStream_t st) {
+  if (A) k_fill<<<grid(A, B * FITEMS, 1u << 30), B, 0, st>>>(off, n, A, R, P);
+  if (m) k_scatter<<<grid(m, B, 148 * 16), B, 0, st>>>(edges, m, cur, P);
+}
+void vpass(bool with_pc, const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* U, uint32_t* NP,
+           cudaStream_t st) {
+  if (!A) return;
+  const uint64_t warps = (A + VCHUNK - 1) / VCHUNK;
+  const unsigned g = (unsigned)((warps * 32 + B - 1) / B);
+  if (with_pc) k_vpass<true><<<g, B, 0, st>>>(R, P, A, U, NP);
+  else k_vpass<false><<<g, B, 0, st>>>(R, P, A, U, NP);
+}
+void ppass(bool first, const uint32_t* R, const uint32_t* P, uint64_t A, const uint32_t* U,
+           const uint32_t* NP, const uint32_t* TB, uint32_t* PMIN, uint32_t* NCP, cudaStream_t st) {
+  if (!A) return;
+  const unsigned g = grid((A + 3) / 4, B, 148 * 8);
+  if (first) k_ppass<true><<<g, B, 0, st>>>(R, P, A, U, NP, TB, PMIN, NCP);
+  else k_ppass<false><<<g, B, 0, st>>>(R, P, A, U, NP, TB, PMIN, NCP);
+}
+void temps(const uint32_t* TB, uint64_t n, const uint32_t* U, uint32_t* PMIN, cudaStream_t st) {
+  if (n) k_temps<<<grid((n + 31) / 32, B, 148 * 4), B, 0, st>>>(TB, n, U, PMIN);
+}
+void pscan(bool first, const uint32_t* PMIN, const uint32_t* NCP, uint64_t n, uint32_t* TB,
+           uint64_t* ctr, cudaStream_t st) {
+  if (!n) return;
+  auto* c = reinterpret_cast<unsigned long long*>(ctr);
+  if (first) k_pscan<true><<<grid(n, B, 148 * 8), B, 0, st>>>(PMIN, NCP, n, TB, c);
+  else k_pscan<false><<<grid(n, B, 148 * 8), B, 0, st>>>(PMIN, NCP, n, TB, c);
+}
+void papply1(const uint32_t* R, const uint32_t* P, uint64_t A, const uint32_t* PMIN,
+             const uint32_t* NCP, uint32_t* R2, uint32_t* P2, uint32_t* label, scan::State& ss,
+             uint64_t* ctr, cudaStream_t st) {
+  if (!A) return;
+  cudaMemsetAsync(ss.ticket, 0, sizeof(uint32_t), st);
+  const uint64_t tiles = (A + CTILE - 1) / CTILE;
+  k_papply1<<<(unsigned)tiles, B, 0, st>>>(R, P, A, PMIN, NCP, R2, P2, label, ss.flags, ss.ticket,
+                                            ++ss.epoch, reinterpret_cast<unsigned long long*>(ctr));
+}
+void papply2(uint32_t* P, uint64_t A, const uint32_t* PMIN, cudaStream_t st) {
+  if (A) k_papply2<<<grid((A + 3) / 4, B, 148 * 8), B, 0, st>>>(P, A, PMIN);
+}
+
+}  // namespace csr
+}  // namespace cc

@@ -24,15 +24,15 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.fixture(scope="module", params=["sort", "direct"])
+@pytest.fixture(scope="module", params=["csr", "sort", "direct"])
 def cc(request):
-    """Both regroup engines: radix-sorted buckets (paper's data movement) and
-    direct-addressed buckets (B200 variant); same sets, same counters."""
+    """All regroup engines: r-stationary CSR (default), the paper's radix
+    regroups, and fully direct-addressed buckets; same sets, same counters."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1607_06156_b200 as ccmod
-    flags = ccmod.CC_FLAG_TRACE | (ccmod.CC_FLAG_REGROUP_DIRECT if request.param == "direct" else 0)
+    flags = ccmod.CC_FLAG_TRACE | ccmod.REGROUP_FLAGS[request.param]
     ctx = ccmod.CC(device=0, flags=flags)
     yield ctx
     ctx.close()
