@@ -218,7 +218,8 @@ def main():
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    fam = {0: [0.0, 0.0, 0], 1: [0.0, 0.0, 0], 2: [0.0, 0.0, 0]}
+    names = cc.kernel_families()
+    fam = {i: [0.0, 0.0, 0] for i in range(len(names))}
     launches = 0
     torch.cuda.synchronize()
     for k in range(args.steps):
@@ -277,14 +278,24 @@ def main():
 
     if rk == 0:
         peak, peak_src = peaks()
-        # dominant kernel family: the onesweep radix regroups (sort = family 0)
-        sort_ms, sort_bytes, sort_launches = fam[0]
-        achieved = (sort_bytes / (sort_ms / 1e3)) / 1e9 if sort_ms > 0 else None
+        # dominant kernel: the single-kernel family with the largest device time in the timed
+        # region (family 1 is the whole-iteration aggregate, excluded)
+        leaf = [i for i in fam if i != 1 and fam[i][0] > 0]
+        dom = max(leaf, key=lambda i: fam[i][0]) if leaf else None
+        kernels = {names[i]: {"ms_per_step": fam[i][0] / args.steps,
+                              "alg_GBps": (fam[i][1] / (fam[i][0] / 1e3)) / 1e9 if fam[i][0] else None,
+                              "launches_per_step": fam[i][2] / args.steps}
+                   for i in fam if fam[i][0] > 0}
+        if dom is not None:
+            d_ms, d_bytes, d_launches = fam[dom]
+            achieved = (d_bytes / (d_ms / 1e3)) / 1e9
+        else:
+            d_ms, d_bytes, d_launches, achieved = 0.0, 0.0, 0, None
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
-            tr = json.load(open(tp)).get(args.config, {})
-            traffic = tr.get("sort_bytes_per_launch")
+            tr = json.load(open(tp)).get(f"{args.config}/{args.regroup}", {})
+            traffic = tr.get(names[dom]) if dom is not None else None
         path_bytes = alg_bytes(rep, n, m)
         step_s = ms_max / 1e3 / args.steps
         line = {
@@ -298,12 +309,15 @@ def main():
                        "sv_iterations": rep["sv_iterations"],
                        "l2": "flushed between timed steps (256 MiB write, outside step events)",
                        "parallelism": f"{ws} independent instance(s)"},
-            "roofline": {"bound": "hbm", "kernel": "k_onesweep+k_hist (radix regroup family)",
+            "roofline": {"bound": "hbm", "kernel": names[dom] if dom is not None else None,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": traffic, "peak_source": peak_src,
-                         "share_of_step": (sort_ms / ms_max) if ms_max else None,
-                         "launches": sort_launches},
+                         "alg_bytes_per_launch": (d_bytes / d_launches) if d_launches else None,
+                         "ms_per_launch": (d_ms / d_launches) if d_launches else None,
+                         "share_of_step": (d_ms / ms_max) if ms_max else None,
+                         "launches_per_step": d_launches / args.steps},
+            "kernels": kernels,
             "path_roofline": {"alg_bytes_per_step": path_bytes,
                               "frac": (path_bytes / (peak * 1e9)) / step_s,
                               "model": "SURVEY.md §8(d): 8m+8A0+sum(32A_i+48A_i+1+40T_i)+4n+4n_p"},

@@ -153,11 +153,14 @@ cc_status cc_labels_device(cc_ctx* ctx, const uint32_t** labels, uint64_t* count
 /* Number of kernel launches enqueued by the last cc_run (evidence for bench.py). */
 uint64_t cc_last_launch_count(const cc_ctx* ctx);
 
-/* Device time (ms, CUDA events on cfg.stream) of a kernel family in the last cc_run
- * (recorded only under CC_FLAG_PROFILE), with its algorithmic bytes (bench.py roofline):
- *   which = 0: radix-sort scatter passes, 1: segmented passes, 2: BFS levels. */
+/* Device time (ms, CUDA events on cfg.stream around each launch) of kernel family
+ * `which` in the last cc_run, recorded only under CC_FLAG_PROFILE, with the family's
+ * algorithmic bytes (DESIGN.md §6 byte model) and launch count.  Families are numbered
+ * 0..N-1; cc_kernel_name(which) names them and returns NULL past the last one.
+ * CC_ERR_INVALID for a bad index. */
 cc_status cc_kernel_stats(const cc_ctx* ctx, int which, double* ms, double* bytes,
                           uint64_t* launches);
+const char* cc_kernel_name(int which);
 
 cc_status cc_destroy(cc_ctx* ctx);
 

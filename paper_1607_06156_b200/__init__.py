@@ -63,8 +63,8 @@ class cc_report(ctypes.Structure):
 
 
 EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
-           "cc_labels_device", "cc_last_launch_count", "cc_kernel_stats", "cc_destroy",
-           "cc_status_string", "cc_last_error"]
+           "cc_labels_device", "cc_last_launch_count", "cc_kernel_stats", "cc_kernel_name",
+           "cc_destroy", "cc_status_string", "cc_last_error"]
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -89,6 +89,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
     lib.cc_destroy.argtypes = [P]
+    lib.cc_kernel_name.restype = ctypes.c_char_p
+    lib.cc_kernel_name.argtypes = [ctypes.c_int]
     for f in ("cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
               "cc_labels_device", "cc_kernel_stats", "cc_destroy"):
         getattr(lib, f).restype = ctypes.c_int
@@ -204,6 +206,16 @@ def cc_kernel_stats(ctx, which):
     ms, by, ln = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
     _check(ctx, lib().cc_kernel_stats(ctx, which, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(ln)))
     return dict(ms=ms.value, bytes=by.value, launches=ln.value)
+
+
+def kernel_families():
+    out, i = [], 0
+    while True:
+        nm = lib().cc_kernel_name(i)
+        if nm is None:
+            return out
+        out.append(nm.decode())
+        i += 1
 
 
 def cc_destroy(ctx):

@@ -67,11 +67,12 @@ struct cc_ctx {
   // profiling (CC_FLAG_TRACE): per-family events
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_sort, prof_seg, prof_bfs;
   std::vector<cudaEvent_t> it_ev;  // SV iteration start events
-  double sort_bytes = 0, seg_bytes = 0, bfs_bytes = 0;
-  double kms[3] = {0, 0, 0}, kbytes[3] = {0, 0, 0};
-  uint64_t klaunch[3] = {0, 0, 0};
+  struct KStat {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    double bytes = 0, ms = 0;
+    uint64_t launches = 0;
+  } kst[16];
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -156,6 +157,32 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 static bool profiling(const cc_ctx* c) { return (c->cfg.flags & CC_FLAG_PROFILE) != 0; }
+
+// kernel families timed under CC_FLAG_PROFILE (cc_kernel_stats / cc_kernel_name)
+enum KFam { KF_RADIX = 0, KF_SVITER, KF_BFS, KF_PPASS, KF_PAPPLY, KF_VPASS, KF_CSR, KF_PREDICT,
+            KF_N };
+static const char* const kKfNames[KF_N] = {
+    "k_hist+k_onesweep (radix regroup)", "SV iteration (all bucket passes)", "k_bfs_level",
+    "k_ppass (partition-bucket minima)", "k_papply1/2 (partition update + compaction)",
+    "k_vpass (vertex-bucket minima)", "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)",
+    "prediction (k_degree, k_deg_hist)"};
+
+struct Prof {
+  cc_ctx* c;
+  int f;
+  cudaEvent_t a = nullptr;
+  Prof(cc_ctx* c_, int f_) : c(c_), f(f_) {
+    if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
+  }
+  void end(double bytes, uint64_t nl) {
+    if (!profiling(c)) return;
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->st);
+    c->kst[f].ev.push_back({a, b});
+    c->kst[f].bytes += bytes;
+    c->kst[f].launches += nl;
+  }
+};
 
 static int bits_for(uint64_t n) {
   int b = 0;
@@ -256,7 +283,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->d_segA, n + 1));
   TRY(dalloc_t(c, &c->d_segB, n + 1));
   TRY(dalloc_t(c, &c->d_ctr, sv::C_NUM));
-  TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM));
+  TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM + 512 + 1024 + 8));  // + CSR group scratch
   c->rws.max_tiles = c->cap / radix::TILE + 2;
   TRY(dalloc_t(c, &c->rws.ghist, radix::MAX_PASSES * radix::RADIX));
   TRY(dalloc_t(c, &c->rws.lookback, c->rws.max_tiles * radix::RADIX));
@@ -304,32 +331,25 @@ static cc_status sync_read(cc_ctx* c) {
 
 // radix sort wrapper with optional per-call timing
 static int do_sort(cc_ctx* c, int cur, uint64_t n, bool pairs) {
-  cudaEvent_t a = nullptr;
-  if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
+  Prof pr(c, KF_RADIX);
   int r = radix::sort_pairs(c->rws, c->d_w, c->d_q, cur, n, c->kbits, pairs, c->st, &c->launches);
-  if (profiling(c)) {
-    cudaEvent_t b = ev_get(c);
-    cudaEventRecord(b, c->st);
-    c->prof_sort.push_back({a, b});
-    const int P = radix::num_passes(c->kbits);
-    // algorithmic bytes: histogram reads the key word once, each pass reads and writes the
-    // element once (8 B word + 4 B payload for the by-p regroups)
-    c->sort_bytes += (double)n * (8.0 + P * 2.0 * (pairs ? 12.0 : 8.0));
-    c->klaunch[0] += (uint64_t)(P + 1);
-  }
+  const int P = radix::num_passes(c->kbits);
+  // algorithmic bytes: the histogram reads the key word once, each pass reads and writes
+  // the element once (8 B word + 4 B payload for the by-p regroups)
+  pr.end((double)n * (8.0 + P * 2.0 * (pairs ? 12.0 : 8.0)), (uint64_t)(P + 1));
   return r;
 }
 
 static void seg_begin(cc_ctx* c, cudaEvent_t* a) {
   if (profiling(c)) { *a = ev_get(c); cudaEventRecord(*a, c->st); }
 }
-static void seg_end(cc_ctx* c, cudaEvent_t a, double bytes, int nl) {
+static void seg_end(cc_ctx* c, cudaEvent_t a, double bytes, int nl, int fam = KF_SVITER) {
   if (profiling(c)) {
     cudaEvent_t b = ev_get(c);
     cudaEventRecord(b, c->st);
-    c->prof_seg.push_back({a, b});
-    c->seg_bytes += bytes;
-    c->klaunch[1] += nl;
+    c->kst[fam].ev.push_back({a, b});
+    c->kst[fam].bytes += bytes;
+    c->kst[fam].launches += nl;
   }
 }
 
@@ -429,17 +449,24 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
   cudaEvent_t a = nullptr;
   seg_begin(c, &a);
   TRY(scan_epoch_guard(c));
-  csr::build(edges, m_sv, c->d_deg, vis, n, off, cur, R[0], P[0], c->ss, c->d_ctr, c->st);
+  const int gshift = csr::group_shift(n, 2 * m_sv + n);
+  uint32_t* garc = reinterpret_cast<uint32_t*>(c->d_gctr + graph::G_NUM);  // 1024 u32
+  uint64_t* gcur = c->d_gctr + graph::G_NUM + 512;                           // 1024 u64
+  uint64_t* nlong = gcur + 1024;
+  csr::build(edges, m_sv, c->d_deg, vis, n, off, cur, garc, gshift, c->ss, c->d_ctr, c->st);
   c->launches += 1;
   CKL();
   TRY(sync_read(c));
   uint64_t A = c->h_ctr[sv::C_VT_OUT];
   if (A == 0) return CC_OK;
   if (A > c->cap) return fail(c, CC_ERR_INVALID, "tuple count %llu exceeds capacity", (unsigned long long)A);
-  csr::fill(edges, m_sv, off, cur, n, A, R[0], P[0], c->st);
-  c->launches += 2;
+  // scratch: the bucketed arc list lives in the second tuple buffer (free until the first
+  // compaction), the long-row list in the vertex-group counter block
+  csr::fill(edges, m_sv, off, cur, n, A, R[0], P[0], garc, gshift, gcur,
+            reinterpret_cast<uint2*>(c->d_w[1]), c->d_segB, nlong, c->st);
+  c->launches += 5;
   CKL();
-  seg_end(c, a, 4.0 * n + 8.0 * m_sv + 8.0 * A + 4.0 * n, 3);
+  seg_end(c, a, 4.0 * n + 8.0 * m_sv + 8.0 * A + 4.0 * n, 6, KF_CSR);
   int cur_buf = 0;
   const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
   uint64_t chg2_prev = 0;
@@ -452,16 +479,18 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
     // ---- lines 8-13: vertex buckets are CSR rows; u_min and 'potentially completed'
     CK(cudaMemsetAsync(U, 0xFF, sizeof(uint32_t) * n, c->st));
     CK(cudaMemsetAsync(NP, 0, sizeof(uint32_t) * nw, c->st));
-    csr::vpass(true, Rc, Pc, A, U, NP, c->st);
+    { Prof k(c, KF_VPASS); csr::vpass(true, Rc, Pc, A, U, NP, c->st); k.end(8.0 * A + 4.0 * n, 1); }
     // ---- lines 14-21: p_min per partition bucket; completion
     CK(cudaMemsetAsync(PMIN, 0xFF, sizeof(uint32_t) * n, c->st));
     CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nw, c->st));
     CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nw, c->st));
     CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_TEMPS + 1), c->st));
-    csr::ppass(true, Rc, Pc, A, U, NP, nullptr, PMIN, NCP, c->st);
+    { Prof k(c, KF_PPASS); csr::ppass(true, Rc, Pc, A, U, NP, nullptr, PMIN, NCP, c->st);
+      k.end(8.0 * A + 8.0 * n, 1); }
     // ---- line 22 (temporaries) + counters; exclusion of completed partitions
     csr::pscan(true, PMIN, NCP, n, TB, c->d_ctr, c->st);
     TRY(scan_epoch_guard(c));
+    Prof kp(c, KF_PAPPLY);
     csr::papply1(Rc, Pc, A, PMIN, NCP, R[cur_buf ^ 1], P[cur_buf ^ 1], c->d_label, c->ss, c->d_ctr,
                  c->st);
     c->launches += 4;
@@ -469,6 +498,7 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
     CKL();
     TRY(sync_read(c));
     const uint64_t A1 = c->h_ctr[sv::C_OUT];
+    kp.end(8.0 * A + 4.0 * n + 8.0 * A1, 1);
     cc_iter_stat s{};
     s.active_in = A;
     s.partitions = c->h_ctr[sv::C_PARTITIONS];
@@ -489,13 +519,14 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
     Pc = P[cur_buf];
     // ---- line 24: vertex buckets again, temporaries <u,_,u> from the TB bitmap
     CK(cudaMemsetAsync(U, 0xFF, sizeof(uint32_t) * n, c->st));
-    csr::vpass(false, Rc, Pc, A1, U, nullptr, c->st);
+    { Prof k(c, KF_VPASS); csr::vpass(false, Rc, Pc, A1, U, nullptr, c->st); k.end(8.0 * A1 + 4.0 * n, 1); }
     // ---- line 25: partition buckets again (+ temporaries), p <- p_min in place
     CK(cudaMemsetAsync(PMIN, 0xFF, sizeof(uint32_t) * n, c->st));
-    csr::ppass(false, Rc, Pc, A1, U, nullptr, TB, PMIN, nullptr, c->st);
+    { Prof k(c, KF_PPASS); csr::ppass(false, Rc, Pc, A1, U, nullptr, TB, PMIN, nullptr, c->st);
+      k.end(8.0 * A1 + 8.0 * n, 1); }
     csr::temps(TB, n, U, PMIN, c->st);
     csr::pscan(false, PMIN, nullptr, n, nullptr, c->d_ctr, c->st);
-    csr::papply2(Pc, A1, PMIN, c->st);
+    { Prof k(c, KF_PAPPLY); csr::papply2(Pc, A1, PMIN, c->st); k.end(8.0 * A1 + 4.0 * n, 1); }
     c->launches += 5;
     CKL();
     // algorithmic bytes streamed by this iteration's tuple passes (R,P u32 each)
@@ -612,9 +643,8 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   c->iters.clear();
   c->launches = 0;
   c->ev_used = 0;
-  c->prof_sort.clear(); c->prof_seg.clear(); c->prof_bfs.clear(); c->it_ev.clear();
-  c->sort_bytes = c->seg_bytes = c->bfs_bytes = 0;
-  for (int i = 0; i < 3; i++) { c->kms[i] = c->kbytes[i] = 0; c->klaunch[i] = 0; }
+  c->it_ev.clear();
+  for (auto& k : c->kst) k = cc_ctx::KStat();
   cc_report& R = c->rep;
   R = cc_report{};
   const uint64_t n = c->n, m = c->m;
@@ -699,17 +729,10 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     while (true) {
       CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
       CK(cudaMemsetAsync(c->d_gctr + graph::G_NEWVIS, 0, sizeof(uint64_t), c->st));
-      cudaEvent_t a = nullptr;
-      if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
+      Prof k(c, KF_BFS);
       graph::launch_bfs_level(c->d_edges, m, F, V, X, c->d_gctr, c->st);
       c->launches += 1;
-      if (profiling(c)) {
-        cudaEvent_t b = ev_get(c);
-        cudaEventRecord(b, c->st);
-        c->prof_bfs.push_back({a, b});
-        c->bfs_bytes += 8.0 * (double)m;
-        c->klaunch[2] += 1;
-      }
+      k.end(8.0 * (double)m + (double)n / 8 * 3, 1);
       CKL();
       TRY(sync_read(c));
       const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
@@ -756,14 +779,9 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   R.ms_finalize = ev_ms(e_sv, e_end);
   for (size_t i = 0; i < c->it_ev.size() && i < c->iters.size(); i++)
     c->iters[i].ms = ev_ms(c->it_ev[i], i + 1 < c->it_ev.size() ? c->it_ev[i + 1] : e_sv);
-  if (profiling(c)) {
-    for (auto& p : c->prof_sort) c->kms[0] += ev_ms(p.first, p.second);
-    for (auto& p : c->prof_seg) c->kms[1] += ev_ms(p.first, p.second);
-    for (auto& p : c->prof_bfs) c->kms[2] += ev_ms(p.first, p.second);
-    c->kbytes[0] = c->sort_bytes;
-    c->kbytes[1] = c->seg_bytes;
-    c->kbytes[2] = c->bfs_bytes;
-  }
+  if (profiling(c))
+    for (auto& k : c->kst)
+      for (auto& p : k.ev) k.ms += ev_ms(p.first, p.second);
   R.iters = c->iters.data();
   R.n_iters = (uint32_t)c->iters.size();
   // components (isolated ids included): computed by the caller from labels if needed;
@@ -804,9 +822,13 @@ extern "C" cc_status cc_labels_device(cc_ctx* c, const uint32_t** labels, uint64
 
 extern "C" cc_status cc_kernel_stats(const cc_ctx* c, int which, double* ms, double* bytes,
                                      uint64_t* launches) {
-  if (!c || which < 0 || which > 2) return CC_ERR_INVALID;
-  if (ms) *ms = c->kms[which];
-  if (bytes) *bytes = c->kbytes[which];
-  if (launches) *launches = c->klaunch[which];
+  if (!c || which < 0 || which >= KF_N) return CC_ERR_INVALID;
+  if (ms) *ms = c->kst[which].ms;
+  if (bytes) *bytes = c->kst[which].bytes;
+  if (launches) *launches = c->kst[which].launches;
   return CC_OK;
+}
+
+extern "C" const char* cc_kernel_name(int which) {
+  return (which >= 0 && which < KF_N) ? kKfNames[which] : nullptr;
 }

@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
                                             const uint32_t* __restrict__ vis, uint64_t n,
                                             uint32_t* __restrict__ off, uint32_t* __restrict__ cur,
                                             uint64_t* flags, uint32_t* ticket, uint32_t epoch,
-                                            unsigned long long* total) {
+                                            unsigned long long* total, uint32_t* garc,
+                                            int gshift) {
   __shared__ uint32_t s_scan[B / 32 + 1];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_pref;
@@ -79,6 +80,16 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
   uint32_t tot;
   const uint32_t excl = block_excl_scan<B>(sum, s_scan, &tot);
   const uint64_t pref = scan::tile_prefix(flags, tile, tot, epoch, &s_pref);
+  // arcs of this tile (tuples minus vertex tuples) for the CSR bucket pass; a tile of
+  // B*SITEMS = 2^11 vertices lies inside one group of 2^gshift vertices (gshift >= 11)
+  {
+    uint32_t nv = 0;
+#pragma unroll
+    for (int k = 0; k < SITEMS; k++) nv += (c[k] != 0);
+    nv = warp_sum(nv);
+    if ((threadIdx.x & 31) == 0 && nv) atomicSub(&garc[(tile * (B * SITEMS)) >> gshift], nv);
+    if (threadIdx.x == 0 && tot) atomicAdd(&garc[(tile * (B * SITEMS)) >> gshift], tot);
+  }
   uint32_t run = (uint32_t)pref + excl;
 #pragma unroll
   for (int k = 0; k < SITEMS; k++) {
@@ -95,37 +106,96 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
   }
 }
 
-// R[i] = owner row of position i (binary search once per thread, then walk); the vertex
-// tuple <r,_,r> sits at the first slot of row r.
-constexpr int FITEMS = 8;
-__global__ void __launch_bounds__(B) k_fill(const uint32_t* __restrict__ off, uint64_t n, uint64_t A,
-                                            uint32_t* __restrict__ R, uint32_t* __restrict__ P) {
-  const uint64_t i0 = (blockIdx.x * (uint64_t)B + threadIdx.x) * FITEMS;
-  if (i0 >= A) return;
-  // last v with off[v] <= i0
-  uint64_t lo = 0, hi = n;  // invariant: off[lo] <= i0 < off[hi] (off[n] = A)
-  while (hi - lo > 1) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (__ldg(&off[mid]) <= i0) lo = mid; else hi = mid;
+// R and the vertex tuple <v,_,v> of each row: thread per vertex; rows longer than
+// LONG_ROW (hubs) are appended to a list and filled by whole blocks.
+constexpr uint32_t LONG_ROW = 64;
+__global__ void __launch_bounds__(B) k_fill_rows(const uint32_t* __restrict__ off, uint64_t n,
+                                                 uint32_t* __restrict__ R, uint32_t* __restrict__ P,
+                                                 uint32_t* longlist, unsigned long long* nlong) {
+  for (uint64_t v = blockIdx.x * (uint64_t)B + threadIdx.x; v < n; v += (uint64_t)gridDim.x * B) {
+    const uint32_t a = off[v], b = off[v + 1];
+    if (a == b) continue;
+    P[a] = (uint32_t)v;
+    if (b - a <= LONG_ROW) {
+      for (uint32_t i = a; i < b; i++) R[i] = (uint32_t)v;
+    } else {
+      longlist[atomicAdd(nlong, 1ull)] = (uint32_t)v;
+    }
   }
-  uint64_t r = lo;
-  uint32_t next = __ldg(&off[r + 1]);
-  for (int k = 0; k < FITEMS; k++) {
-    const uint64_t i = i0 + k;
-    if (i >= A) break;
-    while (next <= i) { r++; next = __ldg(&off[r + 1]); }
-    R[i] = (uint32_t)r;
-    if (i == __ldg(&off[r])) P[i] = (uint32_t)r;
+}
+__global__ void __launch_bounds__(B) k_fill_long(const uint32_t* __restrict__ off,
+                                                 const uint32_t* __restrict__ longlist,
+                                                 const unsigned long long* nlong,
+                                                 uint32_t* __restrict__ R) {
+  const uint64_t cnt = *nlong;
+  for (uint64_t j = blockIdx.x; j < cnt; j += gridDim.x) {
+    const uint32_t v = longlist[j];
+    const uint32_t a = off[v], b = off[v + 1];
+    for (uint32_t i = a + threadIdx.x; i < b; i += B) R[i] = v;
   }
 }
 
-// Alg. 1 line 3: <x,_,y> in VB(y) and <y,_,x> in VB(x) for every edge {x,y}.
-__global__ void __launch_bounds__(B) k_scatter(const uint2* __restrict__ e, uint64_t m,
+// Group start offsets of the bucketed arc list (exclusive scan of per-group arc counts).
+__global__ void k_gscan(const uint32_t* __restrict__ garc, int G, unsigned long long* gcur) {
+  __shared__ uint32_t s_scan[B / 32 + 1];
+  uint64_t carry = 0;
+  for (int base = 0; base < G; base += B) {
+    const int g = base + threadIdx.x;
+    const uint32_t x = g < G ? garc[g] : 0u;
+    uint32_t tot;
+    const uint32_t e = block_excl_scan<B>(x, s_scan, &tot);
+    if (g < G) gcur[g] = carry + e;
+    carry += tot;
+  }
+}
+
+// CSR bucket pass: every arc (r = target, p = source) of Alg. 1 line 3 goes to the group
+// of r (2^gshift consecutive vertices), written as (r,p) pairs; each block reserves one
+// contiguous run per group, so the writes stay coalesced and the second pass below scatters
+// inside one small window of P at a time (L2-resident, no partial-sector DRAM writes).
+constexpr int BITEMS = 8;
+constexpr int MAXG = 1024;
+__global__ void __launch_bounds__(B) k_bucket(const uint2* __restrict__ e, uint64_t m, int gshift,
+                                              int G, unsigned long long* gcur,
+                                              uint2* __restrict__ out) {
+  __shared__ uint32_t s_cnt[MAXG];
+  __shared__ unsigned long long s_base[MAXG];
+  for (int g = threadIdx.x; g < G; g += B) s_cnt[g] = 0;
+  __syncthreads();
+  const uint64_t e0 = (blockIdx.x * (uint64_t)B * BITEMS) + threadIdx.x;
+  uint2 arc[2 * BITEMS];
+  uint32_t slot[2 * BITEMS];
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * B;
+    if (i < m) {
+      const uint2 xy = e[i];
+      arc[2 * k] = make_uint2(xy.y, xy.x);      // <x,_,y>: r = y, p = x
+      arc[2 * k + 1] = make_uint2(xy.x, xy.y);  // <y,_,x>: r = x, p = y
+      slot[2 * k] = atomicAdd(&s_cnt[xy.y >> gshift], 1u);
+      slot[2 * k + 1] = atomicAdd(&s_cnt[xy.x >> gshift], 1u);
+    }
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += B)
+    s_base[g] = s_cnt[g] ? atomicAdd(&gcur[g], (unsigned long long)s_cnt[g]) : 0ull;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * B;
+    if (i < m) {
+      out[s_base[arc[2 * k].x >> gshift] + slot[2 * k]] = arc[2 * k];
+      out[s_base[arc[2 * k + 1].x >> gshift] + slot[2 * k + 1]] = arc[2 * k + 1];
+    }
+  }
+}
+
+// Second pass: place each arc tuple in its row (cursor per vertex).
+__global__ void __launch_bounds__(B) k_scatter(const uint2* __restrict__ arcs, uint64_t na,
                                                uint32_t* cur, uint32_t* __restrict__ P) {
-  for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < m; i += (uint64_t)gridDim.x * B) {
-    const uint2 xy = e[i];
-    P[atomicAdd(&cur[xy.y], 1u)] = xy.x;
-    P[atomicAdd(&cur[xy.x], 1u)] = xy.y;
+  for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < na; i += (uint64_t)gridDim.x * B) {
+    const uint2 rp = arcs[i];
+    P[atomicAdd(&cur[rp.x], 1u)] = rp.y;
   }
 }
 
@@ -217,13 +287,35 @@ __global__ void __launch_bounds__(B) k_ppass(const uint32_t* __restrict__ R,
       for (int j = 0; j < 4; j++)
         if (j < cnt) { r[j] = R[4 * t + j]; p[j] = P[4 * t + j]; }
     }
+    // gather q and flags for all 4 tuples, then the slot reads, then the (rare) atomics.
+    // The check-before reads go through L1 (ld.ca): a stale L1 copy is never below the
+    // true slot value (slots only decrease / only gain bits), so at worst it costs an
+    // unneeded atomic -- while a bucket shared by millions of tuples (the giant partition)
+    // is served from each SM's L1 instead of hammering one L2 slice.
+    uint32_t q[4], cur[4];
+    bool np[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
-      if (j >= cnt) break;
-      uint32_t q = __ldg(&U[r[j]]);
-      if (!FIRST && tbit(TB, r[j])) q = min(q, r[j]);
-      min_slot(PMIN, p[j], q);
-      if (FIRST && tbit(NP, r[j])) set_bit(NCP, p[j]);
+      q[j] = INF;
+      np[j] = false;
+      if (j < cnt) {
+        q[j] = __ldg(&U[r[j]]);
+        if (!FIRST && tbit(TB, r[j])) q[j] = min(q[j], r[j]);
+        if (FIRST) np[j] = tbit(NP, r[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) cur[j] = (j < cnt) ? __ldca(&PMIN[p[j]]) : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      if (j < cnt && q[j] < cur[j]) atomicMin(&PMIN[p[j]], q[j]);
+    if (FIRST) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) w[j] = (j < cnt && np[j]) ? __ldca(&NCP[p[j] >> 5]) : ~0u;
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        if (!((w[j] >> (p[j] & 31)) & 1u)) atomicOr(&NCP[p[j] >> 5], 1u << (p[j] & 31));
     }
   }
 }
@@ -360,20 +452,42 @@ __global__ void __launch_bounds__(B) k_papply2(uint32_t* __restrict__ P, uint64_
 }
 
 // ===================================================================== launchers
+int group_shift(uint64_t n, uint64_t tuples) {
+  int kb = 0;
+  while ((1ull << kb) < n) kb++;
+  int lg = 0;  // log2 G: about 2M tuples per group
+  while (lg < 10 && (tuples >> (21 + lg)) > 0) lg++;
+  int gs = kb - lg;
+  return gs < 11 ? 11 : gs;
+}
+
 void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* vis, uint64_t n,
-           uint32_t* off, uint32_t* cur, uint32_t* R, uint32_t* P, scan::State& ss, uint64_t* ctr,
+           uint32_t* off, uint32_t* cur, uint32_t* garc, int gshift, scan::State& ss, uint64_t* ctr,
            cudaStream_t st) {
   // ctr[C_VT_OUT] receives A_0
   if (!n) return;
+  const int G = (int)(((n - 1) >> gshift) + 1);
   cudaMemsetAsync(ss.ticket, 0, sizeof(uint32_t), st);
+  cudaMemsetAsync(garc, 0, sizeof(uint32_t) * G, st);
   const uint64_t tiles = (n + B * SITEMS - 1) / (B * SITEMS);
   k_rows<<<(unsigned)tiles, B, 0, st>>>(deg, vis, n, off, cur, ss.flags, ss.ticket, ++ss.epoch,
-                                         reinterpret_cast<unsigned long long*>(ctr + sv::C_VT_OUT));
+                                         reinterpret_cast<unsigned long long*>(ctr + sv::C_VT_OUT),
+                                         garc, gshift);
 }
 void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
-          uint32_t* R, uint32_t* P, cudaStream_t st) {
-  if (A) k_fill<<<grid(A, B * FITEMS, 1u << 30), B, 0, st>>>(off, n, A, R, P);
-  if (m) k_scatter<<<grid(m, B, 148 * 16), B, 0, st>>>(edges, m, cur, P);
+          uint32_t* R, uint32_t* P, const uint32_t* garc, int gshift, uint64_t* gcur, uint2* tmp,
+          uint32_t* longlist, uint64_t* nlong, cudaStream_t st) {
+  if (!A) return;
+  const int G = (int)(((n - 1) >> gshift) + 1);
+  auto* nl = reinterpret_cast<unsigned long long*>(nlong);
+  cudaMemsetAsync(nlong, 0, sizeof(uint64_t), st);
+  k_fill_rows<<<grid(n, B, 148 * 8), B, 0, st>>>(off, n, R, P, longlist, nl);
+  k_fill_long<<<148 * 2, B, 0, st>>>(off, longlist, nl, R);
+  if (!m) return;
+  auto* gc = reinterpret_cast<unsigned long long*>(gcur);
+  k_gscan<<<1, B, 0, st>>>(garc, G, gc);
+  k_bucket<<<(unsigned)((m + B * BITEMS - 1) / (B * BITEMS)), B, 0, st>>>(edges, m, gshift, G, gc, tmp);
+  k_scatter<<<grid(2 * m, B, 148 * 16), B, 0, st>>>(tmp, 2 * m, cur, P);
 }
 void vpass(bool with_pc, const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* U, uint32_t* NP,
            cudaStream_t st) {
