@@ -457,17 +457,18 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
   c->launches += 1;
   CKL();
   TRY(sync_read(c));
-  uint64_t A = c->h_ctr[sv::C_VT_OUT];
+  uint64_t A = c->h_ctr[sv::C_VT_OUT];  // live tuples (A_i)
   if (A == 0) return CC_OK;
   if (A > c->cap) return fail(c, CC_ERR_INVALID, "tuple count %llu exceeds capacity", (unsigned long long)A);
   // scratch: the bucketed arc list lives in the second tuple buffer (free until the first
-  // compaction), the long-row list in the vertex-group counter block
+  // compaction), the long-row list in the PMIN slots (free until the first partition pass)
   csr::fill(edges, m_sv, off, cur, n, A, R[0], P[0], garc, gshift, gcur,
             reinterpret_cast<uint2*>(c->d_w[1]), c->d_segB, nlong, c->st);
   c->launches += 5;
   CKL();
   seg_end(c, a, 4.0 * n + 8.0 * m_sv + 8.0 * A + 4.0 * n, 6, KF_CSR);
-  int cur_buf = 0;
+  int cb = 0;           // buffer holding the tuple array
+  uint64_t len = A;     // physical length (live + dead rows)
   const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
   uint64_t chg2_prev = 0;
   for (uint32_t it = 0;; it++) {
@@ -475,30 +476,26 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
     cudaEvent_t ev_it = ev_get(c);
     CK(cudaEventRecord(ev_it, c->st));
     seg_begin(c, &a);
-    uint32_t *Rc = R[cur_buf], *Pc = P[cur_buf];
+    uint32_t *Rc = R[cb], *Pc = P[cb];
     // ---- lines 8-13: vertex buckets are CSR rows; u_min and 'potentially completed'
     CK(cudaMemsetAsync(U, 0xFF, sizeof(uint32_t) * n, c->st));
     CK(cudaMemsetAsync(NP, 0, sizeof(uint32_t) * nw, c->st));
-    { Prof k(c, KF_VPASS); csr::vpass(true, Rc, Pc, A, U, NP, c->st); k.end(8.0 * A + 4.0 * n, 1); }
+    { Prof k(c, KF_VPASS); csr::vpass(true, Rc, Pc, len, U, NP, c->st); k.end(8.0 * len + 4.0 * n, 1); }
     // ---- lines 14-21: p_min per partition bucket; completion
     CK(cudaMemsetAsync(PMIN, 0xFF, sizeof(uint32_t) * n, c->st));
     CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nw, c->st));
     CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nw, c->st));
     CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_TEMPS + 1), c->st));
-    { Prof k(c, KF_PPASS); csr::ppass(true, Rc, Pc, A, U, NP, nullptr, PMIN, NCP, c->st);
-      k.end(8.0 * A + 8.0 * n, 1); }
-    // ---- line 22 (temporaries) + counters; exclusion of completed partitions
+    { Prof k(c, KF_PPASS); csr::ppass(true, Rc, Pc, len, U, NP, nullptr, PMIN, NCP, c->st);
+      k.end(8.0 * len + 8.0 * n, 1); }
+    // ---- line 22 (temporaries) + counters; exclusion of completed partitions (in place)
     csr::pscan(true, PMIN, NCP, n, TB, c->d_ctr, c->st);
-    TRY(scan_epoch_guard(c));
-    Prof kp(c, KF_PAPPLY);
-    csr::papply1(Rc, Pc, A, PMIN, NCP, R[cur_buf ^ 1], P[cur_buf ^ 1], c->d_label, c->ss, c->d_ctr,
-                 c->st);
+    { Prof k(c, KF_PAPPLY); csr::papply1(Rc, Pc, len, PMIN, NCP, c->d_label, c->d_ctr, c->st);
+      k.end(8.0 * len + 4.0 * n, 1); }
     c->launches += 4;
-    cur_buf ^= 1;
     CKL();
     TRY(sync_read(c));
     const uint64_t A1 = c->h_ctr[sv::C_OUT];
-    kp.end(8.0 * A + 4.0 * n + 8.0 * A1, 1);
     cc_iter_stat s{};
     s.active_in = A;
     s.partitions = c->h_ctr[sv::C_PARTITIONS];
@@ -512,25 +509,34 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
     c->iters.push_back(s);
     c->it_ev.push_back(ev_it);
     if (A1 == 0) {
-      seg_end(c, a, 8.0 * A + 8.0 * A + 8.0 * A, 4);
+      seg_end(c, a, 24.0 * len, 4);
       break;
     }
-    Rc = R[cur_buf];
-    Pc = P[cur_buf];
+    // dead rows of completed partitions are squeezed out once they are a third of the array
+    // (the paper's 'swapped to the end of the local array', sec:distSVOpt1)
+    if (3 * (len - A1) > len) {
+      TRY(scan_epoch_guard(c));
+      { Prof k(c, KF_PAPPLY); csr::compact(Rc, Pc, len, R[cb ^ 1], P[cb ^ 1], c->ss, c->st);
+        k.end(8.0 * len + 8.0 * A1, 1); }
+      c->launches += 1;
+      cb ^= 1;
+      len = A1;
+      Rc = R[cb];
+      Pc = P[cb];
+    }
     // ---- line 24: vertex buckets again, temporaries <u,_,u> from the TB bitmap
     CK(cudaMemsetAsync(U, 0xFF, sizeof(uint32_t) * n, c->st));
-    { Prof k(c, KF_VPASS); csr::vpass(false, Rc, Pc, A1, U, nullptr, c->st); k.end(8.0 * A1 + 4.0 * n, 1); }
+    { Prof k(c, KF_VPASS); csr::vpass(false, Rc, Pc, len, U, nullptr, c->st); k.end(8.0 * len + 4.0 * n, 1); }
     // ---- line 25: partition buckets again (+ temporaries), p <- p_min in place
     CK(cudaMemsetAsync(PMIN, 0xFF, sizeof(uint32_t) * n, c->st));
-    { Prof k(c, KF_PPASS); csr::ppass(false, Rc, Pc, A1, U, nullptr, TB, PMIN, nullptr, c->st);
-      k.end(8.0 * A1 + 8.0 * n, 1); }
+    { Prof k(c, KF_PPASS); csr::ppass(false, Rc, Pc, len, U, nullptr, TB, PMIN, nullptr, c->st);
+      k.end(8.0 * len + 8.0 * n, 1); }
     csr::temps(TB, n, U, PMIN, c->st);
     csr::pscan(false, PMIN, nullptr, n, nullptr, c->d_ctr, c->st);
-    { Prof k(c, KF_PAPPLY); csr::papply2(Pc, A1, PMIN, c->st); k.end(8.0 * A1 + 4.0 * n, 1); }
+    { Prof k(c, KF_PAPPLY); csr::papply2(Pc, len, PMIN, c->st); k.end(8.0 * len + 4.0 * n, 1); }
     c->launches += 5;
     CKL();
-    // algorithmic bytes streamed by this iteration's tuple passes (R,P u32 each)
-    seg_end(c, a, 8.0 * A * 3 + 8.0 * A1 * 4, 9);
+    seg_end(c, a, 8.0 * len * 6, 9);
     A = A1;
   }
   TRY(sync_read(c));

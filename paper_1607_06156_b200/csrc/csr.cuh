@@ -22,9 +22,12 @@ void ppass(bool first, const uint32_t* R, const uint32_t* P, uint64_t A, const u
 void temps(const uint32_t* TB, uint64_t n, const uint32_t* U, uint32_t* PMIN, cudaStream_t st);
 void pscan(bool first, const uint32_t* PMIN, const uint32_t* NCP, uint64_t n, uint32_t* TB,
            uint64_t* ctr, cudaStream_t st);
-void papply1(const uint32_t* R, const uint32_t* P, uint64_t A, const uint32_t* PMIN,
-             const uint32_t* NCP, uint32_t* R2, uint32_t* P2, uint32_t* label, scan::State& ss,
-             uint64_t* ctr, cudaStream_t st);
+// in place: completed partitions' tuples become DEAD, survivors p <- p_min; ctr[C_OUT] += live
+void papply1(const uint32_t* R, uint32_t* P, uint64_t A, const uint32_t* PMIN, const uint32_t* NCP,
+             uint32_t* label, uint64_t* ctr, cudaStream_t st);
+// ordered compaction of live tuples (R order kept); output count = live count
+void compact(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2,
+             scan::State& ss, cudaStream_t st);
 void papply2(uint32_t* P, uint64_t A, const uint32_t* PMIN, cudaStream_t st);
 
 }  // namespace csr

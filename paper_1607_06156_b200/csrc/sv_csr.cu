@@ -200,64 +200,93 @@ __global__ void __launch_bounds__(B) k_scatter(const uint2* __restrict__ arcs, u
 }
 
 // ===================================================================== vertex passes
-// Lines 9-13 (WITH_PC) / line 24: per vertex bucket (a run of equal R), u_min = min p and,
-// for PC, whether max p != min p.  Warp chunks with carry (as sv.cu k_seg_reduce).
-constexpr int VSTEPS = 64;
-constexpr int VCHUNK = 32 * VSTEPS;
+// Lines 9-13 (WITH_PC) / line 24: per vertex bucket VB(u) (a run of equal R), u_min = min p
+// and, for PC, whether max p != min p (|M(u)| > 1).  A warp streams its chunk
+// in 128-tuple windows (one 16-byte load of R and of P per lane, next window prefetched),
+// stages the window in shared memory, and every run head walks its run inside the window;
+// the run touching the window end is carried into the next window, so a bucket costs one
+// atomic per 128-tuple window it spans at most.  Tuples of completed partitions are dead
+// (P = DEAD, whole rows) and are skipped.
+constexpr uint32_t DEAD = 0xFFFFFFFFu;
+constexpr int VWIN = 128;
+constexpr int VWINS = 16;  // windows per warp chunk
+constexpr int VCHUNK = VWIN * VWINS;
+CC_DEVI void load_window(const uint32_t* R, const uint32_t* P, uint64_t A, uint64_t base, int lane,
+                         uint4& r4, uint4& p4) {
+  const uint64_t i = base + 4 * (uint64_t)lane;
+  if (i + 3 < A) {
+    r4 = ldg_stream(reinterpret_cast<const uint4*>(R + i));
+    p4 = ldg_stream(reinterpret_cast<const uint4*>(P + i));
+  } else {
+    r4 = make_uint4(INF, INF, INF, INF);
+    p4 = make_uint4(DEAD, DEAD, DEAD, DEAD);
+    if (i < A) { r4.x = R[i]; p4.x = P[i]; }
+    if (i + 1 < A) { r4.y = R[i + 1]; p4.y = P[i + 1]; }
+    if (i + 2 < A) { r4.z = R[i + 2]; p4.z = P[i + 2]; }
+  }
+}
 template <bool WITH_PC>
 __global__ void __launch_bounds__(B) k_vpass(const uint32_t* __restrict__ R,
                                              const uint32_t* __restrict__ P, uint64_t A,
                                              uint32_t* __restrict__ U, uint32_t* __restrict__ NP) {
-  const int lane = threadIdx.x & 31;
+  __shared__ __align__(16) uint32_t s_k[B / 32][VWIN];
+  __shared__ __align__(16) uint32_t s_v[B / 32][VWIN];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t warp = (blockIdx.x * (uint64_t)B + threadIdx.x) >> 5;
   const uint64_t cbase = warp * VCHUNK;
   if (cbase >= A) return;
-  uint32_t ckey = INF, cmin = INF, cmax = 0;
+  uint32_t* sk = s_k[wid];
+  uint32_t* sv = s_v[wid];
   auto emit = [&](uint32_t key, uint32_t mn, uint32_t mx) {
     atomicMin(&U[key], mn);
     if (WITH_PC && mn != mx) atomicOr(&NP[key >> 5], 1u << (key & 31));
   };
-  for (int k = 0; k < VSTEPS; k++) {
-    const uint64_t i = cbase + (uint64_t)k * 32 + lane;
-    uint32_t key = INF, mn = INF, mx = 0;
-    if (i < A) {
-      key = __ldg(&R[i]);
-      mn = mx = __ldg(&P[i]);
-    }
-    if (__all_sync(0xffffffffu, key == INF)) break;
+  uint32_t ckey = INF, cmin = INF, cmax = 0;  // carry (warp-uniform)
+  uint4 r4, p4, nr4, np4;
+  load_window(R, P, A, cbase, lane, r4, p4);
+  for (int w = 0; w < VWINS; w++) {
+    const uint64_t base = cbase + (uint64_t)w * VWIN;
+    if (base >= A) break;
+    if (w + 1 < VWINS && base + VWIN < A) load_window(R, P, A, base + VWIN, lane, nr4, np4);
+    // dead tuples (completed partitions) and padding get key INF
+    uint4 k4 = make_uint4(p4.x == DEAD ? INF : r4.x, p4.y == DEAD ? INF : r4.y,
+                          p4.z == DEAD ? INF : r4.z, p4.w == DEAD ? INF : r4.w);
+    reinterpret_cast<uint4*>(sk)[lane] = k4;
+    reinterpret_cast<uint4*>(sv)[lane] = p4;
+    __syncwarp();
+    // the previous carry ends here unless window element 0 continues its run
+    if (lane == 0 && ckey != INF && sk[0] != ckey) emit(ckey, cmin, cmax);
+    bool tail = false;
+    uint32_t tk = INF, tmn = INF, tmx = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t ko = __shfl_down_sync(0xffffffffu, key, o);
-      const uint32_t a = __shfl_down_sync(0xffffffffu, mn, o);
-      const uint32_t b = WITH_PC ? __shfl_down_sync(0xffffffffu, mx, o) : 0u;
-      if (lane + o < 32 && ko == key) {
-        mn = min(mn, a);
-        if (WITH_PC) mx = max(mx, b);
+    for (int s2 = 0; s2 < 4; s2++) {
+      const int e = lane + 32 * s2;
+      const uint32_t k = sk[e];
+      if (k == INF || (e > 0 && sk[e - 1] == k)) continue;  // not a run head
+      uint32_t mn = sv[e], mx = mn;
+      int j = e + 1;
+      while (j < VWIN && sk[j] == k) {
+        const uint32_t v = sv[j];
+        mn = min(mn, v);
+        mx = max(mx, v);
+        j++;
       }
+      if (e == 0 && k == ckey) { mn = min(mn, cmin); mx = max(mx, cmax); }
+      if (j == VWIN) { tail = true; tk = k; tmn = mn; tmx = mx; }
+      else emit(k, mn, mx);
     }
-    const uint32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
-    const bool head = (lane == 0) || (kprev != key);
-    const uint32_t hmask = __ballot_sync(0xffffffffu, head);
-    const int last = 31 - __clz(hmask);
-    const uint32_t key0 = __shfl_sync(0xffffffffu, key, 0);
-    uint32_t mn0 = __shfl_sync(0xffffffffu, mn, 0);
-    uint32_t mx0 = __shfl_sync(0xffffffffu, mx, 0);
-    const uint32_t keyL = __shfl_sync(0xffffffffu, key, last);
-    const uint32_t mnL = __shfl_sync(0xffffffffu, mn, last);
-    const uint32_t mxL = __shfl_sync(0xffffffffu, mx, last);
-    if (key0 == ckey) {
-      mn0 = min(mn0, cmin);
-      mx0 = max(mx0, cmax);
-    } else if (lane == 0 && ckey != INF) {
-      emit(ckey, cmin, cmax);
-    }
-    if (last == 0) {
-      ckey = key0; cmin = mn0; cmax = mx0;
+    const uint32_t tb = __ballot_sync(0xffffffffu, tail);
+    if (tb) {
+      const int src = __ffs(tb) - 1;
+      ckey = __shfl_sync(0xffffffffu, tk, src);
+      cmin = __shfl_sync(0xffffffffu, tmn, src);
+      cmax = __shfl_sync(0xffffffffu, tmx, src);
     } else {
-      if (lane == 0 && key0 != INF) emit(key0, mn0, mx0);
-      if (head && lane != 0 && lane != last && key != INF) emit(key, mn, mx);
-      ckey = keyL; cmin = mnL; cmax = mxL;
+      ckey = INF; cmin = INF; cmax = 0;
     }
+    __syncwarp();
+    r4 = nr4;
+    p4 = np4;
   }
   if (lane == 0 && ckey != INF) emit(ckey, cmin, cmax);
 }
@@ -266,6 +295,11 @@ __global__ void __launch_bounds__(B) k_vpass(const uint32_t* __restrict__ R,
 // Line 15 (FIRST) / line 25: p_min = min over PB(p) of q = u_min(r) -> PMIN[p]; FIRST also
 // marks PB(p) 'not completed' when a tuple's vertex is not potentially completed.
 // Second pass: q includes the temporary <r,_,r> in VB(r) when TB(r).
+// Each block keeps a small direct-mapped cache of slot values it has seen (key and value in
+// one 64-bit word): slots only decrease, so q >= a cached value needs no global traffic.
+// That keeps a partition shared by millions of tuples (the giant component late in the
+// run) from serialising one L2 slice, while distinct partitions go straight to the atomic.
+constexpr int PCACHE = 1024;
 template <bool FIRST>
 __global__ void __launch_bounds__(B) k_ppass(const uint32_t* __restrict__ R,
                                              const uint32_t* __restrict__ P, uint64_t A,
@@ -273,49 +307,58 @@ __global__ void __launch_bounds__(B) k_ppass(const uint32_t* __restrict__ R,
                                              const uint32_t* __restrict__ NP,
                                              const uint32_t* __restrict__ TB, uint32_t* PMIN,
                                              uint32_t* NCP) {
+  __shared__ unsigned long long s_pc[PCACHE];
+  __shared__ uint32_t s_nc[PCACHE];
+  for (int i = threadIdx.x; i < PCACHE; i += B) {
+    s_pc[i] = ~0ull;
+    s_nc[i] = INF;
+  }
+  __syncthreads();
   const uint64_t nq = (A + 3) >> 2;
   for (uint64_t t = blockIdx.x * (uint64_t)B + threadIdx.x; t < nq; t += (uint64_t)gridDim.x * B) {
     uint32_t r[4], p[4];
-    int cnt = 4;
     if (4 * t + 3 < A) {
       const uint4 a = ldg_stream(reinterpret_cast<const uint4*>(R) + t);
       const uint4 b = ldg_stream(reinterpret_cast<const uint4*>(P) + t);
       r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
       p[0] = b.x; p[1] = b.y; p[2] = b.z; p[3] = b.w;
     } else {
-      cnt = (int)(A - 4 * t);
-      for (int j = 0; j < 4; j++)
-        if (j < cnt) { r[j] = R[4 * t + j]; p[j] = P[4 * t + j]; }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        r[j] = (4 * t + j < A) ? R[4 * t + j] : 0u;
+        p[j] = (4 * t + j < A) ? P[4 * t + j] : DEAD;
+      }
     }
-    // gather q and flags for all 4 tuples, then the slot reads, then the (rare) atomics.
-    // The check-before reads go through L1 (ld.ca): a stale L1 copy is never below the
-    // true slot value (slots only decrease / only gain bits), so at worst it costs an
-    // unneeded atomic -- while a bucket shared by millions of tuples (the giant partition)
-    // is served from each SM's L1 instead of hammering one L2 slice.
-    uint32_t q[4], cur[4];
+    uint32_t q[4];
     bool np[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       q[j] = INF;
       np[j] = false;
-      if (j < cnt) {
+      if (p[j] != DEAD) {
         q[j] = __ldg(&U[r[j]]);
         if (!FIRST && tbit(TB, r[j])) q[j] = min(q[j], r[j]);
         if (FIRST) np[j] = tbit(NP, r[j]);
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; j++) cur[j] = (j < cnt) ? __ldca(&PMIN[p[j]]) : 0u;
-#pragma unroll
-    for (int j = 0; j < 4; j++)
-      if (j < cnt && q[j] < cur[j]) atomicMin(&PMIN[p[j]], q[j]);
+    for (int j = 0; j < 4; j++) {
+      if (p[j] == DEAD) continue;
+      const uint32_t h = (p[j] ^ (p[j] >> 10)) & (PCACHE - 1);
+      const unsigned long long e = *(volatile unsigned long long*)&s_pc[h];
+      if ((uint32_t)(e >> 32) == p[j] && q[j] >= (uint32_t)e) continue;
+      const uint32_t old = atomicMin(&PMIN[p[j]], q[j]);
+      s_pc[h] = ((unsigned long long)p[j] << 32) | min(old, q[j]);
+    }
     if (FIRST) {
-      uint32_t w[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) w[j] = (j < cnt && np[j]) ? __ldca(&NCP[p[j] >> 5]) : ~0u;
-#pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (!((w[j] >> (p[j] & 31)) & 1u)) atomicOr(&NCP[p[j] >> 5], 1u << (p[j] & 31));
+      for (int j = 0; j < 4; j++) {
+        if (!np[j]) continue;
+        const uint32_t h = (p[j] ^ (p[j] >> 10)) & (PCACHE - 1);
+        if (*(volatile uint32_t*)&s_nc[h] == p[j]) continue;
+        atomicOr(&NCP[p[j] >> 5], 1u << (p[j] & 31));
+        s_nc[h] = p[j];
+      }
     }
   }
 }
@@ -370,69 +413,84 @@ __global__ void __launch_bounds__(B) k_pscan(const uint32_t* __restrict__ PMIN,
 }
 
 // Lines 17-21 + sec:distSVOpt1: tuples of completed partitions leave (their vertex takes
-// label p), survivors get p <- p_min.  Ordered stream compaction (tile
-// prefix by decoupled look-back) keeps R sorted.
+// label p), survivors get p <- p_min.  Leaving is done in place (P = DEAD,
+// whole rows, R order untouched); k_compact squeezes dead rows out when they pile up.
+__global__ void __launch_bounds__(B) k_papply1(const uint32_t* __restrict__ R, uint32_t* P,
+                                               uint64_t A, const uint32_t* __restrict__ PMIN,
+                                               const uint32_t* __restrict__ NCP,
+                                               uint32_t* __restrict__ label,
+                                               unsigned long long* ctr) {
+  uint32_t live = 0;
+  const uint64_t nq = (A + 3) >> 2;
+  for (uint64_t t = blockIdx.x * (uint64_t)B + threadIdx.x; t < nq; t += (uint64_t)gridDim.x * B) {
+    uint32_t p[4];
+    const bool full = 4 * t + 3 < A;
+    if (full) {
+      const uint4 b = reinterpret_cast<const uint4*>(P)[t];
+      p[0] = b.x; p[1] = b.y; p[2] = b.z; p[3] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) p[j] = (4 * t + j < A) ? P[4 * t + j] : DEAD;
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      o[j] = DEAD;
+      if (p[j] == DEAD) continue;
+      const uint32_t pm = __ldg(&PMIN[p[j]]);
+      if (pm == p[j] && !tbit(NCP, p[j])) {
+        label[R[4 * t + j]] = p[j];  // completed: every tuple of VB(r) is in p
+      } else {
+        o[j] = pm;
+        live++;
+      }
+    }
+    if (full) reinterpret_cast<uint4*>(P)[t] = make_uint4(o[0], o[1], o[2], o[3]);
+    else
+      for (int j = 0; j < 4; j++)
+        if (4 * t + j < A) P[4 * t + j] = o[j];
+  }
+  live = warp_sum(live);
+  if ((threadIdx.x & 31) == 0 && live) atomicAdd(&ctr[sv::C_OUT], (unsigned long long)live);
+}
+
+// Ordered stream compaction of the live tuples (P != DEAD): tile prefix by decoupled
+// look-back keeps R sorted.  Run when dead rows exceed a fraction of the array.
 constexpr int CITEMS = 8;
 constexpr int CTILE = B * CITEMS;
-__global__ void __launch_bounds__(B) k_papply1(const uint32_t* __restrict__ R,
+__global__ void __launch_bounds__(B) k_compact(const uint32_t* __restrict__ R,
                                                const uint32_t* __restrict__ P, uint64_t A,
-                                               const uint32_t* __restrict__ PMIN,
-                                               const uint32_t* __restrict__ NCP,
                                                uint32_t* __restrict__ R2, uint32_t* __restrict__ P2,
-                                               uint32_t* __restrict__ label, uint64_t* flags,
-                                               uint32_t* ticket, uint32_t epoch,
-                                               unsigned long long* ctr) {
+                                               uint64_t* flags, uint32_t* ticket, uint32_t epoch) {
   __shared__ uint32_t s_scan[B / 32 + 1];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_pref;
+  __shared__ uint32_t s_r[CTILE], s_p[CTILE];
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint64_t i0 = tile * CTILE + (uint64_t)threadIdx.x * CITEMS;
   uint32_t r[CITEMS], p[CITEMS];
-  uint32_t keep = 0;  // bitmask of kept items
-  if (i0 + CITEMS <= A) {
-    const uint4* r4 = reinterpret_cast<const uint4*>(R + i0);
-    const uint4* p4 = reinterpret_cast<const uint4*>(P + i0);
-    uint4 a = ldg_stream(r4), b = ldg_stream(r4 + 1), c = ldg_stream(p4), d = ldg_stream(p4 + 1);
-    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
-    p[0] = c.x; p[1] = c.y; p[2] = c.z; p[3] = c.w; p[4] = d.x; p[5] = d.y; p[6] = d.z; p[7] = d.w;
-  } else {
-#pragma unroll
-    for (int k = 0; k < CITEMS; k++) {
-      r[k] = (i0 + k < A) ? R[i0 + k] : INF;
-      p[k] = (i0 + k < A) ? P[i0 + k] : 0;
-    }
-  }
-  uint32_t prev = (i0 > 0 && i0 <= A) ? __ldg(&R[i0 - 1]) : INF;
-  uint32_t cnt = 0;
 #pragma unroll
   for (int k = 0; k < CITEMS; k++) {
-    if (i0 + k < A) {
-      const uint32_t pm = __ldg(&PMIN[p[k]]);
-      const bool comp = (pm == p[k]) && !tbit(NCP, p[k]);
-      if (comp) {
-        if (r[k] != prev) label[r[k]] = p[k];  // first tuple of VB(r)
-      } else {
-        keep |= 1u << k;
-        p[k] = pm;
-        cnt++;
-      }
-      prev = r[k];
-    }
+    r[k] = (i0 + k < A) ? R[i0 + k] : 0u;
+    p[k] = (i0 + k < A) ? P[i0 + k] : DEAD;
   }
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++) cnt += (p[k] != DEAD);
   uint32_t tot;
   const uint32_t excl = block_excl_scan<B>(cnt, s_scan, &tot);
   const uint64_t pref = scan::tile_prefix(flags, tile, tot, epoch, &s_pref);
-  uint64_t o = pref + excl;
+  uint32_t o = excl;
 #pragma unroll
   for (int k = 0; k < CITEMS; k++)
-    if (keep >> k & 1u) {
-      R2[o] = r[k];
-      P2[o] = p[k];
-      o++;
-    }
-  if (i0 < A && i0 + CITEMS >= A) atomicAdd(&ctr[sv::C_OUT], (unsigned long long)(pref + excl + cnt));
+    if (p[k] != DEAD) { s_r[o] = r[k]; s_p[o] = p[k]; o++; }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < tot; i += B) {
+    R2[pref + i] = s_r[i];
+    P2[pref + i] = s_p[i];
+  }
 }
 
 // Line 25 update: p <- p_min of the second partition pass, in place (temporaries are
@@ -443,10 +501,14 @@ __global__ void __launch_bounds__(B) k_papply2(uint32_t* __restrict__ P, uint64_
   for (uint64_t t = blockIdx.x * (uint64_t)B + threadIdx.x; t < nq; t += (uint64_t)gridDim.x * B) {
     if (4 * t + 3 < A) {
       uint4 b = reinterpret_cast<const uint4*>(P)[t];
-      b.x = __ldg(&PMIN[b.x]); b.y = __ldg(&PMIN[b.y]); b.z = __ldg(&PMIN[b.z]); b.w = __ldg(&PMIN[b.w]);
+      if (b.x != DEAD) b.x = __ldg(&PMIN[b.x]);
+      if (b.y != DEAD) b.y = __ldg(&PMIN[b.y]);
+      if (b.z != DEAD) b.z = __ldg(&PMIN[b.z]);
+      if (b.w != DEAD) b.w = __ldg(&PMIN[b.w]);
       reinterpret_cast<uint4*>(P)[t] = b;
     } else {
-      for (uint64_t i = 4 * t; i < A; i++) P[i] = __ldg(&PMIN[P[i]]);
+      for (uint64_t i = 4 * t; i < A; i++)
+        if (P[i] != DEAD) P[i] = __ldg(&PMIN[P[i]]);
     }
   }
 }
@@ -492,7 +554,7 @@ void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, ui
 void vpass(bool with_pc, const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* U, uint32_t* NP,
            cudaStream_t st) {
   if (!A) return;
-  const uint64_t warps = (A + VCHUNK - 1) / VCHUNK;
+  const uint64_t warps = (A + VCHUNK - 1) / VCHUNK;  // one warp per VCHUNK tuples
   const unsigned g = (unsigned)((warps * 32 + B - 1) / B);
   if (with_pc) k_vpass<true><<<g, B, 0, st>>>(R, P, A, U, NP);
   else k_vpass<false><<<g, B, 0, st>>>(R, P, A, U, NP);
@@ -514,14 +576,18 @@ void pscan(bool first, const uint32_t* PMIN, const uint32_t* NCP, uint64_t n, ui
   if (first) k_pscan<true><<<grid(n, B, 148 * 8), B, 0, st>>>(PMIN, NCP, n, TB, c);
   else k_pscan<false><<<grid(n, B, 148 * 8), B, 0, st>>>(PMIN, NCP, n, TB, c);
 }
-void papply1(const uint32_t* R, const uint32_t* P, uint64_t A, const uint32_t* PMIN,
-             const uint32_t* NCP, uint32_t* R2, uint32_t* P2, uint32_t* label, scan::State& ss,
-             uint64_t* ctr, cudaStream_t st) {
+void papply1(const uint32_t* R, uint32_t* P, uint64_t A, const uint32_t* PMIN, const uint32_t* NCP,
+             uint32_t* label, uint64_t* ctr, cudaStream_t st) {
+  if (A)
+    k_papply1<<<grid((A + 3) / 4, B, 148 * 8), B, 0, st>>>(R, P, A, PMIN, NCP, label,
+                                                           reinterpret_cast<unsigned long long*>(ctr));
+}
+void compact(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2,
+             scan::State& ss, cudaStream_t st) {
   if (!A) return;
   cudaMemsetAsync(ss.ticket, 0, sizeof(uint32_t), st);
   const uint64_t tiles = (A + CTILE - 1) / CTILE;
-  k_papply1<<<(unsigned)tiles, B, 0, st>>>(R, P, A, PMIN, NCP, R2, P2, label, ss.flags, ss.ticket,
-                                            ++ss.epoch, reinterpret_cast<unsigned long long*>(ctr));
+  k_compact<<<(unsigned)tiles, B, 0, st>>>(R, P, A, R2, P2, ss.flags, ss.ticket, ++ss.epoch);
 }
 void papply2(uint32_t* P, uint64_t A, const uint32_t* PMIN, cudaStream_t st) {
   if (A) k_papply2<<<grid((A + 3) / 4, B, 148 * 8), B, 0, st>>>(P, A, PMIN);
