@@ -40,6 +40,7 @@ struct cc_ctx {
   int kbits = 0;
   uint2* d_edges = nullptr;
   uint2* d_rem = nullptr;
+  uint2* d_rem2 = nullptr;
   uint32_t* d_label = nullptr;
   uint32_t* d_deg = nullptr;
   uint32_t* d_hist = nullptr;
@@ -131,7 +132,7 @@ static void dfree_all(cc_ctx* c) {
     else cudaFreeAsync(a.first, c->st);
   }
   c->allocs.clear();
-  c->d_edges = c->d_rem = nullptr;
+  c->d_edges = c->d_rem = c->d_rem2 = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
   c->d_bm[0] = c->d_bm[1] = c->d_bm[2] = nullptr;
   c->d_sbm[0] = c->d_sbm[1] = c->d_sbm[2] = nullptr;
@@ -274,7 +275,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->d_deg, n + 1));
   TRY(dalloc_t(c, &c->d_hist, graph::HIST_DENSE));
   TRY(dalloc_t(c, &c->d_tail, graph::TAIL_CAP));
-  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], nw));
+  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], 2 * nw));  // 2-bit BFS state fits
   for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_sbm[i], nw));
   for (int i = 0; i < 2; i++) {
     TRY(dalloc_t(c, &c->d_w[i], c->cap));
@@ -663,7 +664,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
   CK(cudaMemsetAsync(c->d_gctr + graph::G_MINVIS, 0xFF, sizeof(uint64_t), c->st));
   sv::launch_init_labels(c->d_label, n, c->st);
-  graph::launch_degree(c->d_edges, m, c->d_deg, c->st);
+  graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st);
   const bool want_hist = (mode == CC_MODE_AUTO) || (c->cfg.flags & CC_FLAG_TRACE);
   if (want_hist) CK(cudaMemsetAsync(c->d_hist, 0, sizeof(uint32_t) * graph::HIST_DENSE, c->st));
   graph::launch_deg_hist(c->d_deg, n, c->d_hist, c->d_tail, c->d_gctr, c->st);
@@ -725,43 +726,67 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     R.ran_bfs = 1;
     R.bfs_root = root;
     const uint64_t nw = (n + 31) / 32;
-    uint32_t *V = c->d_bm[0], *F = c->d_bm[1], *X = c->d_bm[2];
-    CK(cudaMemsetAsync(V, 0, sizeof(uint32_t) * nw, c->st));
-    CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * nw, c->st));
-    c->h_word[0] = 1u << (root & 31);
-    CK(cudaMemcpyAsync(V + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(F + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+    uint32_t *V = c->d_bm[0], *S = c->d_bm[1], *X = c->d_bm[2];
+    if (!c->d_rem) TRY(dalloc_t(c, &c->d_rem, m + 1));
+    if (!c->d_rem2) TRY(dalloc_t(c, &c->d_rem2, m + 1));
+    uint2* bufs[2] = {c->d_rem, c->d_rem2};
+    CK(cudaMemsetAsync(S, 0, sizeof(uint32_t) * 2 * nw, c->st));
+    c->h_word[0] = 1u << (2 * (root & 15));
+    CK(cudaMemcpyAsync(S + root / 16, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+    const uint2* cur = c->d_edges;
+    uint64_t mcur = m;
+    int nb = 0;  // next scratch buffer
+    bool last_compacted = false;
     uint64_t visited = 1, levels = 0;
     while (true) {
       CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
-      CK(cudaMemsetAsync(c->d_gctr + graph::G_NEWVIS, 0, sizeof(uint64_t), c->st));
+      CK(cudaMemsetAsync(c->d_gctr + graph::G_NEWVIS, 0, 2 * sizeof(uint64_t), c->st));
+      const bool root_level = levels == 0;
+      // compact once most present vertices are visited: the surviving edges are few
+      const bool compact = !root_level && 2 * visited > R.n_present;
       Prof k(c, KF_BFS);
-      graph::launch_bfs_level(c->d_edges, m, F, V, X, c->d_gctr, c->st);
+      graph::launch_bfs_level(root_level, compact, cur, mcur, (uint32_t)root, S, X, bufs[nb],
+                              c->d_gctr, c->st);
       c->launches += 1;
-      k.end(8.0 * (double)m + (double)n / 8 * 3, 1);
+      k.end(8.0 * (double)mcur + (compact ? 8.0 * (double)mcur / 8 : 0.0) + (double)n / 4, 1);
       CKL();
       TRY(sync_read(c));
+      last_compacted = compact;
+      if (compact) {
+        cur = bufs[nb];
+        mcur = c->h_gctr[graph::G_REMAIN];
+        nb ^= 1;
+      }
       const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
       if (nv == 0) break;
       visited += nv;
       levels++;
-      std::swap(F, X);
+      graph::launch_bfs_advance(S, X, n, c->st);
+      c->launches += 1;
     }
     R.bfs_visited = visited;
     R.bfs_levels = levels;
+    graph::launch_vis_bits(S, n, V, c->st);
     graph::launch_min_visited(V, n, c->d_gctr, c->st);
     graph::launch_bfs_labels(V, n, c->d_label, c->d_gctr, c->st);
-    c->launches += 2;
+    c->launches += 3;
     e_bfs = ev_get(c);
     CK(cudaEventRecord(e_bfs, c->st));
-    if (!c->d_rem) TRY(dalloc_t(c, &c->d_rem, m + 1));
-    graph::launch_filter(c->d_edges, m, V, c->d_rem, c->d_gctr, c->st);
-    c->launches += 1;
-    CKL();
-    TRY(sync_read(c));
-    m_sv = c->h_gctr[graph::G_REMAIN];
+    if (last_compacted) {
+      // a level that discovers nothing leaves no edge with exactly one visited endpoint:
+      // its survivors are exactly E \ {(u,v) | u in VI}
+      m_sv = mcur;
+      sv_edges = cur;
+    } else {
+      CK(cudaMemsetAsync(c->d_gctr + graph::G_REMAIN, 0, sizeof(uint64_t), c->st));
+      graph::launch_filter(cur, mcur, S, bufs[nb], c->d_gctr, c->st);
+      c->launches += 1;
+      CKL();
+      TRY(sync_read(c));
+      m_sv = c->h_gctr[graph::G_REMAIN];
+      sv_edges = bufs[nb];
+    }
     R.remainder_edges = m_sv;
-    sv_edges = c->d_rem;
     vis = V;
     e_filter = ev_get(c);
     CK(cudaEventRecord(e_filter, c->st));

@@ -35,18 +35,37 @@ void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr,
 // ---------------------------------------------------------------- degrees
 // Degree of v = number of arcs with source v, each undirected edge being the two arcs
 // (u,v),(v,u); a self-loop adds 2.  Ids are dense, so a
-// counting increment replaces the paper's sort by source.
-__global__ void k_degree(const uint2* __restrict__ e, uint64_t m, uint32_t* __restrict__ deg) {
-  for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i < m;
+// counting increment replaces the paper's sort by source.  When the
+// counter array is larger than a window that stays L2-resident (2^24 ids = 64 MB), the
+// edge list is streamed once per window and only endpoints inside it are counted, so the
+// random increments never reach DRAM.
+constexpr uint64_t DEG_WINDOW = 1ull << 24;
+__global__ void k_degree(const uint4* __restrict__ e2, uint64_t m, uint32_t* __restrict__ deg,
+                         uint32_t lo, uint32_t hi) {
+  const uint64_t npair = m >> 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i <= npair;
        i += (uint64_t)gridDim.x * BLOCK) {
-    uint2 x = e[i];
-    atomicAdd(&deg[x.x], 1u);
-    atomicAdd(&deg[x.y], 1u);
+    uint32_t v[4];
+    int cnt = 0;
+    if (i < npair) {
+      const uint4 x = ldg_stream(&e2[i]);
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; cnt = 4;
+    } else if (m & 1) {
+      const uint2 x = reinterpret_cast<const uint2*>(e2)[m - 1];
+      v[0] = x.x; v[1] = x.y; cnt = 2;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      if (j < cnt && v[j] >= lo && v[j] < hi) atomicAdd(&deg[v[j]], 1u);
   }
 }
-void launch_degree(const uint2* edges, uint64_t m, uint32_t* deg, cudaStream_t st) {
+void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st) {
   if (!m) return;
-  k_degree<<<grid_for(m, 148 * 16), BLOCK, 0, st>>>(edges, m, deg);
+  for (uint64_t lo = 0; lo < n; lo += DEG_WINDOW) {
+    const uint64_t hi = std::min<uint64_t>(n, lo + DEG_WINDOW);
+    k_degree<<<grid_for((m >> 1) + 1, 148 * 16), BLOCK, 0, st>>>(
+        reinterpret_cast<const uint4*>(edges), m, deg, (uint32_t)lo, (uint32_t)hi);
+  }
 }
 
 // Degree distribution D[d] = #{v : deg(v) = d}, d >= 1 (C10), plus n_present and the
@@ -104,58 +123,104 @@ void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* 
 }
 
 // ---------------------------------------------------------------- BFS peel
-// One level of a level-synchronous BFS from the root (Alg. 2 lines 7-8)
-// over the edge list, with n-bit frontier / visited / next bitmaps (L2 resident for the
-// configs here).  Every live edge is streamed once per level; an endpoint in the
-// frontier claims its unvisited neighbour with atomicOr on the visited bitmap, so each
-// vertex enters `next` exactly once.  (edge-streaming bitmap BFS.)
-CC_DEVI bool bit(const uint32_t* bm, uint32_t v) { return (__ldg(&bm[v >> 5]) >> (v & 31)) & 1u; }
-CC_DEVI bool claim(uint32_t* visited, uint32_t* next, uint32_t v) {
-  uint32_t mask = 1u << (v & 31);
-  if (visited[v >> 5] & mask) return false;  // cheap pre-check (relaxed read)
-  uint32_t old = atomicOr(&visited[v >> 5], mask);
-  if (old & mask) return false;
-  atomicOr(&next[v >> 5], mask);
+// Level-synchronous BFS from the root (Alg. 2 lines 7-8) over the edge
+// list.  Vertex state is 2 bits (bit 0 visited, bit 1 in the current frontier), 16 ids per
+// word, so one random read per endpoint answers both questions; a frontier endpoint claims
+// its unvisited neighbour with atomicOr on the visited bit and marks it in `next`.
+// Level 1 (frontier = {root}) compares ids instead of reading state.  From the level at
+// which most vertices are visited, each level also compacts the edge list to the edges that
+// still have an endpoint unvisited at the start of the level: later levels and the filter
+// stream only those.  (edge-streaming bitmap BFS.)
+CC_DEVI uint32_t st2(const uint32_t* S, uint32_t v) { return (S[v >> 4] >> (2 * (v & 15))) & 3u; }
+CC_DEVI bool claim2(uint32_t* S, uint32_t* next, uint32_t v) {
+  const uint32_t m = 1u << (2 * (v & 15));
+  if (S[v >> 4] & m) return false;  // relaxed pre-check
+  if (atomicOr(&S[v >> 4], m) & m) return false;
+  atomicOr(&next[v >> 5], 1u << (v & 31));
   return true;
 }
-__global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint4* __restrict__ e2, uint64_t m,
-                                                     const uint32_t* __restrict__ frontier,
-                                                     uint32_t* visited, uint32_t* next,
+template <bool ROOT, bool COMPACT>
+__global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e, uint64_t m,
+                                                     uint32_t root, uint32_t* S, uint32_t* next,
+                                                     uint2* __restrict__ out,
                                                      unsigned long long* gctr) {
+  __shared__ uint32_t s_scan[BLOCK / 32 + 1];
+  __shared__ unsigned long long s_base;
   uint32_t found = 0;
-  const uint64_t npair = m >> 1;
-  for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i <= npair;
-       i += (uint64_t)gridDim.x * BLOCK) {
-    uint32_t a[2], b[2];
+  const uint64_t stride = (uint64_t)gridDim.x * BLOCK * 2;
+  const uint64_t iters = (m + stride - 1) / stride;
+  for (uint64_t it = 0; it < iters; it++) {
+    const uint64_t i0 = it * stride + (blockIdx.x * (uint64_t)BLOCK + threadIdx.x) * 2;
+    uint2 x[2];
+    bool keep[2] = {false, false};
     int cnt = 0;
-    if (i < npair) {
-      uint4 x = ldg_stream(&e2[i]);
-      a[0] = x.x; b[0] = x.y; a[1] = x.z; b[1] = x.w; cnt = 2;
-    } else if (m & 1) {
-      uint2 x = reinterpret_cast<const uint2*>(e2)[m - 1];
-      a[0] = x.x; b[0] = x.y; cnt = 1;
+    if (i0 + 1 < m) {
+      const uint4 q = ldg_stream(reinterpret_cast<const uint4*>(e + i0));
+      x[0] = make_uint2(q.x, q.y); x[1] = make_uint2(q.z, q.w); cnt = 2;
+    } else if (i0 < m) {
+      x[0] = e[i0]; cnt = 1;
     }
-    for (int j = 0; j < cnt; j++) {
-      if (bit(frontier, a[j])) found += claim(visited, next, b[j]);
-      if (bit(frontier, b[j])) found += claim(visited, next, a[j]);
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      if (j >= cnt) continue;
+      const uint32_t a = x[j].x, b = x[j].y;
+      if (ROOT) {
+        if (a == root) found += claim2(S, next, b);
+        if (b == root) found += claim2(S, next, a);
+      } else {
+        const uint32_t sa = st2(S, a), sb = st2(S, b);
+        if ((sa & 2u) && !(sb & 1u)) found += claim2(S, next, b);
+        if ((sb & 2u) && !(sa & 1u)) found += claim2(S, next, a);
+        keep[j] = !((sa & 1u) && (sb & 1u));
+      }
+    }
+    if (COMPACT) {
+      const uint32_t nk = (uint32_t)keep[0] + (uint32_t)keep[1];
+      uint32_t tot;
+      const uint32_t off = block_excl_scan<BLOCK>(nk, s_scan, &tot);
+      if (threadIdx.x == 0) s_base = tot ? atomicAdd(&gctr[G_REMAIN], (unsigned long long)tot) : 0ull;
+      __syncthreads();
+      uint2* dst = out + s_base + off;
+      if (keep[0]) *dst++ = x[0];
+      if (keep[1]) *dst = x[1];
+      __syncthreads();
     }
   }
   found = warp_sum(found);
   if ((threadIdx.x & 31) == 0 && found) atomicAdd(&gctr[G_NEWVIS], (unsigned long long)found);
 }
-void launch_bfs_level(const uint2* edges, uint64_t m, const uint32_t* frontier, uint32_t* visited,
-                      uint32_t* next, uint64_t* gctr, cudaStream_t st) {
+// After a level: frontier bits <- next, visited bits already set by the claims.
+__global__ void k_bfs_advance(uint32_t* S, const uint32_t* __restrict__ next, uint64_t nw2) {
+  for (uint64_t w = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; w < nw2; w += (uint64_t)gridDim.x * BLOCK) {
+    const uint32_t nb = (next[w >> 1] >> (16 * (w & 1))) & 0xFFFFu;
+    // spread 16 bits to the odd positions of 32
+    uint32_t x = nb;
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    S[w] = (S[w] & 0x55555555u) | (x << 1);
+  }
+}
+void launch_bfs_level(bool root_level, bool compact, const uint2* edges, uint64_t m, uint32_t root,
+                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, cudaStream_t st) {
   if (!m) return;
-  k_bfs_level<<<grid_for((m >> 1) + 1, 148 * 16), BLOCK, 0, st>>>(
-      reinterpret_cast<const uint4*>(edges), m, frontier, visited, next,
-      reinterpret_cast<unsigned long long*>(gctr));
+  const unsigned g = grid_for((m + 1) / 2, 148 * 8);
+  auto* c = reinterpret_cast<unsigned long long*>(gctr);
+  if (root_level) k_bfs_level<true, false><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c);
+  else if (compact) k_bfs_level<false, true><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c);
+  else k_bfs_level<false, false><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c);
+}
+void launch_bfs_advance(uint32_t* S, const uint32_t* next, uint64_t n, cudaStream_t st) {
+  const uint64_t nw2 = (n + 15) / 16;
+  if (nw2) k_bfs_advance<<<grid_for(nw2, 148 * 8), BLOCK, 0, st>>>(S, next, nw2);
 }
 
 // Filter (Alg. 2 lines 10-11): E <- E \ {(u,v) | u in VI}.  Both arcs of
 // an edge are stored, so keeping edges with an unvisited first endpoint removes both
 // directions (C15).  Block-aggregated compaction.
 __global__ void __launch_bounds__(BLOCK) k_filter(const uint2* __restrict__ e, uint64_t m,
-                                                  const uint32_t* __restrict__ visited,
+                                                  const uint32_t* __restrict__ S,
                                                   uint2* __restrict__ out,
                                                   unsigned long long* gctr) {
   __shared__ uint32_t s_scan[BLOCK / 32 + 1];
@@ -166,7 +231,7 @@ __global__ void __launch_bounds__(BLOCK) k_filter(const uint2* __restrict__ e, u
     uint32_t keep = 0;
     if (i < m) {
       x = e[i];
-      keep = !bit(visited, x.x);
+      keep = !(st2(S, x.x) & 1u);
     }
     uint32_t tot;
     uint32_t off = block_excl_scan<BLOCK>(keep, s_scan, &tot);
@@ -176,12 +241,34 @@ __global__ void __launch_bounds__(BLOCK) k_filter(const uint2* __restrict__ e, u
     __syncthreads();
   }
 }
-void launch_filter(const uint2* edges, uint64_t m, const uint32_t* visited, uint2* out,
+void launch_filter(const uint2* edges, uint64_t m, const uint32_t* S, uint2* out,
                    uint64_t* gctr, cudaStream_t st) {
   if (!m) return;
-  k_filter<<<grid_for(m, 148 * 8), BLOCK, 0, st>>>(edges, m, visited, out,
+  k_filter<<<grid_for(m, 148 * 8), BLOCK, 0, st>>>(edges, m, S, out,
                                                      reinterpret_cast<unsigned long long*>(gctr));
 }
+
+// visited bitmap (1 bit per id) from the 2-bit state, for the SV presence test
+__global__ void k_vis_bits(const uint32_t* __restrict__ S, uint64_t nw, uint32_t* __restrict__ vis) {
+  for (uint64_t w = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * BLOCK) {
+    uint32_t lo = S[2 * w] & 0x55555555u, hi = S[2 * w + 1] & 0x55555555u;
+    // compress even bits to 16
+    auto pack = [](uint32_t x) {
+      x = (x | (x >> 1)) & 0x33333333u;
+      x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+      x = (x | (x >> 4)) & 0x00FF00FFu;
+      x = (x | (x >> 8)) & 0x0000FFFFu;
+      return x;
+    };
+    vis[w] = pack(lo) | (pack(hi) << 16);
+  }
+}
+void launch_vis_bits(const uint32_t* S, uint64_t n, uint32_t* vis, cudaStream_t st) {
+  const uint64_t nw = (n + 31) / 32;
+  if (nw) k_vis_bits<<<grid_for(nw, 148 * 8), BLOCK, 0, st>>>(S, nw, vis);
+}
+
+CC_DEVI bool bit(const uint32_t* bm, uint32_t v) { return (__ldg(&bm[v >> 5]) >> (v & 31)) & 1u; }
 
 // L_bfs = min id in VI: first set bit of the visited bitmap.
 __global__ void k_min_visited(const uint32_t* __restrict__ vis, uint64_t nwords,

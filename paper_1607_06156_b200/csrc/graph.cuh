@@ -21,14 +21,18 @@ enum GCtr : int {
 };
 
 void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr, cudaStream_t st);
-void launch_degree(const uint2* edges, uint64_t m, uint32_t* deg, cudaStream_t st);
+void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st);
 void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* tail,
                      uint64_t* gctr, cudaStream_t st);
-// edge-streaming bitmap BFS level; returns nothing, newly visited count in gctr[G_NEWVIS]
-void launch_bfs_level(const uint2* edges, uint64_t m, const uint32_t* frontier, uint32_t* visited,
-                      uint32_t* next, uint64_t* gctr, cudaStream_t st);
-void launch_filter(const uint2* edges, uint64_t m, const uint32_t* visited, uint2* out,
+// edge-streaming BFS level over 2-bit vertex state S (16 ids per word: bit0 visited, bit1
+// frontier); newly visited count in gctr[G_NEWVIS]; with `compact`, edges with an endpoint
+// unvisited at the start of the level are appended to `out` (count in gctr[G_REMAIN]).
+void launch_bfs_level(bool root_level, bool compact, const uint2* edges, uint64_t m, uint32_t root,
+                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, cudaStream_t st);
+void launch_bfs_advance(uint32_t* S, const uint32_t* next, uint64_t n, cudaStream_t st);
+void launch_filter(const uint2* edges, uint64_t m, const uint32_t* S, uint2* out,
                    uint64_t* gctr, cudaStream_t st);
+void launch_vis_bits(const uint32_t* S, uint64_t n, uint32_t* vis, cudaStream_t st);
 void launch_bfs_labels(const uint32_t* visited, uint64_t n, uint32_t* label, uint64_t* gctr,
                        cudaStream_t st);
 void launch_min_visited(const uint32_t* visited, uint64_t n, uint64_t* gctr, cudaStream_t st);

@@ -234,3 +234,20 @@ def test_device_input_and_output(cc):
     out = torch.empty(g.n, dtype=torch.int32, device="cuda")
     cc.labels(out)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+
+
+def test_config_c4_full(cc, request):
+    """C4 (R-MAT scale 26, 1.07 B edges) at full size through the BFS route: labels
+    bit-identical to union-find; the peeled component is exactly the root's component."""
+    if "csr" not in request.node.name:
+        pytest.skip("full-size C4 runs once, with the default engine")
+    g = graphgen.make("c4")
+    want = oracle.uf_labels(g.n, g.edges)
+    cc.load(g.edges, g.n)
+    rep = cc.run("auto")
+    lab = cc.labels()
+    assert rep["ran_bfs"] == 1
+    assert np.array_equal(lab, want)
+    root = rep["bfs_root"]
+    assert rep["bfs_visited"] == int(np.count_nonzero(want == want[root]))
+    assert rep["max_degree"] == int(np.bincount(g.edges.reshape(-1), minlength=g.n).max())
