@@ -129,6 +129,8 @@ cc_status cc_init(const cc_config* cfg, cc_ctx** out);
  *              u64: must be 0 (V = ids that appear in the edge list)
  *   pairs_on_device  nonzero if `pairs` is a device pointer
  * Ids >= n in u32 mode -> CC_ERR_RANGE (detected on device).  n > 2^30 -> CC_ERR_INVALID.
+ * u64 mode: cc_run first relabels the ids to dense [0, |V|) in id order (Alg. 2 line 4,
+ * PAPER.md:260, :277; timed as ms_relabel); more than 2^30 distinct ids -> CC_ERR_INVALID.
  * Replaces any previously loaded graph. */
 cc_status cc_load_edges(cc_ctx* ctx, cc_idw w, const void* pairs, uint64_t m_local,
                         uint64_t n_vertices, int pairs_on_device);
@@ -142,7 +144,9 @@ cc_status cc_run(cc_ctx* ctx, cc_mode mode, cc_report* out);
 cc_status cc_labels_u32(cc_ctx* ctx, uint32_t* out, uint64_t cap, uint64_t* count,
                         int out_on_device);
 
-/* u64 mode: the distinct ids (ascending) and the label (an id) of each. */
+/* u64 mode: the distinct ids (ascending) into `ids` and the label of each (the minimum id
+ * of its component) into `labels`; both have room for `cap` entries, *count receives the
+ * number of distinct ids.  CC_ERR_STATE on a u32 graph (and cc_labels_u32 on a u64 one). */
 cc_status cc_labels_u64(cc_ctx* ctx, uint64_t* ids, uint64_t* labels, uint64_t cap,
                         uint64_t* count, int out_on_device);
 

@@ -202,6 +202,18 @@ def cc_labels_u32(ctx, out=None):
     return out
 
 
+def cc_labels_u64(ctx):
+    """u64 mode: (sorted distinct ids, label of each) as numpy uint64 arrays."""
+    cnt = ctypes.c_uint64()
+    lib().cc_labels_u64(ctx, None, None, 0, ctypes.byref(cnt), 0)  # query count
+    n = cnt.value
+    ids = np.empty(n, dtype=np.uint64)
+    lab = np.empty(n, dtype=np.uint64)
+    _check(ctx, lib().cc_labels_u64(ctx, ids.ctypes.data_as(ctypes.c_void_p),
+                                    lab.ctypes.data_as(ctypes.c_void_p), n, ctypes.byref(cnt), 0))
+    return ids, lab
+
+
 def cc_kernel_stats(ctx, which):
     ms, by, ln = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
     _check(ctx, lib().cc_kernel_stats(ctx, which, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(ln)))
@@ -237,6 +249,9 @@ class CC:
 
     def labels(self, out=None):
         return cc_labels_u32(self.ctx, out)
+
+    def labels_u64(self):
+        return cc_labels_u64(self.ctx)
 
     def launches(self):
         return int(lib().cc_last_launch_count(self.ctx))

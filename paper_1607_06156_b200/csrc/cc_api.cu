@@ -24,6 +24,7 @@
 #include "radix.cuh"
 #include "sv.cuh"
 #include "csr.cuh"
+#include "relabel.cuh"
 
 using namespace cc;
 
@@ -41,6 +42,9 @@ struct cc_ctx {
   uint2* d_edges = nullptr;
   uint2* d_rem = nullptr;
   uint2* d_rem2 = nullptr;
+  uint64_t* d_ids64 = nullptr;  // u64 mode: loaded endpoints (2m)
+  uint64_t* d_uids = nullptr;   // u64 mode: sorted distinct ids (rank -> id)
+  uint64_t n_alloc = 0;         // id bound the n-sized buffers were sized for
   uint32_t* d_label = nullptr;
   uint32_t* d_deg = nullptr;
   uint32_t* d_hist = nullptr;
@@ -133,6 +137,7 @@ static void dfree_all(cc_ctx* c) {
   }
   c->allocs.clear();
   c->d_edges = c->d_rem = c->d_rem2 = nullptr;
+  c->d_ids64 = c->d_uids = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
   c->d_bm[0] = c->d_bm[1] = c->d_bm[2] = nullptr;
   c->d_sbm[0] = c->d_sbm[1] = c->d_sbm[2] = nullptr;
@@ -257,7 +262,11 @@ cc_status cc_destroy(cc_ctx* c) {
 cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint64_t n, int on_dev) {
   if (!c) return CC_ERR_INVALID;
   if (m && !pairs) return fail(c, CC_ERR_INVALID, "pairs is NULL");
-  if (w != CC_U32) return fail(c, CC_ERR_INVALID, "u64 ids are not supported by this build");
+  if (w != CC_U32 && w != CC_U64) return fail(c, CC_ERR_INVALID, "bad id width %d", (int)w);
+  if (w == CC_U64) {
+    if (n != 0) return fail(c, CC_ERR_INVALID, "u64 ids: n_vertices must be 0");
+    n = std::min<uint64_t>(2 * m, 1ull << 30);  // bound on distinct ids (checked in cc_run)
+  }
   if (n > (1ull << 30)) return fail(c, CC_ERR_INVALID, "n_vertices %llu > 2^30", (unsigned long long)n);
   if (2 * m + 2 * n >= (1ull << 32))
     return fail(c, CC_ERR_INVALID, "tuple count 2m+2n exceeds 2^32 on one GPU");
@@ -266,6 +275,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   c->loaded = c->ran = false;
   c->idw = w;
   c->n = n;
+  c->n_alloc = n;
   c->m = m;
   c->kbits = bits_for(n);
   const uint64_t nw = (n + 31) / 32 + 1;
@@ -285,6 +295,10 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->d_segB, n + 1));
   TRY(dalloc_t(c, &c->d_ctr, sv::C_NUM));
   TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM + 512 + 1024 + 8));  // + CSR group scratch
+  if (w == CC_U64) {
+    TRY(dalloc_t(c, &c->d_ids64, 2 * m + 1));
+    TRY(dalloc_t(c, &c->d_uids, 2 * m + 1));
+  }
   c->rws.max_tiles = c->cap / radix::TILE + 2;
   TRY(dalloc_t(c, &c->rws.ghist, radix::MAX_PASSES * radix::RADIX));
   TRY(dalloc_t(c, &c->rws.lookback, c->rws.max_tiles * radix::RADIX));
@@ -294,6 +308,14 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->ss.ticket, 4));
   CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * c->ss.max_tiles, c->st));
   CK(cudaMemsetAsync(c->rws.lookback, 0, sizeof(uint64_t) * c->rws.max_tiles * radix::RADIX, c->st));
+  if (w == CC_U64) {
+    if (m)
+      CK(cudaMemcpyAsync(c->d_ids64, pairs, 2 * m * sizeof(uint64_t),
+                         on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->loaded = true;
+    return CC_OK;
+  }
   if (m)
     CK(cudaMemcpyAsync(c->d_edges, pairs, m * sizeof(uint2),
                        on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
@@ -654,11 +676,30 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   for (auto& k : c->kst) k = cc_ctx::KStat();
   cc_report& R = c->rep;
   R = cc_report{};
-  const uint64_t n = c->n, m = c->m;
+  const uint64_t m = c->m;
   R.m_edges = m;
 
-  cudaEvent_t e0 = ev_get(c), e_pred, e_bfs, e_filter, e_sv, e_end;
+  cudaEvent_t e0 = ev_get(c), e_rel, e_pred, e_bfs, e_filter, e_sv, e_end;
   CK(cudaEventRecord(e0, c->st));
+  // ------------------------------------------------ relabel (Alg. 2 line 4; u64 ids only)
+  // ids are made dense first: every later stage addresses buckets by id (R18)
+  if (c->idw == CC_U64) {
+    TRY(scan_epoch_guard(c));
+    uint64_t* total = c->d_gctr + graph::G_NUM + 1537;
+    uint32_t* vals[2] = {c->d_q[0], c->d_q[1]};
+    relabel::run(c->d_ids64, 2 * m, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges),
+                 c->d_uids, total, c->st, &c->launches);
+    CKL();
+    CK(cudaMemcpyAsync(c->h_word, total, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    uint64_t nd = m ? *reinterpret_cast<uint64_t*>(c->h_word) : 0;
+    if (nd > (1ull << 30)) return fail(c, CC_ERR_INVALID, "%llu distinct ids > 2^30", (unsigned long long)nd);
+    c->n = nd;
+    c->kbits = bits_for(nd);
+  }
+  const uint64_t n = c->n;
+  e_rel = ev_get(c);
+  CK(cudaEventRecord(e_rel, c->st));
   // ------------------------------------------------ prediction (Alg. 2 lines 2-3)
   CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
   CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
@@ -803,7 +844,8 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
 
   // ------------------------------------------------ report
   R.ms_total = ev_ms(e0, e_end);
-  R.ms_prediction = ev_ms(e0, e_pred);
+  R.ms_relabel = ev_ms(e0, e_rel);
+  R.ms_prediction = ev_ms(e_rel, e_pred);
   R.ms_bfs = run_bfs ? ev_ms(e_pred, e_bfs) : 0;
   R.ms_filter = run_bfs ? ev_ms(e_bfs, e_filter) : 0;
   R.ms_sv = ev_ms(e_filter, e_sv);
@@ -826,6 +868,7 @@ extern "C" cc_status cc_labels_u32(cc_ctx* c, uint32_t* out, uint64_t cap, uint6
                                    int out_on_device) {
   if (!c) return CC_ERR_INVALID;
   if (!c->ran) return fail(c, CC_ERR_STATE, "cc_labels before cc_run");
+  if (c->idw != CC_U32) return fail(c, CC_ERR_STATE, "u64 graph loaded: use cc_labels_u64");
   if (count) *count = c->n;
   if (!out || cap < c->n) return fail(c, CC_ERR_INVALID, "output buffer too small");
   CK(cudaSetDevice(c->cfg.device));
@@ -838,9 +881,22 @@ extern "C" cc_status cc_labels_u32(cc_ctx* c, uint32_t* out, uint64_t cap, uint6
 
 extern "C" cc_status cc_labels_u64(cc_ctx* c, uint64_t* ids, uint64_t* labels, uint64_t cap,
                                    uint64_t* count, int out_on_device) {
-  (void)ids; (void)labels; (void)cap; (void)count; (void)out_on_device;
   if (!c) return CC_ERR_INVALID;
-  return fail(c, CC_ERR_STATE, "no u64 graph loaded");
+  if (!c->ran) return fail(c, CC_ERR_STATE, "cc_labels before cc_run");
+  if (c->idw != CC_U64) return fail(c, CC_ERR_STATE, "u32 graph loaded: use cc_labels_u32");
+  if (count) *count = c->n;
+  if (!ids || !labels || cap < c->n) return fail(c, CC_ERR_INVALID, "output buffers too small");
+  CK(cudaSetDevice(c->cfg.device));
+  if (c->n) {
+    uint64_t* tmp = c->d_w[0];  // SV state is finished; reuse as label staging
+    relabel::labels(c->d_uids, c->d_label, c->n, tmp, c->st);
+    CKL();
+    const cudaMemcpyKind k = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(cudaMemcpyAsync(ids, c->d_uids, sizeof(uint64_t) * c->n, k, c->st));
+    CK(cudaMemcpyAsync(labels, tmp, sizeof(uint64_t) * c->n, k, c->st));
+  }
+  CK(cudaStreamSynchronize(c->st));
+  return CC_OK;
 }
 
 extern "C" cc_status cc_labels_device(cc_ctx* c, const uint32_t** labels, uint64_t* count) {

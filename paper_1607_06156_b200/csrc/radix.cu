@@ -14,7 +14,8 @@ int num_passes(int kbits) { return kbits <= 0 ? 0 : (kbits + RADIX_BITS - 1) / R
 // partition of late SV iterations) does not serialise on one shared-memory bank.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(BLOCK) k_hist(const uint64_t* __restrict__ keys, uint64_t n,
-                                                int passes, uint64_t* __restrict__ ghist) {
+                                                int passes, int base_bit,
+                                                uint64_t* __restrict__ ghist) {
   __shared__ uint32_t sh[MAX_PASSES][RADIX];
   for (int i = threadIdx.x; i < MAX_PASSES * RADIX; i += BLOCK) (&sh[0][0])[i] = 0;
   __syncthreads();
@@ -23,9 +24,10 @@ __global__ void __launch_bounds__(BLOCK) k_hist(const uint64_t* __restrict__ key
   for (uint64_t base = (uint64_t)blockIdx.x * BLOCK; base < n; base += stride) {
     uint64_t i = base + threadIdx.x;
     bool valid = i < n;
-    uint32_t key = valid ? hi32(keys[i]) : 0u;
+    const uint64_t key = valid ? keys[i] : 0ull;
     for (int p = 0; p < passes; p++) {
-      uint32_t d = valid ? ((key >> (p * RADIX_BITS)) & (RADIX - 1)) : (RADIX + lane_id());
+      uint32_t d = valid ? (uint32_t)((key >> (base_bit + p * RADIX_BITS)) & (RADIX - 1))
+                         : (RADIX + lane_id());
       uint32_t peers = __match_any_sync(0xffffffffu, d);
       if (valid && (peers & lt) == 0) atomicAdd(&sh[p][d], (uint32_t)__popc(peers));
     }
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_onesweep(const uint64_t* __restric
   for (int k = 0; k < ITEMS; k++) {
     uint64_t i = wbase + (uint64_t)k * 32;
     bool valid = i < n;
-    uint32_t d = valid ? ((hi32(key[k]) >> shift) & (RADIX - 1)) : (RADIX + lane);
+    uint32_t d = valid ? ((uint32_t)(key[k] >> shift) & (RADIX - 1)) : (RADIX + lane);
     uint32_t peers = __match_any_sync(0xffffffffu, d);
     uint32_t before = 0;
     if (valid) before = s_wcnt[wid][d];
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_onesweep(const uint64_t* __restric
   for (int k = 0; k < ITEMS; k++) {
     uint64_t i = wbase + (uint64_t)k * 32;
     if (i < n) {
-      uint32_t dg = (hi32(key[k]) >> shift) & (RADIX - 1);
+      uint32_t dg = (uint32_t)(key[k] >> shift) & (RADIX - 1);
       uint32_t lp = s_dstart[dg] + s_wcnt[wid][dg] + rank[k];
       s_keys[lp] = key[k];
       if (HAS_VAL) s_vals[lp] = val[k];
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_onesweep(const uint64_t* __restric
   const uint32_t tn = (n - tbase < (uint64_t)TILE) ? (uint32_t)(n - tbase) : (uint32_t)TILE;
   for (uint32_t i = tid; i < tn; i += BLOCK) {
     uint64_t kk = s_keys[i];
-    uint32_t dg = (hi32(kk) >> shift) & (RADIX - 1);
+    uint32_t dg = (uint32_t)(kk >> shift) & (RADIX - 1);
     uint64_t pos = s_gbase[dg] + i;
     kout[pos] = kk;
     if (HAS_VAL) vout[pos] = s_vals[i];
@@ -158,7 +160,7 @@ size_t smem_bytes(bool has_val) {
 }
 
 int sort_pairs(Workspace& ws, uint64_t* k[2], uint32_t* v[2], int cur, uint64_t n, int kbits,
-               bool has_val, cudaStream_t st, uint64_t* launches) {
+               bool has_val, cudaStream_t st, uint64_t* launches, int base_bit) {
   const int passes = num_passes(kbits);
   if (n <= 1 || passes == 0) return cur;
   static bool attr_set = false;
@@ -173,7 +175,7 @@ int sort_pairs(Workspace& ws, uint64_t* k[2], uint32_t* v[2], int cur, uint64_t 
   cudaMemsetAsync(ws.tile_ctr, 0, sizeof(uint32_t) * MAX_PASSES, st);
   const uint64_t tiles = (n + TILE - 1) / TILE;
   int hblocks = (int)std::min<uint64_t>((n + BLOCK - 1) / BLOCK, 148 * 8);
-  k_hist<<<hblocks, BLOCK, 0, st>>>(k[cur], n, passes, ws.ghist);
+  k_hist<<<hblocks, BLOCK, 0, st>>>(k[cur], n, passes, base_bit, ws.ghist);
   *launches += 1;
   for (int p = 0; p < passes; p++) {
     uint32_t epoch = ++ws.epoch;
@@ -183,11 +185,11 @@ int sort_pairs(Workspace& ws, uint64_t* k[2], uint32_t* v[2], int cur, uint64_t 
     }
     if (has_val)
       k_onesweep<true><<<(unsigned)tiles, BLOCK, smem_bytes(true), st>>>(
-          k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, p * RADIX_BITS, ws.ghist + p * RADIX,
+          k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, base_bit + p * RADIX_BITS, ws.ghist + p * RADIX,
           ws.lookback, ws.tile_ctr + p, epoch);
     else
       k_onesweep<false><<<(unsigned)tiles, BLOCK, smem_bytes(false), st>>>(
-          k[cur], nullptr, k[cur ^ 1], nullptr, n, p * RADIX_BITS, ws.ghist + p * RADIX,
+          k[cur], nullptr, k[cur ^ 1], nullptr, n, base_bit + p * RADIX_BITS, ws.ghist + p * RADIX,
           ws.lookback, ws.tile_ctr + p, epoch);
     *launches += 1;
     cur ^= 1;

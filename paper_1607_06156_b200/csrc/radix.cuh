@@ -27,7 +27,7 @@ constexpr int WARPS = BLOCK / 32;
 constexpr int ITEMS = 16;
 constexpr int WARP_ITEMS = 32 * ITEMS;
 constexpr int TILE = BLOCK * ITEMS;  // 4096 elements
-constexpr int MAX_PASSES = 4;        // keys are < 2^30
+constexpr int MAX_PASSES = 8;        // up to 64-bit keys (u64 relabel)
 
 constexpr uint64_t LB_AGG = 1ull << 62;
 constexpr uint64_t LB_INC = 2ull << 62;
@@ -44,10 +44,12 @@ struct Workspace {
   uint32_t epoch = 0;
 };
 
-// Sort `n` elements by key bits [32, 32+kbits) of k[cur] (with u32 payload v[cur] when
-// has_val).  Ping-pongs between buffer 0 and 1; returns the index holding the result.
+// Sort `n` elements by bits [base_bit, base_bit+kbits) of the 64-bit words k[cur] (with u32
+// payload v[cur] when has_val).  Tuple words keep their key in the high half (base_bit 32);
+// u64 ids use the whole word (base_bit 0, kbits 64).  Ping-pongs between buffer 0 and 1;
+// returns the index holding the result.
 int sort_pairs(Workspace& ws, uint64_t* k[2], uint32_t* v[2], int cur, uint64_t n, int kbits,
-               bool has_val, cudaStream_t st, uint64_t* launches);
+               bool has_val, cudaStream_t st, uint64_t* launches, int base_bit = 32);
 
 size_t smem_bytes(bool has_val);
 int num_passes(int kbits);

@@ -1,0 +1,21 @@
+// relabel.cuh -- u64 -> dense u32 relabel (Alg. 2 line 4) launchers.
+#pragma once
+#include "radix.cuh"
+#include "scan.cuh"
+
+namespace cc {
+namespace relabel {
+
+typedef int cc_status_t;
+
+// ids: k = 2m endpoints (device).  Sorts (id, position) with the onesweep radix sort in
+// keys/vals (two buffers each of k), writes dense[position] = rank of the id among the
+// distinct ids and uids[rank] = id; *total (device u64) = number of distinct ids.
+cc_status_t run(const uint64_t* ids, uint64_t k, uint64_t* keys[2], uint32_t* vals[2],
+                radix::Workspace& rws, scan::State& ss, uint32_t* dense, uint64_t* uids,
+                uint64_t* total, cudaStream_t st, uint64_t* launches);
+// out[i] = uids[label[i]] for the n dense ids
+void labels(const uint64_t* uids, const uint32_t* label, uint64_t n, uint64_t* out, cudaStream_t st);
+
+}  // namespace relabel
+}  // namespace cc

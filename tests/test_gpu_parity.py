@@ -251,3 +251,42 @@ def test_config_c4_full(cc, request):
     root = rep["bfs_root"]
     assert rep["bfs_visited"] == int(np.count_nonzero(want == want[root]))
     assert rep["max_degree"] == int(np.bincount(g.edges.reshape(-1), minlength=g.n).max())
+
+
+# ------------------------------------------------------------------ u64 ids (relabel)
+def _u64_graph(seed, nv, m):
+    rng = np.random.default_rng(seed)
+    table = np.unique(rng.integers(0, 2**64 - 1, size=nv, dtype=np.uint64, endpoint=True))
+    table = np.concatenate([table, np.array([0, 2**64 - 1], dtype=np.uint64)])
+    idx = rng.integers(0, table.shape[0], size=(m, 2))
+    return table[idx]
+
+
+@pytest.mark.parametrize("seed,nv,m", [(1, 50, 40), (2, 3000, 5000), (3, 200000, 300000)])
+def test_u64_ids(cc, seed, nv, m):
+    """u64 ids are relabelled in id order (Alg. 2 line 4): labels are the min original id
+    of each component, bit-identical to the oracle; the SV trace runs on the dense ids."""
+    e = _u64_graph(seed, nv, m)
+    ids_o, lab_o = oracle.uf_labels_u64(e)
+    cc.load(e, 0, ids="u64")
+    rep = cc.run("sv")
+    ids, lab = cc.labels_u64()
+    assert np.array_equal(ids, ids_o)
+    assert np.array_equal(lab, lab_o)
+    dense, uniq = oracle.relabel_u64(e)
+    _, tr = osv.sv_trace(uniq.shape[0], dense)
+    assert norm(trace_of(rep)) == norm(tr)
+    rep = cc.run("auto")
+    ids, lab = cc.labels_u64()
+    assert np.array_equal(lab, lab_o)
+
+
+def test_u64_mode_errors(cc):
+    import paper_1607_06156_b200 as ccmod
+    e = _u64_graph(9, 10, 5)
+    cc.load(e, 0, ids="u64")
+    cc.run("auto")
+    with pytest.raises(ccmod.CCError):
+        cc.labels()  # u32 labels of a u64 graph
+    with pytest.raises(ccmod.CCError):
+        cc.load(e, 7, ids="u64")  # n_vertices must be 0
