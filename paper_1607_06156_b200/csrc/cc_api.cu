@@ -56,6 +56,11 @@ struct cc_ctx {
   uint64_t cap = 0;
   uint32_t* d_segA = nullptr;
   uint32_t* d_segB = nullptr;
+  uint64_t* d_umin = nullptr;  // csr engine: tagged partial row minima / maxima
+  uint64_t* d_umax = nullptr;
+  csr::LongSeg* d_lsegs = nullptr;  // csr engine: segments of rows longer than csr::LONG
+  uint64_t* d_nlsegs = nullptr;
+  uint32_t row_tag = 0;
   uint64_t* d_ctr = nullptr;   // sv counters
   uint64_t* d_gctr = nullptr;  // graph counters
   uint64_t* h_ctr = nullptr;   // pinned mirrors
@@ -139,6 +144,9 @@ static void dfree_all(cc_ctx* c) {
   c->d_edges = c->d_rem = c->d_rem2 = nullptr;
   c->d_ids64 = c->d_uids = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
+  c->d_umin = c->d_umax = c->d_nlsegs = nullptr;
+  c->d_lsegs = nullptr;
+  c->row_tag = 0;
   c->d_bm[0] = c->d_bm[1] = c->d_bm[2] = nullptr;
   c->d_sbm[0] = c->d_sbm[1] = c->d_sbm[2] = nullptr;
   c->d_w[0] = c->d_w[1] = nullptr;
@@ -165,13 +173,14 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 static bool profiling(const cc_ctx* c) { return (c->cfg.flags & CC_FLAG_PROFILE) != 0; }
 
 // kernel families timed under CC_FLAG_PROFILE (cc_kernel_stats / cc_kernel_name)
-enum KFam { KF_RADIX = 0, KF_SVITER, KF_BFS, KF_PPASS, KF_PAPPLY, KF_VPASS, KF_CSR, KF_PREDICT,
-            KF_N };
+enum KFam { KF_RADIX = 0, KF_SVITER, KF_BFS, KF_ROWA, KF_ROWB, KF_SLOTS, KF_CSR, KF_PREDICT,
+            KF_COMPACT, KF_N };
 static const char* const kKfNames[KF_N] = {
     "k_hist+k_onesweep (radix regroup)", "SV iteration (all bucket passes)", "k_bfs_level",
-    "k_ppass (partition-bucket minima)", "k_papply1/2 (partition update + compaction)",
-    "k_vpass (vertex-bucket minima)", "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)",
-    "prediction (k_degree, k_deg_hist)"};
+    "k_rowpass<A>+k_rowfix (Alg.1 lines 8-16)", "k_rowpass<B>+k_rowfix (Alg.1 lines 17-25)",
+    "k_pstat1/k_temps2/k_pstat2 (partition slot scans)",
+    "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)", "prediction (k_degree, k_deg_hist)",
+    "k_compact (ordered exclusion of completed rows)"};
 
 struct Prof {
   cc_ctx* c;
@@ -286,13 +295,19 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->d_hist, graph::HIST_DENSE));
   TRY(dalloc_t(c, &c->d_tail, graph::TAIL_CAP));
   for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], 2 * nw));  // 2-bit BFS state fits
-  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_sbm[i], nw));
+  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_sbm[i], nw + 2));
   for (int i = 0; i < 2; i++) {
     TRY(dalloc_t(c, &c->d_w[i], c->cap));
     TRY(dalloc_t(c, &c->d_q[i], c->cap));
   }
-  TRY(dalloc_t(c, &c->d_segA, n + 1));
-  TRY(dalloc_t(c, &c->d_segB, n + 1));
+  TRY(dalloc_t(c, &c->d_segA, n + 64));  // padded: the slot scans read 4 slots per thread
+  TRY(dalloc_t(c, &c->d_segB, n + 64));
+  TRY(dalloc_t(c, &c->d_umin, n + 1));
+  TRY(dalloc_t(c, &c->d_umax, n + 1));
+  TRY(dalloc_t(c, &c->d_lsegs, csr::long_seg_cap(c->cap)));
+  TRY(dalloc_t(c, &c->d_nlsegs, 2));
+  CK(cudaMemsetAsync(c->d_umin, 0xFF, sizeof(uint64_t) * (n + 1), c->st));
+  CK(cudaMemsetAsync(c->d_umax, 0, sizeof(uint64_t) * (n + 1), c->st));
   TRY(dalloc_t(c, &c->d_ctr, sv::C_NUM));
   TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM + 512 + 1024 + 8));  // + CSR group scratch
   if (w == CC_U64) {
@@ -466,8 +481,6 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
   uint32_t* R[2] = {reinterpret_cast<uint32_t*>(c->d_w[0]), reinterpret_cast<uint32_t*>(c->d_w[1])};
   uint32_t* P[2] = {R[0] + c->cap, R[1] + c->cap};
   uint32_t *off = c->d_q[0], *cur = c->d_q[1];
-  uint32_t *U = c->d_segA, *PMIN = c->d_segB;
-  uint32_t *NP = c->d_sbm[0], *NCP = c->d_sbm[1], *TB = c->d_sbm[2];
   CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
   cudaEvent_t a = nullptr;
   seg_begin(c, &a);
@@ -493,29 +506,49 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
   int cb = 0;           // buffer holding the tuple array
   uint64_t len = A;     // physical length (live + dead rows)
   const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
-  uint64_t chg2_prev = 0;
+  // slot arrays: PA (pass A minima), PB (pass B minima), NCP / TB bitmaps.  The slot scans
+  // clear what the next pass needs, so these are the only full clears of the run.
+  uint32_t *PA = c->d_segA, *PB = c->d_segB, *NCP = c->d_sbm[1], *TB = c->d_sbm[2];
+  // P is double-buffered across passes: the P half of the current tuple buffer and the
+  // (free after the CSR build) offsets array
+  uint32_t *Pc = P[0], *Palt = c->d_q[0];
+  // rows longer than csr::LONG exist only if some degree reaches LONG
+  const bool have_long = c->rep.max_degree + 1 > csr::LONG;
+  if (have_long) csr::longlist(R[0], P[0], len, c->d_deg, c->d_lsegs, c->d_nlsegs, c->st);
+  const uint64_t n4 = (n + 3) / 4 * 4;
+  CK(cudaMemsetAsync(PA, 0xFF, sizeof(uint32_t) * n4, c->st));
+  CK(cudaMemsetAsync(PB, 0xFF, sizeof(uint32_t) * n4, c->st));
+  CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * (nw + 2), c->st));
+  CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * (nw + 2), c->st));
   for (uint32_t it = 0;; it++) {
     if (it >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
     cudaEvent_t ev_it = ev_get(c);
     CK(cudaEventRecord(ev_it, c->st));
     seg_begin(c, &a);
-    uint32_t *Rc = R[cb], *Pc = P[cb];
-    // ---- lines 8-13: vertex buckets are CSR rows; u_min and 'potentially completed'
-    CK(cudaMemsetAsync(U, 0xFF, sizeof(uint32_t) * n, c->st));
-    CK(cudaMemsetAsync(NP, 0, sizeof(uint32_t) * nw, c->st));
-    { Prof k(c, KF_VPASS); csr::vpass(true, Rc, Pc, len, U, NP, c->st); k.end(8.0 * len + 4.0 * n, 1); }
-    // ---- lines 14-21: p_min per partition bucket; completion
-    CK(cudaMemsetAsync(PMIN, 0xFF, sizeof(uint32_t) * n, c->st));
-    CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nw, c->st));
-    CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nw, c->st));
-    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_TEMPS + 1), c->st));
-    { Prof k(c, KF_PPASS); csr::ppass(true, Rc, Pc, len, U, NP, nullptr, PMIN, NCP, c->st);
-      k.end(8.0 * len + 8.0 * n, 1); }
-    // ---- line 22 (temporaries) + counters; exclusion of completed partitions (in place)
-    csr::pscan(true, PMIN, NCP, n, TB, c->d_ctr, c->st);
-    { Prof k(c, KF_PAPPLY); csr::papply1(Rc, Pc, len, PMIN, NCP, c->d_label, c->d_ctr, c->st);
-      k.end(8.0 * len + 4.0 * n, 1); }
-    c->launches += 4;
+    uint32_t* Rc = R[cb];
+    // few partitions per live tuple: slot updates repeat, filter them through the block caches
+    const bool hot = it > 0 && c->iters.back().partitions * 16 < len;
+    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_CHANGED2 + 1), c->st));
+    // ---- lines 8-16 (+ line 25 relabel of the previous iteration)
+    { Prof k(c, KF_ROWA);
+      csr::rowpass(true, Rc, Pc, it ? Palt : nullptr, len, it ? PB : nullptr, nullptr, nullptr, PA,
+                   NCP, c->d_label, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs,
+                   have_long, hot, c->d_ctr, c->st);
+      k.end(8.0 * len + (it ? 4.0 * len : 0.0), 2); }
+    if (it) std::swap(Pc, Palt);
+    // ---- line 22 bookkeeping: |P_i|, completed, changed, temporaries
+    { Prof k(c, KF_SLOTS); csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st); k.end(8.0 * n4, 1); }
+    // ---- lines 17-21 (exclusion, p <- p_min), line 24 (+ temporaries), line 25 minima
+    { Prof k(c, KF_ROWB);
+      csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
+                   c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, hot, c->d_ctr, c->st);
+      k.end(12.0 * len, 2); }
+    std::swap(Pc, Palt);
+    { Prof k(c, KF_SLOTS);
+      csr::temps2(TB, n, PB, c->st);
+      csr::pstat2(PB, n, PA, NCP, TB, c->d_ctr, c->st);
+      k.end(8.0 * n4, 2); }
+    c->launches += 8;
     CKL();
     TRY(sync_read(c));
     const uint64_t A1 = c->h_ctr[sv::C_OUT];
@@ -525,45 +558,26 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
     s.completed = c->h_ctr[sv::C_COMPLETED];
     s.changed = c->h_ctr[sv::C_CHANGED];
     s.temps = c->h_ctr[sv::C_TEMPS];
-    if (!c->iters.empty()) {
-      c->iters.back().changed2 = c->h_ctr[sv::C_CHANGED2] - chg2_prev;
-      chg2_prev = c->h_ctr[sv::C_CHANGED2];
-    }
+    s.changed2 = c->h_ctr[sv::C_CHANGED2];
     c->iters.push_back(s);
     c->it_ev.push_back(ev_it);
-    if (A1 == 0) {
-      seg_end(c, a, 24.0 * len, 4);
-      break;
-    }
+    seg_end(c, a, 20.0 * len + 16.0 * n4, 8);
+    if (A1 == 0) break;
     // dead rows of completed partitions are squeezed out once they are a third of the array
     // (the paper's 'swapped to the end of the local array', sec:distSVOpt1)
     if (3 * (len - A1) > len) {
       TRY(scan_epoch_guard(c));
-      { Prof k(c, KF_PAPPLY); csr::compact(Rc, Pc, len, R[cb ^ 1], P[cb ^ 1], c->ss, c->st);
+      { Prof k(c, KF_COMPACT); csr::compact(Rc, Pc, len, R[cb ^ 1], P[cb ^ 1], c->ss, c->st);
         k.end(8.0 * len + 8.0 * A1, 1); }
       c->launches += 1;
       cb ^= 1;
       len = A1;
-      Rc = R[cb];
       Pc = P[cb];
+      Palt = c->d_q[0];
+      if (have_long) csr::longlist(R[cb], Pc, len, c->d_deg, c->d_lsegs, c->d_nlsegs, c->st);
     }
-    // ---- line 24: vertex buckets again, temporaries <u,_,u> from the TB bitmap
-    CK(cudaMemsetAsync(U, 0xFF, sizeof(uint32_t) * n, c->st));
-    { Prof k(c, KF_VPASS); csr::vpass(false, Rc, Pc, len, U, nullptr, c->st); k.end(8.0 * len + 4.0 * n, 1); }
-    // ---- line 25: partition buckets again (+ temporaries), p <- p_min in place
-    CK(cudaMemsetAsync(PMIN, 0xFF, sizeof(uint32_t) * n, c->st));
-    { Prof k(c, KF_PPASS); csr::ppass(false, Rc, Pc, len, U, nullptr, TB, PMIN, nullptr, c->st);
-      k.end(8.0 * len + 8.0 * n, 1); }
-    csr::temps(TB, n, U, PMIN, c->st);
-    csr::pscan(false, PMIN, nullptr, n, nullptr, c->d_ctr, c->st);
-    { Prof k(c, KF_PAPPLY); csr::papply2(Pc, len, PMIN, c->st); k.end(8.0 * len + 4.0 * n, 1); }
-    c->launches += 5;
-    CKL();
-    seg_end(c, a, 8.0 * len * 6, 9);
     A = A1;
   }
-  TRY(sync_read(c));
-  if (!c->iters.empty()) c->iters.back().changed2 = c->h_ctr[sv::C_CHANGED2] - chg2_prev;
   return CC_OK;
 }
 

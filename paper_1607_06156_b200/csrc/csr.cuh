@@ -15,20 +15,41 @@ void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* 
 void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
           uint32_t* R, uint32_t* P, const uint32_t* garc, int gshift, uint64_t* gcur, uint2* tmp,
           uint32_t* longlist, uint64_t* nlong, cudaStream_t st);
-void vpass(bool with_pc, const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* U, uint32_t* NP,
-           cudaStream_t st);
-void ppass(bool first, const uint32_t* R, const uint32_t* P, uint64_t A, const uint32_t* U,
-           const uint32_t* NP, const uint32_t* TB, uint32_t* PMIN, uint32_t* NCP, cudaStream_t st);
-void temps(const uint32_t* TB, uint64_t n, const uint32_t* U, uint32_t* PMIN, cudaStream_t st);
-void pscan(bool first, const uint32_t* PMIN, const uint32_t* NCP, uint64_t n, uint32_t* TB,
-           uint64_t* ctr, cudaStream_t st);
-// in place: completed partitions' tuples become DEAD, survivors p <- p_min; ctr[C_OUT] += live
-void papply1(const uint32_t* R, uint32_t* P, uint64_t A, const uint32_t* PMIN, const uint32_t* NCP,
-             uint32_t* label, uint64_t* ctr, cudaStream_t st);
+// Row passes (sv_rows.cu).  Rows longer than LONG tuples (R_LONG set in R) are handled as
+// segments of at most LSEG tuples by warps (k_long1/k_long2); the segment list is rebuilt
+// after each compaction.
+constexpr uint32_t LONG = 256;
+constexpr uint32_t LSEG = 1024;
+constexpr uint32_t R_LONG = 0x80000000u;  // flag in R of the tuples of long rows (ids < 2^30)
+struct LongSeg {
+  uint64_t start;
+  uint32_t u, len;
+};
+uint64_t row_tiles(uint64_t L);
+uint64_t long_seg_cap(uint64_t L);
+void longlist(const uint32_t* R, const uint32_t* P, uint64_t L, const uint32_t* deg, LongSeg* segs,
+              uint64_t* nsegs, cudaStream_t st);
+// P is read from Pin and the relabelled values written to Pout (NULL: pass A without MAP).
+// pass A (MAP = PB of the previous iteration or NULL; OUT = PA; NCPw = NCP) or pass B
+// (MAP = PA, NCPr = NCP, TB; OUT = PB; label; ctr[C_OUT] += live tuples).  `tag` must
+// increase with every call (tagged long-row partial slots UMIN/UMAX).  `hot`: few distinct
+// partitions per tuple, filter slot updates through the block's cache.
+void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L,
+             const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
+             uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
+             const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
+             cudaStream_t st);
+// partition statistics after pass A (sets TB, clears PB); slot arrays padded to 4*ceil(n/4)
+void pstat1(const uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
+            uint64_t* ctr, cudaStream_t st);
+// temporaries' own contribution to PB
+void temps2(const uint32_t* TB, uint64_t n, uint32_t* PB, cudaStream_t st);
+// changed2 after pass B (clears PA, NCP, TB)
+void pstat2(const uint32_t* PB, uint64_t n, uint32_t* PA, uint32_t* NCP, uint32_t* TB, uint64_t* ctr,
+            cudaStream_t st);
 // ordered compaction of live tuples (R order kept); output count = live count
 void compact(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2,
              scan::State& ss, cudaStream_t st);
-void papply2(uint32_t* P, uint64_t A, const uint32_t* PMIN, cudaStream_t st);
 
 }  // namespace csr
 }  // namespace cc

@@ -1,0 +1,612 @@
+// sv_rows.cu -- row passes of the r-stationary SV engine.
+//
+// The tuple array is stored in CSR order (R sorted, vertex bucket VB(u) = one contiguous row,
+// see sv_csr.cu).  Because a row is contiguous, the vertex-bucket minimum of Alg. 1
+// (lines 9-13 / line 24) is a reduction over one run of the array, and
+// the partition-bucket update that consumes it (lines 15-16 / line 25) can
+// run in the same pass: q = u_min(r) is never written out and read back.  Each iteration of
+// Alg. 1 is two streaming passes over (R, P):
+//
+//   pass A  (lines 8-16)   p <- PB[p]   (line 25 relabel of the previous iteration, if any)
+//                          u_min(r), PC(r) = [min p = max p] per row      (lines 9-13)
+//                          PA[p] <- min(PA[p], u_min(r))                   (lines 15-16)
+//                          NCP(u_min(r)) for a row that is not PC (see below)
+//   pass B  (lines 17-25)  completed(p) = PA[p] = p and not NCP(p): the tuple leaves and its
+//                          vertex takes label p (lines 17-21);
+//                          otherwise p <- PA[p]                             (line 19)
+//                          u_min'(r) over the row plus the temporary <r,_,r> when TB(r)
+//                          (line 22 + line 24, fig:doubling PAPER.md:189-197)
+//                          PB[p] <- min(PB[p], u_min'(r)); the temporary's own q goes to
+//                          PB[r]                                           (line 25)
+//
+// Completion needs only one flag per non-PC row: a partition p with a tuple in a row whose
+// minimum m is below p gets p_min <= m < p and is not completed anyway, so only p = m can
+// be completed-but-for-this-row; NCP(m) is the paper's "not all tuples potentially
+// completed" for exactly the partitions where it decides.
+//
+// Work split.  A block stages a 2048-tuple tile (8 per thread) in shared memory after the
+// relabel; thread t owns the rows whose head lies in its 8-tuple slice and walks each of them
+// (into the next tile through global memory when the row crosses the tile edge), so every
+// row is reduced and applied by exactly one thread with no cross-thread combine.  Rows longer
+// than LONG tuples (hubs) would serialise a warp; they are listed once per compaction as
+// segments of at most LSEG tuples and handled by warps in two small kernels (segment partials
+// into epoch-tagged 64-bit slots whose newer tags always win the atomic, then the apply).
+// Partition slots PA/PB are n-sized u32 arrays that stay resident in L2; each block filters
+// its slot updates through a shared-memory cache of values it has already pushed (slots only
+// decrease), so a partition shared by millions of tuples costs one atomic per block.
+#include <algorithm>
+
+#include "csr.cuh"
+#include "sv.cuh"
+
+namespace cc {
+namespace csr {
+
+namespace {
+
+constexpr int RB = 256;
+constexpr int RITEMS = 8;
+constexpr int RTILE = RB * RITEMS;
+constexpr int RCACHE = 512;
+constexpr uint32_t INF = 0xFFFFFFFFu;
+constexpr uint32_t DEAD = 0xFFFFFFFFu;
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+
+CC_DEVI bool tbit(const uint32_t* bm, uint32_t i) { return (__ldg(&bm[i >> 5]) >> (i & 31)) & 1u; }
+
+// slot update through the block's cache of pushed values (key p, value in one 64-bit word)
+CC_DEVI void push_min(uint32_t* OUT, unsigned long long* s_pc, uint32_t p, uint32_t q) {
+  const uint32_t h = (p ^ (p >> 9)) & (RCACHE - 1);
+  const unsigned long long e = *(volatile unsigned long long*)&s_pc[h];
+  if ((uint32_t)(e >> 32) == p && q >= (uint32_t)e) return;
+  atomicMin(&OUT[p], q);  // result unused: compiles to a fire-and-forget reduction
+  s_pc[h] = ((unsigned long long)p << 32) | q;
+}
+CC_DEVI void set_bit(uint32_t* BM, uint32_t p) {
+  const uint32_t b = 1u << (p & 31);
+  if (!(*(volatile uint32_t*)&BM[p >> 5] & b)) atomicOr(&BM[p >> 5], b);
+}
+// epoch-tagged partial slots: min slot hi word = ~tag (newer = smaller), max slot hi = tag
+CC_DEVI unsigned long long tmin(uint32_t tag, uint32_t v) {
+  return ((unsigned long long)(0xFFFFFFFFu - tag) << 32) | v;
+}
+CC_DEVI unsigned long long tmax(uint32_t tag, uint32_t v) {
+  return ((unsigned long long)tag << 32) | v;
+}
+
+CC_DEVI void load8(const uint32_t* X, uint64_t i0, uint64_t L, uint32_t fill, uint32_t* x) {
+  if (i0 + RITEMS <= L) {
+    const uint4 a = ldg_stream(reinterpret_cast<const uint4*>(X + i0));
+    const uint4 b = ldg_stream(reinterpret_cast<const uint4*>(X + i0 + 4));
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < RITEMS; j++) x[j] = (i0 + j < L) ? X[i0 + j] : fill;
+  }
+}
+CC_DEVI void store8(uint32_t* X, uint64_t i0, uint64_t L, const uint32_t* x) {
+  if (i0 + RITEMS <= L) {
+    reinterpret_cast<uint4*>(X + i0)[0] = make_uint4(x[0], x[1], x[2], x[3]);
+    reinterpret_cast<uint4*>(X + i0)[1] = make_uint4(x[4], x[5], x[6], x[7]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < RITEMS; j++)
+      if (i0 + j < L) X[i0 + j] = x[j];
+  }
+}
+
+// ---- TMA bulk copies (1-D cp.async.bulk, completion counted on an mbarrier)
+CC_DEVI uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+CC_DEVI void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+CC_DEVI void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+CC_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+CC_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// relabel of one input value: A -> MAP (NULL: identity); B -> PA[p], or DEAD if p completed
+template <bool A>
+CC_DEVI uint32_t relabel(uint32_t pv, const uint32_t* __restrict__ MAP, const uint32_t* __restrict__ NCPr) {
+  if (pv == DEAD) return DEAD;
+  if (A) return MAP ? __ldg(&MAP[pv]) : pv;
+  const uint32_t pm = __ldg(&MAP[pv]);
+  if (pm == pv && !tbit(NCPr, pv)) return DEAD;
+  return pm;
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------- row pass
+// A run = a maximal group of equal live keys = one row (or the part of it in the tile).
+// Run minima / maxima are computed branch-free: an inclusive forward and a backward
+// segmented scan over the thread's 8 items, Kogge-Stone shuffles across the lanes of a warp
+// (forward over the threads' last runs, backward over their first runs; keys are sorted and a
+// row is contiguous, so equal keys are always connected), and a walk over the 8 warp
+// aggregates for runs that cross warps.  A row that continues past the tile end is finished
+// by this tile: the last warp reads its extension (< LONG tuples) from global memory, and the
+// next tile skips its leading run.  P is double-buffered (Pin -> Pout), so both tiles see
+// the pass's input at every position.
+struct RunAgg {
+  uint32_t key, mn, mx, pad;
+};
+template <bool A>
+__global__ void __launch_bounds__(RB, 4) k_rowpass(
+    const uint32_t* __restrict__ R, const uint32_t* __restrict__ Pin, uint32_t* __restrict__ Pout,
+    uint64_t L, uint32_t ntiles, const uint32_t* __restrict__ MAP,
+    const uint32_t* __restrict__ NCPr, const uint32_t* __restrict__ TB, uint32_t* OUT,
+    uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int hot) {
+  constexpr int NW = RB / 32;
+  // double-buffered tile staging: TMA brings tile i+2 while tile i is processed
+  __shared__ __align__(128) uint32_t s_r[2][RTILE];
+  __shared__ __align__(128) uint32_t s_in[2][RTILE];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ uint32_t s_last[NW];
+  __shared__ RunAgg s_wt[NW], s_wh[NW + 1];  // per warp: last run (prefix), first run (suffix)
+  __shared__ uint32_t s_kfirst;
+  __shared__ unsigned long long s_pc[RCACHE];
+  for (int i = threadIdx.x; i < RCACHE; i += RB) s_pc[i] = ~0ull;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto issue = [&](uint32_t tl, int b) {  // thread 0: stage tile tl into buffer b
+    if (tl >= ntiles) return;
+    const uint64_t a0 = (uint64_t)tl * RTILE;
+    const uint32_t n = (uint32_t)(L - a0 < (uint64_t)RTILE ? L - a0 : (uint64_t)RTILE);
+    const uint32_t bytes = (n * 4 + 15) & ~15u;  // arrays are padded past L
+    mbar_expect_tx(&s_bar[b], 2 * bytes);
+    bulk_g2s(s_r[b], R + a0, bytes, &s_bar[b]);
+    bulk_g2s(s_in[b], Pin + a0, bytes, &s_bar[b]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    issue(blockIdx.x, 0);
+    issue(blockIdx.x + gridDim.x, 1);
+  }
+  uint32_t live = 0;
+  uint32_t it = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+    const int buf = it & 1;
+    const uint64_t t0 = (uint64_t)tile * RTILE;
+    const uint32_t tlen = (uint32_t)(L - t0 < (uint64_t)RTILE ? L - t0 : (uint64_t)RTILE);
+    const uint64_t i0 = t0 + (uint64_t)threadIdx.x * RITEMS;
+    const uint32_t rprev = (threadIdx.x == 0 && t0 > 0) ? __ldg(&R[t0 - 1]) : INF;
+    uint32_t r[RITEMS], p[RITEMS];
+    mbar_wait(&s_bar[buf], (it >> 1) & 1);
+    {
+      const uint32_t s0 = threadIdx.x * RITEMS;
+      const uint4 a = reinterpret_cast<const uint4*>(s_r[buf] + s0)[0];
+      const uint4 b = reinterpret_cast<const uint4*>(s_r[buf] + s0)[1];
+      const uint4 c = reinterpret_cast<const uint4*>(s_in[buf] + s0)[0];
+      const uint4 d = reinterpret_cast<const uint4*>(s_in[buf] + s0)[1];
+      r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+      p[0] = c.x; p[1] = c.y; p[2] = c.z; p[3] = c.w; p[4] = d.x; p[5] = d.y; p[6] = d.z; p[7] = d.w;
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++)
+        if (s0 + j >= tlen) { r[j] = INF; p[j] = DEAD; }
+    }
+    // ---- relabel (A: line 25 of the previous iteration) / exclusion + line 19 (B)
+    {
+      uint32_t m[RITEMS];
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) m[j] = (p[j] != DEAD && (!A || MAP)) ? __ldg(&MAP[p[j]]) : p[j];
+      if (!A) {
+#pragma unroll
+        for (int j = 0; j < RITEMS; j++) {
+          if (p[j] != DEAD && m[j] == p[j] && !tbit(NCPr, p[j])) {
+            // completed partition: the whole row leaves, its vertex is labelled p
+            if (j == 0 || r[j - 1] != r[j]) label[r[j] & ~R_LONG] = p[j];
+            m[j] = DEAD;
+          }
+          live += m[j] != DEAD;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) p[j] = m[j];
+    }
+    if (Pout) store8(Pout, i0, L, p);
+    // keys: dead tuples and long rows (k_long1/k_long2) take no part
+    uint32_t k[RITEMS];
+#pragma unroll
+    for (int j = 0; j < RITEMS; j++) k[j] = (p[j] == DEAD || (r[j] & R_LONG)) ? INF : r[j];
+    uint32_t prevk = __shfl_up_sync(FULL, k[RITEMS - 1], 1);
+    if (lane == 31) s_last[wid] = k[RITEMS - 1];
+    // the leading run belongs to the previous tile when the tile starts inside a row
+    if (threadIdx.x == 0) s_kfirst = (t0 > 0 && k[0] != INF && rprev == k[0]) ? k[0] : INF;
+    __syncthreads();
+    const uint32_t kfirst = s_kfirst;
+    if (lane == 0) prevk = wid ? s_last[wid - 1] : kfirst;
+    if (threadIdx.x == 0) {  // every thread has its items: refill this buffer
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile + 2 * gridDim.x, buf);
+    }
+    // ---- thread-local scans; the temporary <r,_,r> of line 22 joins VB(r) at the row head
+    uint32_t v[RITEMS];
+    uint32_t heads = 0;
+#pragma unroll
+    for (int j = 0; j < RITEMS; j++) {
+      const uint32_t pk = j ? k[j - 1] : prevk;
+      const bool h = k[j] != INF && k[j] != pk;
+      heads |= (uint32_t)h << j;
+      v[j] = (!A && h && tbit(TB, k[j])) ? min(p[j], k[j]) : p[j];
+    }
+    uint32_t fmn[RITEMS], fmx[RITEMS], bmn[RITEMS], bmx[RITEMS];
+    fmn[0] = v[0]; fmx[0] = p[0];
+#pragma unroll
+    for (int j = 1; j < RITEMS; j++) {
+      const bool c = k[j] == k[j - 1];
+      fmn[j] = c ? min(fmn[j - 1], v[j]) : v[j];
+      if (A) fmx[j] = c ? max(fmx[j - 1], p[j]) : p[j];
+    }
+    bmn[RITEMS - 1] = v[RITEMS - 1]; bmx[RITEMS - 1] = p[RITEMS - 1];
+#pragma unroll
+    for (int j = RITEMS - 2; j >= 0; j--) {
+      const bool c = k[j] == k[j + 1];
+      bmn[j] = c ? min(bmn[j + 1], v[j]) : v[j];
+      if (A) bmx[j] = c ? max(bmx[j + 1], p[j]) : p[j];
+    }
+    // ---- warp: forward over the threads' last runs, backward over their first runs
+    const uint32_t kt = k[RITEMS - 1], kh = k[0];
+    uint32_t tmn = fmn[RITEMS - 1], tmx = A ? fmx[RITEMS - 1] : 0u;
+    uint32_t hmn = bmn[0], hmx = A ? bmx[0] : 0u;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t ok = __shfl_up_sync(FULL, kt, d);
+      const uint32_t om = __shfl_up_sync(FULL, tmn, d);
+      const uint32_t ox = A ? __shfl_up_sync(FULL, tmx, d) : 0u;
+      if (lane >= d && ok == kt) { tmn = min(tmn, om); if (A) tmx = max(tmx, ox); }
+      const uint32_t nk = __shfl_down_sync(FULL, kh, d);
+      const uint32_t nm = __shfl_down_sync(FULL, hmn, d);
+      const uint32_t nx = A ? __shfl_down_sync(FULL, hmx, d) : 0u;
+      if (lane + d < 32 && nk == kh) { hmn = min(hmn, nm); if (A) hmx = max(hmx, nx); }
+    }
+    // carries from the neighbouring lanes (their inclusive scans)
+    uint32_t cin_k = __shfl_up_sync(FULL, kt, 1), cin_m = __shfl_up_sync(FULL, tmn, 1);
+    uint32_t cin_x = A ? __shfl_up_sync(FULL, tmx, 1) : 0u;
+    uint32_t cout_k = __shfl_down_sync(FULL, kh, 1), cout_m = __shfl_down_sync(FULL, hmn, 1);
+    uint32_t cout_x = A ? __shfl_down_sync(FULL, hmx, 1) : 0u;
+    if (lane == 0) cin_k = INF;
+    if (lane == 31) cout_k = INF;
+    if (lane == 31) s_wt[wid] = RunAgg{kt, tmn, tmx, 0u};
+    if (lane == 0) s_wh[wid] = RunAgg{kh, hmn, hmx, 0u};
+    // ---- extension of the tile's last run into the next tile (last warp)
+    if (wid == NW - 1) {
+      uint32_t emn = INF, emx = 0, ek = INF;
+      const uint32_t klast = __shfl_sync(FULL, kt, 31);
+      const uint64_t pos = t0 + tlen;
+      if (klast != INF && pos < L && __ldg(&R[pos]) == klast) {
+        ek = klast;
+        for (uint64_t base = pos; base < pos + LONG; base += 32) {
+          const uint64_t i = base + lane;
+          const bool in = i < L && __ldg(&R[i]) == klast;
+          if (in) {
+            const uint32_t pv = relabel<A>(__ldg(&Pin[i]), MAP, NCPr);  // live row: not DEAD
+            emn = min(emn, pv);
+            emx = max(emx, pv);
+          }
+          if (__ballot_sync(FULL, !in)) break;
+        }
+        emn = __reduce_min_sync(FULL, emn);
+        emx = __reduce_max_sync(FULL, emx);
+      }
+      if (lane == 0) s_wh[NW] = RunAgg{ek, emn, emx, 0u};
+    }
+    __syncthreads();
+    // ---- runs that cross warps: walk the warp aggregates (warp-uniform loops)
+    uint32_t wcin_m = INF, wcin_x = 0, wcout_m = INF, wcout_x = 0;
+    const uint32_t k0w = __shfl_sync(FULL, kh, 0), k31w = __shfl_sync(FULL, kt, 31);
+    for (int w = wid - 1; w >= 0; w--) {
+      const RunAgg a = s_wt[w];
+      if (a.key != k0w || k0w == INF) break;
+      wcin_m = min(wcin_m, a.mn); wcin_x = max(wcin_x, a.mx);
+      if (s_wh[w].key != a.key) break;  // warp w is not one run
+    }
+    for (int w = wid + 1; w <= NW; w++) {
+      const RunAgg a = s_wh[w];
+      if (a.key != k31w || k31w == INF) break;
+      wcout_m = min(wcout_m, a.mn); wcout_x = max(wcout_x, a.mx);
+      if (w == NW || s_wt[w].key != a.key) break;
+    }
+    if (lane == 0) { cin_k = k0w; cin_m = wcin_m; cin_x = wcin_x; }
+    else if (cin_k == k0w) { cin_m = min(cin_m, wcin_m); cin_x = max(cin_x, wcin_x); }
+    if (lane == 31) { cout_k = k31w; cout_m = wcout_m; cout_x = wcout_x; }
+    else if (cout_k == k31w) { cout_m = min(cout_m, wcout_m); cout_x = max(cout_x, wcout_x); }
+    // ---- apply: q = u_min(r) to PA/PB[p] (+ NCP(q) of a non-PC row in A, + the
+    // temporary's own q in B), skipping the leading run owned by the previous tile
+    uint32_t qlast = INF;
+#pragma unroll
+    for (int j = 0; j < RITEMS; j++) {
+      uint32_t q = min(fmn[j], bmn[j]);
+      uint32_t x = A ? max(fmx[j], bmx[j]) : 0u;
+      if (k[j] == k[0] && cin_k == k[0]) { q = min(q, cin_m); if (A) x = max(x, cin_x); }
+      if (k[j] == k[RITEMS - 1] && cout_k == k[RITEMS - 1]) { q = min(q, cout_m); if (A) x = max(x, cout_x); }
+      if (k[j] == INF || k[j] == kfirst) continue;
+      if (j == RITEMS - 1) qlast = q;
+      if (!hot) atomicMin(&OUT[p[j]], q);
+      else if (j == 0 || p[j] != p[j - 1] || k[j] != k[j - 1]) push_min(OUT, s_pc, p[j], q);
+      if ((heads >> j) & 1u) {
+        if (A) {
+          if (q != x) atomicOr(&NCPw[q >> 5], 1u << (q & 31));
+        } else if (tbit(TB, k[j])) {
+          atomicMin(&OUT[k[j]], q);
+        }
+      }
+    }
+    // extension tuples of the last run (owned here): same q as the run
+    if (wid == NW - 1 && s_wh[NW].key != INF) {
+      const uint32_t q = __shfl_sync(FULL, qlast, 31);
+      const uint32_t klast = s_wh[NW].key;
+      const uint64_t pos = t0 + tlen;
+      for (uint64_t base = pos; base < pos + LONG; base += 32) {
+        const uint64_t i = base + lane;
+        const bool in = i < L && __ldg(&R[i]) == klast;
+        if (in) atomicMin(&OUT[relabel<A>(__ldg(&Pin[i]), MAP, NCPr)], q);
+        if (__ballot_sync(FULL, !in)) break;
+      }
+    }
+    __syncthreads();
+  }
+  if (!A) {
+    live = warp_sum(live);
+    if (lane == 0 && live) atomicAdd(&ctr[sv::C_OUT], (unsigned long long)live);
+  }
+}
+
+// --------------------------------------------------------------------------- long rows
+// List the segments (<= LSEG tuples) of live rows longer than LONG (R_LONG flag; their
+// length is deg + 1, the vertex tuple and one tuple per arc): one thread per row head.
+__global__ void __launch_bounds__(RB) k_longlist(const uint32_t* __restrict__ R,
+                                                 const uint32_t* __restrict__ P, uint64_t L,
+                                                 const uint32_t* __restrict__ deg,
+                                                 LongSeg* __restrict__ segs,
+                                                 unsigned long long* nsegs, uint64_t cap) {
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < L; i += (uint64_t)gridDim.x * RB) {
+    const uint32_t ru = R[i];
+    if (!(ru & R_LONG) || (i > 0 && R[i - 1] == ru) || P[i] == DEAD) continue;
+    const uint32_t u = ru & ~R_LONG;
+    const uint64_t len = (uint64_t)deg[u] + 1, ns = (len + LSEG - 1) / LSEG;
+    const uint64_t b = atomicAdd(nsegs, (unsigned long long)ns);
+    for (uint64_t s = 0; s < ns && b + s < cap; s++) {
+      LongSeg sg;
+      sg.u = u;
+      sg.start = i + s * LSEG;
+      sg.len = (uint32_t)(len - s * LSEG < LSEG ? len - s * LSEG : LSEG);
+      segs[b + s] = sg;
+    }
+  }
+}
+
+// Segment partials of long rows (after k_rowpass has written the relabelled values).
+template <bool A>
+__global__ void __launch_bounds__(RB) k_long1(const uint32_t* __restrict__ P,
+                                              const LongSeg* __restrict__ segs,
+                                              const unsigned long long* nsegs,
+                                              const uint32_t* __restrict__ TB,
+                                              unsigned long long* UMIN, unsigned long long* UMAX,
+                                              uint32_t tag) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t cnt = *nsegs;
+  for (uint64_t s = (blockIdx.x * (uint64_t)RB + threadIdx.x) >> 5; s < cnt;
+       s += ((uint64_t)gridDim.x * RB) >> 5) {
+    const LongSeg sg = segs[s];
+    uint32_t mn = INF, mx = 0;
+    for (uint32_t i = lane; i < sg.len; i += 32) {
+      const uint32_t v = P[sg.start + i];
+      mn = min(mn, v);
+      if (v != DEAD) mx = max(mx, v);
+    }
+    mn = __reduce_min_sync(FULL, mn);
+    mx = __reduce_max_sync(FULL, mx);
+    if (lane == 0 && mn != INF) {
+      if (!A && tbit(TB, sg.u)) mn = min(mn, sg.u);
+      atomicMin(&UMIN[sg.u], tmin(tag, mn));
+      if (A) atomicMax(&UMAX[sg.u], tmax(tag, mx));
+    }
+  }
+}
+
+// Apply of long rows: u_min(r) (and the max) are final in the tagged slots.
+template <bool A>
+__global__ void __launch_bounds__(RB) k_long2(const uint32_t* __restrict__ P,
+                                              const LongSeg* __restrict__ segs,
+                                              const unsigned long long* nsegs,
+                                              const unsigned long long* __restrict__ UMIN,
+                                              const unsigned long long* __restrict__ UMAX,
+                                              const uint32_t* __restrict__ TB, uint32_t* OUT,
+                                              uint32_t* NCPw, uint32_t tag) {
+  __shared__ unsigned long long s_pc[RCACHE];
+  for (int i = threadIdx.x; i < RCACHE; i += RB) s_pc[i] = ~0ull;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t cnt = *nsegs;
+  for (uint64_t s = (blockIdx.x * (uint64_t)RB + threadIdx.x) >> 5; s < cnt;
+       s += ((uint64_t)gridDim.x * RB) >> 5) {
+    const LongSeg sg = segs[s];
+    const unsigned long long um = UMIN[sg.u];
+    if ((uint32_t)(um >> 32) != 0xFFFFFFFFu - tag) continue;  // row left (completed)
+    const uint32_t q = (uint32_t)um;
+    for (uint32_t i = lane; i < sg.len; i += 32) push_min(OUT, s_pc, P[sg.start + i], q);
+    if (lane == 0) {
+      if (A) {
+        if (q != (uint32_t)UMAX[sg.u]) set_bit(NCPw, q);
+      } else if (tbit(TB, sg.u)) {
+        push_min(OUT, s_pc, sg.u, q);
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------- slot scans
+// After pass A: |P_i|, completed, changed, T_i from PA/NCP; one temporary per surviving
+// partition marks TB(p_min) (line 22); PB is cleared for pass B.
+__global__ void __launch_bounds__(RB) k_pstat1(const uint32_t* __restrict__ PA,
+                                               const uint32_t* __restrict__ NCP, uint64_t n4,
+                                               uint32_t* TB, uint32_t* __restrict__ PB,
+                                               unsigned long long* ctr) {
+  uint32_t np = 0, nc = 0, ch = 0, nt = 0;
+  for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
+    const uint4 a = reinterpret_cast<const uint4*>(PA)[t];
+    reinterpret_cast<uint4*>(PB)[t] = make_uint4(INF, INF, INF, INF);
+    if ((a.x & a.y & a.z & a.w) == INF) continue;
+    const uint32_t w = __ldg(&NCP[t >> 3]) >> (4 * (t & 7));
+    const uint32_t v[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint32_t pm = v[j];
+      if (pm == INF) continue;
+      const uint32_t pid = (uint32_t)(4 * t + j);
+      np++;
+      ch += pm != pid;
+      const bool comp = pm == pid && !((w >> j) & 1u);
+      nc += comp;
+      if (!comp) {
+        nt++;
+        const uint32_t b = 1u << (pm & 31);
+        if (!(*(volatile uint32_t*)&TB[pm >> 5] & b)) atomicOr(&TB[pm >> 5], b);
+      }
+    }
+  }
+  np = warp_sum(np); nc = warp_sum(nc); ch = warp_sum(ch); nt = warp_sum(nt);
+  if ((threadIdx.x & 31) == 0) {
+    if (np) atomicAdd(&ctr[sv::C_PARTITIONS], (unsigned long long)np);
+    if (nc) atomicAdd(&ctr[sv::C_COMPLETED], (unsigned long long)nc);
+    if (ch) atomicAdd(&ctr[sv::C_CHANGED], (unsigned long long)ch);
+    if (nt) atomicAdd(&ctr[sv::C_TEMPS], (unsigned long long)nt);
+  }
+}
+
+// Temporaries <u,_,u>_tmp in PB(u) (pass 4): q = u_min'(u) <= u; the row part of u_min' was
+// pushed by pass B, the temporary's own element here.
+__global__ void __launch_bounds__(RB) k_temps2(const uint32_t* __restrict__ TB, uint64_t nw,
+                                               uint32_t* PB) {
+  for (uint64_t w = blockIdx.x * (uint64_t)RB + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * RB) {
+    uint32_t bits = TB[w];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint32_t u = (uint32_t)(w * 32 + b);
+      if (u < *(volatile uint32_t*)&PB[u]) atomicMin(&PB[u], u);
+    }
+  }
+}
+
+// After pass B: changed2 from PB; PA, NCP and TB are cleared for the next iteration.
+__global__ void __launch_bounds__(RB) k_pstat2(const uint32_t* __restrict__ PB, uint64_t n4,
+                                               uint32_t* __restrict__ PA, uint32_t* __restrict__ NCP,
+                                               uint32_t* __restrict__ TB, unsigned long long* ctr) {
+  uint32_t ch = 0;
+  for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
+    const uint4 b = reinterpret_cast<const uint4*>(PB)[t];
+    reinterpret_cast<uint4*>(PA)[t] = make_uint4(INF, INF, INF, INF);
+    if ((t & 7) == 0) {
+      NCP[t >> 3] = 0u;
+      TB[t >> 3] = 0u;
+    }
+    const uint32_t v[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) ch += v[j] != INF && v[j] != (uint32_t)(4 * t + j);
+  }
+  ch = warp_sum(ch);
+  if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
+}
+
+// --------------------------------------------------------------------------- launchers
+static unsigned persistent_grid(const void* fn, uint64_t ntiles) {
+  int ps = 0, sms = 148, dev = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, RB, 0);
+  if (ps < 1) ps = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)sms * ps));
+}
+
+uint64_t row_tiles(uint64_t L) { return (L + RTILE - 1) / RTILE; }
+uint64_t long_seg_cap(uint64_t L) { return L / LSEG + L / (LONG + 1) + 2; }
+
+
+void longlist(const uint32_t* R, const uint32_t* P, uint64_t L, const uint32_t* deg, LongSeg* segs,
+              uint64_t* nsegs, cudaStream_t st) {
+  cudaMemsetAsync(nsegs, 0, sizeof(uint64_t), st);
+  if (!L) return;
+  const unsigned g = (unsigned)std::min<uint64_t>((L + RB - 1) / RB, 148 * 8);
+  k_longlist<<<g, RB, 0, st>>>(R, P, L, deg, segs, reinterpret_cast<unsigned long long*>(nsegs),
+                               long_seg_cap(L));
+}
+
+void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L,
+             const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
+             uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
+             const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
+             cudaStream_t st) {
+  if (!L) return;
+  const uint64_t nt = row_tiles(L);
+  auto* umin = reinterpret_cast<unsigned long long*>(UMIN);
+  auto* umax = reinterpret_cast<unsigned long long*>(UMAX);
+  auto* ns = reinterpret_cast<const unsigned long long*>(nsegs);
+  auto* c = reinterpret_cast<unsigned long long*>(ctr);
+  const uint32_t* Pv = Pout ? Pout : Pin;  // relabelled values, for the long-row kernels
+  if (passA) {
+    static unsigned ga = 0;
+    if (!ga) ga = persistent_grid((const void*)k_rowpass<true>, ~0ull);
+    k_rowpass<true><<<(unsigned)std::min<uint64_t>(nt, ga), RB, 0, st>>>(
+        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0);
+    if (have_long) {
+      k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
+      k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
+    }
+  } else {
+    static unsigned gb = 0;
+    if (!gb) gb = persistent_grid((const void*)k_rowpass<false>, ~0ull);
+    k_rowpass<false><<<(unsigned)std::min<uint64_t>(nt, gb), RB, 0, st>>>(
+        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0);
+    if (have_long) {
+      k_long1<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
+      k_long2<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
+    }
+  }
+}
+
+void pstat1(const uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
+            uint64_t* ctr, cudaStream_t st) {
+  const uint64_t n4 = (n + 3) / 4;
+  if (!n4) return;
+  const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
+  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, reinterpret_cast<unsigned long long*>(ctr));
+}
+void temps2(const uint32_t* TB, uint64_t n, uint32_t* PB, cudaStream_t st) {
+  const uint64_t nw = (n + 31) / 32;
+  if (!nw) return;
+  const unsigned g = (unsigned)std::min<uint64_t>((nw + RB - 1) / RB, 148 * 4);
+  k_temps2<<<g, RB, 0, st>>>(TB, nw, PB);
+}
+void pstat2(const uint32_t* PB, uint64_t n, uint32_t* PA, uint32_t* NCP, uint32_t* TB, uint64_t* ctr,
+            cudaStream_t st) {
+  const uint64_t n4 = (n + 3) / 4;
+  if (!n4) return;
+  const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
+  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, NCP, TB, reinterpret_cast<unsigned long long*>(ctr));
+}
+
+}  // namespace csr
+}  // namespace cc

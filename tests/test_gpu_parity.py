@@ -146,6 +146,33 @@ def test_long_path_and_star(cc):
         assert np.all(lab == 0)
 
 
+@pytest.mark.parametrize("seed", [0, 1])
+def test_row_lengths_straddle_tiles(cc, seed):
+    """Vertex buckets (rows) whose lengths straddle the row-pass tile (2048 tuples) and the
+    extension limit (256) land at every offset of a tile edge: short crossing rows are
+    finished by the tile holding their head, long ones by the fix-up.  Stars of those sizes,
+    joined by random leaf-leaf edges so several iterations run."""
+    rng = np.random.default_rng(77 + seed)
+    sizes = [1, 2, 3, 7, 31, 32, 33, 254, 255, 256, 257, 258, 1000, 2046, 2047, 2048, 2049,
+             2302, 2303, 2304, 2305, 4095, 4096, 4097, 6000]
+    sizes = sizes * 3 + list(rng.integers(1, 400, size=200))
+    n = int(sum(sizes) + len(sizes) + 1000)
+    perm = rng.permutation(n).astype(np.uint32)
+    edges, nxt = [], 0
+    for s in rng.permutation(np.array(sizes)):
+        c = perm[nxt]
+        leaves = perm[nxt + 1:nxt + 1 + int(s) - 1]  # row length = degree + 1 = s
+        edges.append(np.stack([np.full(leaves.shape[0], c, np.uint32), leaves], 1))
+        nxt += int(s)
+    used = perm[:nxt]
+    joins = rng.choice(used, size=(len(sizes) // 2, 2)).astype(np.uint32)
+    e = np.concatenate(edges + [joins]).astype(np.uint32)
+    want, tr = osv.sv_trace(n, e)
+    lab, rep = run(cc, n, e, "sv")
+    assert np.array_equal(lab, want)
+    assert norm(trace_of(rep)) == norm(tr)
+
+
 # ------------------------------------------------------------------ configs (BASELINE.json)
 @pytest.mark.parametrize("cfg,scale", [("c1", 1.0), ("c2", 0.02), ("c3", 0.02)])
 def test_config_trace_parity(cc, cfg, scale):
