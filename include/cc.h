@@ -70,6 +70,26 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
 #define CC_FLAG_REGROUP_DIRECT 0x20u
 #define CC_FLAG_PROFILE 0x10u        /* CUDA-event timing of kernel families (cc_kernel_stats) */
 
+/* ---- multi-GPU exchange (world_size > 1).  The library runs one process per GPU; the
+ * caller supplies the collectives (e.g. torch.distributed over NCCL, NVLink/NVSwitch).  Every
+ * callback is entered with all earlier work on `stream` complete and must return 0 only once
+ * its result is in place in the (device) buffers; nonzero -> CC_ERR_COMM.  All ranks call the
+ * same sequence of collectives (SPMD).  Element types follow cc_dtype; the library maps its
+ * unsigned slot values to an order-preserving signed form before MIN / MAX. */
+typedef enum { CC_DT_I32 = 0, CC_DT_I64 = 1, CC_DT_U8 = 2 } cc_dtype;
+typedef enum { CC_OP_SUM = 0, CC_OP_MIN = 1, CC_OP_MAX = 2 } cc_redop;
+typedef struct {
+  void* user;
+  /* in place: buf[i] <- op over ranks of buf[i], i < count */
+  int (*allreduce)(void* user, void* buf, uint64_t count, int dtype, int op, void* stream);
+  /* recv (world_size * bytes) <- concatenation, rank-major, of every rank's `bytes` at send */
+  int (*allgather)(void* user, const void* send, void* recv, uint64_t bytes, void* stream);
+  /* send: world_size consecutive blocks, send_bytes[k] for rank k; recv: recv_bytes[k] from
+   * rank k, rank-major.  The byte-count arrays are host arrays of world_size entries. */
+  int (*alltoallv)(void* user, const void* send, const uint64_t* send_bytes, void* recv,
+                   const uint64_t* recv_bytes, void* stream);
+} cc_comm;
+
 typedef void* (*cc_alloc_fn)(size_t bytes, void* stream, void* user);
 typedef void (*cc_free_fn)(void* ptr, size_t bytes, void* stream, void* user);
 
@@ -77,6 +97,7 @@ typedef struct {
   int device;          /* CUDA device ordinal                                         */
   void* stream;        /* cudaStream_t; NULL = legacy default stream                   */
   int rank, world_size;/* SPMD position; world_size == 1 for a single GPU              */
+  const cc_comm* comm; /* collectives for world_size > 1 (borrowed; must outlive ctx)  */
   cc_alloc_fn alloc;   /* optional device allocator hooks (NULL => cudaMallocAsync)     */
   cc_free_fn free;
   void* alloc_user;
@@ -116,7 +137,9 @@ typedef struct {
 const char* cc_version(void);
 
 /* Create a context on cfg->device.  cfg is copied.  Returns CC_ERR_INVALID for a NULL
- * argument or bad world_size, CC_ERR_CUDA if the device cannot be used. */
+ * argument, a bad rank / world_size, or world_size > 1 without cfg->comm; CC_ERR_CUDA if the
+ * device cannot be used.  Multi-GPU contexts (world_size > 1) take u32 ids; cc_load_edges,
+ * cc_run are collective (every rank calls them, each with its own block of edges). */
 cc_status cc_init(const cc_config* cfg, cc_ctx** out);
 
 /* Load an undirected edge list (the input G(V,E) of Alg. 1/2; PAPER.md:205 block
@@ -139,8 +162,9 @@ cc_status cc_load_edges(cc_ctx* ctx, cc_idw w, const void* pairs, uint64_t m_loc
  * the device for cc_labels_*.  CC_ERR_STATE if no graph is loaded. */
 cc_status cc_run(cc_ctx* ctx, cc_mode mode, cc_report* out);
 
-/* u32 mode: labels of ids [0, n) (this rank's block when world_size > 1).  `out` has
- * room for `cap` labels; *count receives n.  CC_ERR_INVALID if cap < n. */
+/* u32 mode: labels of ids [0, n), or of this rank's block [lo, hi) (cc_block_range) when
+ * world_size > 1.  `out` has room for `cap` labels; *count receives the label count.
+ * CC_ERR_INVALID if cap is smaller. */
 cc_status cc_labels_u32(cc_ctx* ctx, uint32_t* out, uint64_t cap, uint64_t* count,
                         int out_on_device);
 
@@ -149,6 +173,11 @@ cc_status cc_labels_u32(cc_ctx* ctx, uint32_t* out, uint64_t cap, uint64_t* coun
  * number of distinct ids.  CC_ERR_STATE on a u32 graph (and cc_labels_u32 on a u64 one). */
 cc_status cc_labels_u64(cc_ctx* ctx, uint64_t* ids, uint64_t* labels, uint64_t cap,
                         uint64_t* count, int out_on_device);
+
+/* Multi-GPU (world_size > 1): rank k owns the vertex block [k*B, min((k+1)*B, n)) with
+ * B = 32*ceil(n / (32*world_size)) -- its CSR rows (owner-computes) and its
+ * labels.  Writes the block of this rank (lo = 0, hi = n on one GPU). */
+cc_status cc_block_range(const cc_ctx* ctx, uint64_t* lo, uint64_t* hi);
 
 /* Device pointer of the label array (u32 mode), valid until the next load/destroy, and
  * the device stream all work is enqueued on.  For zero-copy consumers. */

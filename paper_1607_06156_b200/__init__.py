@@ -34,9 +34,26 @@ ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, c
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 
 
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                ctypes.c_int, ctypes.c_int, ctypes.c_void_p)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_uint64, ctypes.c_void_p)
+ALLTOALLV_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p,
+                                ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p)
+CC_DT_I32, CC_DT_I64, CC_DT_U8 = 0, 1, 2
+CC_OP_SUM, CC_OP_MIN, CC_OP_MAX = 0, 1, 2
+
+
+class cc_comm(ctypes.Structure):
+    _fields_ = [("user", ctypes.c_void_p), ("allreduce", ALLREDUCE_FN), ("allgather", ALLGATHER_FN),
+                ("alltoallv", ALLTOALLV_FN)]
+
+
 class cc_config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
-                ("world_size", ctypes.c_int), ("alloc", ALLOC_FN), ("free", FREE_FN),
+                ("world_size", ctypes.c_int), ("comm", ctypes.POINTER(cc_comm)),
+                ("alloc", ALLOC_FN), ("free", FREE_FN),
                 ("alloc_user", ctypes.c_void_p), ("tau", ctypes.c_double),
                 ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32)]
 
@@ -63,8 +80,8 @@ class cc_report(ctypes.Structure):
 
 
 EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
-           "cc_labels_device", "cc_last_launch_count", "cc_kernel_stats", "cc_kernel_name",
-           "cc_destroy", "cc_status_string", "cc_last_error"]
+           "cc_labels_device", "cc_block_range", "cc_last_launch_count", "cc_kernel_stats",
+           "cc_kernel_name", "cc_destroy", "cc_status_string", "cc_last_error"]
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
@@ -84,6 +101,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_labels_u32.argtypes = [P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     lib.cc_labels_u64.argtypes = [P, P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     lib.cc_labels_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_uint64)]
+    lib.cc_block_range.argtypes = [P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
     lib.cc_last_launch_count.restype = ctypes.c_uint64
     lib.cc_last_launch_count.argtypes = [P]
     lib.cc_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
@@ -92,7 +110,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_kernel_name.restype = ctypes.c_char_p
     lib.cc_kernel_name.argtypes = [ctypes.c_int]
     for f in ("cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
-              "cc_labels_device", "cc_kernel_stats", "cc_destroy"):
+              "cc_labels_device", "cc_block_range", "cc_kernel_stats", "cc_destroy"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -119,11 +137,105 @@ def _check(ctx, status):
         raise CCError(status, msg)
 
 
+# ------------------------------------------------------------------ collectives (cc_comm)
+class _CudaBuf:
+    """A raw device pointer seen by torch.as_tensor (no copy)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
+                                         "data": (int(ptr or 0), False), "version": 3}
+
+
+class TorchComm:
+    """The cc_comm collectives (include/cc.h) over torch.distributed: NCCL over NVLink for
+    device buffers, or gloo, which the binding feeds through host copies.  With
+    ``device=None`` the buffers are host memory (used by the CPU tests).  Argument marshalling
+    only: every element the library exchanges is produced and consumed by its kernels."""
+
+    _DT = {CC_DT_I32: "int32", CC_DT_I64: "int64", CC_DT_U8: "uint8"}
+    _SZ = {CC_DT_I32: 4, CC_DT_I64: 8, CC_DT_U8: 1}
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = device
+        self.host_copy = dist.get_backend(group) != "nccl"
+        self._fns = (ALLREDUCE_FN(self._allreduce), ALLGATHER_FN(self._allgather),
+                     ALLTOALLV_FN(self._alltoallv))
+        self.struct = cc_comm(None, *self._fns)
+
+    def _bytes(self, ptr, nbytes):
+        import torch
+        if nbytes == 0:
+            return torch.empty(0, dtype=torch.uint8, device=self.device or "cpu")
+        if self.device is None:
+            arr = np.ctypeslib.as_array((ctypes.c_uint8 * int(nbytes)).from_address(int(ptr)))
+            return torch.from_numpy(arr)
+        return torch.as_tensor(_CudaBuf(ptr, nbytes), device=self.device)
+
+    def _run(self, fn, *tensors):
+        """Run collective ``fn`` on ``tensors`` (device or host), results written back."""
+        import torch
+        if self.device is not None and self.host_copy:
+            host = [t.cpu() for t in tensors]
+            fn(*host)
+            for t, h in zip(tensors, host):
+                t.copy_(h)
+        else:
+            fn(*tensors)
+        if self.device is not None:
+            torch.cuda.synchronize(self.device)
+
+    def _allreduce(self, user, buf, count, dtype, op, stream):
+        try:
+            import torch
+            t = self._bytes(buf, count * self._SZ[dtype]).view(getattr(torch, self._DT[dtype]))
+            rop = {CC_OP_SUM: self.dist.ReduceOp.SUM, CC_OP_MIN: self.dist.ReduceOp.MIN,
+                   CC_OP_MAX: self.dist.ReduceOp.MAX}[op]
+            self._run(lambda x: self.dist.all_reduce(x, op=rop, group=self.group), t)
+            return 0
+        except Exception as e:  # reported to the library as CC_ERR_COMM
+            print(f"cc comm allreduce failed: {e!r}")
+            return 1
+
+    def _allgather(self, user, send, recv, nbytes, stream):
+        try:
+            src = self._bytes(send, nbytes)
+            dst = self._bytes(recv, nbytes * self.world)
+
+            def fn(s, d):
+                if self.host_copy:
+                    self.dist.all_gather(list(d.chunk(self.world)), s, group=self.group)
+                else:
+                    self.dist.all_gather_into_tensor(d, s, group=self.group)
+            self._run(fn, src, dst)
+            return 0
+        except Exception as e:
+            print(f"cc comm allgather failed: {e!r}")
+            return 1
+
+    def _alltoallv(self, user, send, send_bytes, recv, recv_bytes, stream):
+        try:
+            sb = [int(send_bytes[k]) for k in range(self.world)]
+            rb = [int(recv_bytes[k]) for k in range(self.world)]
+            src = self._bytes(send, sum(sb))
+            dst = self._bytes(recv, sum(rb))
+            self._run(lambda s, d: self.dist.all_to_all_single(d, s, rb, sb, group=self.group), src, dst)
+            return 0
+        except Exception as e:
+            print(f"cc comm alltoallv failed: {e!r}")
+            return 1
+
+
 # ------------------------------------------------------------------ C-ABI-named wrappers
-def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True):
+def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=None):
     """Create a context.  ``stream``: a torch.cuda.Stream or raw cudaStream_t int (default:
     torch's current stream).  ``torch_alloc``: route device allocations through PyTorch's
-    caching allocator."""
+    caching allocator.  ``comm``: a :class:`TorchComm` for a multi-GPU (world_size > 1)
+    context; rank and world size are taken from it."""
     import torch
     if stream is None:
         stream = torch.cuda.current_stream(device)
@@ -131,11 +243,13 @@ def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True):
     cfg = cc_config()
     cfg.device = device
     cfg.stream = sptr
-    cfg.rank = 0
-    cfg.world_size = 1
+    cfg.rank = comm.rank if comm else 0
+    cfg.world_size = comm.world if comm else 1
+    if comm:
+        cfg.comm = ctypes.pointer(comm.struct)
     cfg.tau = tau
     cfg.flags = flags
-    keep = []
+    keep = [comm]
     if torch_alloc:
         dev = device
 
@@ -214,6 +328,13 @@ def cc_labels_u64(ctx):
     return ids, lab
 
 
+def cc_block_range(ctx):
+    """(lo, hi): the vertex block whose labels cc_labels_u32 returns on this rank."""
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(ctx, lib().cc_block_range(ctx, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
 def cc_kernel_stats(ctx, which):
     ms, by, ln = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
     _check(ctx, lib().cc_kernel_stats(ctx, which, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(ln)))
@@ -237,8 +358,8 @@ def cc_destroy(ctx):
 class CC:
     """Convenience wrapper: ``CC().load(edges, n).run('auto')`` then ``.labels()``."""
 
-    def __init__(self, device=0, stream=None, flags=0, tau=0.05, torch_alloc=True):
-        self.ctx, self._keep = cc_init(device, stream, flags, tau, torch_alloc)
+    def __init__(self, device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=None):
+        self.ctx, self._keep = cc_init(device, stream, flags, tau, torch_alloc, comm)
 
     def load(self, pairs, n_vertices, ids="u32"):
         cc_load_edges(self.ctx, pairs, n_vertices, ids)
@@ -249,6 +370,9 @@ class CC:
 
     def labels(self, out=None):
         return cc_labels_u32(self.ctx, out)
+
+    def block_range(self):
+        return cc_block_range(self.ctx)
 
     def labels_u64(self):
         return cc_labels_u64(self.ctx)

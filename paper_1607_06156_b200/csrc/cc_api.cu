@@ -25,187 +25,12 @@
 #include "sv.cuh"
 #include "csr.cuh"
 #include "relabel.cuh"
+#include "ctx.cuh"
 
 using namespace cc;
 
 #define CC_VERSION_STR "cc-b200 0.1.0 (sm_100a)"
 
-struct cc_ctx {
-  cc_config cfg{};
-  cudaStream_t st = nullptr;
-  std::string err;
-  // graph
-  bool loaded = false, ran = false;
-  cc_idw idw = CC_U32;
-  uint64_t n = 0, m = 0;
-  int kbits = 0;
-  uint2* d_edges = nullptr;
-  uint2* d_rem = nullptr;
-  uint2* d_rem2 = nullptr;
-  uint64_t* d_ids64 = nullptr;  // u64 mode: loaded endpoints (2m)
-  uint64_t* d_uids = nullptr;   // u64 mode: sorted distinct ids (rank -> id)
-  uint64_t n_alloc = 0;         // id bound the n-sized buffers were sized for
-  uint32_t* d_label = nullptr;
-  uint32_t* d_deg = nullptr;
-  uint32_t* d_hist = nullptr;
-  uint32_t* d_tail = nullptr;
-  uint32_t* d_bm[3] = {nullptr, nullptr, nullptr};  // visited, frontier, next
-  uint32_t* d_sbm[3] = {nullptr, nullptr, nullptr}; // direct SV: notpc, ncp, head
-  uint64_t* d_w[2] = {nullptr, nullptr};
-  uint32_t* d_q[2] = {nullptr, nullptr};
-  uint64_t cap = 0;
-  uint32_t* d_segA = nullptr;
-  uint32_t* d_segB = nullptr;
-  uint64_t* d_umin = nullptr;  // csr engine: tagged partial row minima / maxima
-  uint64_t* d_umax = nullptr;
-  csr::LongSeg* d_lsegs = nullptr;  // csr engine: segments of rows longer than csr::LONG
-  uint64_t* d_nlsegs = nullptr;
-  uint32_t row_tag = 0;
-  uint64_t* d_ctr = nullptr;   // sv counters
-  uint64_t* d_gctr = nullptr;  // graph counters
-  uint64_t* h_ctr = nullptr;   // pinned mirrors
-  uint64_t* h_gctr = nullptr;
-  uint32_t* h_hist = nullptr;  // pinned histogram staging
-  uint32_t* h_word = nullptr;
-  radix::Workspace rws;
-  scan::State ss;
-  std::vector<std::pair<void*, size_t>> allocs;
-  // report
-  std::vector<cc_iter_stat> iters;
-  cc_report rep{};
-  uint64_t launches = 0;
-  // profiling (CC_FLAG_TRACE): per-family events
-  std::vector<cudaEvent_t> ev_pool;
-  size_t ev_used = 0;
-  std::vector<cudaEvent_t> it_ev;  // SV iteration start events
-  struct KStat {
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-    double bytes = 0, ms = 0;
-    uint64_t launches = 0;
-  } kst[16];
-};
-
-// ------------------------------------------------------------------------------ helpers
-static cc_status fail(cc_ctx* c, cc_status s, const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  if (c) c->err = buf;
-  return s;
-}
-#define CK(call)                                                                          \
-  do {                                                                                    \
-    cudaError_t e_ = (call);                                                              \
-    if (e_ != cudaSuccess)                                                                \
-      return fail(c, e_ == cudaErrorMemoryAllocation ? CC_ERR_NOMEM : CC_ERR_CUDA,        \
-                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
-  } while (0)
-#define CKL()                                                                             \
-  do {                                                                                    \
-    cudaError_t e_ = cudaGetLastError();                                                  \
-    if (e_ != cudaSuccess)                                                                \
-      return fail(c, CC_ERR_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
-                  __FILE__, __LINE__);                                                    \
-  } while (0)
-#define TRY(x)                        \
-  do {                                \
-    cc_status s_ = (x);               \
-    if (s_ != CC_OK) return s_;       \
-  } while (0)
-
-static cc_status dalloc(cc_ctx* c, void** p, size_t bytes) {
-  *p = nullptr;
-  if (bytes == 0) bytes = 16;
-  if (c->cfg.alloc) {
-    *p = c->cfg.alloc(bytes, (void*)c->st, c->cfg.alloc_user);
-    if (!*p) return fail(c, CC_ERR_NOMEM, "allocator hook returned NULL for %zu bytes", bytes);
-  } else {
-    cudaError_t e = cudaMallocAsync(p, bytes, c->st);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(c, CC_ERR_NOMEM, "cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
-    }
-  }
-  c->allocs.push_back({*p, bytes});
-  return CC_OK;
-}
-template <typename T>
-static cc_status dalloc_t(cc_ctx* c, T** p, size_t count) {
-  return dalloc(c, reinterpret_cast<void**>(p), count * sizeof(T));
-}
-static void dfree_all(cc_ctx* c) {
-  for (auto& a : c->allocs) {
-    if (c->cfg.free) c->cfg.free(a.first, a.second, (void*)c->st, c->cfg.alloc_user);
-    else cudaFreeAsync(a.first, c->st);
-  }
-  c->allocs.clear();
-  c->d_edges = c->d_rem = c->d_rem2 = nullptr;
-  c->d_ids64 = c->d_uids = nullptr;
-  c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
-  c->d_umin = c->d_umax = c->d_nlsegs = nullptr;
-  c->d_lsegs = nullptr;
-  c->row_tag = 0;
-  c->d_bm[0] = c->d_bm[1] = c->d_bm[2] = nullptr;
-  c->d_sbm[0] = c->d_sbm[1] = c->d_sbm[2] = nullptr;
-  c->d_w[0] = c->d_w[1] = nullptr;
-  c->d_q[0] = c->d_q[1] = nullptr;
-  c->d_ctr = c->d_gctr = nullptr;
-  c->rws = radix::Workspace();
-  c->ss = scan::State();
-  c->cap = 0;
-}
-
-static cudaEvent_t ev_get(cc_ctx* c) {
-  if (c->ev_used == c->ev_pool.size()) {
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    c->ev_pool.push_back(e);
-  }
-  return c->ev_pool[c->ev_used++];
-}
-static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
-  float ms = 0;
-  cudaEventElapsedTime(&ms, a, b);
-  return ms;
-}
-static bool profiling(const cc_ctx* c) { return (c->cfg.flags & CC_FLAG_PROFILE) != 0; }
-
-// kernel families timed under CC_FLAG_PROFILE (cc_kernel_stats / cc_kernel_name)
-enum KFam { KF_RADIX = 0, KF_SVITER, KF_BFS, KF_ROWA, KF_ROWB, KF_SLOTS, KF_CSR, KF_PREDICT,
-            KF_COMPACT, KF_N };
-static const char* const kKfNames[KF_N] = {
-    "k_hist+k_onesweep (radix regroup)", "SV iteration (all bucket passes)", "k_bfs_level",
-    "k_rowpass<A>+k_rowfix (Alg.1 lines 8-16)", "k_rowpass<B>+k_rowfix (Alg.1 lines 17-25)",
-    "k_pstat1/k_temps2/k_pstat2 (partition slot scans)",
-    "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)", "prediction (k_degree, k_deg_hist)",
-    "k_compact (ordered exclusion of completed rows)"};
-
-struct Prof {
-  cc_ctx* c;
-  int f;
-  cudaEvent_t a = nullptr;
-  Prof(cc_ctx* c_, int f_) : c(c_), f(f_) {
-    if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
-  }
-  void end(double bytes, uint64_t nl) {
-    if (!profiling(c)) return;
-    cudaEvent_t b = ev_get(c);
-    cudaEventRecord(b, c->st);
-    c->kst[f].ev.push_back({a, b});
-    c->kst[f].bytes += bytes;
-    c->kst[f].launches += nl;
-  }
-};
-
-static int bits_for(uint64_t n) {
-  int b = 0;
-  while (b < 63 && (1ull << b) < n) b++;
-  return b;
-}
-
-// ------------------------------------------------------------------------------ ABI
 extern "C" {
 
 const char* cc_version(void) { return CC_VERSION_STR; }
@@ -231,8 +56,10 @@ uint64_t cc_last_launch_count(const cc_ctx* c) { return c ? c->launches : 0; }
 cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
   if (!cfg || !out) return CC_ERR_INVALID;
   *out = nullptr;
-  if (cfg->world_size != 1 || cfg->rank != 0)
-    return CC_ERR_INVALID;  // multi-GPU contexts: see DESIGN.md §7 (not in this build)
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return CC_ERR_INVALID;
+  if (cfg->world_size > 1 && (!cfg->comm || !cfg->comm->allreduce || !cfg->comm->allgather ||
+                              !cfg->comm->alltoallv))
+    return CC_ERR_INVALID;  // multi-GPU contexts need the caller's collectives
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
     cudaGetLastError();
@@ -272,6 +99,8 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   if (!c) return CC_ERR_INVALID;
   if (m && !pairs) return fail(c, CC_ERR_INVALID, "pairs is NULL");
   if (w != CC_U32 && w != CC_U64) return fail(c, CC_ERR_INVALID, "bad id width %d", (int)w);
+  if (w == CC_U64 && c->cfg.world_size > 1)
+    return fail(c, CC_ERR_INVALID, "u64 ids are single-GPU in this build (DESIGN.md §7)");
   if (w == CC_U64) {
     if (n != 0) return fail(c, CC_ERR_INVALID, "u64 ids: n_vertices must be 0");
     n = std::min<uint64_t>(2 * m, 1ull << 30);  // bound on distinct ids (checked in cc_run)
@@ -294,7 +123,14 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->d_deg, n + 1));
   TRY(dalloc_t(c, &c->d_hist, graph::HIST_DENSE));
   TRY(dalloc_t(c, &c->d_tail, graph::TAIL_CAP));
-  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], 2 * nw));  // 2-bit BFS state fits
+  // owned vertex block (multi-GPU): blk = 32 * ceil(n / (32 * world))
+  const uint64_t world = (uint64_t)c->cfg.world_size;
+  c->blk = std::max<uint64_t>(32, (n + 32 * world - 1) / (32 * world) * 32);
+  c->lo = std::min<uint64_t>(n, c->blk * (uint64_t)c->cfg.rank);
+  c->hi = world > 1 ? std::min<uint64_t>(n, c->lo + c->blk) : n;
+  if (world == 1) c->lo = 0;
+  const uint64_t bmw = std::max<uint64_t>(2 * nw, world * c->blk / 32) + 2;
+  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], bmw));  // 2-bit BFS state fits
   for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_sbm[i], nw + 2));
   for (int i = 0; i < 2; i++) {
     TRY(dalloc_t(c, &c->d_w[i], c->cap));
@@ -306,6 +142,10 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->d_umax, n + 1));
   TRY(dalloc_t(c, &c->d_lsegs, csr::long_seg_cap(c->cap)));
   TRY(dalloc_t(c, &c->d_nlsegs, 2));
+  if (world > 1) {
+    TRY(dalloc_t(c, &c->d_send, 2 * m + 1));
+    TRY(dalloc_t(c, &c->d_cnt, 2 * world + world * world));
+  }
   CK(cudaMemsetAsync(c->d_umin, 0xFF, sizeof(uint64_t) * (n + 1), c->st));
   CK(cudaMemsetAsync(c->d_umax, 0, sizeof(uint64_t) * (n + 1), c->st));
   TRY(dalloc_t(c, &c->d_ctr, sv::C_NUM));
@@ -328,6 +168,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
       CK(cudaMemcpyAsync(c->d_ids64, pairs, 2 * m * sizeof(uint64_t),
                          on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
     CK(cudaStreamSynchronize(c->st));
+    c->m_total = m;
     c->loaded = true;
     return CC_OK;
   }
@@ -339,7 +180,17 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   graph::launch_validate(c->d_edges, m, n, c->d_gctr, c->st);
   CKL();
   CK(cudaMemcpyAsync(c->h_gctr, c->d_gctr, sizeof(uint64_t) * graph::G_NUM, cudaMemcpyDeviceToHost, c->st));
+  // every rank learns whether any rank's ids were out of range, and the global edge count
+  TRY(comm_allreduce(c, c->d_gctr + graph::G_ERR, 1, CC_DT_I64, CC_OP_MAX));
+  c->m_total = m;
+  if (multi_gpu(c)) {
+    CK(cudaMemcpyAsync(c->d_gctr + graph::G_REMAIN, &c->m_total, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                       c->st));
+    TRY(comm_allreduce(c, c->d_gctr + graph::G_REMAIN, 1, CC_DT_I64, CC_OP_SUM));
+  }
+  CK(cudaMemcpyAsync(c->h_gctr, c->d_gctr, sizeof(uint64_t) * graph::G_NUM, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  if (multi_gpu(c)) c->m_total = c->h_gctr[graph::G_REMAIN];
   if (c->h_gctr[graph::G_ERR]) return fail(c, CC_ERR_RANGE, "edge endpoint >= n_vertices");
   c->loaded = true;
   return CC_OK;
@@ -348,26 +199,6 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
 }  // extern "C"
 
 // ------------------------------------------------------------------------------ stages
-struct Timer {
-  cc_ctx* c;
-  cudaEvent_t a;
-  explicit Timer(cc_ctx* c_) : c(c_), a(ev_get(c_)) { cudaEventRecord(a, c->st); }
-  std::pair<cudaEvent_t, cudaEvent_t> stop() {
-    cudaEvent_t b = ev_get(c);
-    cudaEventRecord(b, c->st);
-    return {a, b};
-  }
-};
-
-static cc_status sync_read(cc_ctx* c) {
-  CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(uint64_t) * sv::C_NUM, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(c->h_gctr, c->d_gctr, sizeof(uint64_t) * graph::G_NUM, cudaMemcpyDeviceToHost,
-                     c->st));
-  CK(cudaStreamSynchronize(c->st));
-  return CC_OK;
-}
-
-// radix sort wrapper with optional per-call timing
 static int do_sort(cc_ctx* c, int cur, uint64_t n, bool pairs) {
   Prof pr(c, KF_RADIX);
   int r = radix::sort_pairs(c->rws, c->d_w, c->d_q, cur, n, c->kbits, pairs, c->st, &c->launches);
@@ -376,19 +207,6 @@ static int do_sort(cc_ctx* c, int cur, uint64_t n, bool pairs) {
   // the element once (8 B word + 4 B payload for the by-p regroups)
   pr.end((double)n * (8.0 + P * 2.0 * (pairs ? 12.0 : 8.0)), (uint64_t)(P + 1));
   return r;
-}
-
-static void seg_begin(cc_ctx* c, cudaEvent_t* a) {
-  if (profiling(c)) { *a = ev_get(c); cudaEventRecord(*a, c->st); }
-}
-static void seg_end(cc_ctx* c, cudaEvent_t a, double bytes, int nl, int fam = KF_SVITER) {
-  if (profiling(c)) {
-    cudaEvent_t b = ev_get(c);
-    cudaEventRecord(b, c->st);
-    c->kst[fam].ev.push_back({a, b});
-    c->kst[fam].bytes += bytes;
-    c->kst[fam].launches += nl;
-  }
 }
 
 // Alg. 1 with direct-addressed buckets (sv_direct.cu): same passes, no tuple movement
@@ -467,17 +285,8 @@ static cc_status run_sv_direct(cc_ctx* c, uint64_t A, int cur) {
 // Alg. 1, r-stationary engine (sv_csr.cu): one counting regroup by r (CSR build), then
 // per iteration: vertex pass, partition pass, partition statistics + temporaries,
 // ordered exclusion of completed partitions; second vertex/partition pass in place.
-static cc_status scan_epoch_guard(cc_ctx* c) {
-  if (((c->ss.epoch + 4) & scan::EPOCH_MASK) < 4) {
-    CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * c->ss.max_tiles, c->st));
-    c->ss.epoch += 8;
-  }
-  return CC_OK;
-}
-
 static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint32_t* vis) {
   const uint64_t n = c->n;
-  const uint64_t nw = (n + 31) / 32;
   uint32_t* R[2] = {reinterpret_cast<uint32_t*>(c->d_w[0]), reinterpret_cast<uint32_t*>(c->d_w[1])};
   uint32_t* P[2] = {R[0] + c->cap, R[1] + c->cap};
   uint32_t *off = c->d_q[0], *cur = c->d_q[1];
@@ -503,8 +312,21 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
   c->launches += 5;
   CKL();
   seg_end(c, a, 4.0 * n + 8.0 * m_sv + 8.0 * A + 4.0 * n, 6, KF_CSR);
-  int cb = 0;           // buffer holding the tuple array
-  uint64_t len = A;     // physical length (live + dead rows)
+  return sv_iterate(c, A, A);
+}
+
+// Alg. 1 iterations on the tuple array in buffer 0 (R, P), `len` entries of which A (summed
+// over ranks) are live.  Multi-GPU: rows are owned (r in this rank's block), partitions are
+// global, so after each row pass the partition slots are combined across ranks (min of the
+// minima, OR of the NCP bitmap) and every rank derives identical statistics and temporaries.
+cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len) {
+  const uint64_t n = c->n;
+  const uint64_t nw = (n + 31) / 32;
+  const bool multi = c->cfg.world_size > 1;
+  uint32_t* R[2] = {reinterpret_cast<uint32_t*>(c->d_w[0]), reinterpret_cast<uint32_t*>(c->d_w[1])};
+  uint32_t* P[2] = {R[0] + c->cap, R[1] + c->cap};
+  cudaEvent_t a = nullptr;
+  int cb = 0;  // buffer holding the tuple array
   const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
   // slot arrays: PA (pass A minima), PB (pass B minima), NCP / TB bitmaps.  The slot scans
   // clear what the next pass needs, so these are the only full clears of the run.
@@ -516,10 +338,12 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
   const bool have_long = c->rep.max_degree + 1 > csr::LONG;
   if (have_long) csr::longlist(R[0], P[0], len, c->d_deg, c->d_lsegs, c->d_nlsegs, c->st);
   const uint64_t n4 = (n + 3) / 4 * 4;
+  const uint64_t nwp = nw + 2;
   CK(cudaMemsetAsync(PA, 0xFF, sizeof(uint32_t) * n4, c->st));
   CK(cudaMemsetAsync(PB, 0xFF, sizeof(uint32_t) * n4, c->st));
-  CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * (nw + 2), c->st));
-  CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * (nw + 2), c->st));
+  CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nwp, c->st));
+  CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nwp, c->st));
+  uint64_t len_live = len;  // live tuples of this rank (compaction decision)
   for (uint32_t it = 0;; it++) {
     if (it >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
     cudaEvent_t ev_it = ev_get(c);
@@ -528,30 +352,42 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
     uint32_t* Rc = R[cb];
     // few partitions per live tuple: slot updates repeat, filter them through the block caches
     const bool hot = it > 0 && c->iters.back().partitions * 16 < len;
-    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_CHANGED2 + 1), c->st));
+    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_SURVIVORS + 1), c->st));
     // ---- lines 8-16 (+ line 25 relabel of the previous iteration)
     { Prof k(c, KF_ROWA);
       csr::rowpass(true, Rc, Pc, it ? Palt : nullptr, len, it ? PB : nullptr, nullptr, nullptr, PA,
                    NCP, c->d_label, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs,
                    have_long, hot, c->d_ctr, c->st);
-      k.end(8.0 * len + (it ? 4.0 * len : 0.0), 2); }
+      k.end(8.0 * len + (it ? 4.0 * len : 0.0), 1 + (have_long ? 2 : 0)); }
     if (it) std::swap(Pc, Palt);
+    if (multi) {  // partition minima and 'not completed' flags over all ranks
+      TRY(comm_min_u32(c, PA, n4));
+      TRY(comm_or_bits(c, NCP, nwp));
+    }
     // ---- line 22 bookkeeping: |P_i|, completed, changed, temporaries
     { Prof k(c, KF_SLOTS); csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st); k.end(8.0 * n4, 1); }
     // ---- lines 17-21 (exclusion, p <- p_min), line 24 (+ temporaries), line 25 minima
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
                    c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, hot, c->d_ctr, c->st);
-      k.end(12.0 * len, 2); }
+      k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
+    // live tuples: this rank's (compaction) and the global count (convergence)
+    CK(cudaMemcpyAsync(c->d_ctr + sv::C_SURVIVORS, c->d_ctr + sv::C_OUT, sizeof(uint64_t),
+                       cudaMemcpyDeviceToDevice, c->st));
+    if (multi) {
+      TRY(comm_min_u32(c, PB, n4));
+      TRY(comm_allreduce(c, c->d_ctr + sv::C_OUT, 1, CC_DT_I64, CC_OP_SUM));
+    }
     { Prof k(c, KF_SLOTS);
       csr::temps2(TB, n, PB, c->st);
       csr::pstat2(PB, n, PA, NCP, TB, c->d_ctr, c->st);
       k.end(8.0 * n4, 2); }
-    c->launches += 8;
+    c->launches += 6 + (have_long ? 4 : 0);
     CKL();
     TRY(sync_read(c));
     const uint64_t A1 = c->h_ctr[sv::C_OUT];
+    len_live = c->h_ctr[sv::C_SURVIVORS];
     cc_iter_stat s{};
     s.active_in = A;
     s.partitions = c->h_ctr[sv::C_PARTITIONS];
@@ -565,13 +401,13 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
     if (A1 == 0) break;
     // dead rows of completed partitions are squeezed out once they are a third of the array
     // (the paper's 'swapped to the end of the local array', sec:distSVOpt1)
-    if (3 * (len - A1) > len) {
+    if (3 * (len - len_live) > len) {
       TRY(scan_epoch_guard(c));
       { Prof k(c, KF_COMPACT); csr::compact(Rc, Pc, len, R[cb ^ 1], P[cb ^ 1], c->ss, c->st);
-        k.end(8.0 * len + 8.0 * A1, 1); }
+        k.end(8.0 * len + 8.0 * len_live, 1); }
       c->launches += 1;
       cb ^= 1;
-      len = A1;
+      len = len_live;
       Pc = P[cb];
       Palt = c->d_q[0];
       if (have_long) csr::longlist(R[cb], Pc, len, c->d_deg, c->d_lsegs, c->d_nlsegs, c->st);
@@ -676,60 +512,16 @@ static cc_status run_sv(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint
   return CC_OK;
 }
 
-extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
-  if (!c) return CC_ERR_INVALID;
-  if (!c->loaded) return fail(c, CC_ERR_STATE, "cc_run before cc_load_edges");
-  if (mode != CC_MODE_AUTO && mode != CC_MODE_SV && mode != CC_MODE_BFS_SV)
-    return fail(c, CC_ERR_INVALID, "bad mode %d", (int)mode);
-  CK(cudaSetDevice(c->cfg.device));
-  c->ran = false;
-  c->iters.clear();
-  c->launches = 0;
-  c->ev_used = 0;
-  c->it_ev.clear();
-  for (auto& k : c->kst) k = cc_ctx::KStat();
+// Alg. 2 lines 2-3 on the host: read the degree statistics and histogram the prediction
+// kernels left in d_gctr / d_hist / d_tail (summed over ranks when world_size > 1), fit the
+// gate, decide the route.
+cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs_out, uint64_t* root) {
   cc_report& R = c->rep;
-  R = cc_report{};
-  const uint64_t m = c->m;
-  R.m_edges = m;
-
-  cudaEvent_t e0 = ev_get(c), e_rel, e_pred, e_bfs, e_filter, e_sv, e_end;
-  CK(cudaEventRecord(e0, c->st));
-  // ------------------------------------------------ relabel (Alg. 2 line 4; u64 ids only)
-  // ids are made dense first: every later stage addresses buckets by id (DESIGN.md R18)
-  if (c->idw == CC_U64) {
-    TRY(scan_epoch_guard(c));
-    uint64_t* total = c->d_gctr + graph::G_NUM + 1537;
-    uint32_t* vals[2] = {c->d_q[0], c->d_q[1]};
-    relabel::run(c->d_ids64, 2 * m, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges),
-                 c->d_uids, total, c->st, &c->launches);
-    CKL();
-    CK(cudaMemcpyAsync(c->h_word, total, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    uint64_t nd = m ? *reinterpret_cast<uint64_t*>(c->h_word) : 0;
-    if (nd > (1ull << 30)) return fail(c, CC_ERR_INVALID, "%llu distinct ids > 2^30", (unsigned long long)nd);
-    c->n = nd;
-    c->kbits = bits_for(nd);
-  }
-  const uint64_t n = c->n;
-  e_rel = ev_get(c);
-  CK(cudaEventRecord(e_rel, c->st));
-  // ------------------------------------------------ prediction (Alg. 2 lines 2-3)
-  CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
-  CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
-  CK(cudaMemsetAsync(c->d_gctr + graph::G_MINVIS, 0xFF, sizeof(uint64_t), c->st));
-  sv::launch_init_labels(c->d_label, n, c->st);
-  graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st);
-  const bool want_hist = (mode == CC_MODE_AUTO) || (c->cfg.flags & CC_FLAG_TRACE);
-  if (want_hist) CK(cudaMemsetAsync(c->d_hist, 0, sizeof(uint32_t) * graph::HIST_DENSE, c->st));
-  graph::launch_deg_hist(c->d_deg, n, c->d_hist, c->d_tail, c->d_gctr, c->st);
-  c->launches += 3;
-  CKL();
   TRY(sync_read(c));
   R.n_present = c->h_gctr[graph::G_NPRESENT];
   const uint64_t maxkey = c->h_gctr[graph::G_MAXKEY];
   R.max_degree = maxkey >> 32;
-  const uint64_t root = maxkey ? (uint64_t)(0xFFFFFFFFu - (uint32_t)maxkey) : 0;
+  *root = maxkey ? (uint64_t)(0xFFFFFFFFu - (uint32_t)maxkey) : 0;
   bool run_bfs = (mode == CC_MODE_BFS_SV);
   R.ls_alpha = R.ls_r2 = R.ks_stat = R.ks_alpha = NAN;
   if (want_hist && R.max_degree > 0) {
@@ -769,6 +561,76 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
       run_bfs = (c->cfg.flags & CC_FLAG_GATE_KS) ? (ks_ok && R.ks_stat < c->cfg.tau) : g.scale_free;
   }
   if (R.max_degree == 0) run_bfs = false;
+  *run_bfs_out = run_bfs;
+  return CC_OK;
+}
+
+extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
+  if (!c) return CC_ERR_INVALID;
+  if (!c->loaded) return fail(c, CC_ERR_STATE, "cc_run before cc_load_edges");
+  if (mode != CC_MODE_AUTO && mode != CC_MODE_SV && mode != CC_MODE_BFS_SV)
+    return fail(c, CC_ERR_INVALID, "bad mode %d", (int)mode);
+  CK(cudaSetDevice(c->cfg.device));
+  c->ran = false;
+  c->iters.clear();
+  c->launches = 0;
+  c->ev_used = 0;
+  c->it_ev.clear();
+  for (auto& k : c->kst) k = cc_ctx::KStat();
+  cc_report& R = c->rep;
+  R = cc_report{};
+  const uint64_t m = c->m;
+  R.m_edges = c->m_total;
+  if (multi_gpu(c)) {
+    TRY(run_dist(c, mode));
+    R.iters = c->iters.data();
+    R.n_iters = (uint32_t)c->iters.size();
+    for (size_t i = 0; i < c->it_ev.size() && i < c->iters.size(); i++)
+      c->iters[i].ms = i + 1 < c->it_ev.size() ? ev_ms(c->it_ev[i], c->it_ev[i + 1]) : 0.0;
+    if (profiling(c))
+      for (auto& k : c->kst)
+        for (auto& p : k.ev) k.ms += ev_ms(p.first, p.second);
+    c->ran = true;
+    if (out) *out = R;
+    return CC_OK;
+  }
+
+  cudaEvent_t e0 = ev_get(c), e_rel, e_pred, e_bfs, e_filter, e_sv, e_end;
+  CK(cudaEventRecord(e0, c->st));
+  // ------------------------------------------------ relabel (Alg. 2 line 4; u64 ids only)
+  // ids are made dense first: every later stage addresses buckets by id (DESIGN.md R18)
+  if (c->idw == CC_U64) {
+    TRY(scan_epoch_guard(c));
+    uint64_t* total = c->d_gctr + graph::G_NUM + 1537;
+    uint32_t* vals[2] = {c->d_q[0], c->d_q[1]};
+    relabel::run(c->d_ids64, 2 * m, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges),
+                 c->d_uids, total, c->st, &c->launches);
+    CKL();
+    CK(cudaMemcpyAsync(c->h_word, total, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    uint64_t nd = m ? *reinterpret_cast<uint64_t*>(c->h_word) : 0;
+    if (nd > (1ull << 30)) return fail(c, CC_ERR_INVALID, "%llu distinct ids > 2^30", (unsigned long long)nd);
+    c->n = nd;
+    c->hi = nd;
+    c->kbits = bits_for(nd);
+  }
+  const uint64_t n = c->n;
+  e_rel = ev_get(c);
+  CK(cudaEventRecord(e_rel, c->st));
+  // ------------------------------------------------ prediction (Alg. 2 lines 2-3)
+  CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
+  CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
+  CK(cudaMemsetAsync(c->d_gctr + graph::G_MINVIS, 0xFF, sizeof(uint64_t), c->st));
+  sv::launch_init_labels(c->d_label, n, c->st);
+  graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st);
+  const bool want_hist = (mode == CC_MODE_AUTO) || (c->cfg.flags & CC_FLAG_TRACE);
+  if (want_hist) CK(cudaMemsetAsync(c->d_hist, 0, sizeof(uint32_t) * graph::HIST_DENSE, c->st));
+  graph::launch_deg_hist(c->d_deg, n, c->d_hist, c->d_tail, c->d_gctr, c->st);
+  c->launches += 3;
+  CKL();
+  bool run_bfs = false;
+  uint64_t root = 0;
+  TRY(predict_gate(c, mode, want_hist, &run_bfs, &root));
   e_pred = ev_get(c);
   CK(cudaEventRecord(e_pred, c->st));
 
@@ -883,11 +745,12 @@ extern "C" cc_status cc_labels_u32(cc_ctx* c, uint32_t* out, uint64_t cap, uint6
   if (!c) return CC_ERR_INVALID;
   if (!c->ran) return fail(c, CC_ERR_STATE, "cc_labels before cc_run");
   if (c->idw != CC_U32) return fail(c, CC_ERR_STATE, "u64 graph loaded: use cc_labels_u64");
-  if (count) *count = c->n;
-  if (!out || cap < c->n) return fail(c, CC_ERR_INVALID, "output buffer too small");
+  const uint64_t cnt = c->hi - c->lo;  // this rank's block ([0, n) on one GPU)
+  if (count) *count = cnt;
+  if (!out || cap < cnt) return fail(c, CC_ERR_INVALID, "output buffer too small");
   CK(cudaSetDevice(c->cfg.device));
-  if (c->n)
-    CK(cudaMemcpyAsync(out, c->d_label, sizeof(uint32_t) * c->n,
+  if (cnt)
+    CK(cudaMemcpyAsync(out, c->d_label + c->lo, sizeof(uint32_t) * cnt,
                        out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   return CC_OK;
@@ -910,6 +773,14 @@ extern "C" cc_status cc_labels_u64(cc_ctx* c, uint64_t* ids, uint64_t* labels, u
     CK(cudaMemcpyAsync(labels, tmp, sizeof(uint64_t) * c->n, k, c->st));
   }
   CK(cudaStreamSynchronize(c->st));
+  return CC_OK;
+}
+
+extern "C" cc_status cc_block_range(const cc_ctx* c, uint64_t* lo, uint64_t* hi) {
+  if (!c || !lo || !hi) return CC_ERR_INVALID;
+  if (!c->loaded) return CC_ERR_STATE;
+  *lo = c->lo;
+  *hi = c->hi;
   return CC_OK;
 }
 

@@ -1,0 +1,376 @@
+// cc_dist.cu -- the multi-GPU driver of cc_run (world_size > 1): SURVEY.md §8(e).
+//
+// One process per GPU.  Rank k owns the vertex block [lo, hi) = [k*blk, (k+1)*blk) (blk a
+// multiple of 32) and, after the one exchange of the run, every tuple whose third element r
+// lies in its block: Alg. 1's regroup by r becomes one all-to-all of
+// arcs to their owners (the distributed counterpart of the single-GPU CSR build, PAPER.md:
+// 204-215 block distribution), and since r never changes no tuple moves again.
+//   prediction  degrees of owned vertices from the received arcs; the histogram, the vertex
+//               count and the max-degree key are reduced over ranks, every rank fits the
+//               same gate (Alg. 2 lines 2-3)
+//   BFS peel    bottom-up over owned rows with a replicated frontier bitmap; the owned
+//               slices of each level's new frontier are all-gathered (Alg. 2 lines 7-8)
+//   filter      rows of visited vertices leave before SV (lines 10-11)
+//   SV          sv_iterate(): rows are local, partition slots are combined over ranks after
+//               each row pass (min of minima, OR of NCP), statistics are identical on all ranks
+// The exchange goes through the caller's cc_comm (torch.distributed over NCCL/NVLink in
+// bench.py; gloo in the tests).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace cc {
+namespace dist {
+
+constexpr int DB = 256;
+constexpr int MAXW = 256;        // ranks supported by the shared-memory owner histograms
+constexpr uint32_t TAILX = 8192; // degrees >= HIST_DENSE per rank that the gate exchange carries
+constexpr uint32_t DEAD = 0xFFFFFFFFu;
+
+CC_DEVI bool bit(const uint32_t* bm, uint32_t v) { return (bm[v >> 5] >> (v & 31)) & 1u; }
+
+// arcs per owner rank of this rank's edges: {x,y} gives <x,_,y> to owner(y), <y,_,x> to owner(x)
+__global__ void k_owner_count(const uint2* __restrict__ e, uint64_t m, uint32_t blk, int world,
+                              unsigned long long* cnt) {
+  __shared__ unsigned long long s[MAXW];
+  for (int i = threadIdx.x; i < world; i += DB) s[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)DB + threadIdx.x; i < m; i += (uint64_t)gridDim.x * DB) {
+    const uint2 xy = e[i];
+    atomicAdd(&s[xy.y / blk], 1ull);
+    atomicAdd(&s[xy.x / blk], 1ull);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < world; i += DB)
+    if (s[i]) atomicAdd(&cnt[i], s[i]);
+}
+
+// arcs (r, p) into per-owner runs of `out`; cursor[k] = next free slot of owner k's run.
+constexpr int SITEMS = 4;
+__global__ void __launch_bounds__(DB) k_owner_scatter(const uint2* __restrict__ e, uint64_t m,
+                                                      uint32_t blk, int world,
+                                                      unsigned long long* cursor,
+                                                      uint2* __restrict__ out) {
+  __shared__ uint32_t s_cnt[MAXW];
+  __shared__ unsigned long long s_base[MAXW];
+  for (int i = threadIdx.x; i < world; i += DB) s_cnt[i] = 0;
+  __syncthreads();
+  const uint64_t e0 = blockIdx.x * (uint64_t)DB * SITEMS + threadIdx.x;
+  uint2 arc[2 * SITEMS];
+  uint32_t slot[2 * SITEMS];
+#pragma unroll
+  for (int k = 0; k < SITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * DB;
+    if (i < m) {
+      const uint2 xy = e[i];
+      arc[2 * k] = make_uint2(xy.y, xy.x);      // <x,_,y>: r = y, p = x
+      arc[2 * k + 1] = make_uint2(xy.x, xy.y);  // <y,_,x>: r = x, p = y
+      slot[2 * k] = atomicAdd(&s_cnt[xy.y / blk], 1u);
+      slot[2 * k + 1] = atomicAdd(&s_cnt[xy.x / blk], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < world; i += DB)
+    s_base[i] = s_cnt[i] ? atomicAdd(&cursor[i], (unsigned long long)s_cnt[i]) : 0ull;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < SITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * DB;
+    if (i < m) {
+      out[s_base[arc[2 * k].x / blk] + slot[2 * k]] = arc[2 * k];
+      out[s_base[arc[2 * k + 1].x / blk] + slot[2 * k + 1]] = arc[2 * k + 1];
+    }
+  }
+}
+
+// deg(r) = arcs with third element r (all of them arrive at r's owner; a self-loop gives 2)
+__global__ void k_arc_degree(const uint2* __restrict__ arcs, uint64_t na, uint32_t* deg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)DB + threadIdx.x; i < na; i += (uint64_t)gridDim.x * DB)
+    atomicAdd(&deg[arcs[i].x], 1u);
+}
+
+// Bottom-up BFS level over owned rows: an unvisited u joins the next frontier when one of
+// its neighbours (the p of its arcs, PAPER.md:103 <x,_,u>) is in the frontier.  Row u of the
+// CSR is [off[u], off[u+1]): its vertex tuple first, then one tuple per arc.
+__global__ void k_bfs_up(const uint32_t* __restrict__ off, const uint32_t* __restrict__ P,
+                         uint64_t lo, uint64_t hi, const uint32_t* __restrict__ V,
+                         const uint32_t* __restrict__ F, uint32_t* X, unsigned long long* cnt) {
+  uint32_t found = 0;
+  for (uint64_t u = lo + blockIdx.x * (uint64_t)DB + threadIdx.x; u < hi; u += (uint64_t)gridDim.x * DB) {
+    if (bit(V, (uint32_t)u)) continue;
+    const uint32_t a = off[u], b = off[u + 1];
+    for (uint32_t i = a + 1; i < b; i++) {
+      if (bit(F, P[i])) {
+        atomicOr(&X[u >> 5], 1u << (u & 31));
+        found++;
+        break;
+      }
+    }
+  }
+  found = warp_sum(found);
+  if ((threadIdx.x & 31) == 0 && found) atomicAdd(cnt, (unsigned long long)found);
+}
+__global__ void k_bfs_merge(uint32_t* V, const uint32_t* __restrict__ F, uint64_t words) {
+  for (uint64_t i = blockIdx.x * (uint64_t)DB + threadIdx.x; i < words; i += (uint64_t)gridDim.x * DB)
+    V[i] |= F[i];
+}
+
+// Filter (Alg. 2 lines 10-11): tuples of visited rows leave; live tuples and live rows counted
+// (remainder arcs = live tuples - live rows, one vertex tuple per row).
+__global__ void k_drop_visited(const uint32_t* __restrict__ R, uint32_t* P, uint64_t L,
+                               const uint32_t* __restrict__ V, unsigned long long* live,
+                               unsigned long long* rows) {
+  uint32_t nl = 0, nr = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)DB + threadIdx.x; i < L; i += (uint64_t)gridDim.x * DB) {
+    const uint32_t r = R[i] & ~csr::R_LONG;
+    if (bit(V, r)) {
+      P[i] = DEAD;
+    } else {
+      nl++;
+      nr += (i == 0 || R[i - 1] != R[i]);
+    }
+  }
+  nl = warp_sum(nl);
+  nr = warp_sum(nr);
+  if ((threadIdx.x & 31) == 0) {
+    if (nl) atomicAdd(live, (unsigned long long)nl);
+    if (nr) atomicAdd(rows, (unsigned long long)nr);
+  }
+}
+
+static unsigned gsz(uint64_t work, unsigned cap) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + DB - 1) / DB, cap));
+}
+
+}  // namespace dist
+}  // namespace cc
+
+using namespace cc::dist;
+
+// (re)allocate the tuple buffers when the arcs this rank owns exceed what the load sized
+static cc_status ensure_tuple_cap(cc_ctx* c, uint64_t tuples) {
+  if (tuples + 64 <= c->cap) return CC_OK;
+  const uint64_t cap = (tuples + 64 + 1023) & ~1023ull;
+  for (int i = 0; i < 2; i++) {
+    TRY(dalloc_t(c, &c->d_w[i], cap));
+    TRY(dalloc_t(c, &c->d_q[i], cap));
+  }
+  c->cap = cap;
+  c->ss.max_tiles = (cap + c->n) / 2048 + 4;
+  TRY(dalloc_t(c, &c->ss.flags, c->ss.max_tiles));
+  CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * c->ss.max_tiles, c->st));
+  TRY(dalloc_t(c, &c->d_lsegs, csr::long_seg_cap(cap)));
+  return CC_OK;
+}
+
+cc_status run_dist(cc_ctx* c, cc_mode mode) {
+  cc_report& R = c->rep;
+  const int world = c->cfg.world_size, rank = c->cfg.rank;
+  const uint64_t n = c->n, m = c->m;
+  const uint64_t blk = c->blk, lo = c->lo, hi = c->hi;
+  const uint64_t nw = (n + 31) / 32;
+  if (world > MAXW) return fail(c, CC_ERR_INVALID, "world_size %d > %d", world, MAXW);
+  cudaEvent_t e0 = ev_get(c), e_pred, e_bfs, e_filter, e_sv;
+  CK(cudaEventRecord(e0, c->st));
+
+  // ------------------------------------------------ regroup by r: arcs to their owners
+  uint64_t* cnt = c->d_cnt;  // [0, world): my arcs per owner; [world, 2 world): cursors;
+                             // [2 world, 2 world + world^2): everyone's counts (gathered)
+  CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * world, c->st));
+  auto* ucnt = reinterpret_cast<unsigned long long*>(cnt);
+  if (m) k_owner_count<<<gsz(m, 148 * 4), DB, 0, c->st>>>(c->d_edges, m, (uint32_t)blk, world, ucnt);
+  CKL();
+  std::vector<uint64_t> mine(world), allc((size_t)world * world), sb(world), rb(world);
+  CK(cudaMemcpyAsync(mine.data(), cnt, sizeof(uint64_t) * world, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  {
+    std::vector<uint64_t> cur(world);
+    uint64_t acc = 0;
+    for (int k = 0; k < world; k++) { cur[k] = acc; acc += mine[k]; }
+    CK(cudaMemcpyAsync(cnt + world, cur.data(), sizeof(uint64_t) * world, cudaMemcpyHostToDevice, c->st));
+  }
+  if (m)
+    k_owner_scatter<<<(unsigned)((m + DB * SITEMS - 1) / (DB * SITEMS)), DB, 0, c->st>>>(
+        c->d_edges, m, (uint32_t)blk, world, ucnt + world, c->d_send);
+  CKL();
+  TRY(comm_allgather(c, cnt, cnt + 2 * world, sizeof(uint64_t) * world));
+  CK(cudaMemcpyAsync(allc.data(), cnt + 2 * world, sizeof(uint64_t) * world * world,
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  uint64_t na = 0;
+  for (int k = 0; k < world; k++) {
+    sb[k] = mine[k] * sizeof(uint2);
+    rb[k] = allc[(size_t)k * world + rank] * sizeof(uint2);
+    na += allc[(size_t)k * world + rank];
+  }
+  if (!c->d_recv || c->recv_cap < na + 1) {
+    TRY(dalloc_t(c, &c->d_recv, na + 1));
+    c->recv_cap = na + 1;
+  }
+  TRY(comm_alltoallv(c, c->d_send, sb.data(), c->d_recv, rb.data()));
+  TRY(ensure_tuple_cap(c, na + (hi - lo)));
+  c->launches += 2;
+
+  // ------------------------------------------------ prediction (Alg. 2 lines 2-3)
+  CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * (n + 1), c->st));
+  CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
+  CK(cudaMemsetAsync(c->d_gctr + graph::G_MINVIS, 0xFF, sizeof(uint64_t), c->st));
+  sv::launch_init_labels(c->d_label, n, c->st);
+  if (na) k_arc_degree<<<gsz(na, 148 * 16), DB, 0, c->st>>>(c->d_recv, na, c->d_deg);
+  const bool want_hist = (mode == CC_MODE_AUTO) || (c->cfg.flags & CC_FLAG_TRACE);
+  CK(cudaMemsetAsync(c->d_hist, 0, sizeof(uint32_t) * graph::HIST_DENSE, c->st));
+  if (hi > lo) graph::launch_deg_hist(c->d_deg + lo, hi - lo, c->d_hist, c->d_tail, c->d_gctr, c->st, lo);
+  c->launches += 3;
+  CKL();
+  TRY(comm_allreduce(c, c->d_gctr + graph::G_MAXKEY, 1, CC_DT_I64, CC_OP_MAX));
+  TRY(comm_allreduce(c, c->d_gctr + graph::G_NPRESENT, 1, CC_DT_I64, CC_OP_SUM));
+  TRY(sync_read(c));
+  const uint64_t dmax = c->h_gctr[graph::G_MAXKEY] >> 32;
+  if (want_hist && dmax > 0) {
+    const uint64_t dense_n = std::min<uint64_t>(dmax + 1, graph::HIST_DENSE);
+    TRY(comm_allreduce(c, c->d_hist, dense_n, CC_DT_I32, CC_OP_SUM));
+    // degrees beyond the dense bins: gather every rank's short tail list
+    if (dmax >= graph::HIST_DENSE) {
+      const uint64_t mytail = c->h_gctr[graph::G_TAIL];
+      if (mytail > TAILX) return fail(c, CC_ERR_INVALID, "more than %u degrees >= 2^20 on one rank", TAILX);
+      const uint64_t need = (uint64_t)world * (TAILX + 1);
+      if (!c->d_gath || c->gath_cap < need) {
+        TRY(dalloc_t(c, &c->d_gath, need));
+        c->gath_cap = need;
+      }
+      uint32_t* stage = c->d_gath + (uint64_t)world * TAILX;  // my count, then my entries
+      uint32_t nt32 = (uint32_t)mytail;
+      CK(cudaMemcpyAsync(stage, &nt32, sizeof(uint32_t), cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(stage + 1, c->d_tail, sizeof(uint32_t) * TAILX, cudaMemcpyDeviceToDevice, c->st));
+      uint32_t* gathered = nullptr;
+      TRY(dalloc_t(c, &gathered, (uint64_t)world * (TAILX + 1)));
+      TRY(comm_allgather(c, stage, gathered, sizeof(uint32_t) * (TAILX + 1)));
+      std::vector<uint32_t> h((size_t)world * (TAILX + 1)), merged;
+      CK(cudaMemcpyAsync(h.data(), gathered, sizeof(uint32_t) * h.size(), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      for (int k = 0; k < world; k++) {
+        const uint32_t* b = h.data() + (size_t)k * (TAILX + 1);
+        merged.insert(merged.end(), b + 1, b + 1 + b[0]);
+      }
+      CK(cudaMemcpyAsync(c->d_tail, merged.data(), sizeof(uint32_t) * merged.size(), cudaMemcpyHostToDevice,
+                         c->st));
+      const uint64_t tn = merged.size();
+      CK(cudaMemcpyAsync(c->d_gctr + graph::G_TAIL, &tn, sizeof(uint64_t), cudaMemcpyHostToDevice, c->st));
+      CK(cudaStreamSynchronize(c->st));
+    }
+  }
+  bool run_bfs = false;
+  uint64_t root = 0;
+  TRY(predict_gate(c, mode, want_hist, &run_bfs, &root));
+  e_pred = ev_get(c);
+  CK(cudaEventRecord(e_pred, c->st));
+
+  // ------------------------------------------------ owned CSR rows from the received arcs
+  uint32_t* Rt = reinterpret_cast<uint32_t*>(c->d_w[0]);
+  uint32_t* Pt = Rt + c->cap;
+  uint32_t *off = c->d_q[0], *cur = c->d_q[1];
+  CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
+  TRY(scan_epoch_guard(c));
+  const int gshift = csr::group_shift(n, na + (hi - lo));
+  uint32_t* garc = reinterpret_cast<uint32_t*>(c->d_gctr + graph::G_NUM);
+  uint64_t* gcur = c->d_gctr + graph::G_NUM + 512;
+  uint64_t* nlong = gcur + 1024;
+  csr::build(nullptr, na, c->d_deg, nullptr, n, off, cur, garc, gshift, c->ss, c->d_ctr, c->st);
+  CKL();
+  TRY(sync_read(c));
+  const uint64_t len = c->h_ctr[sv::C_VT_OUT];  // tuples of owned rows
+  if (len > c->cap) return fail(c, CC_ERR_INVALID, "tuple count exceeds capacity");
+  csr::fill(c->d_recv, na, off, cur, n, len, Rt, Pt, garc, gshift, gcur,
+            reinterpret_cast<uint2*>(c->d_w[1]), c->d_segB, nlong, c->st, /*directed=*/true);
+  c->launches += 6;
+  CKL();
+
+  // ------------------------------------------------ BFS peel (Alg. 2 lines 7-8)
+  uint64_t A_local = len;
+  e_bfs = e_filter = e_pred;
+  if (run_bfs) {
+    R.ran_bfs = 1;
+    R.bfs_root = root;
+    const uint64_t words = (uint64_t)world * blk / 32;  // >= nw: full bitmap in rank order
+    uint32_t *V = c->d_bm[0], *F = c->d_bm[1], *X = c->d_bm[2];
+    CK(cudaMemsetAsync(V, 0, sizeof(uint32_t) * words, c->st));
+    CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * words, c->st));
+    const uint32_t rw = 1u << (root & 31);
+    CK(cudaMemcpyAsync(V + root / 32, &rw, 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(F + root / 32, &rw, 4, cudaMemcpyHostToDevice, c->st));
+    uint64_t visited = 1, levels = 0;
+    uint64_t* newc = c->d_gctr + graph::G_NEWVIS;
+    while (true) {
+      CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * words, c->st));
+      CK(cudaMemsetAsync(newc, 0, sizeof(uint64_t), c->st));
+      { Prof k(c, KF_BFS);
+        if (hi > lo)
+          k_bfs_up<<<gsz(hi - lo, 148 * 16), DB, 0, c->st>>>(off, Pt, lo, hi, V, F, X,
+                                                            reinterpret_cast<unsigned long long*>(newc));
+        k.end(4.0 * (hi - lo) + 4.0 * (double)A_local, 1); }
+      CKL();
+      // the next frontier is the concatenation of the owned slices
+      TRY(comm_allgather(c, X + lo / 32, F, blk / 8));
+      if (!multi_gpu(c)) CK(cudaMemcpyAsync(F, X, sizeof(uint32_t) * words, cudaMemcpyDeviceToDevice, c->st));
+      k_bfs_merge<<<gsz(words, 148 * 8), DB, 0, c->st>>>(V, F, words);
+      TRY(comm_allreduce(c, newc, 1, CC_DT_I64, CC_OP_SUM));
+      c->launches += 2;
+      TRY(sync_read(c));
+      const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
+      if (nv == 0) break;
+      visited += nv;
+      levels++;
+    }
+    R.bfs_visited = visited;
+    R.bfs_levels = levels;
+    graph::launch_min_visited(V, n, c->d_gctr, c->st);
+    graph::launch_bfs_labels(V, n, c->d_label, c->d_gctr, c->st);
+    e_bfs = ev_get(c);
+    CK(cudaEventRecord(e_bfs, c->st));
+    // ---- filter: visited rows leave the tuple array
+    uint64_t* live = c->d_gctr + graph::G_REMAIN;
+    uint64_t* rows = c->d_ctr + sv::C_ERR;  // scratch counter
+    CK(cudaMemsetAsync(live, 0, sizeof(uint64_t), c->st));
+    CK(cudaMemsetAsync(rows, 0, sizeof(uint64_t), c->st));
+    if (len)
+      k_drop_visited<<<gsz(len, 148 * 8), DB, 0, c->st>>>(Rt, Pt, len, V,
+                                                         reinterpret_cast<unsigned long long*>(live),
+                                                         reinterpret_cast<unsigned long long*>(rows));
+    c->launches += 3;
+    CKL();
+    TRY(sync_read(c));
+    A_local = c->h_gctr[graph::G_REMAIN];
+    const uint64_t arcs_local = A_local - c->h_ctr[sv::C_ERR];
+    uint64_t* tmp = c->d_ctr + sv::C_ERR;
+    CK(cudaMemcpyAsync(tmp, &arcs_local, sizeof(uint64_t), cudaMemcpyHostToDevice, c->st));
+    TRY(comm_allreduce(c, tmp, 1, CC_DT_I64, CC_OP_SUM));
+    uint64_t arcs_all = 0;
+    CK(cudaMemcpyAsync(&arcs_all, tmp, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    R.remainder_edges = arcs_all / 2;
+    e_filter = ev_get(c);
+    CK(cudaEventRecord(e_filter, c->st));
+  }
+
+  // ------------------------------------------------ SV on the remaining rows (Alg. 2 line 13)
+  uint64_t* tmp = c->d_ctr + sv::C_ERR;
+  CK(cudaMemcpyAsync(tmp, &A_local, sizeof(uint64_t), cudaMemcpyHostToDevice, c->st));
+  TRY(comm_allreduce(c, tmp, 1, CC_DT_I64, CC_OP_SUM));
+  uint64_t A = 0;
+  CK(cudaMemcpyAsync(&A, tmp, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (A) TRY(sv_iterate(c, A, len));
+  R.sv_iterations = (uint32_t)c->iters.size();
+  e_sv = ev_get(c);
+  CK(cudaEventRecord(e_sv, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  R.ms_total = ev_ms(e0, e_sv);
+  R.ms_prediction = ev_ms(e0, e_pred);
+  R.ms_bfs = run_bfs ? ev_ms(e_pred, e_bfs) : 0;
+  R.ms_filter = run_bfs ? ev_ms(e_bfs, e_filter) : 0;
+  R.ms_sv = ev_ms(e_filter, e_sv);
+  (void)nw;
+  return CC_OK;
+}

@@ -11,10 +11,11 @@ void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* 
            uint32_t* off, uint32_t* cur, uint32_t* garc, int gshift, scan::State& ss, uint64_t* ctr,
            cudaStream_t st);
 // R fill, vertex tuples, and the two-level arc scatter (bucket by vertex group, then rows).
-// tmp: 2m uint2 scratch; longlist: n uint32 scratch; garc/gcur: 1024 entries.
+// tmp: 2m uint2 scratch; longlist: n uint32 scratch; garc/gcur: 1024 entries.  `directed`:
+// `edges` holds m arcs (r, p) instead of m undirected edges (two arcs each).
 void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
           uint32_t* R, uint32_t* P, const uint32_t* garc, int gshift, uint64_t* gcur, uint2* tmp,
-          uint32_t* longlist, uint64_t* nlong, cudaStream_t st);
+          uint32_t* longlist, uint64_t* nlong, cudaStream_t st, bool directed = false);
 // Row passes (sv_rows.cu).  Rows longer than LONG tuples (R_LONG set in R) are handled as
 // segments of at most LSEG tuples by warps (k_long1/k_long2); the segment list is rebuilt
 // after each compaction.
@@ -47,6 +48,9 @@ void temps2(const uint32_t* TB, uint64_t n, uint32_t* PB, cudaStream_t st);
 // changed2 after pass B (clears PA, NCP, TB)
 void pstat2(const uint32_t* PB, uint64_t n, uint32_t* PA, uint32_t* NCP, uint32_t* TB, uint64_t* ctr,
             cudaStream_t st);
+// multi-GPU slot exchange helpers: a[i] ^= 0x80000000; out[i] = OR_k parts[k*words + i]
+void flip_sign(uint32_t* a, uint64_t n, cudaStream_t st);
+void or_parts(const uint32_t* parts, uint64_t words, int world, uint32_t* out, cudaStream_t st);
 // ordered compaction of live tuples (R order kept); output count = live count
 void compact(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2,
              scan::State& ss, cudaStream_t st);

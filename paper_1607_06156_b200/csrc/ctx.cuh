@@ -1,0 +1,311 @@
+// ctx.cuh -- the library context (opaque cc_ctx of include/cc.h) and host helpers shared by
+// the single-GPU driver (cc_api.cu) and the multi-GPU driver (cc_dist.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/cc.h"
+#include "csr.cuh"
+#include "graph.cuh"
+#include "radix.cuh"
+#include "scan.cuh"
+#include "sv.cuh"
+
+using namespace cc;
+
+struct cc_ctx {
+  cc_config cfg{};
+  cudaStream_t st = nullptr;
+  std::string err;
+  // graph
+  bool loaded = false, ran = false;
+  cc_idw idw = CC_U32;
+  uint64_t n = 0, m = 0;
+  uint64_t m_total = 0;  // edges over all ranks
+  int kbits = 0;
+  uint2* d_edges = nullptr;
+  uint2* d_rem = nullptr;
+  uint2* d_rem2 = nullptr;
+  uint64_t* d_ids64 = nullptr;  // u64 mode: loaded endpoints (2m)
+  uint64_t* d_uids = nullptr;   // u64 mode: sorted distinct ids (rank -> id)
+  uint64_t n_alloc = 0;         // id bound the n-sized buffers were sized for
+  uint32_t* d_label = nullptr;
+  uint32_t* d_deg = nullptr;
+  uint32_t* d_hist = nullptr;
+  uint32_t* d_tail = nullptr;
+  uint32_t* d_bm[3] = {nullptr, nullptr, nullptr};  // visited, frontier, next
+  uint32_t* d_sbm[3] = {nullptr, nullptr, nullptr}; // direct SV: notpc, ncp, head
+  uint64_t* d_w[2] = {nullptr, nullptr};
+  uint32_t* d_q[2] = {nullptr, nullptr};
+  uint64_t cap = 0;
+  uint32_t* d_segA = nullptr;
+  uint32_t* d_segB = nullptr;
+  uint64_t* d_umin = nullptr;  // csr engine: tagged partial row minima / maxima
+  uint64_t* d_umax = nullptr;
+  csr::LongSeg* d_lsegs = nullptr;  // csr engine: segments of rows longer than csr::LONG
+  uint64_t* d_nlsegs = nullptr;
+  uint32_t row_tag = 0;
+  // multi-GPU (cc_dist.cu): owned vertex block [lo, hi), block size blk (multiple of 32)
+  uint64_t blk = 0, lo = 0, hi = 0;
+  uint2* d_send = nullptr;       // arcs grouped by owner rank
+  uint2* d_recv = nullptr;       // arcs received from all ranks (r in [lo, hi))
+  uint64_t recv_cap = 0;
+  uint32_t* d_gath = nullptr;    // allgather scratch (world_size x bitmap words)
+  uint64_t gath_cap = 0;
+  uint64_t* d_cnt = nullptr;     // per-owner arc counts (world_size^2 after the gather)
+  uint64_t* d_ctr = nullptr;   // sv counters
+  uint64_t* d_gctr = nullptr;  // graph counters
+  uint64_t* h_ctr = nullptr;   // pinned mirrors
+  uint64_t* h_gctr = nullptr;
+  uint32_t* h_hist = nullptr;  // pinned histogram staging
+  uint32_t* h_word = nullptr;
+  radix::Workspace rws;
+  scan::State ss;
+  std::vector<std::pair<void*, size_t>> allocs;
+  // report
+  std::vector<cc_iter_stat> iters;
+  cc_report rep{};
+  uint64_t launches = 0;
+  // profiling (CC_FLAG_TRACE): per-family events
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<cudaEvent_t> it_ev;  // SV iteration start events
+  struct KStat {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    double bytes = 0, ms = 0;
+    uint64_t launches = 0;
+  } kst[16];
+};
+
+// ------------------------------------------------------------------------------ helpers
+static inline cc_status fail(cc_ctx* c, cc_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, e_ == cudaErrorMemoryAllocation ? CC_ERR_NOMEM : CC_ERR_CUDA,        \
+                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define CKL()                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, CC_ERR_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+#define TRY(x)                        \
+  do {                                \
+    cc_status s_ = (x);               \
+    if (s_ != CC_OK) return s_;       \
+  } while (0)
+
+static inline cc_status dalloc(cc_ctx* c, void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (c->cfg.alloc) {
+    *p = c->cfg.alloc(bytes, (void*)c->st, c->cfg.alloc_user);
+    if (!*p) return fail(c, CC_ERR_NOMEM, "allocator hook returned NULL for %zu bytes", bytes);
+  } else {
+    cudaError_t e = cudaMallocAsync(p, bytes, c->st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, CC_ERR_NOMEM, "cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
+  }
+  c->allocs.push_back({*p, bytes});
+  return CC_OK;
+}
+template <typename T>
+static inline cc_status dalloc_t(cc_ctx* c, T** p, size_t count) {
+  return dalloc(c, reinterpret_cast<void**>(p), count * sizeof(T));
+}
+static inline void dfree_all(cc_ctx* c) {
+  for (auto& a : c->allocs) {
+    if (c->cfg.free) c->cfg.free(a.first, a.second, (void*)c->st, c->cfg.alloc_user);
+    else cudaFreeAsync(a.first, c->st);
+  }
+  c->allocs.clear();
+  c->d_edges = c->d_rem = c->d_rem2 = nullptr;
+  c->d_ids64 = c->d_uids = nullptr;
+  c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
+  c->d_umin = c->d_umax = c->d_nlsegs = nullptr;
+  c->d_send = c->d_recv = nullptr;
+  c->d_gath = nullptr;
+  c->d_cnt = nullptr;
+  c->recv_cap = c->gath_cap = 0;
+  c->d_lsegs = nullptr;
+  c->row_tag = 0;
+  c->d_bm[0] = c->d_bm[1] = c->d_bm[2] = nullptr;
+  c->d_sbm[0] = c->d_sbm[1] = c->d_sbm[2] = nullptr;
+  c->d_w[0] = c->d_w[1] = nullptr;
+  c->d_q[0] = c->d_q[1] = nullptr;
+  c->d_ctr = c->d_gctr = nullptr;
+  c->rws = radix::Workspace();
+  c->ss = scan::State();
+  c->cap = 0;
+}
+
+static inline cudaEvent_t ev_get(cc_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+static inline float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+static inline bool profiling(const cc_ctx* c) { return (c->cfg.flags & CC_FLAG_PROFILE) != 0; }
+
+// kernel families timed under CC_FLAG_PROFILE (cc_kernel_stats / cc_kernel_name)
+enum KFam { KF_RADIX = 0, KF_SVITER, KF_BFS, KF_ROWA, KF_ROWB, KF_SLOTS, KF_CSR, KF_PREDICT,
+            KF_COMPACT, KF_N };
+static const char* const kKfNames[KF_N] = {
+    "k_hist+k_onesweep (radix regroup)", "SV iteration (all bucket passes)", "k_bfs_level",
+    "k_rowpass<A>+k_rowfix (Alg.1 lines 8-16)", "k_rowpass<B>+k_rowfix (Alg.1 lines 17-25)",
+    "k_pstat1/k_temps2/k_pstat2 (partition slot scans)",
+    "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)", "prediction (k_degree, k_deg_hist)",
+    "k_compact (ordered exclusion of completed rows)"};
+
+struct Prof {
+  cc_ctx* c;
+  int f;
+  cudaEvent_t a = nullptr;
+  Prof(cc_ctx* c_, int f_) : c(c_), f(f_) {
+    if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
+  }
+  void end(double bytes, uint64_t nl) {
+    if (!profiling(c)) return;
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->st);
+    c->kst[f].ev.push_back({a, b});
+    c->kst[f].bytes += bytes;
+    c->kst[f].launches += nl;
+  }
+};
+
+static inline int bits_for(uint64_t n) {
+  int b = 0;
+  while (b < 63 && (1ull << b) < n) b++;
+  return b;
+}
+
+// ------------------------------------------------------------------------------ ABI
+
+struct Timer {
+  cc_ctx* c;
+  cudaEvent_t a;
+  explicit Timer(cc_ctx* c_) : c(c_), a(ev_get(c_)) { cudaEventRecord(a, c->st); }
+  std::pair<cudaEvent_t, cudaEvent_t> stop() {
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->st);
+    return {a, b};
+  }
+};
+
+static inline cc_status sync_read(cc_ctx* c) {
+  CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(uint64_t) * sv::C_NUM, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->h_gctr, c->d_gctr, sizeof(uint64_t) * graph::G_NUM, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return CC_OK;
+}
+
+// radix sort wrapper with optional per-call timing
+static inline void seg_begin(cc_ctx* c, cudaEvent_t* a) {
+  if (profiling(c)) { *a = ev_get(c); cudaEventRecord(*a, c->st); }
+}
+static inline void seg_end(cc_ctx* c, cudaEvent_t a, double bytes, int nl, int fam = KF_SVITER) {
+  if (profiling(c)) {
+    cudaEvent_t b = ev_get(c);
+    cudaEventRecord(b, c->st);
+    c->kst[fam].ev.push_back({a, b});
+    c->kst[fam].bytes += bytes;
+    c->kst[fam].launches += nl;
+  }
+}
+
+static inline cc_status scan_epoch_guard(cc_ctx* c) {
+  if (((c->ss.epoch + 4) & scan::EPOCH_MASK) < 4) {
+    CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * c->ss.max_tiles, c->st));
+    c->ss.epoch += 8;
+  }
+  return CC_OK;
+}
+
+// ------------------------------------------------------------------------------ collectives
+// Thin wrappers over the caller's cc_comm (world_size > 1): synchronise the stream, call,
+// map a nonzero return to CC_ERR_COMM.  No-ops on one GPU.
+static inline bool multi_gpu(const cc_ctx* c) { return c->cfg.world_size > 1; }
+static inline cc_status comm_allreduce(cc_ctx* c, void* buf, uint64_t count, int dt, int op) {
+  if (!multi_gpu(c)) return CC_OK;
+  CK(cudaStreamSynchronize(c->st));
+  if (c->cfg.comm->allreduce(c->cfg.comm->user, buf, count, dt, op, (void*)c->st) != 0)
+    return fail(c, CC_ERR_COMM, "allreduce(count=%llu, dtype=%d, op=%d) failed",
+                (unsigned long long)count, dt, op);
+  return CC_OK;
+}
+static inline cc_status comm_allgather(cc_ctx* c, const void* send, void* recv, uint64_t bytes) {
+  if (!multi_gpu(c)) return CC_OK;
+  CK(cudaStreamSynchronize(c->st));
+  if (c->cfg.comm->allgather(c->cfg.comm->user, send, recv, bytes, (void*)c->st) != 0)
+    return fail(c, CC_ERR_COMM, "allgather(%llu bytes) failed", (unsigned long long)bytes);
+  return CC_OK;
+}
+static inline cc_status comm_alltoallv(cc_ctx* c, const void* send, const uint64_t* sb, void* recv,
+                                       const uint64_t* rb) {
+  if (!multi_gpu(c)) return CC_OK;
+  CK(cudaStreamSynchronize(c->st));
+  if (c->cfg.comm->alltoallv(c->cfg.comm->user, send, sb, recv, rb, (void*)c->st) != 0)
+    return fail(c, CC_ERR_COMM, "alltoallv failed");
+  return CC_OK;
+}
+// min over ranks of u32 slots (INF = 0xFFFFFFFF): flip the sign bit so that the signed order of
+// the exchanged int32 equals the unsigned order, reduce, flip back
+static inline cc_status comm_min_u32(cc_ctx* c, uint32_t* a, uint64_t count) {
+  if (!multi_gpu(c)) return CC_OK;
+  csr::flip_sign(a, count, c->st);
+  TRY(comm_allreduce(c, a, count, CC_DT_I32, CC_OP_MIN));
+  csr::flip_sign(a, count, c->st);
+  c->launches += 2;
+  return CC_OK;
+}
+// OR over ranks of a bitmap (NCCL has no bitwise reduction): gather every rank's words, fold
+static inline cc_status comm_or_bits(cc_ctx* c, uint32_t* bm, uint64_t words) {
+  if (!multi_gpu(c)) return CC_OK;
+  const uint64_t need = words * (uint64_t)c->cfg.world_size;
+  if (!c->d_gath || c->gath_cap < need) {
+    TRY(dalloc_t(c, &c->d_gath, need));
+    c->gath_cap = need;
+  }
+  TRY(comm_allgather(c, bm, c->d_gath, words * sizeof(uint32_t)));
+  csr::or_parts(c->d_gath, words, c->cfg.world_size, bm, c->st);
+  c->launches += 1;
+  return CC_OK;
+}
+
+// Prediction stage on the host (cc_api.cu): gate fit and route from the device statistics.
+cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs, uint64_t* root);
+
+// Alg. 1 iterations of the r-stationary engine on a built tuple array (cc_api.cu); with
+// world_size > 1 the partition slots are combined across ranks after each row pass.
+cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len);
+
+// cc_run for world_size > 1 (cc_dist.cu).
+cc_status run_dist(cc_ctx* c, cc_mode mode);

@@ -75,7 +75,7 @@ constexpr int SBINS = 2048;
 __global__ void __launch_bounds__(BLOCK) k_deg_hist(const uint32_t* __restrict__ deg, uint64_t n,
                                                     uint32_t* __restrict__ hist,
                                                     uint32_t* __restrict__ tail,
-                                                    unsigned long long* gctr) {
+                                                    unsigned long long* gctr, uint64_t id0) {
   __shared__ uint32_t sh[SBINS];
   for (int i = threadIdx.x; i < SBINS; i += BLOCK) sh[i] = 0;
   __syncthreads();
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(BLOCK) k_deg_hist(const uint32_t* __restrict__
     uint32_t d = v < n ? deg[v] : 0u;
     if (d) {
       npres++;
-      unsigned long long key = ((unsigned long long)d << 32) | (0xFFFFFFFFu - (uint32_t)v);
+      unsigned long long key = ((unsigned long long)d << 32) | (0xFFFFFFFFu - (uint32_t)(v + id0));
       best = key > best ? key : best;
     }
     uint32_t bin = (d && d < SBINS) ? d : (SBINS + (threadIdx.x & 31));
@@ -116,10 +116,10 @@ __global__ void __launch_bounds__(BLOCK) k_deg_hist(const uint32_t* __restrict__
   }
 }
 void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* tail,
-                     uint64_t* gctr, cudaStream_t st) {
+                     uint64_t* gctr, cudaStream_t st, uint64_t base) {
   if (!n) return;
   k_deg_hist<<<grid_for(n, 148 * 4), BLOCK, 0, st>>>(deg, n, hist, tail,
-                                                       reinterpret_cast<unsigned long long*>(gctr));
+                                                       reinterpret_cast<unsigned long long*>(gctr), base);
 }
 
 // ---------------------------------------------------------------- BFS peel

@@ -22,8 +22,9 @@ enum GCtr : int {
 
 void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr, cudaStream_t st);
 void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st);
+// deg[0, n) are the degrees of ids base .. base+n-1 (base > 0: a rank's vertex block)
 void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* tail,
-                     uint64_t* gctr, cudaStream_t st);
+                     uint64_t* gctr, cudaStream_t st, uint64_t base = 0);
 // edge-streaming BFS level over 2-bit vertex state S (16 ids per word: bit0 visited, bit1
 // frontier); newly visited count in gctr[G_NEWVIS]; with `compact`, edges with an endpoint
 // unvisited at the start of the level are appended to `out` (count in gctr[G_REMAIN]).

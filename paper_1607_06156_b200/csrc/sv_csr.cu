@@ -26,7 +26,6 @@ namespace cc {
 namespace csr {
 
 constexpr int B = 256;
-constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr uint32_t DEAD = 0xFFFFFFFFu;  // P of a tuple whose partition completed
 
 CC_DEVI void min_slot(uint32_t* a, uint32_t i, uint32_t v) {
@@ -159,25 +158,34 @@ __global__ void k_gscan(const uint32_t* __restrict__ garc, int G, unsigned long 
 // inside one small window of P at a time (L2-resident, no partial-sector DRAM writes).
 constexpr int BITEMS = 8;
 constexpr int MAXG = 1024;
+// DIRECTED: the input is already arcs (r, p) (multi-GPU: arcs received by their owner),
+// one tuple each; otherwise undirected edges, two tuples each.
+template <bool DIRECTED>
 __global__ void __launch_bounds__(B) k_bucket(const uint2* __restrict__ e, uint64_t m, int gshift,
                                               int G, unsigned long long* gcur,
                                               uint2* __restrict__ out) {
+  constexpr int PER = DIRECTED ? 1 : 2;
   __shared__ uint32_t s_cnt[MAXG];
   __shared__ unsigned long long s_base[MAXG];
   for (int g = threadIdx.x; g < G; g += B) s_cnt[g] = 0;
   __syncthreads();
   const uint64_t e0 = (blockIdx.x * (uint64_t)B * BITEMS) + threadIdx.x;
-  uint2 arc[2 * BITEMS];
-  uint32_t slot[2 * BITEMS];
+  uint2 arc[PER * BITEMS];
+  uint32_t slot[PER * BITEMS];
 #pragma unroll
   for (int k = 0; k < BITEMS; k++) {
     const uint64_t i = e0 + (uint64_t)k * B;
     if (i < m) {
       const uint2 xy = e[i];
-      arc[2 * k] = make_uint2(xy.y, xy.x);      // <x,_,y>: r = y, p = x
-      arc[2 * k + 1] = make_uint2(xy.x, xy.y);  // <y,_,x>: r = x, p = y
-      slot[2 * k] = atomicAdd(&s_cnt[xy.y >> gshift], 1u);
-      slot[2 * k + 1] = atomicAdd(&s_cnt[xy.x >> gshift], 1u);
+      if (DIRECTED) {
+        arc[k] = xy;
+        slot[k] = atomicAdd(&s_cnt[xy.x >> gshift], 1u);
+      } else {
+        arc[PER * k] = make_uint2(xy.y, xy.x);      // <x,_,y>: r = y, p = x
+        arc[PER * k + PER - 1] = make_uint2(xy.x, xy.y);  // <y,_,x>: r = x, p = y
+        slot[PER * k] = atomicAdd(&s_cnt[xy.y >> gshift], 1u);
+        slot[PER * k + PER - 1] = atomicAdd(&s_cnt[xy.x >> gshift], 1u);
+      }
     }
   }
   __syncthreads();
@@ -188,8 +196,9 @@ __global__ void __launch_bounds__(B) k_bucket(const uint2* __restrict__ e, uint6
   for (int k = 0; k < BITEMS; k++) {
     const uint64_t i = e0 + (uint64_t)k * B;
     if (i < m) {
-      out[s_base[arc[2 * k].x >> gshift] + slot[2 * k]] = arc[2 * k];
-      out[s_base[arc[2 * k + 1].x >> gshift] + slot[2 * k + 1]] = arc[2 * k + 1];
+#pragma unroll
+      for (int t = 0; t < PER; t++)
+        out[s_base[arc[PER * k + t].x >> gshift] + slot[PER * k + t]] = arc[PER * k + t];
     }
   }
 }
@@ -268,7 +277,7 @@ void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* 
 }
 void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
           uint32_t* R, uint32_t* P, const uint32_t* garc, int gshift, uint64_t* gcur, uint2* tmp,
-          uint32_t* longlist, uint64_t* nlong, cudaStream_t st) {
+          uint32_t* longlist, uint64_t* nlong, cudaStream_t st, bool directed) {
   if (!A) return;
   const int G = (int)(((n - 1) >> gshift) + 1);
   auto* nl = reinterpret_cast<unsigned long long*>(nlong);
@@ -278,8 +287,11 @@ void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, ui
   if (!m) return;
   auto* gc = reinterpret_cast<unsigned long long*>(gcur);
   k_gscan<<<1, B, 0, st>>>(garc, G, gc);
-  k_bucket<<<(unsigned)((m + B * BITEMS - 1) / (B * BITEMS)), B, 0, st>>>(edges, m, gshift, G, gc, tmp);
-  k_scatter<<<grid(2 * m, B, 148 * 16), B, 0, st>>>(tmp, 2 * m, cur, P);
+  const unsigned gb = (unsigned)((m + B * BITEMS - 1) / (B * BITEMS));
+  if (directed) k_bucket<true><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp);
+  else k_bucket<false><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp);
+  const uint64_t na = directed ? m : 2 * m;
+  k_scatter<<<grid(na, B, 148 * 16), B, 0, st>>>(tmp, na, cur, P);
 }
 void compact(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2,
              scan::State& ss, cudaStream_t st) {

@@ -74,17 +74,6 @@ CC_DEVI unsigned long long tmax(uint32_t tag, uint32_t v) {
   return ((unsigned long long)tag << 32) | v;
 }
 
-CC_DEVI void load8(const uint32_t* X, uint64_t i0, uint64_t L, uint32_t fill, uint32_t* x) {
-  if (i0 + RITEMS <= L) {
-    const uint4 a = ldg_stream(reinterpret_cast<const uint4*>(X + i0));
-    const uint4 b = ldg_stream(reinterpret_cast<const uint4*>(X + i0 + 4));
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-  } else {
-#pragma unroll
-    for (int j = 0; j < RITEMS; j++) x[j] = (i0 + j < L) ? X[i0 + j] : fill;
-  }
-}
 CC_DEVI void store8(uint32_t* X, uint64_t i0, uint64_t L, const uint32_t* x) {
   if (i0 + RITEMS <= L) {
     reinterpret_cast<uint4*>(X + i0)[0] = make_uint4(x[0], x[1], x[2], x[3]);
@@ -532,7 +521,30 @@ __global__ void __launch_bounds__(RB) k_pstat2(const uint32_t* __restrict__ PB, 
   if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
 }
 
+// --------------------------------------------------------------------------- exchange helpers
+__global__ void k_flip_sign(uint32_t* a, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < n; i += (uint64_t)gridDim.x * RB)
+    a[i] ^= 0x80000000u;
+}
+__global__ void k_or_parts(const uint32_t* __restrict__ parts, uint64_t words, int world,
+                           uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < words; i += (uint64_t)gridDim.x * RB) {
+    uint32_t x = 0;
+    for (int k = 0; k < world; k++) x |= parts[(uint64_t)k * words + i];
+    out[i] = x;
+  }
+}
+
 // --------------------------------------------------------------------------- launchers
+void flip_sign(uint32_t* a, uint64_t n, cudaStream_t st) {
+  if (n) k_flip_sign<<<(unsigned)std::min<uint64_t>((n + RB - 1) / RB, 148 * 8), RB, 0, st>>>(a, n);
+}
+void or_parts(const uint32_t* parts, uint64_t words, int world, uint32_t* out, cudaStream_t st) {
+  if (words)
+    k_or_parts<<<(unsigned)std::min<uint64_t>((words + RB - 1) / RB, 148 * 8), RB, 0, st>>>(parts, words,
+                                                                                            world, out);
+}
+
 static unsigned persistent_grid(const void* fn, uint64_t ntiles) {
   int ps = 0, sms = 148, dev = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, RB, 0);

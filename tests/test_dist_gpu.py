@@ -1,0 +1,103 @@
+"""Multi-GPU path (world_size > 1) on one B200: 2-4 ranks run as processes
+that share cuda:0 and exchange through gloo (host copies) -- no kernel waits on another rank,
+so sharing the device is safe.  Each rank loads its block of the edge list; the concatenated
+label blocks must equal the union-find oracle bit for bit, and the SV counters (computed
+from the rank-combined partition slots) must equal the Alg. 1 transcription, i.e. be
+independent of the number of ranks (SURVEY.md §8(c) 'multi-GPU' pin)."""
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from oracle import sv as osv
+from dist_util import run_ranks
+
+pytestmark = pytest.mark.gpu
+
+
+def _rank_run(rank, world, n, edges, modes, flags):
+    import torch
+    import paper_1607_06156_b200 as cc
+    torch.cuda.set_device(0)
+    comm = cc.TorchComm(device=torch.device("cuda", 0))
+    ctx = cc.CC(device=0, flags=cc.CC_FLAG_TRACE | flags, comm=comm)
+    m = edges.shape[0]
+    a, b = m * rank // world, m * (rank + 1) // world  # block distribution
+    ctx.load(np.ascontiguousarray(edges[a:b]), n)
+    out = {}
+    for mode in modes:
+        rep = ctx.run(mode)
+        lo, hi = ctx.block_range()
+        out[mode] = (lo, hi, ctx.labels().copy(), rep)
+    ctx.close()
+    return out
+
+
+def _check(res, n, edges, modes, trace=True):
+    want = oracle.uf_labels(n, edges)
+    for mode in modes:
+        lab = np.zeros(n, dtype=np.uint32)
+        covered = 0
+        for r in res:
+            lo, hi, l, rep = r[mode]
+            lab[lo:hi] = l
+            covered += hi - lo
+        assert covered == n
+        assert np.array_equal(lab, want), mode
+        reps = [r[mode][3] for r in res]
+        assert len({rep["sv_iterations"] for rep in reps}) == 1
+        assert all(rep["m_edges"] == edges.shape[0] for rep in reps)
+        if trace and mode == "sv":
+            _, tr = osv.sv_trace(n, edges)
+            got = [dict(A=it["active_in"], P=it["partitions"], T=it["temps"],
+                        completed=it["completed"], changed=it["changed"], changed2=it["changed2"])
+                   for it in reps[0]["iters"]]
+            assert [{k: int(v) for k, v in d.items()} for d in got] == \
+                [{k: int(d[k]) for k in ("A", "P", "T", "completed", "changed", "changed2")} for d in tr]
+    return want
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_c1(world):
+    g = graphgen.make("c1", 0.5)
+    modes = ("sv", "auto", "bfs+sv")
+    _check(run_ranks(_rank_run, world, g.n, g.edges, modes, 0), g.n, g.edges, modes)
+
+
+def test_dist_rmat_bfs_route():
+    g = graphgen.rmat_scale_graph(14)
+    modes = ("auto", "sv")
+    res = run_ranks(_rank_run, 2, g.n, g.edges, modes, 0)
+    want = _check(res, g.n, g.edges, modes)
+    from oracle import bfs as obfs
+    from oracle import degree as odeg
+    deg, _ = odeg.degree_distribution(g.n, g.edges)
+    root = obfs.bfs_root(deg)
+    vis, levels = obfs.bfs(g.n, g.edges, root)
+    for r in res:
+        rep = r["auto"][3]
+        assert rep["ran_bfs"] == 1
+        assert rep["bfs_root"] == root
+        assert rep["bfs_visited"] == int(vis.sum())
+        assert rep["bfs_levels"] == levels
+        assert rep["remainder_edges"] == obfs.filter_edges(g.edges, vis).shape[0]
+        assert rep["n_present"] == int(np.count_nonzero(deg))
+        assert rep["max_degree"] == int(deg.max())
+
+
+def test_dist_edge_cases():
+    # a path and a star whose rows cross rank blocks and tile edges; an isolated tail of ids
+    n = 70000
+    perm = np.random.default_rng(5).permutation(n - 100).astype(np.uint32)
+    path = np.stack([perm[:-1], perm[1:]], 1)
+    star = np.stack([np.full(3000, 11, np.uint32), np.arange(20000, 23000, dtype=np.uint32)], 1)
+    e = np.concatenate([path[:40000], star, path[40000:], [[5, 5], [5, 5]]]).astype(np.uint32)
+    _check(run_ranks(_rank_run, 2, n, e, ("sv", "bfs+sv"), 0), n, e, ("sv", "bfs+sv"))
+    # fewer edges than ranks: some ranks load nothing
+    e2 = np.array([[0, 1], [2, 3]], np.uint32)
+    _check(run_ranks(_rank_run, 3, 40, e2, ("sv", "auto"), 0), 40, e2, ("sv", "auto"))
+
+
+def test_dist_matches_single_gpu_c2_sample():
+    g = graphgen.make("c2", 0.05)
+    _check(run_ranks(_rank_run, 2, g.n, g.edges, ("auto",), 0), g.n, g.edges, ("auto",), trace=False)
