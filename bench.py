@@ -9,8 +9,9 @@ list already resident in HBM.  See DESIGN.md §6 for the byte models behind `roo
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--mode auto]
   python bench.py --impl reference ...      # the CPU oracle, timed on the host cores
 
-N > 1 (torchrun, one process per GPU): every rank runs its own graph instance (seed offset
-by rank) -- independent problems, weak scaling, no data-path collective.
+N > 1 (torchrun, one process per GPU): the same workload sharded over the ranks -- rank k
+loads block k of the edge list, the library regroups arcs to vertex-block owners and combines
+partition slots over NCCL (cc_comm over torch.distributed) -- strong scaling.
 """
 from __future__ import annotations
 
@@ -107,10 +108,15 @@ def dist_info():
     return ws, rk, lr
 
 
-def make_graph(cfg, rank):
+def make_graph(cfg):
     import graphgen
-    seed = None if rank == 0 else graphgen.BASE_SEED + {"c1": 1, "c2": 2, "c3": 3, "c4": 4}[cfg] + 1000 * rank
-    return graphgen.make(cfg, 1.0, seed=seed)
+    return graphgen.make(cfg, 1.0)
+
+
+def shard(edges, rank, ws):
+    """Block distribution of the edge list over the ranks."""
+    m = edges.shape[0]
+    return np.ascontiguousarray(edges[m * rank // ws:m * (rank + 1) // ws])
 
 
 def alg_bytes(rep, n, m):
@@ -136,7 +142,7 @@ def run_reference(args):
     if rk != 0:
         return 0
     import oracle
-    g = make_graph(args.config, 0)
+    g = make_graph(args.config)
     oracle.build()
     for _ in range(args.warmup):
         oracle.uf_labels(g.n, g.edges)
@@ -148,7 +154,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "n": g.n, "m": g.m, "mode": "auto"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -195,17 +201,27 @@ def main():
     import paper_1607_06156_b200 as cc
 
     ws, rk, lr = dist_info()
+    # CC_DIST_BACKEND=gloo CC_SHARE_GPU=1 exercise the N > 1 code path on one GPU (correctness
+    # only: ranks then share the device and exchange through host memory)
+    backend = os.environ.get("CC_DIST_BACKEND", "nccl")
+    if os.environ.get("CC_SHARE_GPU") == "1":
+        lr = 0
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(lr)
     dev = torch.device("cuda", lr)
     stream = torch.cuda.current_stream(dev)
 
-    g = make_graph(args.config, rk)
+    g = make_graph(args.config)
     n, m = g.n, g.m
+    mine = shard(g.edges, rk, ws)
     flags = cc.CC_FLAG_PROFILE | cc.REGROUP_FLAGS[args.regroup]
-    ctx = cc.CC(device=lr, stream=stream, flags=flags)
-    d_edges = torch.from_numpy(g.edges.view(np.int32)).to(dev)
+    comm = cc.TorchComm(device=dev) if ws > 1 else None
+    ctx = cc.CC(device=lr, stream=stream, flags=flags, comm=comm)
+    d_edges = torch.from_numpy(mine.view(np.int32)).to(dev)
     ctx.load(d_edges, n)
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -238,17 +254,19 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    red_dev = dev if backend == "nccl" else "cpu"
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = ws * m * args.steps / (ms_max / 1e3)
+    value = m * args.steps / (ms_max / 1e3)
 
     # ---------------- e2e: host buffers through the public API (H2D + run + D2H)
     e2e = None
     if not args.no_e2e:
-        host = torch.from_numpy(g.edges.view(np.int32)).pin_memory()
-        hout = torch.empty(n, dtype=torch.int32).pin_memory()
+        host = torch.from_numpy(mine.view(np.int32)).pin_memory()
+        lo, hi = ctx.block_range()
+        hout = torch.empty(hi - lo, dtype=torch.int32).pin_memory()
         hnp = host.numpy().view(np.uint32)
         onp = hout.numpy().view(np.uint32)
         for _ in range(2):
@@ -268,13 +286,15 @@ def main():
             ctx.labels(onp)
         e1.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
         if ws > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": ws * m * ke / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(g.edges.nbytes), "d2h_bytes_per_step": int(4 * n),
+        e2e = {"value": m * ke / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(mine.nbytes), "d2h_bytes_per_step": int(4 * (hi - lo)),
                "steps": ke}
-        ok = np.array_equal(onp, __import__("oracle").uf_labels(n, g.edges)) if rk == 0 else None
+        ok = None
+        if rk == 0:
+            ok = bool(np.array_equal(onp, __import__("oracle").uf_labels(n, g.edges)[lo:hi]))
 
     if rk == 0:
         peak, peak_src = peaks()
@@ -301,14 +321,15 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "n": n, "m": m, "mode": args.mode,
                        "regroup": args.regroup,
                        "route": "bfs+sv" if rep["ran_bfs"] else "sv",
                        "sv_iterations": rep["sv_iterations"],
                        "l2": "flushed between timed steps (256 MiB write, outside step events)",
-                       "parallelism": f"{ws} independent instance(s)"},
+                       "parallelism": (f"{ws} ranks: edge blocks, vertex-block owners, NCCL slot "
+                                       "exchange" if ws > 1 else "1 GPU")},
             "roofline": {"bound": "hbm", "kernel": names[dom] if dom is not None else None,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
