@@ -187,7 +187,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="auto", choices=["auto", "sv", "bfs+sv"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--regroup", default="csr", choices=["csr", "direct", "sort"],
+    ap.add_argument("--regroup", default="csr", choices=["csr", "csrbfs", "direct", "sort"],
                     help="SV bucket regroup engine (DESIGN.md §5.3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -69,6 +69,9 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
 #define CC_FLAG_REGROUP_SORT 0x8u
 #define CC_FLAG_REGROUP_DIRECT 0x20u
 #define CC_FLAG_PROFILE 0x10u        /* CUDA-event timing of kernel families (cc_kernel_stats) */
+#define CC_FLAG_BFS_CSR 0x40u        /* csr engine: degrees from the bucketed CSR build and a
+                                        direction-optimising (top-down / bottom-up) BFS on the
+                                        CSR rows instead of the edge-streaming BFS            */
 
 /* ---- multi-GPU exchange (world_size > 1).  The library runs one process per GPU; the
  * caller supplies the collectives (e.g. torch.distributed over NCCL, NVLink/NVSwitch).  Every

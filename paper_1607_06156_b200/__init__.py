@@ -27,8 +27,9 @@ CC_FLAG_GATE_KS = 0x2
 CC_FLAG_NO_EARLY_EXCLUDE = 0x4
 CC_FLAG_REGROUP_SORT = 0x8
 CC_FLAG_REGROUP_DIRECT = 0x20
-REGROUP_FLAGS = {"csr": 0, "sort": 0x8, "direct": 0x20}
+REGROUP_FLAGS = {"csr": 0, "sort": 0x8, "direct": 0x20, "csrbfs": 0x40}
 CC_FLAG_PROFILE = 0x10
+CC_FLAG_BFS_CSR = 0x40
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)

@@ -26,6 +26,7 @@
 #include "csr.cuh"
 #include "relabel.cuh"
 #include "ctx.cuh"
+#include "bfs.cuh"
 
 using namespace cc;
 
@@ -149,7 +150,9 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   CK(cudaMemsetAsync(c->d_umin, 0xFF, sizeof(uint64_t) * (n + 1), c->st));
   CK(cudaMemsetAsync(c->d_umax, 0, sizeof(uint64_t) * (n + 1), c->st));
   TRY(dalloc_t(c, &c->d_ctr, sv::C_NUM));
-  TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM + 512 + 1024 + 8));  // + CSR group scratch
+  TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM + 512 + 1024 + 8));  // + relabel scratch
+  TRY(dalloc_t(c, &c->d_garc, 2048 + 8));
+  TRY(dalloc_t(c, &c->d_gcur, 2048 + 8));
   if (w == CC_U64) {
     TRY(dalloc_t(c, &c->d_ids64, 2 * m + 1));
     TRY(dalloc_t(c, &c->d_uids, 2 * m + 1));
@@ -295,9 +298,9 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
   seg_begin(c, &a);
   TRY(scan_epoch_guard(c));
   const int gshift = csr::group_shift(n, 2 * m_sv + n);
-  uint32_t* garc = reinterpret_cast<uint32_t*>(c->d_gctr + graph::G_NUM);  // 1024 u32
-  uint64_t* gcur = c->d_gctr + graph::G_NUM + 512;                           // 1024 u64
-  uint64_t* nlong = gcur + 1024;
+  uint32_t* garc = c->d_garc;
+  uint64_t* gcur = c->d_gcur;
+  uint64_t* nlong = gcur + 2048;
   csr::build(edges, m_sv, c->d_deg, vis, n, off, cur, garc, gshift, c->ss, c->d_ctr, c->st);
   c->launches += 1;
   CKL();
@@ -618,11 +621,29 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   e_rel = ev_get(c);
   CK(cudaEventRecord(e_rel, c->st));
   // ------------------------------------------------ prediction (Alg. 2 lines 2-3)
-  CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
+  // csr engine, n <= 2^26: the arcs are bucketed by vertex group (the CSR build needs this
+  // pass anyway) and degrees are counted per group in shared memory; otherwise counting
+  // increments in L2 windows.
+  // CC_FLAG_BFS_CSR: build the full CSR during prediction (degrees counted per bucketed vertex
+  // group in shared memory) and peel with the direction-optimising BFS on it.  Off by default:
+  // on C4 the 2.2 G-tuple CSR build costs more than the edge-streaming BFS saves.
+  const bool csr_engine = !(c->cfg.flags & (CC_FLAG_REGROUP_SORT | CC_FLAG_REGROUP_DIRECT));
+  const int gsf = (csr_engine && (c->cfg.flags & CC_FLAG_BFS_CSR)) ? csr::group_shift_full(n) : -1;
+  uint2* bucketed = reinterpret_cast<uint2*>(c->d_w[1]);  // 2m arcs fit: cap >= 2m + 2n
   CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
   CK(cudaMemsetAsync(c->d_gctr + graph::G_MINVIS, 0xFF, sizeof(uint64_t), c->st));
   sv::launch_init_labels(c->d_label, n, c->st);
-  graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st);
+  {
+    Prof k(c, KF_PREDICT);
+    if (gsf >= 0) {
+      csr::bucket_degrees(c->d_edges, m, n, gsf, c->d_garc, c->d_gcur, bucketed, c->d_deg, c->st);
+      k.end(8.0 * m + 8.0 * m + 16.0 * m + 16.0 * m + 4.0 * n, 4);
+    } else {
+      CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
+      graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st);
+      k.end(8.0 * m + 4.0 * n, 1);
+    }
+  }
   const bool want_hist = (mode == CC_MODE_AUTO) || (c->cfg.flags & CC_FLAG_TRACE);
   if (want_hist) CK(cudaMemsetAsync(c->d_hist, 0, sizeof(uint32_t) * graph::HIST_DENSE, c->st));
   graph::launch_deg_hist(c->d_deg, n, c->d_hist, c->d_tail, c->d_gctr, c->st);
@@ -634,12 +655,92 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   e_pred = ev_get(c);
   CK(cudaEventRecord(e_pred, c->st));
 
+  // ------------------------------------------------ full CSR rows (csr engine, both routes)
+  uint64_t A_full = 0;
+  if (gsf >= 0) {
+    uint32_t* R0 = reinterpret_cast<uint32_t*>(c->d_w[0]);
+    uint32_t* P0 = R0 + c->cap;
+    cudaEvent_t a = nullptr;
+    seg_begin(c, &a);
+    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
+    TRY(scan_epoch_guard(c));
+    csr::build(nullptr, m, c->d_deg, nullptr, n, c->d_q[0], c->d_q[1], c->d_garc, gsf, c->ss, c->d_ctr,
+               c->st, /*count_groups=*/false);
+    CKL();
+    TRY(sync_read(c));
+    A_full = c->h_ctr[sv::C_VT_OUT];
+    if (A_full > c->cap) return fail(c, CC_ERR_INVALID, "tuple count exceeds capacity");
+    csr::fill_from_buckets(c->d_q[0], c->d_q[1], n, A_full, R0, P0, bucketed, 2 * m, c->d_segB,
+                           c->d_gcur + 2048, c->st);
+    c->launches += 4;
+    CKL();
+    seg_end(c, a, 8.0 * n + 24.0 * m + 4.0 * (double)A_full, 4, KF_CSR);
+  }
+
   // ------------------------------------------------ BFS peel + filter (lines 7-11)
   const uint2* sv_edges = c->d_edges;
   uint64_t m_sv = m;
   const uint32_t* vis = nullptr;
   e_bfs = e_filter = e_pred;
-  if (run_bfs) {
+  if (run_bfs && gsf >= 0) {
+    // direction-optimising BFS over the CSR rows (bfs.cu)
+    R.ran_bfs = 1;
+    R.bfs_root = root;
+    const uint64_t nw = (n + 31) / 32;
+    uint32_t* P0 = reinterpret_cast<uint32_t*>(c->d_w[0]) + c->cap;
+    uint32_t *V = c->d_bm[0], *F = c->d_bm[1], *X = c->d_bm[2];
+    uint32_t *list = c->d_segA, *next = c->d_segB;
+    CK(cudaMemsetAsync(V, 0, sizeof(uint32_t) * nw, c->st));
+    CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * nw, c->st));
+    c->h_word[0] = 1u << (root & 31);
+    c->h_word[1] = (uint32_t)root;
+    CK(cudaMemcpyAsync(V + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(F + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(list, c->h_word + 1, 4, cudaMemcpyHostToDevice, c->st));
+    uint64_t nf = 1, mf = R.max_degree, mu = 2 * m - R.max_degree;
+    uint64_t visited = 1, levels = 0;
+    uint64_t* bctr = c->d_gctr + graph::G_NEWVIS;  // [G_NEWVIS, G_REMAIN]: next count, its arcs
+    static_assert(graph::G_REMAIN == graph::G_NEWVIS + 1, "level counters are adjacent");
+    while (true) {
+      CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
+      CK(cudaMemsetAsync(bctr, 0, 2 * sizeof(uint64_t), c->st));
+      const bool bottom_up = mf * 14 > mu;  // Beamer's direction rule on arc counts
+      Prof k(c, KF_BFS);
+      bfs::level(bottom_up, c->d_q[0], P0, c->d_deg, n, list, nf, F, V, X, next, bctr, c->st);
+      k.end(bottom_up ? 8.0 * n + 4.0 * (double)mu : 8.0 * nf + 4.0 * (double)mf, 1);
+      c->launches += 1;
+      CKL();
+      TRY(sync_read(c));
+      const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
+      if (nv == 0) break;
+      visited += nv;
+      levels++;
+      mf = c->h_gctr[graph::G_REMAIN];
+      mu = mu > mf ? mu - mf : 0;
+      nf = nv;
+      std::swap(F, X);
+      std::swap(list, next);
+    }
+    R.bfs_visited = visited;
+    R.bfs_levels = levels;
+    graph::launch_min_visited(V, n, c->d_gctr, c->st);
+    graph::launch_bfs_labels(V, n, c->d_label, c->d_gctr, c->st);
+    c->launches += 2;
+    e_bfs = ev_get(c);
+    CK(cudaEventRecord(e_bfs, c->st));
+    if (!c->d_rem) TRY(dalloc_t(c, &c->d_rem, m + 1));
+    CK(cudaMemsetAsync(c->d_gctr + graph::G_REMAIN, 0, sizeof(uint64_t), c->st));
+    bfs::filter(c->d_edges, m, V, c->d_rem, c->d_gctr + graph::G_REMAIN, c->st);
+    c->launches += 1;
+    CKL();
+    TRY(sync_read(c));
+    m_sv = c->h_gctr[graph::G_REMAIN];
+    sv_edges = c->d_rem;
+    R.remainder_edges = m_sv;
+    vis = V;
+    e_filter = ev_get(c);
+    CK(cudaEventRecord(e_filter, c->st));
+  } else if (run_bfs) {
     R.ran_bfs = 1;
     R.bfs_root = root;
     const uint64_t nw = (n + 31) / 32;
@@ -710,7 +811,11 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   }
 
   // ------------------------------------------------ SV (line 13)
-  TRY(run_sv(c, sv_edges, m_sv, vis));
+  if (gsf >= 0 && !run_bfs) {
+    if (A_full) TRY(sv_iterate(c, A_full, A_full));  // the rows built above
+  } else {
+    TRY(run_sv(c, sv_edges, m_sv, vis));
+  }
   R.sv_iterations = (uint32_t)c->iters.size();
   e_sv = ev_get(c);
   CK(cudaEventRecord(e_sv, c->st));

@@ -274,9 +274,9 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
   CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
   TRY(scan_epoch_guard(c));
   const int gshift = csr::group_shift(n, na + (hi - lo));
-  uint32_t* garc = reinterpret_cast<uint32_t*>(c->d_gctr + graph::G_NUM);
-  uint64_t* gcur = c->d_gctr + graph::G_NUM + 512;
-  uint64_t* nlong = gcur + 1024;
+  uint32_t* garc = c->d_garc;
+  uint64_t* gcur = c->d_gcur;
+  uint64_t* nlong = gcur + 2048;
   csr::build(nullptr, na, c->d_deg, nullptr, n, off, cur, garc, gshift, c->ss, c->d_ctr, c->st);
   CKL();
   TRY(sync_read(c));

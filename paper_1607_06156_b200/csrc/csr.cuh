@@ -7,9 +7,21 @@ namespace csr {
 
 // CSR build (counting regroup by r): off[v] / cur[v] from degrees; ctr[C_VT_OUT] = A_0.
 int group_shift(uint64_t n, uint64_t tuples);
+// count_groups: also accumulate per-group arc counts into garc (false when bucket_degrees
+// already produced them).
 void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* vis, uint64_t n,
            uint32_t* off, uint32_t* cur, uint32_t* garc, int gshift, scan::State& ss, uint64_t* ctr,
-           cudaStream_t st);
+           cudaStream_t st, bool count_groups = true);
+// Full-graph CSR path (n <= 2^26): gshift for groups of <= 2^15 ids (-1: n too large).
+int group_shift_full(uint64_t n);
+// Bucket both arcs of every edge by the group of r into tmp (2m uint2) and count degrees per
+// group in shared memory (Alg. 2 line 2 without global atomics); garc/gcur: group scratch.
+void bucket_degrees(const uint2* edges, uint64_t m, uint64_t n, int gshift, uint32_t* garc,
+                    uint64_t* gcur, uint2* tmp, uint32_t* deg, cudaStream_t st);
+// R, vertex tuples and the row scatter of the bucketed arcs (after build with the same deg).
+void fill_from_buckets(const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A, uint32_t* R,
+                       uint32_t* P, const uint2* tmp, uint64_t na, uint32_t* longlist, uint64_t* nlong,
+                       cudaStream_t st);
 // R fill, vertex tuples, and the two-level arc scatter (bucket by vertex group, then rows).
 // tmp: 2m uint2 scratch; longlist: n uint32 scratch; garc/gcur: 1024 entries.  `directed`:
 // `edges` holds m arcs (r, p) instead of m undirected edges (two arcs each).

@@ -58,6 +58,8 @@ struct cc_ctx {
   uint32_t* d_gath = nullptr;    // allgather scratch (world_size x bitmap words)
   uint64_t gath_cap = 0;
   uint64_t* d_cnt = nullptr;     // per-owner arc counts (world_size^2 after the gather)
+  uint32_t* d_garc = nullptr;  // CSR vertex-group scratch: arcs per group (<= 2048 groups)
+  uint64_t* d_gcur = nullptr;  // group cursors [0, 2048), long-row count at [2048]
   uint64_t* d_ctr = nullptr;   // sv counters
   uint64_t* d_gctr = nullptr;  // graph counters
   uint64_t* h_ctr = nullptr;   // pinned mirrors
@@ -142,6 +144,8 @@ static inline void dfree_all(cc_ctx* c) {
   c->d_ids64 = c->d_uids = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
   c->d_umin = c->d_umax = c->d_nlsegs = nullptr;
+  c->d_garc = nullptr;
+  c->d_gcur = nullptr;
   c->d_send = c->d_recv = nullptr;
   c->d_gath = nullptr;
   c->d_cnt = nullptr;

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
                                             uint32_t* __restrict__ off, uint32_t* __restrict__ cur,
                                             uint64_t* flags, uint32_t* ticket, uint32_t epoch,
                                             unsigned long long* total, uint32_t* garc,
-                                            int gshift) {
+                                            int gshift, int count_groups) {
   __shared__ uint32_t s_scan[B / 32 + 1];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_pref;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
   const uint64_t pref = scan::tile_prefix(flags, tile, tot, epoch, &s_pref);
   // arcs of this tile (tuples minus vertex tuples) for the CSR bucket pass; a tile of
   // B*SITEMS = 2^11 vertices lies inside one group of 2^gshift vertices (gshift >= 11)
-  {
+  if (count_groups) {
     uint32_t nv = 0;
 #pragma unroll
     for (int k = 0; k < SITEMS; k++) nv += (c[k] != 0);
@@ -157,7 +157,7 @@ __global__ void k_gscan(const uint32_t* __restrict__ garc, int G, unsigned long 
 // contiguous run per group, so the writes stay coalesced and the second pass below scatters
 // inside one small window of P at a time (L2-resident, no partial-sector DRAM writes).
 constexpr int BITEMS = 8;
-constexpr int MAXG = 1024;
+constexpr int MAXG = 2048;
 // DIRECTED: the input is already arcs (r, p) (multi-GPU: arcs received by their owner),
 // one tuple each; otherwise undirected edges, two tuples each.
 template <bool DIRECTED>
@@ -201,6 +201,46 @@ __global__ void __launch_bounds__(B) k_bucket(const uint2* __restrict__ e, uint6
         out[s_base[arc[PER * k + t].x >> gshift] + slot[PER * k + t]] = arc[PER * k + t];
     }
   }
+}
+
+// ---- degrees without global atomics (prediction of the csr engine, n <= 2^26)
+// Alg. 2 line 2 counts arcs per source (sort + run lengths in the paper).  Here the
+// arcs are first bucketed by the vertex group of r (the CSR bucket pass above, which the
+// build needs anyway); a group is 2^gshift <= 2^15 vertices, so one block counts its arcs
+// in shared memory.
+__global__ void __launch_bounds__(B) k_group_hist(const uint2* __restrict__ e, uint64_t m, int gshift,
+                                                  int G, uint32_t* garc) {
+  __shared__ uint32_t s[MAXG];
+  for (int g = threadIdx.x; g < G; g += B) s[g] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < m; i += (uint64_t)gridDim.x * B) {
+    const uint2 xy = e[i];
+    atomicAdd(&s[xy.x >> gshift], 1u);
+    atomicAdd(&s[xy.y >> gshift], 1u);
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += B)
+    if (s[g]) atomicAdd(&garc[g], s[g]);
+}
+__global__ void __launch_bounds__(1024) k_group_degree(const uint2* __restrict__ arcs,
+                                                       const unsigned long long* __restrict__ gend,
+                                                       int gshift, uint64_t n, uint32_t* deg) {
+  extern __shared__ uint32_t s_deg[];
+  const uint64_t g = blockIdx.x, base = g << gshift;
+  const uint32_t cnt = (uint32_t)min((uint64_t)1 << gshift, n - base);
+  for (uint32_t v = threadIdx.x; v < cnt; v += blockDim.x) s_deg[v] = 0;
+  __syncthreads();
+  const uint64_t a = g ? gend[g - 1] : 0, b = gend[g];
+  const uint32_t lt = lanemask_lt();
+  for (uint64_t i0 = a; i0 < b; i0 += blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    const uint32_t v = i < b ? (uint32_t)(arcs[i].x - base) : 0xFFFFFFFFu;
+    // hubs: lanes holding the same vertex add once (__match_any_sync)
+    const uint32_t peers = __match_any_sync(0xffffffffu, v);
+    if (v != 0xFFFFFFFFu && (peers & lt) == 0) atomicAdd(&s_deg[v], (uint32_t)__popc(peers));
+  }
+  __syncthreads();
+  for (uint32_t v = threadIdx.x; v < cnt; v += blockDim.x) deg[base + v] = s_deg[v];
 }
 
 // Second pass: place each arc tuple in its row (cursor per vertex).
@@ -262,18 +302,57 @@ int group_shift(uint64_t n, uint64_t tuples) {
   return gs < 11 ? 11 : gs;
 }
 
+int group_shift_full(uint64_t n) {
+  int kb = 0;
+  while ((1ull << kb) < n) kb++;
+  if (kb > 26) return -1;  // more than MAXG groups of 2^15 ids: use graph::launch_degree
+  return kb - 11 < 11 ? 11 : kb - 11;
+}
+
 void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* vis, uint64_t n,
            uint32_t* off, uint32_t* cur, uint32_t* garc, int gshift, scan::State& ss, uint64_t* ctr,
-           cudaStream_t st) {
+           cudaStream_t st, bool count_groups) {
   // ctr[C_VT_OUT] receives A_0
   if (!n) return;
   const int G = (int)(((n - 1) >> gshift) + 1);
   cudaMemsetAsync(ss.ticket, 0, sizeof(uint32_t), st);
-  cudaMemsetAsync(garc, 0, sizeof(uint32_t) * G, st);
+  if (count_groups) cudaMemsetAsync(garc, 0, sizeof(uint32_t) * G, st);
   const uint64_t tiles = (n + B * SITEMS - 1) / (B * SITEMS);
   k_rows<<<(unsigned)tiles, B, 0, st>>>(deg, vis, n, off, cur, ss.flags, ss.ticket, ++ss.epoch,
                                          reinterpret_cast<unsigned long long*>(ctr + sv::C_VT_OUT),
-                                         garc, gshift);
+                                         garc, gshift, count_groups ? 1 : 0);
+}
+
+void bucket_degrees(const uint2* edges, uint64_t m, uint64_t n, int gshift, uint32_t* garc,
+                    uint64_t* gcur, uint2* tmp, uint32_t* deg, cudaStream_t st) {
+  if (!n) return;
+  const int G = (int)(((n - 1) >> gshift) + 1);
+  auto* gc = reinterpret_cast<unsigned long long*>(gcur);
+  cudaMemsetAsync(garc, 0, sizeof(uint32_t) * G, st);
+  if (m) k_group_hist<<<grid(m, B, 148 * 4), B, 0, st>>>(edges, m, gshift, G, garc);
+  k_gscan<<<1, B, 0, st>>>(garc, G, gc);
+  if (m)
+    k_bucket<false><<<(unsigned)((m + B * BITEMS - 1) / (B * BITEMS)), B, 0, st>>>(edges, m, gshift, G,
+                                                                                  gc, tmp);
+  // k_bucket advanced every group cursor to its group's end
+  const int smem = (int)(sizeof(uint32_t) << gshift);
+  static int attr_set = 0;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_group_degree, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << 15);
+    attr_set = 1;
+  }
+  k_group_degree<<<G, 1024, smem, st>>>(tmp, gc, gshift, n, deg);
+}
+
+void fill_from_buckets(const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A, uint32_t* R,
+                       uint32_t* P, const uint2* tmp, uint64_t na, uint32_t* longlist, uint64_t* nlong,
+                       cudaStream_t st) {
+  if (!A) return;
+  auto* nl = reinterpret_cast<unsigned long long*>(nlong);
+  cudaMemsetAsync(nlong, 0, sizeof(uint64_t), st);
+  k_fill_rows<<<grid(n, B, 148 * 8), B, 0, st>>>(off, n, R, P, longlist, nl);
+  k_fill_long<<<148 * 2, B, 0, st>>>(off, longlist, nl, R);
+  if (na) k_scatter<<<grid(na, B, 148 * 16), B, 0, st>>>(tmp, na, cur, P);
 }
 void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
           uint32_t* R, uint32_t* P, const uint32_t* garc, int gshift, uint64_t* gcur, uint2* tmp,

@@ -24,15 +24,19 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.fixture(scope="module", params=["csr", "sort", "direct"])
+@pytest.fixture(scope="module", params=["csr", "csrbfs", "sort", "direct"])
 def cc(request):
-    """All regroup engines: r-stationary CSR (default), the paper's radix
+    """All regroup engines: r-stationary CSR (default), the same with the
+    full-CSR prediction and direction-optimising BFS (CC_FLAG_BFS_CSR), the paper's radix
     regroups, and fully direct-addressed buckets; same sets, same counters."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_1607_06156_b200 as ccmod
-    flags = ccmod.CC_FLAG_TRACE | ccmod.REGROUP_FLAGS[request.param]
+    if request.param == "csrbfs":
+        flags = ccmod.CC_FLAG_TRACE | ccmod.CC_FLAG_BFS_CSR
+    else:
+        flags = ccmod.CC_FLAG_TRACE | ccmod.REGROUP_FLAGS[request.param]
     ctx = ccmod.CC(device=0, flags=flags)
     yield ctx
     ctx.close()
@@ -266,7 +270,7 @@ def test_device_input_and_output(cc):
 def test_config_c4_full(cc, request):
     """C4 (R-MAT scale 26, 1.07 B edges) at full size through the BFS route: labels
     bit-identical to union-find; the peeled component is exactly the root's component."""
-    if "csr" not in request.node.name:
+    if "[csr]" not in request.node.name:
         pytest.skip("full-size C4 runs once, with the default engine")
     g = graphgen.make("c4")
     want = oracle.uf_labels(g.n, g.edges)
