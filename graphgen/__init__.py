@@ -50,7 +50,10 @@ def _L():
         lib.gg_paths.argtypes = [u64, u64, dbl, u64, u64, p64, p32]
         lib.gg_grid.argtypes = [u64, u64, u32, u64, p64, p32]
         lib.gg_rmat.argtypes = [u64, u32, u64, u32, u32, u32, i32, p32]
-        for f in (lib.gg_blocks, lib.gg_er, lib.gg_paths, lib.gg_grid, lib.gg_rmat):
+        lib.gg_union_u64.argtypes = [u64, p32, u64, u64, p32, u64, p32]
+        lib.gg_mix64_value.restype = u64
+        lib.gg_mix64_value.argtypes = [u64]
+        for f in (lib.gg_blocks, lib.gg_er, lib.gg_paths, lib.gg_grid, lib.gg_rmat, lib.gg_union_u64):
             f.restype = i32
         _lib = lib
     return _lib
@@ -63,8 +66,8 @@ def _ptr(a: np.ndarray):
 @dataclass
 class Graph:
     name: str
-    n: int              # id bound: ids are in [0, n)
-    edges: np.ndarray   # (m, 2) uint32, undirected edge records
+    n: int              # id bound: ids are in [0, n) (0 for u64 ids: V = ids that appear)
+    edges: np.ndarray   # (m, 2) uint32 (u64 for c5), undirected edge records
     params: dict
 
     @property
@@ -118,13 +121,27 @@ def perm_value(n: int, seed: int, stream: int, x: int) -> int:
     return int(_L().gg_perm_value(n, seed, stream, x))
 
 
+def union_u64(seed: int, a: np.ndarray, na: int, b: np.ndarray) -> np.ndarray:
+    """Edges of a (indices < na) and b (indices offset by na) as u64 ids mix64(index), edge
+    order scrambled (gen.c gg_union_u64)."""
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    b = np.ascontiguousarray(b, dtype=np.uint32)
+    out = np.empty((a.shape[0] + b.shape[0], 2), dtype=np.uint64)
+    _L().gg_union_u64(seed, _ptr(a), a.shape[0], na, _ptr(b), b.shape[0], _ptr(out))
+    return out
+
+
+def mix64(k: int) -> int:
+    return int(_L().gg_mix64_value(k))
+
+
 def make(config: str, scale: float = 1.0, seed: int | None = None) -> Graph:
-    """Draw one BASELINE.json config (``c1``..``c4``) at a fraction ``scale`` of its size.
+    """Draw one BASELINE.json config (``c1``..``c5``) at a fraction ``scale`` of its size.
 
     ``scale`` shrinks the vertex/edge counts while keeping the structure (block size,
     path length mix, keep probability, R-MAT parameters); scale=1 is the full config.
     """
-    k = {"c1": 1, "c2": 2, "c3": 3, "c4": 4}[config]
+    k = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}[config]
     s = BASE_SEED + k if seed is None else seed
     if config == "c1":
         # 65,536 vertices in 4,096 blocks of 16; 200,000 edges (BASELINE configs[0])
@@ -147,6 +164,16 @@ def make(config: str, scale: float = 1.0, seed: int | None = None) -> Graph:
         sc = max(4, 26 + int(round(np.log2(scale))) if scale != 1.0 else 26)
         e = rmat(s, sc, 16)
         return Graph("c4", 1 << sc, e, dict(rmat_scale=sc, scale=scale))
+    if config == "c5":
+        # R-MAT scale 28 (C4's parameters) U 10,000,000 geometric(mean 64) paths on fresh
+        # indices 2^28 + j; u64 id = mix64(index); edge order scrambled (configs[4]).
+        # Graph.n = 0: u64 ids, V = the ids that appear (C2).
+        sc = max(4, 28 + int(round(np.log2(scale))) if scale != 1.0 else 28)
+        a = rmat(s, sc, 16)
+        npaths = max(1, int(10_000_000 * scale))
+        _, b = paths(s + 100, npaths, 64.0, 0, 0)
+        return Graph("c5", 0, union_u64(s, a, 1 << sc, b), dict(rmat_scale=sc, n_paths=npaths,
+                                                                  scale=scale))
     raise KeyError(config)
 
 

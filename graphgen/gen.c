@@ -247,3 +247,36 @@ int gg_rmat(uint64_t seed, uint32_t scale, uint64_t m, uint32_t ta, uint32_t tab
 }
 
 int gg_num_threads(void) { return omp_get_max_threads(); }
+
+/* ---- C5: union of an R-MAT part and a path part on disjoint dense indices, relabelled to
+ * u64 ids by a 64-bit bijective integer mix (Thomas Wang / Jenkins style 7-step hash; the
+ * id space of the configs' "u64 ids"), edge order scrambled by a seeded bijection.
+ * in:  a (ma pairs, indices < na) and b (mb pairs, indices < nb, offset by na)
+ * out: 2*(ma+mb) uint64 ids.                                                              */
+static inline uint64_t gg_mix64(uint64_t k) {
+  k = (~k) + (k << 21);
+  k = k ^ (k >> 24);
+  k = (k + (k << 3)) + (k << 8);
+  k = k ^ (k >> 14);
+  k = (k + (k << 2)) + (k << 4);
+  k = k ^ (k >> 28);
+  k = k + (k << 31);
+  return k;
+}
+uint64_t gg_mix64_value(uint64_t k) { return gg_mix64(k); }
+int gg_union_u64(uint64_t seed, const uint32_t* a, uint64_t ma, uint64_t na, const uint32_t* b,
+                 uint64_t mb, uint64_t* out) {
+  const uint64_t m = ma + mb;
+  gg_perm pe;
+  perm_init(&pe, m ? m : 1, seed, 9);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)m; i++) {
+    uint64_t j = perm_apply(&pe, (uint64_t)i);
+    uint64_t u, v;
+    if (j < ma) { u = a[2 * j]; v = a[2 * j + 1]; }
+    else { j -= ma; u = na + b[2 * j]; v = na + b[2 * j + 1]; }
+    out[2 * i] = gg_mix64(u);
+    out[2 * i + 1] = gg_mix64(v);
+  }
+  return 0;
+}

@@ -3,6 +3,7 @@
 #include "graph.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace cc {
 namespace graph {
@@ -61,8 +62,13 @@ __global__ void k_degree(const uint4* __restrict__ e2, uint64_t m, uint32_t* __r
 }
 void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st) {
   if (!m) return;
-  for (uint64_t lo = 0; lo < n; lo += DEG_WINDOW) {
-    const uint64_t hi = std::min<uint64_t>(n, lo + DEG_WINDOW);
+  static uint64_t window = 0;
+  if (!window) {  // CC_DEG_WINDOW_LOG2: experiment hook for the counter window
+    const char* e = getenv("CC_DEG_WINDOW_LOG2");
+    window = e ? (1ull << atoi(e)) : DEG_WINDOW;
+  }
+  for (uint64_t lo = 0; lo < n; lo += window) {
+    const uint64_t hi = std::min<uint64_t>(n, lo + window);
     k_degree<<<grid_for((m >> 1) + 1, 148 * 16), BLOCK, 0, st>>>(
         reinterpret_cast<const uint4*>(edges), m, deg, (uint32_t)lo, (uint32_t)hi);
   }

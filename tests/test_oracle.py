@@ -399,3 +399,20 @@ def test_generators_deterministic_and_sized():
     n = 1000
     vals = {graphgen.perm_value(n, 1, 2, x) for x in range(n)}
     assert vals == set(range(n))
+
+
+def test_c5_generator_is_a_relabelled_union():
+    """graphgen C5 (inputs only): the u64 ids are a bijective mix of the dense indices of an
+    R-MAT part and a path part on disjoint index ranges; edge order is scrambled, not the
+    multiset (checked against the two parts drawn separately)."""
+    import graphgen
+    g = graphgen.make("c5", 1 / 4096)
+    sc, npaths = g.params["rmat_scale"], g.params["n_paths"]
+    a = graphgen.rmat(graphgen.BASE_SEED + 5, sc, 16)
+    _, b = graphgen.paths(graphgen.BASE_SEED + 5 + 100, npaths, 64.0, 0, 0)
+    idx = np.concatenate([a.astype(np.uint64), b.astype(np.uint64) + np.uint64(1 << sc)])
+    mixed = np.vectorize(graphgen.mix64, otypes=[np.uint64])(idx)
+    assert g.edges.shape == mixed.shape
+    assert np.array_equal(np.sort(g.edges.reshape(-1)), np.sort(mixed.reshape(-1)))
+    sample = np.arange(20000, dtype=np.uint64)
+    assert len({graphgen.mix64(int(x)) for x in sample}) == sample.shape[0]
