@@ -60,7 +60,12 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
 #define CC_FLAG_TRACE 0x1u           /* also fit the histogram + K-S in forced modes        */
 #define CC_FLAG_GATE_KS 0x2u         /* decide with the paper's K-S < tau
                                         instead of gate G (least-squares fit)  */
-#define CC_FLAG_NO_EARLY_EXCLUDE 0x4u /* reserved: end-of-iteration exclusion timing        */
+#define CC_FLAG_NO_EARLY_EXCLUDE 0x4u /* csr engine: completed partitions leave at the end of
+                                        the iteration (the paper's timing; their
+                                        temporaries are made, T_i = |P_i|) -- SURVEY C4    */
+#define CC_FLAG_NO_EXCLUDE 0x80u     /* csr engine: completed partitions never leave
+                                        (fig:loadbal 'Naive'): iterate until no
+                                        partition changes in either partition pass         */
 /* SV regroup engine (all three compute identical sets and counters):
  *   default : r-stationary -- tuples regrouped by r once (CSR build), partition buckets
  *             addressed directly in L2-resident slots, ordered compaction
@@ -117,6 +122,8 @@ typedef struct {
   uint64_t completed;  /* partitions found completed                    */
   uint64_t changed;    /* #{p : p_min != p} at the first partition pass        */
   uint64_t changed2;   /* same count at the second partition pass             */
+  uint64_t active_min; /* live tuples entering the iteration on the least / most loaded */
+  uint64_t active_max; /* rank (fig:loadbal); = active_in on one GPU        */
   double ms;           /* device time of the iteration                                 */
 } cc_iter_stat;
 

@@ -30,6 +30,8 @@ CC_FLAG_REGROUP_DIRECT = 0x20
 REGROUP_FLAGS = {"csr": 0, "sort": 0x8, "direct": 0x20, "csrbfs": 0x40}
 CC_FLAG_PROFILE = 0x10
 CC_FLAG_BFS_CSR = 0x40
+CC_FLAG_NO_EXCLUDE = 0x80
+EXCLUSION_FLAGS = {"early": 0, "end": CC_FLAG_NO_EARLY_EXCLUDE, "none": CC_FLAG_NO_EXCLUDE}
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -62,7 +64,9 @@ class cc_config(ctypes.Structure):
 class cc_iter_stat(ctypes.Structure):
     _fields_ = [("active_in", ctypes.c_uint64), ("partitions", ctypes.c_uint64),
                 ("temps", ctypes.c_uint64), ("completed", ctypes.c_uint64),
-                ("changed", ctypes.c_uint64), ("changed2", ctypes.c_uint64), ("ms", ctypes.c_double)]
+                ("changed", ctypes.c_uint64), ("changed2", ctypes.c_uint64),
+                ("active_min", ctypes.c_uint64), ("active_max", ctypes.c_uint64),
+                ("ms", ctypes.c_double)]
 
 
 class cc_report(ctypes.Structure):

@@ -249,6 +249,7 @@ static cc_status run_sv_direct(cc_ctx* c, uint64_t A, int cur) {
     const uint64_t A1 = out - T;
     cc_iter_stat s{};
     s.active_in = A;
+    s.active_min = s.active_max = A;
     s.partitions = c->h_ctr[sv::C_PARTITIONS];
     s.completed = c->h_ctr[sv::C_COMPLETED];
     s.changed = c->h_ctr[sv::C_CHANGED];
@@ -315,14 +316,14 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
   c->launches += 5;
   CKL();
   seg_end(c, a, 4.0 * n + 8.0 * m_sv + 8.0 * A + 4.0 * n, 6, KF_CSR);
-  return sv_iterate(c, A, A);
+  return sv_iterate(c, A, A, A);
 }
 
 // Alg. 1 iterations on the tuple array in buffer 0 (R, P), `len` entries of which A (summed
 // over ranks) are live.  Multi-GPU: rows are owned (r in this rank's block), partitions are
 // global, so after each row pass the partition slots are combined across ranks (min of the
 // minima, OR of the NCP bitmap) and every rank derives identical statistics and temporaries.
-cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len) {
+cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   const uint64_t n = c->n;
   const uint64_t nw = (n + 31) / 32;
   const bool multi = c->cfg.world_size > 1;
@@ -347,6 +348,10 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len) {
   CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nwp, c->st));
   CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nwp, c->st));
   uint64_t len_live = len;  // live tuples of this rank (compaction decision)
+  // exclusion of completed partitions (fig:loadbal variants)
+  const bool excl = !(c->cfg.flags & CC_FLAG_NO_EXCLUDE);
+  const bool temps_all = !excl || (c->cfg.flags & CC_FLAG_NO_EARLY_EXCLUDE);
+  uint64_t local_in = A_local;
   for (uint32_t it = 0;; it++) {
     if (it >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
     cudaEvent_t ev_it = ev_get(c);
@@ -368,11 +373,12 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len) {
       TRY(comm_or_bits(c, NCP, nwp));
     }
     // ---- line 22 bookkeeping: |P_i|, completed, changed, temporaries
-    { Prof k(c, KF_SLOTS); csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st); k.end(8.0 * n4, 1); }
+    { Prof k(c, KF_SLOTS); csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all); k.end(8.0 * n4, 1); }
     // ---- lines 17-21 (exclusion, p <- p_min), line 24 (+ temporaries), line 25 minima
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
-                   c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, hot, c->d_ctr, c->st);
+                   c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, hot, c->d_ctr, c->st,
+                   excl);
       k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
     // live tuples: this rank's (compaction) and the global count (convergence)
@@ -393,14 +399,39 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len) {
     len_live = c->h_ctr[sv::C_SURVIVORS];
     cc_iter_stat s{};
     s.active_in = A;
+    s.active_min = s.active_max = A;
     s.partitions = c->h_ctr[sv::C_PARTITIONS];
     s.completed = c->h_ctr[sv::C_COMPLETED];
     s.changed = c->h_ctr[sv::C_CHANGED];
     s.temps = c->h_ctr[sv::C_TEMPS];
     s.changed2 = c->h_ctr[sv::C_CHANGED2];
+    s.active_min = s.active_max = local_in;
+    if (multi) {  // per-rank load (fig:loadbal): min and max of the live tuples over ranks
+      uint64_t* mm = c->d_gcur + 2050;
+      const uint64_t v2[2] = {local_in, local_in};
+      CK(cudaMemcpyAsync(mm, v2, sizeof(v2), cudaMemcpyHostToDevice, c->st));
+      TRY(comm_allreduce(c, mm, 1, CC_DT_I64, CC_OP_MIN));
+      TRY(comm_allreduce(c, mm + 1, 1, CC_DT_I64, CC_OP_MAX));
+      uint64_t r2[2];
+      CK(cudaMemcpyAsync(r2, mm, sizeof(r2), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      s.active_min = r2[0];
+      s.active_max = r2[1];
+    }
+    local_in = len_live;
     c->iters.push_back(s);
     c->it_ev.push_back(ev_it);
     seg_end(c, a, 20.0 * len + 16.0 * n4, 8);
+    if (!excl) {
+      // 'Naive': nothing leaves; the partition passes decide convergence
+      if (s.changed == 0 && s.changed2 == 0) {
+        csr::final_labels(R[cb], Pc, len, c->d_label, c->st);
+        c->launches += 1;
+        break;
+      }
+      A = A1;
+      continue;
+    }
     if (A1 == 0) break;
     // dead rows of completed partitions are squeezed out once they are a third of the array
     // (the paper's 'swapped to the end of the local array', sec:distSVOpt1)
@@ -471,6 +502,7 @@ static cc_status run_sv(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint
     seg_end(c, a, (double)A * (12 + 12) + (double)out * 8, 2);
     cc_iter_stat s{};
     s.active_in = A;
+    s.active_min = s.active_max = A;
     s.partitions = c->h_ctr[sv::C_PARTITIONS];
     s.completed = c->h_ctr[sv::C_COMPLETED];
     s.changed = c->h_ctr[sv::C_CHANGED];
@@ -573,6 +605,9 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   if (!c->loaded) return fail(c, CC_ERR_STATE, "cc_run before cc_load_edges");
   if (mode != CC_MODE_AUTO && mode != CC_MODE_SV && mode != CC_MODE_BFS_SV)
     return fail(c, CC_ERR_INVALID, "bad mode %d", (int)mode);
+  if ((c->cfg.flags & (CC_FLAG_NO_EXCLUDE | CC_FLAG_NO_EARLY_EXCLUDE)) &&
+      (c->cfg.flags & (CC_FLAG_REGROUP_SORT | CC_FLAG_REGROUP_DIRECT)))
+    return fail(c, CC_ERR_INVALID, "exclusion variants are implemented by the csr engine");
   CK(cudaSetDevice(c->cfg.device));
   c->ran = false;
   c->iters.clear();
@@ -812,7 +847,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
 
   // ------------------------------------------------ SV (line 13)
   if (gsf >= 0 && !run_bfs) {
-    if (A_full) TRY(sv_iterate(c, A_full, A_full));  // the rows built above
+    if (A_full) TRY(sv_iterate(c, A_full, A_full, A_full));  // the rows built above
   } else {
     TRY(run_sv(c, sv_edges, m_sv, vis));
   }

@@ -361,7 +361,7 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
   uint64_t A = 0;
   CK(cudaMemcpyAsync(&A, tmp, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  if (A) TRY(sv_iterate(c, A, len));
+  if (A) TRY(sv_iterate(c, A, len, A_local));
   R.sv_iterations = (uint32_t)c->iters.size();
   e_sv = ev_get(c);
   CK(cudaEventRecord(e_sv, c->st));

@@ -44,17 +44,22 @@ void longlist(const uint32_t* R, const uint32_t* P, uint64_t L, const uint32_t* 
               uint64_t* nsegs, cudaStream_t st);
 // P is read from Pin and the relabelled values written to Pout (NULL: pass A without MAP).
 // pass A (MAP = PB of the previous iteration or NULL; OUT = PA; NCPw = NCP) or pass B
-// (MAP = PA, NCPr = NCP, TB; OUT = PB; label; ctr[C_OUT] += live tuples).  `tag` must
+// (MAP = PA, NCPr = NCP, TB; OUT = PB; label; ctr[C_OUT] += live tuples; excl: completed
+// partitions leave, else they stay).  `tag` must
 // increase with every call (tagged long-row partial slots UMIN/UMAX).  `hot`: few distinct
 // partitions per tuple, filter slot updates through the block's cache.
 void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L,
              const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
-             cudaStream_t st);
+             cudaStream_t st, bool excl = true);
 // partition statistics after pass A (sets TB, clears PB); slot arrays padded to 4*ceil(n/4)
+// temps_all: a temporary for every partition, completed ones included (their tuples leave at
+// the end of the iteration or never)
 void pstat1(const uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
-            uint64_t* ctr, cudaStream_t st);
+            uint64_t* ctr, cudaStream_t st, bool temps_all = false);
+// labels of the rows still in the array (no-exclusion variant)
+void final_labels(const uint32_t* R, const uint32_t* P, uint64_t L, uint32_t* label, cudaStream_t st);
 // temporaries' own contribution to PB
 void temps2(const uint32_t* TB, uint64_t n, uint32_t* PB, cudaStream_t st);
 // changed2 after pass B (clears PA, NCP, TB)

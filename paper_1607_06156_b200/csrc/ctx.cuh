@@ -309,7 +309,7 @@ cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs, u
 
 // Alg. 1 iterations of the r-stationary engine on a built tuple array (cc_api.cu); with
 // world_size > 1 the partition slots are combined across ranks after each row pass.
-cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len);
+cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local);
 
 // cc_run for world_size > 1 (cc_dist.cu).
 cc_status run_dist(cc_ctx* c, cc_mode mode);

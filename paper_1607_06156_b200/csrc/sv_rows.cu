@@ -115,11 +115,12 @@ CC_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 
 // relabel of one input value: A -> MAP (NULL: identity); B -> PA[p], or DEAD if p completed
 template <bool A>
-CC_DEVI uint32_t relabel(uint32_t pv, const uint32_t* __restrict__ MAP, const uint32_t* __restrict__ NCPr) {
+CC_DEVI uint32_t relabel(uint32_t pv, const uint32_t* __restrict__ MAP, const uint32_t* __restrict__ NCPr,
+                         int excl) {
   if (pv == DEAD) return DEAD;
   if (A) return MAP ? __ldg(&MAP[pv]) : pv;
   const uint32_t pm = __ldg(&MAP[pv]);
-  if (pm == pv && !tbit(NCPr, pv)) return DEAD;
+  if (excl && pm == pv && !tbit(NCPr, pv)) return DEAD;
   return pm;
 }
 
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
     const uint32_t* __restrict__ R, const uint32_t* __restrict__ Pin, uint32_t* __restrict__ Pout,
     uint64_t L, uint32_t ntiles, const uint32_t* __restrict__ MAP,
     const uint32_t* __restrict__ NCPr, const uint32_t* __restrict__ TB, uint32_t* OUT,
-    uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int hot) {
+    uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int hot, int excl) {
   constexpr int NW = RB / 32;
   // double-buffered tile staging: TMA brings tile i+2 while tile i is processed
   __shared__ __align__(128) uint32_t s_r[2][RTILE];
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
       if (!A) {
 #pragma unroll
         for (int j = 0; j < RITEMS; j++) {
-          if (p[j] != DEAD && m[j] == p[j] && !tbit(NCPr, p[j])) {
+          if (excl && p[j] != DEAD && m[j] == p[j] && !tbit(NCPr, p[j])) {
             // completed partition: the whole row leaves, its vertex is labelled p
             if (j == 0 || r[j - 1] != r[j]) label[r[j] & ~R_LONG] = p[j];
             m[j] = DEAD;
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
           const uint64_t i = base + lane;
           const bool in = i < L && __ldg(&R[i]) == klast;
           if (in) {
-            const uint32_t pv = relabel<A>(__ldg(&Pin[i]), MAP, NCPr);  // live row: not DEAD
+            const uint32_t pv = relabel<A>(__ldg(&Pin[i]), MAP, NCPr, excl);  // live row: not DEAD
             emn = min(emn, pv);
             emx = max(emx, pv);
           }
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
       for (uint64_t base = pos; base < pos + LONG; base += 32) {
         const uint64_t i = base + lane;
         const bool in = i < L && __ldg(&R[i]) == klast;
-        if (in) atomicMin(&OUT[relabel<A>(__ldg(&Pin[i]), MAP, NCPr)], q);
+        if (in) atomicMin(&OUT[relabel<A>(__ldg(&Pin[i]), MAP, NCPr, excl)], q);
         if (__ballot_sync(FULL, !in)) break;
       }
     }
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(RB) k_long2(const uint32_t* __restrict__ P,
 __global__ void __launch_bounds__(RB) k_pstat1(const uint32_t* __restrict__ PA,
                                                const uint32_t* __restrict__ NCP, uint64_t n4,
                                                uint32_t* TB, uint32_t* __restrict__ PB,
-                                               unsigned long long* ctr) {
+                                               unsigned long long* ctr, int temps_all) {
   uint32_t np = 0, nc = 0, ch = 0, nt = 0;
   for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
     const uint4 a = reinterpret_cast<const uint4*>(PA)[t];
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(RB) k_pstat1(const uint32_t* __restrict__ PA,
       ch += pm != pid;
       const bool comp = pm == pid && !((w >> j) & 1u);
       nc += comp;
-      if (!comp) {
+      if (!comp || temps_all) {  // temps_all: completed partitions stay for this iteration
         nt++;
         const uint32_t b = 1u << (pm & 31);
         if (!(*(volatile uint32_t*)&TB[pm >> 5] & b)) atomicOr(&TB[pm >> 5], b);
@@ -521,6 +522,14 @@ __global__ void __launch_bounds__(RB) k_pstat2(const uint32_t* __restrict__ PB, 
   if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
 }
 
+// Without exclusion (fig:loadbal 'Naive') every row is still in the array at convergence:
+// its vertex takes the (now common) partition id of its tuples.
+__global__ void k_final_labels(const uint32_t* __restrict__ R, const uint32_t* __restrict__ P, uint64_t L,
+                               uint32_t* __restrict__ label) {
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < L; i += (uint64_t)gridDim.x * RB)
+    if (P[i] != DEAD && (i == 0 || R[i - 1] != R[i])) label[R[i] & ~R_LONG] = P[i];
+}
+
 // --------------------------------------------------------------------------- exchange helpers
 __global__ void k_flip_sign(uint32_t* a, uint64_t n) {
   for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < n; i += (uint64_t)gridDim.x * RB)
@@ -536,6 +545,9 @@ __global__ void k_or_parts(const uint32_t* __restrict__ parts, uint64_t words, i
 }
 
 // --------------------------------------------------------------------------- launchers
+void final_labels(const uint32_t* R, const uint32_t* P, uint64_t L, uint32_t* label, cudaStream_t st) {
+  if (L) k_final_labels<<<(unsigned)std::min<uint64_t>((L + RB - 1) / RB, 148 * 8), RB, 0, st>>>(R, P, L, label);
+}
 void flip_sign(uint32_t* a, uint64_t n, cudaStream_t st) {
   if (n) k_flip_sign<<<(unsigned)std::min<uint64_t>((n + RB - 1) / RB, 148 * 8), RB, 0, st>>>(a, n);
 }
@@ -570,7 +582,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
-             cudaStream_t st) {
+             cudaStream_t st, bool excl) {
   if (!L) return;
   const uint64_t nt = row_tiles(L);
   auto* umin = reinterpret_cast<unsigned long long*>(UMIN);
@@ -582,7 +594,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
     static unsigned ga = 0;
     if (!ga) ga = persistent_grid((const void*)k_rowpass<true>, ~0ull);
     k_rowpass<true><<<(unsigned)std::min<uint64_t>(nt, ga), RB, 0, st>>>(
-        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0);
+        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0, excl ? 1 : 0);
     if (have_long) {
       k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
@@ -591,7 +603,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
     static unsigned gb = 0;
     if (!gb) gb = persistent_grid((const void*)k_rowpass<false>, ~0ull);
     k_rowpass<false><<<(unsigned)std::min<uint64_t>(nt, gb), RB, 0, st>>>(
-        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0);
+        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0, excl ? 1 : 0);
     if (have_long) {
       k_long1<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
@@ -600,11 +612,12 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
 }
 
 void pstat1(const uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
-            uint64_t* ctr, cudaStream_t st) {
+            uint64_t* ctr, cudaStream_t st, bool temps_all) {
   const uint64_t n4 = (n + 3) / 4;
   if (!n4) return;
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
-  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, reinterpret_cast<unsigned long long*>(ctr));
+  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, reinterpret_cast<unsigned long long*>(ctr),
+                             temps_all ? 1 : 0);
 }
 void temps2(const uint32_t* TB, uint64_t n, uint32_t* PB, cudaStream_t st) {
   const uint64_t nw = (n + 31) / 32;

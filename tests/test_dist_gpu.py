@@ -47,6 +47,9 @@ def _check(res, n, edges, modes, trace=True):
         reps = [r[mode][3] for r in res]
         assert len({rep["sv_iterations"] for rep in reps}) == 1
         assert all(rep["m_edges"] == edges.shape[0] for rep in reps)
+        for it in reps[0]["iters"]:  # per-rank load (fig:loadbal): min <= mean <= max
+            w = len(res)
+            assert it["active_min"] * w <= it["active_in"] <= it["active_max"] * w
         if trace and mode == "sv":
             _, tr = osv.sv_trace(n, edges)
             got = [dict(A=it["active_in"], P=it["partitions"], T=it["temps"],
@@ -96,6 +99,23 @@ def test_dist_edge_cases():
     # fewer edges than ranks: some ranks load nothing
     e2 = np.array([[0, 1], [2, 3]], np.uint32)
     _check(run_ranks(_rank_run, 3, 40, e2, ("sv", "auto"), 0), 40, e2, ("sv", "auto"))
+
+
+def test_dist_exclusion_variants():
+    """fig:loadbal variants on 2 ranks: same trace as the transcription with that choice."""
+    import paper_1607_06156_b200 as cc
+    g = graphgen.make("c1", 0.25)
+    for excl in ("none", "end"):
+        res = run_ranks(_rank_run, 2, g.n, g.edges, ("sv",), cc.EXCLUSION_FLAGS[excl])
+        want, tr = osv.sv_trace(g.n, g.edges, exclusion=excl)
+        lab = np.zeros(g.n, dtype=np.uint32)
+        for r in res:
+            lo, hi, l, rep = r["sv"]
+            lab[lo:hi] = l
+        assert np.array_equal(lab, want)
+        got = [(it["active_in"], it["partitions"], it["temps"], it["completed"], it["changed"],
+                it["changed2"]) for it in res[0]["sv"][3]["iters"]]
+        assert got == [(d["A"], d["P"], d["T"], d["completed"], d["changed"], d["changed2"]) for d in tr]
 
 
 def test_dist_matches_single_gpu_c2_sample():

@@ -177,6 +177,38 @@ def test_row_lengths_straddle_tiles(cc, seed):
     assert norm(trace_of(rep)) == norm(tr)
 
 
+@pytest.mark.parametrize("exclusion", ["end", "none"])
+def test_exclusion_variants_trace(exclusion):
+    """The paper's exclusion timings (SURVEY C4, sec:distSVOpt1 P:220-225) and the
+    fig:loadbal 'Naive' variant with no exclusion: labels and every per-iteration counter
+    equal the Alg. 1 transcription run with the same choice."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_06156_b200 as ccmod
+    ctx = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE | ccmod.EXCLUSION_FLAGS[exclusion])
+    try:
+        graphs = [graphgen.er(s, 3000, 2500 + 700 * s) for s in range(4)]
+        graphs.append(graphgen.make("c1", 1.0).edges)
+        graphs.append(graphgen.make("c3", 0.01).edges)
+        for e in graphs:
+            n = int(e.max()) + 1 if e.size else 1
+            want, tr = osv.sv_trace(n, e, exclusion=exclusion)
+            lab, rep = run(ctx, n, e, "sv")
+            assert np.array_equal(lab, want)
+            assert norm(trace_of(rep)) == norm(tr)
+            for it in rep["iters"]:
+                assert it["active_min"] == it["active_max"] == it["active_in"]
+        with pytest.raises(ccmod.CCError):  # variants are a csr-engine feature
+            bad = ccmod.CC(device=0, flags=ccmod.EXCLUSION_FLAGS[exclusion] | ccmod.CC_FLAG_REGROUP_SORT)
+            try:
+                run(bad, 4, [(0, 1)], "sv")
+            finally:
+                bad.close()
+    finally:
+        ctx.close()
+
+
 # ------------------------------------------------------------------ configs (BASELINE.json)
 @pytest.mark.parametrize("cfg,scale", [("c1", 1.0), ("c2", 0.02), ("c3", 0.02)])
 def test_config_trace_parity(cc, cfg, scale):
