@@ -343,6 +343,8 @@ def main():
                               "frac": (path_bytes / (peak * 1e9)) / step_s,
                               "model": "SURVEY.md §8(d): 8m+8A0+sum(32A_i+48A_i+1+40T_i)+4n+4n_p"},
             "stages_ms": {k: rep[k] for k in ("ms_prediction", "ms_bfs", "ms_filter", "ms_sv")},
+            "sv_iters": [{"A": it["active_in"], "P": it["partitions"], "ms": round(it["ms"], 4)}
+                         for it in rep["iters"]],
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,

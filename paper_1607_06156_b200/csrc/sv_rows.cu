@@ -62,6 +62,13 @@ CC_DEVI void push_min(uint32_t* OUT, unsigned long long* s_pc, uint32_t p, uint3
   atomicMin(&OUT[p], q);  // result unused: compiles to a fire-and-forget reduction
   s_pc[h] = ((unsigned long long)p << 32) | q;
 }
+CC_DEVI void push_bit(uint32_t* BM, uint32_t* s_nc, uint32_t p) {
+  const uint32_t h = (p ^ (p >> 9)) & (RCACHE - 1);
+  if (*(volatile uint32_t*)&s_nc[h] == p) return;
+  s_nc[h] = p;
+  const uint32_t b = 1u << (p & 31);
+  if (!(*(volatile uint32_t*)&BM[p >> 5] & b)) atomicOr(&BM[p >> 5], b);
+}
 CC_DEVI void set_bit(uint32_t* BM, uint32_t p) {
   const uint32_t b = 1u << (p & 31);
   if (!(*(volatile uint32_t*)&BM[p >> 5] & b)) atomicOr(&BM[p >> 5], b);
@@ -153,9 +160,20 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
   __shared__ uint32_t s_last[NW];
   __shared__ RunAgg s_wt[NW], s_wh[NW + 1];  // per warp: last run (prefix), first run (suffix)
   __shared__ uint32_t s_kfirst;
-  __shared__ unsigned long long s_pc[RCACHE];
-  for (int i = threadIdx.x; i < RCACHE; i += RB) s_pc[i] = ~0ull;
+  // hot mode: per-block aggregation of slot updates (key claimed once per block, value
+  // min-reduced in shared memory, flushed with one global atomic per key at the end)
+  constexpr int RAGG = 1024;
+  __shared__ uint32_t s_akey[RAGG], s_aval[RAGG];
+  __shared__ uint32_t s_nc[A ? RCACHE : 1];
+  for (int i = threadIdx.x; i < RAGG; i += RB) {
+    s_akey[i] = INF;
+    s_aval[i] = INF;
+  }
+  for (int i = threadIdx.x; i < (A ? RCACHE : 1); i += RB) s_nc[i] = INF;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // the last slot update / NCP flag this thread issued (slots only decrease): repeats are
+  // common once a few partitions hold most tuples
+  uint32_t last_p = INF, last_q = INF, last_nc = INF;
   auto issue = [&](uint32_t tl, int b) {  // thread 0: stage tile tl into buffer b
     if (tl >= ntiles) return;
     const uint64_t a0 = (uint64_t)tl * RTILE;
@@ -199,13 +217,25 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
     }
     // ---- relabel (A: line 25 of the previous iteration) / exclusion + line 19 (B)
     {
-      uint32_t m[RITEMS];
+      // one gather per run of equal p in the thread's slice: once a few partitions hold most
+      // tuples, thousands of threads would otherwise hit the same L2 line at once
+      uint32_t m[RITEMS], cpl = 0;
 #pragma unroll
-      for (int j = 0; j < RITEMS; j++) m[j] = (p[j] != DEAD && (!A || MAP)) ? __ldg(&MAP[p[j]]) : p[j];
+      for (int j = 0; j < RITEMS; j++) {
+        const bool fresh = p[j] != DEAD && (!A || MAP) && (j == 0 || p[j] != p[j - 1]);
+        m[j] = fresh ? __ldg(&MAP[p[j]]) : p[j];
+        if (!A && fresh && m[j] == p[j] && !tbit(NCPr, p[j])) cpl |= 1u << j;
+      }
+#pragma unroll
+      for (int j = 1; j < RITEMS; j++)
+        if (p[j] != DEAD && (!A || MAP) && p[j] == p[j - 1]) {
+          m[j] = m[j - 1];
+          cpl |= ((cpl >> (j - 1)) & 1u) << j;
+        }
       if (!A) {
 #pragma unroll
         for (int j = 0; j < RITEMS; j++) {
-          if (excl && p[j] != DEAD && m[j] == p[j] && !tbit(NCPr, p[j])) {
+          if (excl && p[j] != DEAD && ((cpl >> j) & 1u)) {
             // completed partition: the whole row leaves, its vertex is labelled p
             if (j == 0 || r[j - 1] != r[j]) label[r[j] & ~R_LONG] = p[j];
             m[j] = DEAD;
@@ -334,11 +364,28 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
       if (k[j] == k[RITEMS - 1] && cout_k == k[RITEMS - 1]) { q = min(q, cout_m); if (A) x = max(x, cout_x); }
       if (k[j] == INF || k[j] == kfirst) continue;
       if (j == RITEMS - 1) qlast = q;
-      if (!hot) atomicMin(&OUT[p[j]], q);
-      else if (j == 0 || p[j] != p[j - 1] || k[j] != k[j - 1]) push_min(OUT, s_pc, p[j], q);
+      if (!hot) {
+        atomicMin(&OUT[p[j]], q);
+      } else if (p[j] != last_p || q < last_q) {  // this thread's last update covers it
+        const uint32_t h = (p[j] ^ (p[j] >> 10)) & (RAGG - 1);
+        uint32_t key = *(volatile uint32_t*)&s_akey[h];
+        if (key == INF) {
+          key = atomicCAS(&s_akey[h], INF, p[j]);
+          if (key == INF) key = p[j];
+        }
+        if (key == p[j]) atomicMin(&s_aval[h], q);
+        else atomicMin(&OUT[p[j]], q);
+        last_p = p[j];
+        last_q = q;
+      }
       if ((heads >> j) & 1u) {
         if (A) {
-          if (q != x) atomicOr(&NCPw[q >> 5], 1u << (q & 31));
+          // many non-PC rows share one minimum late in the run: filter through a block cache
+          // and a read of the word before the atomic
+          if (q != x && q != last_nc) {
+            push_bit(NCPw, s_nc, q);
+            last_nc = q;
+          }
         } else if (tbit(TB, k[j])) {
           atomicMin(&OUT[k[j]], q);
         }
@@ -357,6 +404,11 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
       }
     }
     __syncthreads();
+  }
+  if (hot) {  // flush the block's aggregated slot updates
+    __syncthreads();
+    for (int i = threadIdx.x; i < RAGG; i += RB)
+      if (s_akey[i] != INF) atomicMin(&OUT[s_akey[i]], s_aval[i]);
   }
   if (!A) {
     live = warp_sum(live);
