@@ -63,6 +63,9 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
 #define CC_FLAG_NO_EARLY_EXCLUDE 0x4u /* csr engine: completed partitions leave at the end of
                                         the iteration (the paper's timing; their
                                         temporaries are made, T_i = |P_i|) -- SURVEY C4    */
+#define CC_FLAG_PERMUTE_IDS 0x100u   /* u64 ids: run on ids permuted by a 64-bit invertible
+                                        mix, labels mapped back to the minimum
+                                        original id of each component (C1)               */
 #define CC_FLAG_NO_EXCLUDE 0x80u     /* csr engine: completed partitions never leave
                                         (fig:loadbal 'Naive'): iterate until no
                                         partition changes in either partition pass         */
@@ -188,6 +191,13 @@ cc_status cc_labels_u64(cc_ctx* ctx, uint64_t* ids, uint64_t* labels, uint64_t c
  * B = 32*ceil(n / (32*world_size)) -- its CSR rows (owner-computes) and its
  * labels.  Writes the block of this rank (lo = 0, hi = n on one GPU). */
 cc_status cc_block_range(const cc_ctx* ctx, uint64_t* lo, uint64_t* hi);
+
+/* BFS eccentricity (depth of the BFS tree within the seed's component) of each of `count`
+ * seeds into ecc[i]: the paper's approximate diameter is the maximum over random seeds
+ * (PAPER.md:307).  u32 graphs on one GPU, n <= 2^26 (CC_ERR_INVALID otherwise); seeds >= n ->
+ * CC_ERR_RANGE.  Uses the direction-optimising BFS on the CSR rows; invalidates the labels of
+ * an earlier cc_run (CC_ERR_STATE from cc_labels_* until the next cc_run). */
+cc_status cc_bfs_eccentricity(cc_ctx* ctx, const uint64_t* seeds, uint32_t count, uint64_t* ecc);
 
 /* Device pointer of the label array (u32 mode), valid until the next load/destroy, and
  * the device stream all work is enqueued on.  For zero-copy consumers. */

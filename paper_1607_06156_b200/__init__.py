@@ -31,6 +31,7 @@ REGROUP_FLAGS = {"csr": 0, "sort": 0x8, "direct": 0x20, "csrbfs": 0x40}
 CC_FLAG_PROFILE = 0x10
 CC_FLAG_BFS_CSR = 0x40
 CC_FLAG_NO_EXCLUDE = 0x80
+CC_FLAG_PERMUTE_IDS = 0x100
 EXCLUSION_FLAGS = {"early": 0, "end": CC_FLAG_NO_EARLY_EXCLUDE, "none": CC_FLAG_NO_EXCLUDE}
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -85,7 +86,8 @@ class cc_report(ctypes.Structure):
 
 
 EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
-           "cc_labels_device", "cc_block_range", "cc_last_launch_count", "cc_kernel_stats",
+           "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_last_launch_count",
+           "cc_kernel_stats",
            "cc_kernel_name", "cc_destroy", "cc_status_string", "cc_last_error"]
 
 
@@ -107,6 +109,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_labels_u64.argtypes = [P, P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     lib.cc_labels_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_uint64)]
     lib.cc_block_range.argtypes = [P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+    lib.cc_bfs_eccentricity.argtypes = [P, P, ctypes.c_uint32, P]
     lib.cc_last_launch_count.restype = ctypes.c_uint64
     lib.cc_last_launch_count.argtypes = [P]
     lib.cc_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
@@ -115,7 +118,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_kernel_name.restype = ctypes.c_char_p
     lib.cc_kernel_name.argtypes = [ctypes.c_int]
     for f in ("cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
-              "cc_labels_device", "cc_block_range", "cc_kernel_stats", "cc_destroy"):
+              "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_kernel_stats",
+              "cc_destroy"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -340,6 +344,24 @@ def cc_block_range(ctx):
     return lo.value, hi.value
 
 
+def cc_bfs_eccentricity(ctx, seeds):
+    """BFS eccentricity of each seed (numpy uint64 array)."""
+    s = np.ascontiguousarray(seeds, dtype=np.uint64)
+    out = np.zeros(s.shape[0], dtype=np.uint64)
+    _check(ctx, lib().cc_bfs_eccentricity(ctx, s.ctypes.data_as(ctypes.c_void_p), s.shape[0],
+                                          out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def approx_diameter(ctx, n, runs=100, seed=0, present=None):
+    """The paper's approximate diameter: max BFS depth over ``runs`` random
+    seed vertices (drawn among ``present`` ids if given)."""
+    rng = np.random.default_rng(seed)
+    pool = np.arange(n) if present is None else np.flatnonzero(present)
+    seeds = rng.choice(pool, size=min(runs, pool.shape[0]), replace=False)
+    return int(cc_bfs_eccentricity(ctx, seeds).max()) if seeds.size else 0
+
+
 def cc_kernel_stats(ctx, which):
     ms, by, ln = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
     _check(ctx, lib().cc_kernel_stats(ctx, which, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(ln)))
@@ -375,6 +397,9 @@ class CC:
 
     def labels(self, out=None):
         return cc_labels_u32(self.ctx, out)
+
+    def eccentricity(self, seeds):
+        return cc_bfs_eccentricity(self.ctx, seeds)
 
     def block_range(self):
         return cc_block_range(self.ctx)

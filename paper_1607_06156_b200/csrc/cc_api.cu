@@ -156,6 +156,10 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   if (w == CC_U64) {
     TRY(dalloc_t(c, &c->d_ids64, 2 * m + 1));
     TRY(dalloc_t(c, &c->d_uids, 2 * m + 1));
+    if (c->cfg.flags & CC_FLAG_PERMUTE_IDS) {
+      TRY(dalloc_t(c, &c->d_mix, n + 1));
+      TRY(dalloc_t(c, &c->d_pi, n + 1));
+    }
   }
   c->rws.max_tiles = c->cap / radix::TILE + 2;
   TRY(dalloc_t(c, &c->rws.ghist, radix::MAX_PASSES * radix::RADIX));
@@ -600,6 +604,79 @@ cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs_ou
   return CC_OK;
 }
 
+// CSR rows of the whole graph from the bucketed arcs (csr::bucket_degrees already ran with
+// the same gsf): offsets in c->d_q[0], tuples in buffer 0.  *A = tuple count.
+static cc_status build_full_rows(cc_ctx* c, int gsf, uint64_t* A_out) {
+  const uint64_t n = c->n, m = c->m;
+  uint2* bucketed = reinterpret_cast<uint2*>(c->d_w[1]);
+  uint32_t* R0 = reinterpret_cast<uint32_t*>(c->d_w[0]);
+  uint32_t* P0 = R0 + c->cap;
+  cudaEvent_t a = nullptr;
+  seg_begin(c, &a);
+  CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
+  TRY(scan_epoch_guard(c));
+  csr::build(nullptr, m, c->d_deg, nullptr, n, c->d_q[0], c->d_q[1], c->d_garc, gsf, c->ss, c->d_ctr,
+             c->st, /*count_groups=*/false);
+  CKL();
+  TRY(sync_read(c));
+  const uint64_t A = c->h_ctr[sv::C_VT_OUT];
+  if (A > c->cap) return fail(c, CC_ERR_INVALID, "tuple count exceeds capacity");
+  csr::fill_from_buckets(c->d_q[0], c->d_q[1], n, A, R0, P0, bucketed, 2 * m, c->d_segB, c->d_gcur + 2048,
+                         c->st);
+  c->launches += 4;
+  CKL();
+  seg_end(c, a, 8.0 * n + 24.0 * m + 4.0 * (double)A, 4, KF_CSR);
+  *A_out = A;
+  return CC_OK;
+}
+
+// Direction-optimising BFS from `root` over the full CSR rows (c->d_q[0] offsets, P of tuple
+// buffer 0, degrees in c->d_deg); visited bitmap in c->d_bm[0].  *levels = eccentricity of root.
+static cc_status bfs_csr(cc_ctx* c, uint64_t root, uint64_t m, uint64_t* visited_out, uint64_t* levels_out) {
+  const uint64_t n = c->n;
+  const uint64_t nw = (n + 31) / 32;
+  uint32_t* P0 = reinterpret_cast<uint32_t*>(c->d_w[0]) + c->cap;
+  uint32_t *V = c->d_bm[0], *F = c->d_bm[1], *X = c->d_bm[2];
+  uint32_t *list = c->d_segA, *next = c->d_segB;
+  CK(cudaMemsetAsync(V, 0, sizeof(uint32_t) * nw, c->st));
+  CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * nw, c->st));
+  c->h_word[0] = 1u << (root & 31);
+  c->h_word[1] = (uint32_t)root;
+  CK(cudaMemcpyAsync(V + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(F + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(list, c->h_word + 1, 4, cudaMemcpyHostToDevice, c->st));
+  uint32_t droot = 0;
+  CK(cudaMemcpyAsync(&droot, c->d_deg + root, 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  uint64_t nf = 1, mf = droot, mu = 2 * m - droot;
+  uint64_t visited = 1, levels = 0;
+  uint64_t* bctr = c->d_gctr + graph::G_NEWVIS;  // [G_NEWVIS, G_REMAIN]: next count, its arcs
+  static_assert(graph::G_REMAIN == graph::G_NEWVIS + 1, "level counters are adjacent");
+  while (true) {
+    CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
+    CK(cudaMemsetAsync(bctr, 0, 2 * sizeof(uint64_t), c->st));
+    const bool bottom_up = mf * 14 > mu;  // Beamer's direction rule on arc counts
+    Prof k(c, KF_BFS);
+    bfs::level(bottom_up, c->d_q[0], P0, c->d_deg, n, list, nf, F, V, X, next, bctr, c->st);
+    k.end(bottom_up ? 8.0 * n + 4.0 * (double)mu : 8.0 * nf + 4.0 * (double)mf, 1);
+    c->launches += 1;
+    CKL();
+    TRY(sync_read(c));
+    const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
+    if (nv == 0) break;
+    visited += nv;
+    levels++;
+    mf = c->h_gctr[graph::G_REMAIN];
+    mu = mu > mf ? mu - mf : 0;
+    nf = nv;
+    std::swap(F, X);
+    std::swap(list, next);
+  }
+  *visited_out = visited;
+  *levels_out = levels;
+  return CC_OK;
+}
+
 extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   if (!c) return CC_ERR_INVALID;
   if (!c->loaded) return fail(c, CC_ERR_STATE, "cc_run before cc_load_edges");
@@ -651,6 +728,15 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     c->n = nd;
     c->hi = nd;
     c->kbits = bits_for(nd);
+    if (c->cfg.flags & CC_FLAG_PERMUTE_IDS) {
+      // SV runs on ids permuted by the 64-bit mix; pi[v] = rank of mix(id_v)
+      relabel::mix(c->d_uids, nd, c->d_mix, c->st);
+      relabel::run(c->d_mix, nd, c->d_w, vals, c->rws, c->ss, c->d_pi, c->d_mix, total, c->st,
+                   &c->launches);
+      relabel::apply(reinterpret_cast<uint32_t*>(c->d_edges), 2 * m, c->d_pi, c->st);
+      c->launches += 2;
+      CKL();
+    }
   }
   const uint64_t n = c->n;
   e_rel = ev_get(c);
@@ -692,25 +778,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
 
   // ------------------------------------------------ full CSR rows (csr engine, both routes)
   uint64_t A_full = 0;
-  if (gsf >= 0) {
-    uint32_t* R0 = reinterpret_cast<uint32_t*>(c->d_w[0]);
-    uint32_t* P0 = R0 + c->cap;
-    cudaEvent_t a = nullptr;
-    seg_begin(c, &a);
-    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * sv::C_NUM, c->st));
-    TRY(scan_epoch_guard(c));
-    csr::build(nullptr, m, c->d_deg, nullptr, n, c->d_q[0], c->d_q[1], c->d_garc, gsf, c->ss, c->d_ctr,
-               c->st, /*count_groups=*/false);
-    CKL();
-    TRY(sync_read(c));
-    A_full = c->h_ctr[sv::C_VT_OUT];
-    if (A_full > c->cap) return fail(c, CC_ERR_INVALID, "tuple count exceeds capacity");
-    csr::fill_from_buckets(c->d_q[0], c->d_q[1], n, A_full, R0, P0, bucketed, 2 * m, c->d_segB,
-                           c->d_gcur + 2048, c->st);
-    c->launches += 4;
-    CKL();
-    seg_end(c, a, 8.0 * n + 24.0 * m + 4.0 * (double)A_full, 4, KF_CSR);
-  }
+  if (gsf >= 0) TRY(build_full_rows(c, gsf, &A_full));
 
   // ------------------------------------------------ BFS peel + filter (lines 7-11)
   const uint2* sv_edges = c->d_edges;
@@ -721,41 +789,9 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     // direction-optimising BFS over the CSR rows (bfs.cu)
     R.ran_bfs = 1;
     R.bfs_root = root;
-    const uint64_t nw = (n + 31) / 32;
-    uint32_t* P0 = reinterpret_cast<uint32_t*>(c->d_w[0]) + c->cap;
-    uint32_t *V = c->d_bm[0], *F = c->d_bm[1], *X = c->d_bm[2];
-    uint32_t *list = c->d_segA, *next = c->d_segB;
-    CK(cudaMemsetAsync(V, 0, sizeof(uint32_t) * nw, c->st));
-    CK(cudaMemsetAsync(F, 0, sizeof(uint32_t) * nw, c->st));
-    c->h_word[0] = 1u << (root & 31);
-    c->h_word[1] = (uint32_t)root;
-    CK(cudaMemcpyAsync(V + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(F + root / 32, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(list, c->h_word + 1, 4, cudaMemcpyHostToDevice, c->st));
-    uint64_t nf = 1, mf = R.max_degree, mu = 2 * m - R.max_degree;
-    uint64_t visited = 1, levels = 0;
-    uint64_t* bctr = c->d_gctr + graph::G_NEWVIS;  // [G_NEWVIS, G_REMAIN]: next count, its arcs
-    static_assert(graph::G_REMAIN == graph::G_NEWVIS + 1, "level counters are adjacent");
-    while (true) {
-      CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
-      CK(cudaMemsetAsync(bctr, 0, 2 * sizeof(uint64_t), c->st));
-      const bool bottom_up = mf * 14 > mu;  // Beamer's direction rule on arc counts
-      Prof k(c, KF_BFS);
-      bfs::level(bottom_up, c->d_q[0], P0, c->d_deg, n, list, nf, F, V, X, next, bctr, c->st);
-      k.end(bottom_up ? 8.0 * n + 4.0 * (double)mu : 8.0 * nf + 4.0 * (double)mf, 1);
-      c->launches += 1;
-      CKL();
-      TRY(sync_read(c));
-      const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
-      if (nv == 0) break;
-      visited += nv;
-      levels++;
-      mf = c->h_gctr[graph::G_REMAIN];
-      mu = mu > mf ? mu - mf : 0;
-      nf = nv;
-      std::swap(F, X);
-      std::swap(list, next);
-    }
+    uint64_t visited = 0, levels = 0;
+    TRY(bfs_csr(c, root, m, &visited, &levels));
+    uint32_t* V = c->d_bm[0];
     R.bfs_visited = visited;
     R.bfs_levels = levels;
     graph::launch_min_visited(V, n, c->d_gctr, c->st);
@@ -851,9 +887,22 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   } else {
     TRY(run_sv(c, sv_edges, m_sv, vis));
   }
+  if (c->idw == CC_U64 && (c->cfg.flags & CC_FLAG_PERMUTE_IDS)) {
+    // labels back to the minimum original id of each component (C1)
+    relabel::canonicalize(c->d_pi, c->d_label, n, c->d_segA, c->d_segB, c->st);
+    CK(cudaMemcpyAsync(c->d_label, c->d_segB, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, c->st));
+    c->launches += 2;
+    CKL();
+  }
   R.sv_iterations = (uint32_t)c->iters.size();
   e_sv = ev_get(c);
   CK(cudaEventRecord(e_sv, c->st));
+  // components, isolated ids included (each has exactly one root: its minimum id)
+  uint64_t* roots = c->d_gctr + graph::G_TAIL;
+  CK(cudaMemsetAsync(roots, 0, sizeof(uint64_t), c->st));
+  graph::launch_count_roots(c->d_label, 0, n, roots, c->st);
+  c->launches += 1;
+  CK(cudaMemcpyAsync(&R.components, roots, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
   e_end = ev_get(c);
   CK(cudaEventRecord(e_end, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -873,8 +922,6 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
       for (auto& p : k.ev) k.ms += ev_ms(p.first, p.second);
   R.iters = c->iters.data();
   R.n_iters = (uint32_t)c->iters.size();
-  // components (isolated ids included): computed by the caller from labels if needed;
-  // here: n_present-independent count of roots is not materialised (see cc_labels_u32).
   c->ran = true;
   if (out) *out = R;
   return CC_OK;
@@ -943,4 +990,31 @@ extern "C" cc_status cc_kernel_stats(const cc_ctx* c, int which, double* ms, dou
 
 extern "C" const char* cc_kernel_name(int which) {
   return (which >= 0 && which < KF_N) ? kKfNames[which] : nullptr;
+}
+
+// Eccentricity of each seed in its component (BFS depth), the paper's approximate diameter
+// being the maximum over random seeds.  u32 graphs on one GPU
+// with n <= 2^26: builds the full CSR rows and runs the direction-optimising BFS per seed.
+extern "C" cc_status cc_bfs_eccentricity(cc_ctx* c, const uint64_t* seeds, uint32_t count, uint64_t* ecc) {
+  if (!c || (count && (!seeds || !ecc))) return CC_ERR_INVALID;
+  if (!c->loaded) return fail(c, CC_ERR_STATE, "cc_bfs_eccentricity before cc_load_edges");
+  if (c->idw != CC_U32 || multi_gpu(c)) return fail(c, CC_ERR_STATE, "u32 ids on one GPU only");
+  const int gsf = csr::group_shift_full(c->n);
+  if (gsf < 0) return fail(c, CC_ERR_INVALID, "n > 2^26 is not supported here");
+  for (uint32_t i = 0; i < count; i++)
+    if (seeds[i] >= c->n) return fail(c, CC_ERR_RANGE, "seed %llu >= n", (unsigned long long)seeds[i]);
+  CK(cudaSetDevice(c->cfg.device));
+  c->ran = false;  // the SV buffers are reused
+  const uint64_t n = c->n, m = c->m;
+  csr::bucket_degrees(c->d_edges, m, n, gsf, c->d_garc, c->d_gcur, reinterpret_cast<uint2*>(c->d_w[1]),
+                      c->d_deg, c->st);
+  uint64_t A = 0;
+  TRY(build_full_rows(c, gsf, &A));
+  for (uint32_t i = 0; i < count; i++) {
+    uint64_t vis = 0, lev = 0;
+    TRY(bfs_csr(c, seeds[i], m, &vis, &lev));
+    ecc[i] = lev;
+  }
+  CK(cudaStreamSynchronize(c->st));
+  return CC_OK;
 }

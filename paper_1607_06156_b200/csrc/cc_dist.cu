@@ -363,6 +363,12 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
   CK(cudaStreamSynchronize(c->st));
   if (A) TRY(sv_iterate(c, A, len, A_local));
   R.sv_iterations = (uint32_t)c->iters.size();
+  // components: roots of the owned block, summed over ranks
+  uint64_t* roots = c->d_ctr + sv::C_ERR;
+  CK(cudaMemsetAsync(roots, 0, sizeof(uint64_t), c->st));
+  graph::launch_count_roots(c->d_label, lo, hi, roots, c->st);
+  TRY(comm_allreduce(c, roots, 1, CC_DT_I64, CC_OP_SUM));
+  CK(cudaMemcpyAsync(&R.components, roots, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
   e_sv = ev_get(c);
   CK(cudaEventRecord(e_sv, c->st));
   CK(cudaStreamSynchronize(c->st));

@@ -33,6 +33,8 @@ struct cc_ctx {
   uint2* d_rem2 = nullptr;
   uint64_t* d_ids64 = nullptr;  // u64 mode: loaded endpoints (2m)
   uint64_t* d_uids = nullptr;   // u64 mode: sorted distinct ids (rank -> id)
+  uint64_t* d_mix = nullptr;    // CC_FLAG_PERMUTE_IDS: mixed ids / their sorted copy
+  uint32_t* d_pi = nullptr;     // CC_FLAG_PERMUTE_IDS: original rank -> permuted rank
   uint64_t n_alloc = 0;         // id bound the n-sized buffers were sized for
   uint32_t* d_label = nullptr;
   uint32_t* d_deg = nullptr;
@@ -141,7 +143,8 @@ static inline void dfree_all(cc_ctx* c) {
   }
   c->allocs.clear();
   c->d_edges = c->d_rem = c->d_rem2 = nullptr;
-  c->d_ids64 = c->d_uids = nullptr;
+  c->d_ids64 = c->d_uids = c->d_mix = nullptr;
+  c->d_pi = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
   c->d_umin = c->d_umax = c->d_nlsegs = nullptr;
   c->d_garc = nullptr;

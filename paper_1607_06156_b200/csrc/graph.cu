@@ -309,5 +309,21 @@ void launch_bfs_labels(const uint32_t* visited, uint64_t n, uint32_t* label, uin
       visited, n, label, reinterpret_cast<const unsigned long long*>(gctr));
 }
 
+// components = #{v : label[v] = v} over [lo, hi) (every component has exactly one root,
+// its minimum id); added to *cnt
+__global__ void k_count_roots(const uint32_t* __restrict__ label, uint64_t lo, uint64_t hi,
+                              unsigned long long* cnt) {
+  uint32_t c = 0;
+  for (uint64_t v = lo + blockIdx.x * (uint64_t)BLOCK + threadIdx.x; v < hi; v += (uint64_t)gridDim.x * BLOCK)
+    c += label[v] == (uint32_t)v;
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, (unsigned long long)c);
+}
+void launch_count_roots(const uint32_t* label, uint64_t lo, uint64_t hi, uint64_t* cnt, cudaStream_t st) {
+  if (hi > lo)
+    k_count_roots<<<grid_for(hi - lo, 148 * 8), BLOCK, 0, st>>>(label, lo, hi,
+                                                                reinterpret_cast<unsigned long long*>(cnt));
+}
+
 }  // namespace graph
 }  // namespace cc

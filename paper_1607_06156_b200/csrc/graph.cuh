@@ -38,5 +38,8 @@ void launch_bfs_labels(const uint32_t* visited, uint64_t n, uint32_t* label, uin
                        cudaStream_t st);
 void launch_min_visited(const uint32_t* visited, uint64_t n, uint64_t* gctr, cudaStream_t st);
 
+// *cnt += #{v in [lo, hi) : label[v] = v} (caller-zeroed)
+void launch_count_roots(const uint32_t* label, uint64_t lo, uint64_t hi, uint64_t* cnt, cudaStream_t st);
+
 }  // namespace graph
 }  // namespace cc

@@ -98,6 +98,54 @@ cc_status_t run(const uint64_t* ids, uint64_t k, uint64_t* keys[2], uint32_t* va
   return 0;
 }
 
+// ---- id permutation ("permuting the vertex ids using Robert Jenkins' 64 bit mix
+// invertible hash function").  The 64-bit integer mix below (shift-add/xor rounds, each a
+// bijection of 64-bit words) is that family's 7-step variant; SV then runs in the order of
+// the mixed ids and the labels are mapped back to the minimum original id (C1).
+CC_DEVI uint64_t mix64(uint64_t k) {
+  k = (~k) + (k << 21);
+  k = k ^ (k >> 24);
+  k = (k + (k << 3)) + (k << 8);
+  k = k ^ (k >> 14);
+  k = (k + (k << 2)) + (k << 4);
+  k = k ^ (k >> 28);
+  k = k + (k << 31);
+  return k;
+}
+__global__ void k_mix(const uint64_t* __restrict__ uids, uint64_t n, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < n; i += (uint64_t)gridDim.x * B)
+    out[i] = mix64(uids[i]);
+}
+__global__ void k_apply(uint32_t* __restrict__ e, uint64_t k, const uint32_t* __restrict__ pi) {
+  for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < k; i += (uint64_t)gridDim.x * B)
+    e[i] = pi[e[i]];
+}
+// mino[c] = min original rank v of the vertices whose permuted label is c
+__global__ void k_canon1(const uint32_t* __restrict__ pi, const uint32_t* __restrict__ label, uint64_t n,
+                         uint32_t* mino) {
+  for (uint64_t v = blockIdx.x * (uint64_t)B + threadIdx.x; v < n; v += (uint64_t)gridDim.x * B)
+    atomicMin(&mino[label[pi[v]]], (uint32_t)v);
+}
+__global__ void k_canon2(const uint32_t* __restrict__ pi, const uint32_t* __restrict__ label, uint64_t n,
+                         const uint32_t* __restrict__ mino, uint32_t* __restrict__ out) {
+  for (uint64_t v = blockIdx.x * (uint64_t)B + threadIdx.x; v < n; v += (uint64_t)gridDim.x * B)
+    out[v] = mino[label[pi[v]]];
+}
+
+void mix(const uint64_t* uids, uint64_t n, uint64_t* out, cudaStream_t st) {
+  if (n) k_mix<<<grid(n, 148 * 16), B, 0, st>>>(uids, n, out);
+}
+void apply(uint32_t* e, uint64_t k, const uint32_t* pi, cudaStream_t st) {
+  if (k) k_apply<<<grid(k, 148 * 16), B, 0, st>>>(e, k, pi);
+}
+void canonicalize(const uint32_t* pi, const uint32_t* label, uint64_t n, uint32_t* mino, uint32_t* out,
+                  cudaStream_t st) {
+  if (!n) return;
+  cudaMemsetAsync(mino, 0xFF, sizeof(uint32_t) * n, st);
+  k_canon1<<<grid(n, 148 * 16), B, 0, st>>>(pi, label, n, mino);
+  k_canon2<<<grid(n, 148 * 16), B, 0, st>>>(pi, label, n, mino, out);
+}
+
 void labels(const uint64_t* uids, const uint32_t* label, uint64_t n, uint64_t* out, cudaStream_t st) {
   if (n) k_labels<<<grid(n, 148 * 16), B, 0, st>>>(uids, label, n, out);
 }

@@ -14,6 +14,12 @@ typedef int cc_status_t;
 cc_status_t run(const uint64_t* ids, uint64_t k, uint64_t* keys[2], uint32_t* vals[2],
                 radix::Workspace& rws, scan::State& ss, uint32_t* dense, uint64_t* uids,
                 uint64_t* total, cudaStream_t st, uint64_t* launches);
+// Id permutation: out[i] = mix64(uids[i]); e[i] = pi[e[i]];
+// canonicalize: out[v] = min { w : label[pi[w]] = label[pi[v]] } (v, w original dense ranks)
+void mix(const uint64_t* uids, uint64_t n, uint64_t* out, cudaStream_t st);
+void apply(uint32_t* e, uint64_t k, const uint32_t* pi, cudaStream_t st);
+void canonicalize(const uint32_t* pi, const uint32_t* label, uint64_t n, uint32_t* mino, uint32_t* out,
+                  cudaStream_t st);
 // out[i] = uids[label[i]] for the n dense ids
 void labels(const uint64_t* uids, const uint32_t* label, uint64_t n, uint64_t* out, cudaStream_t st);
 

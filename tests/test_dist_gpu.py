@@ -45,6 +45,7 @@ def _check(res, n, edges, modes, trace=True):
         assert covered == n
         assert np.array_equal(lab, want), mode
         reps = [r[mode][3] for r in res]
+        assert all(rep["components"] == np.unique(want).shape[0] for rep in reps)
         assert len({rep["sv_iterations"] for rep in reps}) == 1
         assert all(rep["m_edges"] == edges.shape[0] for rep in reps)
         for it in reps[0]["iters"]:  # per-rank load (fig:loadbal): min <= mean <= max

@@ -46,7 +46,9 @@ def run(cc, n, edges, mode="auto"):
     e = np.asarray(edges, dtype=np.uint32).reshape(-1, 2)
     cc.load(e, n)
     rep = cc.run(mode)
-    return cc.labels().astype(np.int64), rep
+    lab = cc.labels().astype(np.int64)
+    assert rep["components"] == np.unique(lab).shape[0]  # isolated ids included
+    return lab, rep
 
 
 def trace_of(rep):
@@ -361,6 +363,75 @@ def test_config_c5_scaled(cc, request, scale):
     assert np.array_equal(lab, lab_o)
     assert rep["ran_bfs"] == 1
     assert rep["n_present"] == ids_o.shape[0]
+
+
+def _mix64_ref(x):
+    """Independent transcription of the 64-bit integer mix named by PAPER.md:320 (test side)."""
+    M = (1 << 64) - 1
+    k = int(x)
+    k = ((~k) + (k << 21)) & M
+    k ^= k >> 24
+    k = (k + (k << 3) + (k << 8)) & M
+    k ^= k >> 14
+    k = (k + (k << 2) + (k << 4)) & M
+    k ^= k >> 28
+    k = (k + (k << 31)) & M
+    return k
+
+
+@pytest.mark.parametrize("seed,nv,m", [(4, 40, 60), (5, 20000, 30000)])
+def test_permute_ids(seed, nv, m):
+    """CC_FLAG_PERMUTE_IDS: SV runs on the ids ordered by their 64-bit mix, the
+    labels come back as each component's minimum ORIGINAL id (C1); the trace equals the
+    transcription run on the permuted dense ids."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_06156_b200 as ccmod
+    e = _u64_graph(seed, nv, m)
+    ids_o, lab_o = oracle.uf_labels_u64(e)
+    dense, uniq = oracle.relabel_u64(e)
+    mixed = np.array([_mix64_ref(x) for x in uniq], dtype=np.uint64)
+    pi = np.empty(uniq.shape[0], dtype=np.int64)
+    pi[np.argsort(mixed, kind="stable")] = np.arange(uniq.shape[0])
+    _, tr = osv.sv_trace(uniq.shape[0], pi[dense])
+    ctx = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE | ccmod.CC_FLAG_PERMUTE_IDS)
+    try:
+        ctx.load(e, 0, ids="u64")
+        for mode in ("sv", "auto"):
+            rep = ctx.run(mode)
+            ids, lab = ctx.labels_u64()
+            assert np.array_equal(ids, ids_o)
+            assert np.array_equal(lab, lab_o), mode
+            if mode == "sv":
+                assert norm(trace_of(rep)) == norm(tr)
+    finally:
+        ctx.close()
+
+
+def test_bfs_eccentricity():
+    """BFS depth from seeds (the paper's approximate diameter) equals the
+    oracle's level count; on an ordered path the depth from an end is the path length."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_06156_b200 as ccmod
+    ctx = ccmod.CC(device=0)
+    try:
+        for g in (graphgen.make("c3", 0.01), graphgen.rmat_scale_graph(14), graphgen.make("c2", 0.01)):
+            rng = np.random.default_rng(3)
+            seeds = rng.integers(0, g.n, size=6).astype(np.uint64)
+            ctx.load(g.edges, g.n)
+            got = ctx.eccentricity(seeds)
+            for s, lev in zip(seeds, got):
+                _, want = obfs.bfs(g.n, g.edges, int(s))
+                assert int(lev) == want
+        path = np.stack([np.arange(999), np.arange(1, 1000)], 1).astype(np.uint32)
+        ctx.load(path, 1000)
+        assert ctx.eccentricity(np.array([0, 500, 999], np.uint64)).tolist() == [999, 499, 999]
+        assert ccmod.approx_diameter(ctx.ctx, 1000, runs=20, seed=1) <= 999
+    finally:
+        ctx.close()
 
 
 def test_u64_mode_errors(cc):
