@@ -428,7 +428,7 @@ def test_bfs_eccentricity():
                 assert int(lev) == want
         path = np.stack([np.arange(999), np.arange(1, 1000)], 1).astype(np.uint32)
         ctx.load(path, 1000)
-        assert ctx.eccentricity(np.array([0, 500, 999], np.uint64)).tolist() == [999, 499, 999]
+        assert ctx.eccentricity(np.array([0, 500, 999], np.uint64)).tolist() == [999, 500, 999]
         assert ccmod.approx_diameter(ctx.ctx, 1000, runs=20, seed=1) <= 999
     finally:
         ctx.close()
