@@ -199,6 +199,15 @@ cc_status cc_block_range(const cc_ctx* ctx, uint64_t* lo, uint64_t* hi);
  * an earlier cc_run (CC_ERR_STATE from cc_labels_* until the next cc_run). */
 cc_status cc_bfs_eccentricity(cc_ctx* ctx, const uint64_t* seeds, uint32_t count, uint64_t* ecc);
 
+/* Stable LSD radix sort (the onesweep regroup primitive of the sort engine, PAPER.md:207
+ * "the bulk step of the algorithm is the sorting of tuples") of n 64-bit keys by their bits
+ * [0, key_bits), key_bits in 1..64, carrying a u32 payload.  keys/vals: device arrays of n,
+ * sorted in place; tmp_keys/tmp_vals: device scratch of n each.  Enqueued on `stream`
+ * (cudaStream_t) and synchronised; its look-back workspace (8 B x 256 per 4096 keys) comes
+ * from cudaMallocAsync.  For the SURVEY NEXT-3 sort microbenchmark (scripts/sort_bench.py). */
+cc_status cc_radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* tmp_keys, uint32_t* tmp_vals,
+                              uint64_t n, int key_bits, void* stream);
+
 /* Device pointer of the label array (u32 mode), valid until the next load/destroy, and
  * the device stream all work is enqueued on.  For zero-copy consumers. */
 cc_status cc_labels_device(cc_ctx* ctx, const uint32_t** labels, uint64_t* count);

@@ -86,7 +86,8 @@ class cc_report(ctypes.Structure):
 
 
 EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
-           "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_last_launch_count",
+           "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_radix_sort_pairs",
+           "cc_last_launch_count",
            "cc_kernel_stats",
            "cc_kernel_name", "cc_destroy", "cc_status_string", "cc_last_error"]
 
@@ -110,6 +111,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_labels_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_uint64)]
     lib.cc_block_range.argtypes = [P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
     lib.cc_bfs_eccentricity.argtypes = [P, P, ctypes.c_uint32, P]
+    lib.cc_radix_sort_pairs.argtypes = [P, P, P, P, ctypes.c_uint64, ctypes.c_int, P]
+    lib.cc_radix_sort_pairs.restype = ctypes.c_int
     lib.cc_last_launch_count.restype = ctypes.c_uint64
     lib.cc_last_launch_count.argtypes = [P]
     lib.cc_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
@@ -360,6 +363,18 @@ def approx_diameter(ctx, n, runs=100, seed=0, present=None):
     pool = np.arange(n) if present is None else np.flatnonzero(present)
     seeds = rng.choice(pool, size=min(runs, pool.shape[0]), replace=False)
     return int(cc_bfs_eccentricity(ctx, seeds).max()) if seeds.size else 0
+
+
+def cc_radix_sort_pairs(keys, vals, tmp_keys, tmp_vals, key_bits=64, stream=None):
+    """Sort torch CUDA tensors keys (int64/uint64, n) with payload vals (int32/uint32, n) in
+    place by the low ``key_bits`` bits (stable LSD onesweep); tmp_*: scratch of the same shape."""
+    import torch
+    st = stream if stream is not None else torch.cuda.current_stream(keys.device)
+    sptr = st.cuda_stream if hasattr(st, "cuda_stream") else int(st)
+    _check(None, lib().cc_radix_sort_pairs(ctypes.c_void_p(keys.data_ptr()), ctypes.c_void_p(vals.data_ptr()),
+                                           ctypes.c_void_p(tmp_keys.data_ptr()),
+                                           ctypes.c_void_p(tmp_vals.data_ptr()), keys.numel(), key_bits,
+                                           ctypes.c_void_p(sptr)))
 
 
 def cc_kernel_stats(ctx, which):

@@ -1018,3 +1018,35 @@ extern "C" cc_status cc_bfs_eccentricity(cc_ctx* c, const uint64_t* seeds, uint3
   CK(cudaStreamSynchronize(c->st));
   return CC_OK;
 }
+
+extern "C" cc_status cc_radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* tmp_keys,
+                                         uint32_t* tmp_vals, uint64_t n, int key_bits, void* stream) {
+  if (key_bits < 1 || key_bits > 64 || (n && (!keys || !vals || !tmp_keys || !tmp_vals)))
+    return CC_ERR_INVALID;
+  if (n < 2) return CC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  radix::Workspace ws;
+  ws.max_tiles = n / radix::TILE + 2;
+  if (cudaMallocAsync(&ws.ghist, sizeof(uint64_t) * radix::MAX_PASSES * radix::RADIX, st) != cudaSuccess ||
+      cudaMallocAsync(&ws.lookback, sizeof(uint64_t) * ws.max_tiles * radix::RADIX, st) != cudaSuccess ||
+      cudaMallocAsync(&ws.tile_ctr, sizeof(uint32_t) * radix::MAX_PASSES, st) != cudaSuccess) {
+    cudaGetLastError();
+    if (ws.ghist) cudaFreeAsync(ws.ghist, st);
+    if (ws.lookback) cudaFreeAsync(ws.lookback, st);
+    return CC_ERR_NOMEM;
+  }
+  cudaMemsetAsync(ws.lookback, 0, sizeof(uint64_t) * ws.max_tiles * radix::RADIX, st);
+  uint64_t* k[2] = {keys, tmp_keys};
+  uint32_t* v[2] = {vals, tmp_vals};
+  uint64_t launches = 0;
+  const int cur = radix::sort_pairs(ws, k, v, 0, n, key_bits, true, st, &launches, 0);
+  if (cur == 1) {
+    cudaMemcpyAsync(keys, tmp_keys, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(vals, tmp_vals, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st);
+  }
+  cudaFreeAsync(ws.ghist, st);
+  cudaFreeAsync(ws.lookback, st);
+  cudaFreeAsync(ws.tile_ctr, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? CC_OK : CC_ERR_CUDA;
+}

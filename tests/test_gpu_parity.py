@@ -443,3 +443,23 @@ def test_u64_mode_errors(cc):
         cc.labels()  # u32 labels of a u64 graph
     with pytest.raises(ccmod.CCError):
         cc.load(e, 7, ids="u64")  # n_vertices must be 0
+
+
+@pytest.mark.parametrize("n,bits", [(1, 64), (4097, 64), (100003, 40), (300000, 17)])
+def test_radix_sort_pairs(n, bits):
+    """The onesweep regroup primitive through the ABI: stable sort by the low `bits` bits,
+    payload carried (checked against numpy's stable argsort)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_06156_b200 as ccmod
+    rng = np.random.default_rng(n)
+    k = rng.integers(0, 2**63, size=n, dtype=np.int64) * 2 + rng.integers(0, 2, size=n)
+    mask = np.uint64((1 << bits) - 1) if bits < 64 else np.uint64(2**64 - 1)
+    key = k.view(np.uint64) & mask
+    order = np.argsort(key, kind="stable")
+    dk = torch.from_numpy(k).cuda()
+    dv = torch.arange(n, dtype=torch.int32, device="cuda")
+    ccmod.cc_radix_sort_pairs(dk, dv, torch.empty_like(dk), torch.empty_like(dv), bits)
+    assert np.array_equal(dv.cpu().numpy(), order.astype(np.int32))
+    assert np.array_equal(dk.cpu().numpy(), k[order])
