@@ -201,7 +201,7 @@ cc_status cc_bfs_eccentricity(cc_ctx* ctx, const uint64_t* seeds, uint32_t count
 
 /* Stable LSD radix sort (the onesweep regroup primitive of the sort engine, PAPER.md:207
  * "the bulk step of the algorithm is the sorting of tuples") of n 64-bit keys by their bits
- * [0, key_bits), key_bits in 1..64, carrying a u32 payload.  keys/vals: device arrays of n,
+ * [0, key_bits), key_bits in 1..64 (keys must be < 2^key_bits), carrying a u32 payload.  keys/vals: device arrays of n,
  * sorted in place; tmp_keys/tmp_vals: device scratch of n each.  Enqueued on `stream`
  * (cudaStream_t) and synchronised; its look-back workspace (8 B x 256 per 4096 keys) comes
  * from cudaMallocAsync.  For the SURVEY NEXT-3 sort microbenchmark (scripts/sort_bench.py). */

@@ -30,7 +30,8 @@ def timed(fn, reps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--log2n", type=int, default=31)
+    ap.add_argument("--log2n", type=int, default=30,
+                    help="torch.sort takes at most INT_MAX elements: 30 for the comparison")
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
     n = 1 << args.log2n

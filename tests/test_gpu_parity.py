@@ -455,8 +455,9 @@ def test_radix_sort_pairs(n, bits):
     import paper_1607_06156_b200 as ccmod
     rng = np.random.default_rng(n)
     k = rng.integers(0, 2**63, size=n, dtype=np.int64) * 2 + rng.integers(0, 2, size=n)
-    mask = np.uint64((1 << bits) - 1) if bits < 64 else np.uint64(2**64 - 1)
-    key = k.view(np.uint64) & mask
+    if bits < 64:  # the ABI sorts keys < 2^key_bits
+        k = (k.view(np.uint64) & np.uint64((1 << bits) - 1)).view(np.int64)
+    key = k.view(np.uint64)
     order = np.argsort(key, kind="stable")
     dk = torch.from_numpy(k).cuda()
     dv = torch.arange(n, dtype=torch.int32, device="cuda")
