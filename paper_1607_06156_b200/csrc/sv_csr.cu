@@ -244,11 +244,27 @@ __global__ void __launch_bounds__(1024) k_group_degree(const uint2* __restrict__
 }
 
 // Second pass: place each arc tuple in its row (cursor per vertex).
+// SITEMS arcs per thread per step: their cursor atomics are independent and in flight
+// together (the returned slot is needed before the store, so one arc at a time would expose
+// the full L2 atomic round trip per arc).
+constexpr int XITEMS = 8;
 __global__ void __launch_bounds__(B) k_scatter(const uint2* __restrict__ arcs, uint64_t na,
                                                uint32_t* cur, uint32_t* __restrict__ P) {
-  for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < na; i += (uint64_t)gridDim.x * B) {
-    const uint2 rp = arcs[i];
-    P[atomicAdd(&cur[rp.x], 1u)] = rp.y;
+  const uint64_t stride = (uint64_t)gridDim.x * B * XITEMS;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)B * XITEMS + threadIdx.x; i0 < na; i0 += stride) {
+    uint2 rp[XITEMS];
+    uint32_t slot[XITEMS];
+#pragma unroll
+    for (int k = 0; k < XITEMS; k++) {
+      const uint64_t i = i0 + (uint64_t)k * B;
+      rp[k] = i < na ? arcs[i] : make_uint2(0xFFFFFFFFu, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < XITEMS; k++)
+      if (rp[k].x != 0xFFFFFFFFu) slot[k] = atomicAdd(&cur[rp[k].x], 1u);
+#pragma unroll
+    for (int k = 0; k < XITEMS; k++)
+      if (rp[k].x != 0xFFFFFFFFu) P[slot[k]] = rp[k].y;
   }
 }
 
@@ -352,7 +368,7 @@ void fill_from_buckets(const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t 
   cudaMemsetAsync(nlong, 0, sizeof(uint64_t), st);
   k_fill_rows<<<grid(n, B, 148 * 8), B, 0, st>>>(off, n, R, P, longlist, nl);
   k_fill_long<<<148 * 2, B, 0, st>>>(off, longlist, nl, R);
-  if (na) k_scatter<<<grid(na, B, 148 * 16), B, 0, st>>>(tmp, na, cur, P);
+  if (na) k_scatter<<<grid((na + XITEMS - 1) / XITEMS, B, 148 * 8), B, 0, st>>>(tmp, na, cur, P);
 }
 void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
           uint32_t* R, uint32_t* P, const uint32_t* garc, int gshift, uint64_t* gcur, uint2* tmp,
@@ -370,7 +386,7 @@ void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, ui
   if (directed) k_bucket<true><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp);
   else k_bucket<false><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp);
   const uint64_t na = directed ? m : 2 * m;
-  k_scatter<<<grid(na, B, 148 * 16), B, 0, st>>>(tmp, na, cur, P);
+  k_scatter<<<grid((na + XITEMS - 1) / XITEMS, B, 148 * 8), B, 0, st>>>(tmp, na, cur, P);
 }
 void compact(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2,
              scan::State& ss, cudaStream_t st) {
