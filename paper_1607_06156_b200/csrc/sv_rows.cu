@@ -47,6 +47,8 @@ namespace {
 constexpr int RB = 256;
 constexpr int RITEMS = 8;
 constexpr int RTILE = RB * RITEMS;
+constexpr int PB = 256;               // row-pass block: 8 warps, tiles of PB * RITEMS tuples (128: slower)
+constexpr int PTILE = PB * RITEMS;
 constexpr int RCACHE = 512;
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr uint32_t DEAD = 0xFFFFFFFFu;
@@ -147,15 +149,15 @@ struct RunAgg {
   uint32_t key, mn, mx, pad;
 };
 template <bool A>
-__global__ void __launch_bounds__(RB, 4) k_rowpass(
+__global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     const uint32_t* __restrict__ R, const uint32_t* __restrict__ Pin, uint32_t* __restrict__ Pout,
     uint64_t L, uint32_t ntiles, const uint32_t* __restrict__ MAP,
     const uint32_t* __restrict__ NCPr, const uint32_t* __restrict__ TB, uint32_t* OUT,
     uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int hot, int excl) {
-  constexpr int NW = RB / 32;
+  constexpr int NW = PB / 32;
   // double-buffered tile staging: TMA brings tile i+2 while tile i is processed
-  __shared__ __align__(128) uint32_t s_r[2][RTILE];
-  __shared__ __align__(128) uint32_t s_in[2][RTILE];
+  __shared__ __align__(128) uint32_t s_r[2][PTILE];
+  __shared__ __align__(128) uint32_t s_in[2][PTILE];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_last[NW];
   __shared__ RunAgg s_wt[NW], s_wh[NW + 1];  // per warp: last run (prefix), first run (suffix)
@@ -165,19 +167,19 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
   constexpr int RAGG = 1024;
   __shared__ uint32_t s_akey[RAGG], s_aval[RAGG];
   __shared__ uint32_t s_nc[A ? RCACHE : 1];
-  for (int i = threadIdx.x; i < RAGG; i += RB) {
+  for (int i = threadIdx.x; i < RAGG; i += PB) {
     s_akey[i] = INF;
     s_aval[i] = INF;
   }
-  for (int i = threadIdx.x; i < (A ? RCACHE : 1); i += RB) s_nc[i] = INF;
+  for (int i = threadIdx.x; i < (A ? RCACHE : 1); i += PB) s_nc[i] = INF;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // the last slot update / NCP flag this thread issued (slots only decrease): repeats are
   // common once a few partitions hold most tuples
   uint32_t last_p = INF, last_q = INF, last_nc = INF;
   auto issue = [&](uint32_t tl, int b) {  // thread 0: stage tile tl into buffer b
     if (tl >= ntiles) return;
-    const uint64_t a0 = (uint64_t)tl * RTILE;
-    const uint32_t n = (uint32_t)(L - a0 < (uint64_t)RTILE ? L - a0 : (uint64_t)RTILE);
+    const uint64_t a0 = (uint64_t)tl * PTILE;
+    const uint32_t n = (uint32_t)(L - a0 < (uint64_t)PTILE ? L - a0 : (uint64_t)PTILE);
     const uint32_t bytes = (n * 4 + 15) & ~15u;  // arrays are padded past L
     mbar_expect_tx(&s_bar[b], 2 * bytes);
     bulk_g2s(s_r[b], R + a0, bytes, &s_bar[b]);
@@ -197,8 +199,8 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
   uint32_t it = 0;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
     const int buf = it & 1;
-    const uint64_t t0 = (uint64_t)tile * RTILE;
-    const uint32_t tlen = (uint32_t)(L - t0 < (uint64_t)RTILE ? L - t0 : (uint64_t)RTILE);
+    const uint64_t t0 = (uint64_t)tile * PTILE;
+    const uint32_t tlen = (uint32_t)(L - t0 < (uint64_t)PTILE ? L - t0 : (uint64_t)PTILE);
     const uint64_t i0 = t0 + (uint64_t)threadIdx.x * RITEMS;
     const uint32_t rprev = (threadIdx.x == 0 && t0 > 0) ? __ldg(&R[t0 - 1]) : INF;
     uint32_t r[RITEMS], p[RITEMS];
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(RB, 4) k_rowpass(
   }
   if (hot) {  // flush the block's aggregated slot updates
     __syncthreads();
-    for (int i = threadIdx.x; i < RAGG; i += RB)
+    for (int i = threadIdx.x; i < RAGG; i += PB)
       if (s_akey[i] != INF) atomicMin(&OUT[s_akey[i]], s_aval[i]);
   }
   if (!A) {
@@ -611,13 +613,13 @@ void or_parts(const uint32_t* parts, uint64_t words, int world, uint32_t* out, c
 
 static unsigned persistent_grid(const void* fn, uint64_t ntiles) {
   int ps = 0, sms = 148, dev = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, RB, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, PB, 0);
   if (ps < 1) ps = 1;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)sms * ps));
 }
 
-uint64_t row_tiles(uint64_t L) { return (L + RTILE - 1) / RTILE; }
+uint64_t row_tiles(uint64_t L) { return (L + PTILE - 1) / PTILE; }
 uint64_t long_seg_cap(uint64_t L) { return L / LSEG + L / (LONG + 1) + 2; }
 
 
@@ -645,7 +647,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
   if (passA) {
     static unsigned ga = 0;
     if (!ga) ga = persistent_grid((const void*)k_rowpass<true>, ~0ull);
-    k_rowpass<true><<<(unsigned)std::min<uint64_t>(nt, ga), RB, 0, st>>>(
+    k_rowpass<true><<<(unsigned)std::min<uint64_t>(nt, ga), PB, 0, st>>>(
         R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0, excl ? 1 : 0);
     if (have_long) {
       k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
@@ -654,7 +656,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
   } else {
     static unsigned gb = 0;
     if (!gb) gb = persistent_grid((const void*)k_rowpass<false>, ~0ull);
-    k_rowpass<false><<<(unsigned)std::min<uint64_t>(nt, gb), RB, 0, st>>>(
+    k_rowpass<false><<<(unsigned)std::min<uint64_t>(nt, gb), PB, 0, st>>>(
         R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0, excl ? 1 : 0);
     if (have_long) {
       k_long1<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
