@@ -83,10 +83,14 @@ CC_DEVI unsigned long long tmax(uint32_t tag, uint32_t v) {
   return ((unsigned long long)tag << 32) | v;
 }
 
+CC_DEVI void st_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
 CC_DEVI void store8(uint32_t* X, uint64_t i0, uint64_t L, const uint32_t* x) {
-  if (i0 + RITEMS <= L) {
-    reinterpret_cast<uint4*>(X + i0)[0] = make_uint4(x[0], x[1], x[2], x[3]);
-    reinterpret_cast<uint4*>(X + i0)[1] = make_uint4(x[4], x[5], x[6], x[7]);
+  if (i0 + RITEMS <= L) {  // streaming stores: the next pass reads them back from DRAM anyway
+    st_stream(reinterpret_cast<uint4*>(X + i0), make_uint4(x[0], x[1], x[2], x[3]));
+    st_stream(reinterpret_cast<uint4*>(X + i0) + 1, make_uint4(x[4], x[5], x[6], x[7]));
   } else {
 #pragma unroll
     for (int j = 0; j < RITEMS; j++)
@@ -114,11 +118,18 @@ CC_DEVI void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
-CC_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// the tuple stream is read once per pass: evict-first in L2, so the partition slots (the
+// random-access working set of the pass) stay resident
+CC_DEVI uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+CC_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+      "[%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 
@@ -181,9 +192,10 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     const uint64_t a0 = (uint64_t)tl * PTILE;
     const uint32_t n = (uint32_t)(L - a0 < (uint64_t)PTILE ? L - a0 : (uint64_t)PTILE);
     const uint32_t bytes = (n * 4 + 15) & ~15u;  // arrays are padded past L
+    const uint64_t pol = l2_evict_first_policy();
     mbar_expect_tx(&s_bar[b], 2 * bytes);
-    bulk_g2s(s_r[b], R + a0, bytes, &s_bar[b]);
-    bulk_g2s(s_in[b], Pin + a0, bytes, &s_bar[b]);
+    bulk_g2s(s_r[b], R + a0, bytes, &s_bar[b], pol);
+    bulk_g2s(s_in[b], Pin + a0, bytes, &s_bar[b], pol);
   };
   if (threadIdx.x == 0) {
     mbar_init(&s_bar[0], 1);
