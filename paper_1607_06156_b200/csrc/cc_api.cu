@@ -372,9 +372,17 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
                    have_long, hot, c->d_ctr, c->st);
       k.end(8.0 * len + (it ? 4.0 * len : 0.0), 1 + (have_long ? 2 : 0)); }
     if (it) std::swap(Pc, Palt);
+    // sparse exchange once few partitions remain: the entries all ranks touched (at most
+    // |P_i-1| per rank) cost less than the dense n-slot reduction
+    const bool sparse = multi && it > 0 &&
+                        c->iters.back().partitions * (uint64_t)c->cfg.world_size * 2 < n4;
     if (multi) {  // partition minima and 'not completed' flags over all ranks
-      TRY(comm_min_u32(c, PA, n4));
-      TRY(comm_or_bits(c, NCP, nwp));
+      if (sparse) {
+        TRY(comm_sparse_slots(c, PA, NCP, n4));
+      } else {
+        TRY(comm_min_u32(c, PA, n4));
+        TRY(comm_or_bits(c, NCP, nwp));
+      }
     }
     // ---- line 22 bookkeeping: |P_i|, completed, changed, temporaries
     { Prof k(c, KF_SLOTS); csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all); k.end(8.0 * n4, 1); }
@@ -389,7 +397,8 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     CK(cudaMemcpyAsync(c->d_ctr + sv::C_SURVIVORS, c->d_ctr + sv::C_OUT, sizeof(uint64_t),
                        cudaMemcpyDeviceToDevice, c->st));
     if (multi) {
-      TRY(comm_min_u32(c, PB, n4));
+      if (sparse) TRY(comm_sparse_slots(c, PB, nullptr, n4));
+      else TRY(comm_min_u32(c, PB, n4));
       TRY(comm_allreduce(c, c->d_ctr + sv::C_OUT, 1, CC_DT_I64, CC_OP_SUM));
     }
     { Prof k(c, KF_SLOTS);

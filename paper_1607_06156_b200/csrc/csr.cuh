@@ -65,6 +65,11 @@ void temps2(const uint32_t* TB, uint64_t n, uint32_t* PB, cudaStream_t st);
 // changed2 after pass B (clears PA, NCP, TB)
 void pstat2(const uint32_t* PB, uint64_t n, uint32_t* PA, uint32_t* NCP, uint32_t* TB, uint64_t* ctr,
             cudaStream_t st);
+// multi-GPU sparse slot exchange: touched slots as (p, value | NCP(p) << 31) entries (*cnt =
+// their number), and min / OR application of a list (entries with p = ~0 are padding)
+void extract_slots(const uint32_t* S, const uint32_t* BM, uint64_t n, uint2* out, uint64_t* cnt,
+                   cudaStream_t st);
+void apply_slots(const uint2* in, uint64_t count, uint32_t* S, uint32_t* BM, cudaStream_t st);
 // multi-GPU slot exchange helpers: a[i] ^= 0x80000000; out[i] = OR_k parts[k*words + i]
 void flip_sign(uint32_t* a, uint64_t n, cudaStream_t st);
 void or_parts(const uint32_t* parts, uint64_t words, int world, uint32_t* out, cudaStream_t st);

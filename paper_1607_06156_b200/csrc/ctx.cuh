@@ -60,6 +60,9 @@ struct cc_ctx {
   uint32_t* d_gath = nullptr;    // allgather scratch (world_size x bitmap words)
   uint64_t gath_cap = 0;
   uint64_t* d_cnt = nullptr;     // per-owner arc counts (world_size^2 after the gather)
+  uint2* d_xsend = nullptr;      // sparse slot exchange: my touched entries / everyone's
+  uint2* d_xrecv = nullptr;
+  uint64_t xsend_cap = 0, xrecv_cap = 0;
   uint32_t* d_garc = nullptr;  // CSR vertex-group scratch: arcs per group (<= 2048 groups)
   uint64_t* d_gcur = nullptr;  // group cursors [0, 2048), long-row count at [2048]
   uint64_t* d_ctr = nullptr;   // sv counters
@@ -152,6 +155,8 @@ static inline void dfree_all(cc_ctx* c) {
   c->d_send = c->d_recv = nullptr;
   c->d_gath = nullptr;
   c->d_cnt = nullptr;
+  c->d_xsend = c->d_xrecv = nullptr;
+  c->xsend_cap = c->xrecv_cap = 0;
   c->recv_cap = c->gath_cap = 0;
   c->d_lsegs = nullptr;
   c->row_tag = 0;
@@ -304,6 +309,38 @@ static inline cc_status comm_or_bits(cc_ctx* c, uint32_t* bm, uint64_t words) {
   TRY(comm_allgather(c, bm, c->d_gath, words * sizeof(uint32_t)));
   csr::or_parts(c->d_gath, words, c->cfg.world_size, bm, c->st);
   c->launches += 1;
+  return CC_OK;
+}
+
+// Sparse form of the slot exchange for late iterations (few partitions): every rank
+// all-gathers its touched (slot, value | NCP bit) entries, padded to the largest list, and
+// min-applies everyone's entries to its own copy -- the same result as comm_min_u32 (and
+// comm_or_bits for NCP) with volume proportional to the touched partitions.
+static inline cc_status comm_sparse_slots(cc_ctx* c, uint32_t* S, uint32_t* BM, uint64_t count) {
+  if (!multi_gpu(c)) return CC_OK;
+  const uint64_t world = (uint64_t)c->cfg.world_size;
+  if (!c->d_xsend || c->xsend_cap < count + 1) {
+    TRY(dalloc_t(c, &c->d_xsend, count + 1));
+    c->xsend_cap = count + 1;
+  }
+  uint64_t* cnt = c->d_gcur + 2052;  // [2052]: my entries, [2053]: max over ranks
+  csr::extract_slots(S, BM, count, c->d_xsend, cnt, c->st);
+  CK(cudaMemcpyAsync(cnt + 1, cnt, sizeof(uint64_t), cudaMemcpyDeviceToDevice, c->st));
+  TRY(comm_allreduce(c, cnt + 1, 1, CC_DT_I64, CC_OP_MAX));
+  uint64_t cm[2] = {0, 0};
+  CK(cudaMemcpyAsync(cm, cnt, sizeof(cm), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const uint64_t mine = cm[0], pad = cm[1];
+  if (pad == 0) return CC_OK;
+  if (pad > mine)  // padding entries (slot ~0) up to the common length
+    CK(cudaMemsetAsync(c->d_xsend + mine, 0xFF, sizeof(uint2) * (pad - mine), c->st));
+  if (!c->d_xrecv || c->xrecv_cap < world * pad + 1) {
+    TRY(dalloc_t(c, &c->d_xrecv, world * pad + 1));
+    c->xrecv_cap = world * pad + 1;
+  }
+  TRY(comm_allgather(c, c->d_xsend, c->d_xrecv, pad * sizeof(uint2)));
+  csr::apply_slots(c->d_xrecv, world * pad, S, BM, c->st);
+  c->launches += 2;
   return CC_OK;
 }
 

@@ -610,7 +610,49 @@ __global__ void k_or_parts(const uint32_t* __restrict__ parts, uint64_t words, i
   }
 }
 
+// Sparse slot exchange (multi-GPU, late iterations): the touched partition slots of a rank as
+// (p, value | NCP(p) << 31) entries (NCP is only ever set on touched slots: the row minimum's
+// own tuple touches it), and their application to a rank's copy.
+__global__ void k_extract_slots(const uint32_t* __restrict__ S, const uint32_t* __restrict__ BM,
+                                uint64_t n, uint2* __restrict__ out, unsigned long long* cnt) {
+  for (uint64_t p0 = blockIdx.x * (uint64_t)RB; p0 < n; p0 += (uint64_t)gridDim.x * RB) {
+    const uint64_t p = p0 + threadIdx.x;
+    const uint32_t v = p < n ? S[p] : INF;
+    const bool take = v != INF;
+    const uint32_t mask = __ballot_sync(FULL, take);
+    if (!mask) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(cnt, (unsigned long long)__popc(mask));
+    base = __shfl_sync(FULL, base, leader);
+    if (take) {
+      const uint32_t ncp = BM ? (BM[p >> 5] >> (p & 31)) & 1u : 0u;
+      out[base + __popc(mask & ((1u << lane) - 1u))] = make_uint2((uint32_t)p, v | (ncp << 31));
+    }
+  }
+}
+__global__ void k_apply_slots(const uint2* __restrict__ in, uint64_t count, uint32_t* S, uint32_t* BM) {
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < count; i += (uint64_t)gridDim.x * RB) {
+    const uint2 e = in[i];
+    if (e.x == INF) continue;  // padding
+    const uint32_t v = e.y & 0x7FFFFFFFu;
+    if (v < S[e.x]) atomicMin(&S[e.x], v);
+    if ((e.y >> 31) && BM) atomicOr(&BM[e.x >> 5], 1u << (e.x & 31));
+  }
+}
+
 // --------------------------------------------------------------------------- launchers
+void extract_slots(const uint32_t* S, const uint32_t* BM, uint64_t n, uint2* out, uint64_t* cnt,
+                   cudaStream_t st) {
+  cudaMemsetAsync(cnt, 0, sizeof(uint64_t), st);
+  if (n)
+    k_extract_slots<<<(unsigned)std::min<uint64_t>((n + RB - 1) / RB, 148 * 8), RB, 0, st>>>(
+        S, BM, n, out, reinterpret_cast<unsigned long long*>(cnt));
+}
+void apply_slots(const uint2* in, uint64_t count, uint32_t* S, uint32_t* BM, cudaStream_t st) {
+  if (count)
+    k_apply_slots<<<(unsigned)std::min<uint64_t>((count + RB - 1) / RB, 148 * 8), RB, 0, st>>>(in, count, S, BM);
+}
 void final_labels(const uint32_t* R, const uint32_t* P, uint64_t L, uint32_t* label, cudaStream_t st) {
   if (L) k_final_labels<<<(unsigned)std::min<uint64_t>((L + RB - 1) / RB, 148 * 8), RB, 0, st>>>(R, P, L, label);
 }
