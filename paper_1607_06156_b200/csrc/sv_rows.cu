@@ -46,7 +46,7 @@ namespace {
 
 constexpr int RB = 256;
 constexpr int RITEMS = 8;
-constexpr int RTILE = RB * RITEMS;
+
 constexpr int PB = 256;               // row-pass block: 8 warps, tiles of PB * RITEMS tuples (128: slower)
 constexpr int PTILE = PB * RITEMS;
 constexpr int RCACHE = 512;
