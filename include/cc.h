@@ -212,6 +212,10 @@ cc_status cc_radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* tmp_keys
  * the device stream all work is enqueued on.  For zero-copy consumers. */
 cc_status cc_labels_device(cc_ctx* ctx, const uint32_t** labels, uint64_t* count);
 
+/* Switch the CC_FLAG_PROFILE event timing on (nonzero) or off for the following cc_run calls
+ * (bench.py times the step without events, then the per-kernel breakdown with them). */
+cc_status cc_set_profiling(cc_ctx* ctx, int on);
+
 /* Number of kernel launches enqueued by the last cc_run (evidence for bench.py). */
 uint64_t cc_last_launch_count(const cc_ctx* ctx);
 

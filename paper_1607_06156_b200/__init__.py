@@ -87,7 +87,7 @@ class cc_report(ctypes.Structure):
 
 EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
            "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_radix_sort_pairs",
-           "cc_last_launch_count",
+           "cc_set_profiling", "cc_last_launch_count",
            "cc_kernel_stats",
            "cc_kernel_name", "cc_destroy", "cc_status_string", "cc_last_error"]
 
@@ -113,6 +113,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_bfs_eccentricity.argtypes = [P, P, ctypes.c_uint32, P]
     lib.cc_radix_sort_pairs.argtypes = [P, P, P, P, ctypes.c_uint64, ctypes.c_int, P]
     lib.cc_radix_sort_pairs.restype = ctypes.c_int
+    lib.cc_set_profiling.argtypes = [P, ctypes.c_int]
+    lib.cc_set_profiling.restype = ctypes.c_int
     lib.cc_last_launch_count.restype = ctypes.c_uint64
     lib.cc_last_launch_count.argtypes = [P]
     lib.cc_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
@@ -421,6 +423,9 @@ class CC:
 
     def labels_u64(self):
         return cc_labels_u64(self.ctx)
+
+    def set_profiling(self, on):
+        _check(self.ctx, lib().cc_set_profiling(self.ctx, 1 if on else 0))
 
     def launches(self):
         return int(lib().cc_last_launch_count(self.ctx))

@@ -54,6 +54,13 @@ const char* cc_last_error(const cc_ctx* c) { return c ? c->err.c_str() : "null c
 
 uint64_t cc_last_launch_count(const cc_ctx* c) { return c ? c->launches : 0; }
 
+cc_status cc_set_profiling(cc_ctx* c, int on) {
+  if (!c) return CC_ERR_INVALID;
+  if (on) c->cfg.flags |= CC_FLAG_PROFILE;
+  else c->cfg.flags &= ~CC_FLAG_PROFILE;
+  return CC_OK;
+}
+
 cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
   if (!cfg || !out) return CC_ERR_INVALID;
   *out = nullptr;
