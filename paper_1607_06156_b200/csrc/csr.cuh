@@ -22,8 +22,10 @@ void bucket_degrees(const uint2* edges, uint64_t m, uint64_t n, int gshift, uint
 void fill_from_buckets(const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A, uint32_t* R,
                        uint32_t* P, const uint2* tmp, uint64_t na, uint32_t* longlist, uint64_t* nlong,
                        cudaStream_t st);
-// R fill, vertex tuples, and the two-level arc scatter (bucket by vertex group, then rows).
-// tmp: 2m uint2 scratch; longlist: n uint32 scratch; garc/gcur: 1024 entries.  `directed`:
+// R fill, vertex tuples, and the arc placement: bucket by vertex group, re-bucket by
+// subgroup of 2^13 ids into P-aligned scratch, place rows with shared-memory cursors.  R and
+// P must be the two halves of one allocation (P - R >= 2m; the group buckets use it), tmp
+// is cap uint2 of scratch; longlist: n uint32 scratch; garc/gcur: group entries.  `directed`:
 // `edges` holds m arcs (r, p) instead of m undirected edges (two arcs each).
 void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, uint64_t n, uint64_t A,
           uint32_t* R, uint32_t* P, const uint32_t* garc, int gshift, uint64_t* gcur, uint2* tmp,

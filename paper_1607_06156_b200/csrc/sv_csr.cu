@@ -243,6 +243,156 @@ __global__ void __launch_bounds__(1024) k_group_degree(const uint2* __restrict__
   for (uint32_t v = threadIdx.x; v < cnt; v += blockDim.x) deg[base + v] = s_deg[v];
 }
 
+// ---- row placement without global cursor atomics (default path).  The arcs bucketed by
+// group (k_bucket) are re-bucketed by subgroup of 2^SUBG ids into a P-aligned scratch array
+// (subgroup s's arcs land in [off[v0], ...), inside the P range its rows will occupy), then
+// one block per subgroup places its arcs with shared-memory row cursors and writes R and the
+// vertex tuples of its rows: every global write stays inside the subgroup's own P window.
+constexpr int SUBG = 11;
+constexpr int MAXS2 = 512;
+__global__ void k_sub_init(const uint32_t* __restrict__ off, uint64_t ns, uint32_t* __restrict__ scur) {
+  for (uint64_t s = blockIdx.x * (uint64_t)B + threadIdx.x; s < ns; s += (uint64_t)gridDim.x * B)
+    scur[s] = off[s << SUBG];
+}
+__global__ void __launch_bounds__(B) k_bucket2(const uint2* __restrict__ in, uint64_t na,
+                                               uint32_t* scur, uint2* __restrict__ out) {
+  __shared__ uint32_t s_cnt[MAXS2];
+  __shared__ uint32_t s_base[MAXS2];
+  __shared__ uint32_t s_lo, s_hi;
+  if (threadIdx.x == 0) {
+    s_lo = 0xFFFFFFFFu;
+    s_hi = 0;
+  }
+  for (int i = threadIdx.x; i < MAXS2; i += B) s_cnt[i] = 0;
+  __syncthreads();
+  const uint64_t e0 = blockIdx.x * (uint64_t)B * BITEMS + threadIdx.x;
+  uint2 arc[BITEMS];
+  uint32_t lo = 0xFFFFFFFFu, hi = 0;
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * B;
+    arc[k] = i < na ? in[i] : make_uint2(0xFFFFFFFFu, 0);
+    if (i < na) {
+      lo = min(lo, arc[k].x >> SUBG);
+      hi = max(hi, arc[k].x >> SUBG);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&s_lo, lo);
+    atomicMax(&s_hi, hi);
+  }
+  __syncthreads();
+  const uint32_t slo = s_lo;
+  const bool local = s_hi - slo < (uint32_t)MAXS2;  // the tile's subgroups fit the counters
+  uint32_t slot[BITEMS];
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    if (arc[k].x == 0xFFFFFFFFu) continue;
+    const uint32_t sg = arc[k].x >> SUBG;
+    slot[k] = local ? atomicAdd(&s_cnt[sg - slo], 1u) : atomicAdd(&scur[sg], 1u);
+  }
+  if (local) {
+    __syncthreads();
+    for (int l = threadIdx.x; l < MAXS2; l += B)
+      s_base[l] = s_cnt[l] ? atomicAdd(&scur[slo + l], s_cnt[l]) : 0u;
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    if (arc[k].x == 0xFFFFFFFFu) continue;
+    const uint32_t pos = local ? s_base[(arc[k].x >> SUBG) - slo] + slot[k] : slot[k];
+    out[pos] = arc[k];
+  }
+}
+constexpr int PLACE_LONG_CAP = 64;
+constexpr int PLACE_CAP = 7168;  // tuples of a subgroup assembled in shared memory
+constexpr size_t PLACE_SMEM = sizeof(uint32_t) * (2 * ((1 << SUBG) + 1) + 2 * PLACE_CAP);
+__global__ void __launch_bounds__(B) k_place(const uint32_t* __restrict__ off, uint64_t n,
+                                             const uint32_t* __restrict__ scur_end,
+                                             const uint2* __restrict__ arcs, uint32_t* __restrict__ R,
+                                             uint32_t* __restrict__ P) {
+  extern __shared__ uint32_t smem[];
+  uint32_t* s_off = smem;                          // row starts relative to the subgroup
+  uint32_t* s_cur = s_off + (1 << SUBG) + 1;       // next free slot of each row
+  uint32_t* s_p = s_cur + (1 << SUBG) + 1;         // the subgroup's P, assembled
+  uint32_t* s_r = s_p + PLACE_CAP;                 // and its R
+  __shared__ uint32_t s_long[PLACE_LONG_CAP];
+  __shared__ uint32_t s_nlong;
+  const uint64_t s = blockIdx.x, v0 = s << SUBG;
+  const uint32_t cnt = (uint32_t)min((uint64_t)1 << SUBG, n - v0);
+  const uint32_t base0 = off[v0], T = off[v0 + cnt] - base0;
+  const bool staged = T <= (uint32_t)PLACE_CAP;  // else rows are written in place
+  if (threadIdx.x == 0) s_nlong = 0;
+  for (uint32_t l = threadIdx.x; l <= cnt; l += B) s_off[l] = off[v0 + l] - base0;
+  __syncthreads();
+  // rows: vertex tuple <v,_,v> first, R over the row; cursors after it
+  for (uint32_t l = threadIdx.x; l < cnt; l += B) {
+    const uint32_t a = s_off[l], b = s_off[l + 1];
+    s_cur[l] = a + 1;
+    if (a == b) continue;
+    const uint32_t v = (uint32_t)(v0 + l);
+    if (staged) {
+      s_p[a] = v;
+      for (uint32_t i = a; i < b; i++) s_r[i] = v;  // staged rows are short (T <= PLACE_CAP)
+      if (b - a > LONG)
+        for (uint32_t i = a; i < b; i++) s_r[i] = v | R_LONG;
+    } else {
+      P[base0 + a] = v;
+      if (b - a <= LONG_ROW) {
+        for (uint32_t i = a; i < b; i++) R[base0 + i] = v;
+      } else {
+        const uint32_t j = atomicAdd(&s_nlong, 1u);
+        if (j < PLACE_LONG_CAP) {
+          s_long[j] = l;
+        } else {
+          const uint32_t rv = v | (b - a > LONG ? R_LONG : 0u);
+          for (uint32_t i = a; i < b; i++) R[base0 + i] = rv;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // arcs of the subgroup: shared-memory row cursors
+  const uint32_t a1 = scur_end[s];
+  constexpr int PI = 8;  // arcs per thread in flight
+  for (uint32_t i0 = base0; i0 < a1; i0 += B * PI) {
+    uint2 rp[PI];
+#pragma unroll
+    for (int k = 0; k < PI; k++) {
+      const uint32_t i = i0 + k * B + threadIdx.x;
+      rp[k] = i < a1 ? arcs[i] : make_uint2(0xFFFFFFFFu, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < PI; k++) {
+      if (rp[k].x == 0xFFFFFFFFu) continue;
+      // shared-memory cursor: native atomics, same-row lanes serialise only among themselves
+      const uint32_t slot = atomicAdd(&s_cur[rp[k].x - v0], 1u);
+      if (staged) s_p[slot] = rp[k].y;
+      else P[base0 + slot] = rp[k].y;
+    }
+  }
+  if (staged) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < T; i += B) {  // contiguous runs out
+      P[base0 + i] = s_p[i];
+      R[base0 + i] = s_r[i];
+    }
+  } else {
+    const uint32_t nl = min(s_nlong, (uint32_t)PLACE_LONG_CAP);
+    for (uint32_t j = 0; j < nl; j++) {
+      const uint32_t l = s_long[j];
+      const uint32_t a = s_off[l], b = s_off[l + 1];
+      const uint32_t rv = (uint32_t)(v0 + l) | (b - a > LONG ? R_LONG : 0u);  // long rows skipped by row passes
+      for (uint32_t i = a + threadIdx.x; i < b; i += B) R[base0 + i] = rv;
+    }
+  }
+}
+
 // Second pass: place each arc tuple in its row (cursor per vertex).
 // SITEMS arcs per thread per step: their cursor atomics are independent and in flight
 // together (the returned slot is needed before the store, so one arc at a time would expose
@@ -375,6 +525,29 @@ void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, ui
           uint32_t* longlist, uint64_t* nlong, cudaStream_t st, bool directed) {
   if (!A) return;
   const int G = (int)(((n - 1) >> gshift) + 1);
+  if (m && P > R && (uint64_t)(P - R) * 2 >= (directed ? 2 * m : 4 * m) && gshift >= SUBG) {
+    // default: the group buckets go into R's buffer (R and P are the two halves of one
+    // 8-byte-per-tuple allocation, free until placement), the P-aligned subgroup buckets
+    // into tmp, then k_place writes R and P
+    auto* gc = reinterpret_cast<unsigned long long*>(gcur);
+    uint2* tmp1 = reinterpret_cast<uint2*>(R);
+    k_gscan<<<1, B, 0, st>>>(garc, G, gc);
+    const unsigned gb = (unsigned)((m + B * BITEMS - 1) / (B * BITEMS));
+    if (directed) k_bucket<true><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp1);
+    else k_bucket<false><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp1);
+    const uint64_t na = directed ? m : 2 * m;
+    const uint64_t ns = ((n - 1) >> SUBG) + 1;
+    uint32_t* scur = longlist;  // n-sized scratch, ns entries used
+    k_sub_init<<<grid(ns, B, 148 * 4), B, 0, st>>>(off, ns, scur);
+    k_bucket2<<<(unsigned)((na + B * BITEMS - 1) / (B * BITEMS)), B, 0, st>>>(tmp1, na, scur, tmp);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLACE_SMEM);
+      attr = true;
+    }
+    k_place<<<(unsigned)ns, B, PLACE_SMEM, st>>>(off, n, scur, tmp, R, P);
+    return;
+  }
   auto* nl = reinterpret_cast<unsigned long long*>(nlong);
   cudaMemsetAsync(nlong, 0, sizeof(uint64_t), st);
   k_fill_rows<<<grid(n, B, 148 * 8), B, 0, st>>>(off, n, R, P, longlist, nl);
