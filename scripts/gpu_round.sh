@@ -15,5 +15,5 @@ CMD="python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_c2.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 $CMD > gpurun_out/${TAG}_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:${NCU_KERNELS:-k_vpass|k_ppass|k_papply|k_compact|k_pscan|k_temps}" -s ${NCU_SKIP:-60} -c ${NCU_COUNT:-8} \
+ncu --set full --clock-control none --import-source on -k "regex:${NCU_KERNELS:-k_rowpass|k_pstat1|k_place|k_bucket2}" -s ${NCU_SKIP:-60} -c ${NCU_COUNT:-8} \
   -o gpurun_out/${TAG}_full_c2 $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"

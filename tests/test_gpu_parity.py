@@ -318,6 +318,26 @@ def test_config_c4_full(cc, request):
     assert rep["max_degree"] == int(np.bincount(g.edges.reshape(-1), minlength=g.n).max())
 
 
+def test_degree_counts_large_id_range(cc, request):
+    """n = 2^25 (> the 2^24-id L2 window: the degree count streams the edges once per
+    window); the degree statistics and gate equal the oracle's (numpy bincount of the arc
+    sources) and the labels the union-find's."""
+    if "[csr]" not in request.node.name:
+        pytest.skip("prediction is shared by the engines: once")
+    e = graphgen.rmat(graphgen.BASE_SEED + 25, 25, 2)
+    e = np.concatenate([e, np.array([[7, 7], [7, 7], [2**25 - 1, 3]], np.uint32)])
+    n = 1 << 25
+    deg, hist = odeg.degree_distribution(n, e)
+    gl = odeg.gate_ls(hist)
+    lab, rep = run(cc, n, e, "auto")
+    assert rep["max_degree"] == int(deg.max())
+    assert rep["n_present"] == int(np.count_nonzero(deg))
+    assert rep["ls_alpha"] == pytest.approx(gl["alpha"], rel=1e-9)
+    assert rep["ls_r2"] == pytest.approx(gl["r2"], rel=1e-9)
+    assert rep["ran_bfs"] == int(gl["scale_free"])
+    assert np.array_equal(lab, oracle.uf_labels(n, e).astype(np.int64))
+
+
 # ------------------------------------------------------------------ u64 ids (relabel)
 def _u64_graph(seed, nv, m):
     rng = np.random.default_rng(seed)
