@@ -69,3 +69,20 @@ int main(){printf("%zu %zu %zu %zu\n", sizeof(cc_config), sizeof(cc_report), siz
         sizes = list(map(int, subprocess.check_output([exe]).split()))
     assert sizes == [ctypes.sizeof(cc.cc_config), ctypes.sizeof(cc.cc_report),
                      ctypes.sizeof(cc.cc_iter_stat), cc.cc_report.iters.offset]
+
+
+def test_bench_reference_arm_prints_contract_line():
+    """bench.py --impl reference (the oracle arm) runs on CPU and prints one JSON line with
+    the contract's keys (small config to keep the CPU suite fast)."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.check_output([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                                   "--config", "c1", "--steps", "2", "--warmup", "1"], text=True,
+                                  cwd=ROOT, timeout=600)
+    line = json.loads(out.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
