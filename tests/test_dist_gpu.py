@@ -122,3 +122,39 @@ def test_dist_exclusion_variants():
 def test_dist_matches_single_gpu_c2_sample():
     g = graphgen.make("c2", 0.05)
     _check(run_ranks(_rank_run, 2, g.n, g.edges, ("auto",), 0), g.n, g.edges, ("auto",), trace=False)
+
+
+def _nccl_world1(rank, world):
+    """The NCCL forms of the TorchComm collectives (all_gather_into_tensor, uneven
+    all_to_all_single, typed all_reduce) on device buffers, on a 1-rank NCCL group."""
+    import ctypes
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_1607_06156_b200 as cc
+    dev = torch.device("cuda", 0)
+    g = dist.new_group([0], backend="nccl")
+    comm = cc.TorchComm(group=g, device=dev)
+    assert not comm.host_copy
+    s = comm.struct
+    a = torch.tensor([5, 0x7FFFFFFF, -3], dtype=torch.int32, device=dev)
+    assert s.allreduce(None, a.data_ptr(), 3, cc.CC_DT_I32, cc.CC_OP_MIN, None) == 0
+    b = torch.tensor([1, 2], dtype=torch.int64, device=dev)
+    assert s.allreduce(None, b.data_ptr(), 2, cc.CC_DT_I64, cc.CC_OP_SUM, None) == 0
+    src = torch.arange(12, dtype=torch.uint8, device=dev)
+    dst = torch.zeros(12, dtype=torch.uint8, device=dev)
+    assert s.allgather(None, src.data_ptr(), dst.data_ptr(), 12, None) == 0
+    sb = (ctypes.c_uint64 * 1)(8)
+    rb = (ctypes.c_uint64 * 1)(8)
+    x = torch.arange(8, dtype=torch.uint8, device=dev) + 100
+    y = torch.zeros(8, dtype=torch.uint8, device=dev)
+    assert s.alltoallv(None, x.data_ptr(), sb, y.data_ptr(), rb, None) == 0
+    return a.tolist(), b.tolist(), dst.tolist(), y.tolist()
+
+
+def test_torchcomm_nccl_world1():
+    res = run_ranks(_nccl_world1, 1)[0]
+    assert res[0] == [5, 0x7FFFFFFF, -3]
+    assert res[1] == [1, 2]
+    assert res[2] == list(range(12))
+    assert res[3] == [100 + i for i in range(8)]
