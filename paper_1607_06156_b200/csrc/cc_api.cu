@@ -168,7 +168,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
       TRY(dalloc_t(c, &c->d_pi, n + 1));
     }
   }
-  c->rws.max_tiles = c->cap / radix::TILE + 2;
+  c->rws.max_tiles = c->cap / radix::TILE_MIN + 2;
   TRY(dalloc_t(c, &c->rws.ghist, radix::MAX_PASSES * radix::RADIX));
   TRY(dalloc_t(c, &c->rws.lookback, c->rws.max_tiles * radix::RADIX));
   TRY(dalloc_t(c, &c->rws.tile_ctr, radix::MAX_PASSES));
@@ -1042,7 +1042,7 @@ extern "C" cc_status cc_radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_
   if (n < 2) return CC_OK;
   cudaStream_t st = (cudaStream_t)stream;
   radix::Workspace ws;
-  ws.max_tiles = n / radix::TILE + 2;
+  ws.max_tiles = n / radix::TILE_MIN + 2;
   if (cudaMallocAsync(&ws.ghist, sizeof(uint64_t) * radix::MAX_PASSES * radix::RADIX, st) != cudaSuccess ||
       cudaMallocAsync(&ws.lookback, sizeof(uint64_t) * ws.max_tiles * radix::RADIX, st) != cudaSuccess ||
       cudaMallocAsync(&ws.tile_ctr, sizeof(uint32_t) * radix::MAX_PASSES, st) != cudaSuccess) {
