@@ -151,7 +151,7 @@ const char* cc_version(void);
 
 /* Create a context on cfg->device.  cfg is copied.  Returns CC_ERR_INVALID for a NULL
  * argument, a bad rank / world_size, or world_size > 1 without cfg->comm; CC_ERR_CUDA if the
- * device cannot be used.  Multi-GPU contexts (world_size > 1) take u32 ids; cc_load_edges,
+ * device cannot be used.  In multi-GPU contexts (world_size > 1) cc_load_edges,
  * cc_run are collective (every rank calls them, each with its own block of edges). */
 cc_status cc_init(const cc_config* cfg, cc_ctx** out);
 
@@ -183,7 +183,14 @@ cc_status cc_labels_u32(cc_ctx* ctx, uint32_t* out, uint64_t cap, uint64_t* coun
 
 /* u64 mode: the distinct ids (ascending) into `ids` and the label of each (the minimum id
  * of its component) into `labels`; both have room for `cap` entries, *count receives the
- * number of distinct ids.  CC_ERR_STATE on a u32 graph (and cc_labels_u32 on a u64 one). */
+ * number of distinct ids.  CC_ERR_STATE on a u32 graph (and cc_labels_u32 on a u64 one).
+ * world_size > 1: the ids are relabelled over all ranks by a distributed sort-unique
+ * (sample-sort splitters, two all-to-all-v exchanges), rank k owns the
+ * block [lo, hi) of the dense ids (cc_block_range) and receives the original ids of that
+ * block with their labels (*count = hi - lo; the ranks' outputs concatenate to the global
+ * sorted id list).  Collective then: every rank calls it with buffers (a call with NULL
+ * buffers only reports *count and returns CC_ERR_INVALID, without communicating).
+ * CC_FLAG_PERMUTE_IDS is single-GPU (CC_ERR_INVALID from cc_load_edges otherwise). */
 cc_status cc_labels_u64(cc_ctx* ctx, uint64_t* ids, uint64_t* labels, uint64_t cap,
                         uint64_t* count, int out_on_device);
 

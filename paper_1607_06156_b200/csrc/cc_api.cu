@@ -103,12 +103,46 @@ cc_status cc_destroy(cc_ctx* c) {
   return CC_OK;
 }
 
+}  // extern "C"
+
+// n-sized buffers (labels, degrees, bitmaps, partition slots) and the owned vertex block:
+// at load time, or after the distributed u64 relabel once the global id count is known
+cc_status alloc_vertex_buffers(cc_ctx* c, uint64_t n) {
+  const uint64_t world = (uint64_t)c->cfg.world_size;
+  const uint64_t nw = (n + 31) / 32 + 1;
+  c->n = n;
+  c->n_alloc = n;
+  c->kbits = bits_for(n);
+  TRY(dalloc_t(c, &c->d_label, n + 1));
+  TRY(dalloc_t(c, &c->d_deg, n + 1));
+  // owned vertex block (multi-GPU): blk = 32 * ceil(n / (32 * world))
+  c->blk = std::max<uint64_t>(32, (n + 32 * world - 1) / (32 * world) * 32);
+  c->lo = std::min<uint64_t>(n, c->blk * (uint64_t)c->cfg.rank);
+  c->hi = world > 1 ? std::min<uint64_t>(n, c->lo + c->blk) : n;
+  if (world == 1) c->lo = 0;
+  const uint64_t bmw = std::max<uint64_t>(2 * nw, world * c->blk / 32) + 2;
+  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], bmw));  // 2-bit BFS state fits
+  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_sbm[i], nw + 2));
+  TRY(dalloc_t(c, &c->d_segA, n + 64));  // padded: the slot scans read 4 slots per thread
+  TRY(dalloc_t(c, &c->d_segB, n + 64));
+  TRY(dalloc_t(c, &c->d_umin, n + 1));
+  TRY(dalloc_t(c, &c->d_umax, n + 1));
+  CK(cudaMemsetAsync(c->d_umin, 0xFF, sizeof(uint64_t) * (n + 1), c->st));
+  CK(cudaMemsetAsync(c->d_umax, 0, sizeof(uint64_t) * (n + 1), c->st));
+  return ensure_scan_tiles(c);
+}
+
+extern "C" {
+
 cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint64_t n, int on_dev) {
   if (!c) return CC_ERR_INVALID;
   if (m && !pairs) return fail(c, CC_ERR_INVALID, "pairs is NULL");
   if (w != CC_U32 && w != CC_U64) return fail(c, CC_ERR_INVALID, "bad id width %d", (int)w);
-  if (w == CC_U64 && c->cfg.world_size > 1)
-    return fail(c, CC_ERR_INVALID, "u64 ids are single-GPU in this build (DESIGN.md §7)");
+  // u64 ids over several ranks: the global id count is known only after the distributed
+  // relabel in cc_run, which then allocates the n-sized buffers (relabel_dist.cu)
+  const bool dist64 = w == CC_U64 && c->cfg.world_size > 1;
+  if (dist64 && (c->cfg.flags & CC_FLAG_PERMUTE_IDS))
+    return fail(c, CC_ERR_INVALID, "CC_FLAG_PERMUTE_IDS is single-GPU in this build");
   if (w == CC_U64) {
     if (n != 0) return fail(c, CC_ERR_INVALID, "u64 ids: n_vertices must be 0");
     n = std::min<uint64_t>(2 * m, 1ull << 30);  // bound on distinct ids (checked in cc_run)
@@ -121,41 +155,24 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   c->loaded = c->ran = false;
   c->idw = w;
   c->n = n;
-  c->n_alloc = n;
+  c->n_alloc = 0;
   c->m = m;
   c->kbits = bits_for(n);
-  const uint64_t nw = (n + 31) / 32 + 1;
   c->cap = (2 * m + 2 * n + 64 + 1023) & ~1023ull;  // keeps P = R + cap 16-byte aligned
+  const uint64_t world = (uint64_t)c->cfg.world_size;
   TRY(dalloc_t(c, &c->d_edges, m + 1));
-  TRY(dalloc_t(c, &c->d_label, n + 1));
-  TRY(dalloc_t(c, &c->d_deg, n + 1));
   TRY(dalloc_t(c, &c->d_hist, graph::HIST_DENSE));
   TRY(dalloc_t(c, &c->d_tail, graph::TAIL_CAP));
-  // owned vertex block (multi-GPU): blk = 32 * ceil(n / (32 * world))
-  const uint64_t world = (uint64_t)c->cfg.world_size;
-  c->blk = std::max<uint64_t>(32, (n + 32 * world - 1) / (32 * world) * 32);
-  c->lo = std::min<uint64_t>(n, c->blk * (uint64_t)c->cfg.rank);
-  c->hi = world > 1 ? std::min<uint64_t>(n, c->lo + c->blk) : n;
-  if (world == 1) c->lo = 0;
-  const uint64_t bmw = std::max<uint64_t>(2 * nw, world * c->blk / 32) + 2;
-  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_bm[i], bmw));  // 2-bit BFS state fits
-  for (int i = 0; i < 3; i++) TRY(dalloc_t(c, &c->d_sbm[i], nw + 2));
   for (int i = 0; i < 2; i++) {
     TRY(dalloc_t(c, &c->d_w[i], c->cap));
     TRY(dalloc_t(c, &c->d_q[i], c->cap));
   }
-  TRY(dalloc_t(c, &c->d_segA, n + 64));  // padded: the slot scans read 4 slots per thread
-  TRY(dalloc_t(c, &c->d_segB, n + 64));
-  TRY(dalloc_t(c, &c->d_umin, n + 1));
-  TRY(dalloc_t(c, &c->d_umax, n + 1));
   TRY(dalloc_t(c, &c->d_lsegs, csr::long_seg_cap(c->cap)));
   TRY(dalloc_t(c, &c->d_nlsegs, 2));
   if (world > 1) {
     TRY(dalloc_t(c, &c->d_send, 2 * m + 1));
     TRY(dalloc_t(c, &c->d_cnt, 2 * world + world * world));
   }
-  CK(cudaMemsetAsync(c->d_umin, 0xFF, sizeof(uint64_t) * (n + 1), c->st));
-  CK(cudaMemsetAsync(c->d_umax, 0, sizeof(uint64_t) * (n + 1), c->st));
   TRY(dalloc_t(c, &c->d_ctr, sv::C_NUM));
   TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM + 512 + 1024 + 8));  // + relabel scratch
   TRY(dalloc_t(c, &c->d_garc, 2048 + 8));
@@ -172,17 +189,23 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   TRY(dalloc_t(c, &c->rws.ghist, radix::MAX_PASSES * radix::RADIX));
   TRY(dalloc_t(c, &c->rws.lookback, c->rws.max_tiles * radix::RADIX));
   TRY(dalloc_t(c, &c->rws.tile_ctr, radix::MAX_PASSES));
-  c->ss.max_tiles = (c->cap + n) / 2048 + 4;
-  TRY(dalloc_t(c, &c->ss.flags, c->ss.max_tiles));
   TRY(dalloc_t(c, &c->ss.ticket, 4));
-  CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * c->ss.max_tiles, c->st));
   CK(cudaMemsetAsync(c->rws.lookback, 0, sizeof(uint64_t) * c->rws.max_tiles * radix::RADIX, c->st));
+  if (!dist64) TRY(alloc_vertex_buffers(c, n));
+  else TRY(ensure_scan_tiles(c));
   if (w == CC_U64) {
     if (m)
       CK(cudaMemcpyAsync(c->d_ids64, pairs, 2 * m * sizeof(uint64_t),
                          on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
-    CK(cudaStreamSynchronize(c->st));
     c->m_total = m;
+    if (dist64) {  // every rank learns the global edge count
+      CK(cudaMemcpyAsync(c->d_gctr + graph::G_REMAIN, &c->m_total, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                         c->st));
+      TRY(comm_allreduce(c, c->d_gctr + graph::G_REMAIN, 1, CC_DT_I64, CC_OP_SUM));
+      CK(cudaMemcpyAsync(&c->m_total, c->d_gctr + graph::G_REMAIN, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                         c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
     c->loaded = true;
     return CC_OK;
   }
@@ -713,7 +736,25 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   const uint64_t m = c->m;
   R.m_edges = c->m_total;
   if (multi_gpu(c)) {
+    double ms_rel = 0;
+    if (c->idw == CC_U64) {  // Alg. 2 line 4 over all ranks (relabel_dist.cu)
+      cudaEvent_t r0 = ev_get(c), r1 = ev_get(c);
+      CK(cudaEventRecord(r0, c->st));
+      TRY(dist_relabel(c));
+      CK(cudaEventRecord(r1, c->st));
+      CK(cudaEventSynchronize(r1));
+      ms_rel = ev_ms(r0, r1);
+    }
+    if (c->n == 0) {  // no ids on any rank (u64 mode): nothing to label
+      R.components = 0;
+      R.ms_relabel = R.ms_total = ms_rel;
+      c->ran = true;
+      if (out) *out = R;
+      return CC_OK;
+    }
     TRY(run_dist(c, mode));
+    R.ms_relabel = ms_rel;
+    R.ms_total += ms_rel;
     R.iters = c->iters.data();
     R.n_iters = (uint32_t)c->iters.size();
     for (size_t i = 0; i < c->it_ev.size() && i < c->iters.size(); i++)
@@ -964,6 +1005,13 @@ extern "C" cc_status cc_labels_u64(cc_ctx* c, uint64_t* ids, uint64_t* labels, u
   if (!c) return CC_ERR_INVALID;
   if (!c->ran) return fail(c, CC_ERR_STATE, "cc_labels before cc_run");
   if (c->idw != CC_U64) return fail(c, CC_ERR_STATE, "u32 graph loaded: use cc_labels_u32");
+  if (multi_gpu(c)) {  // this rank's block of the dense ids; collective
+    const uint64_t cnt = c->hi - c->lo;
+    if (count) *count = cnt;
+    if (!ids || !labels || cap < cnt) return fail(c, CC_ERR_INVALID, "output buffers too small");
+    CK(cudaSetDevice(c->cfg.device));
+    return dist_labels_u64(c, ids, labels, out_on_device);
+  }
   if (count) *count = c->n;
   if (!ids || !labels || cap < c->n) return fail(c, CC_ERR_INVALID, "output buffers too small");
   CK(cudaSetDevice(c->cfg.device));

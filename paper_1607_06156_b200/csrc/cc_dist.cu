@@ -149,22 +149,6 @@ static unsigned gsz(uint64_t work, unsigned cap) {
 
 using namespace cc::dist;
 
-// (re)allocate the tuple buffers when the arcs this rank owns exceed what the load sized
-static cc_status ensure_tuple_cap(cc_ctx* c, uint64_t tuples) {
-  if (tuples + 64 <= c->cap) return CC_OK;
-  const uint64_t cap = (tuples + 64 + 1023) & ~1023ull;
-  for (int i = 0; i < 2; i++) {
-    TRY(dalloc_t(c, &c->d_w[i], cap));
-    TRY(dalloc_t(c, &c->d_q[i], cap));
-  }
-  c->cap = cap;
-  c->ss.max_tiles = (cap + c->n) / 2048 + 4;
-  TRY(dalloc_t(c, &c->ss.flags, c->ss.max_tiles));
-  CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * c->ss.max_tiles, c->st));
-  TRY(dalloc_t(c, &c->d_lsegs, csr::long_seg_cap(cap)));
-  return CC_OK;
-}
-
 cc_status run_dist(cc_ctx* c, cc_mode mode) {
   cc_report& R = c->rep;
   const int world = c->cfg.world_size, rank = c->cfg.rank;

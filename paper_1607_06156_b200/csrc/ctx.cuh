@@ -36,6 +36,17 @@ struct cc_ctx {
   uint64_t* d_mix = nullptr;    // CC_FLAG_PERMUTE_IDS: mixed ids / their sorted copy
   uint32_t* d_pi = nullptr;     // CC_FLAG_PERMUTE_IDS: original rank -> permuted rank
   uint64_t n_alloc = 0;         // id bound the n-sized buffers were sized for
+  // u64 ids, world_size > 1 (relabel_dist.cu): this rank's share of the sorted distinct ids
+  // (dense ids [gbase[rank], gbase[rank + 1])), and every rank's share boundaries
+  uint64_t* d_gids = nullptr;
+  uint64_t gids_cap = 0;
+  std::vector<uint64_t> gbase;
+  uint64_t* d_xid = nullptr;    // exchange scratch: received ids / label requests
+  uint64_t xid_cap = 0;
+  uint32_t* d_xu32 = nullptr;   // exchange scratch: dense ids of the received ids
+  uint64_t xu32_cap = 0;
+  uint64_t* d_out64 = nullptr;  // staging of the u64 label output (ids, labels)
+  uint64_t out64_cap = 0;
   uint32_t* d_label = nullptr;
   uint32_t* d_deg = nullptr;
   uint32_t* d_hist = nullptr;
@@ -147,6 +158,10 @@ static inline void dfree_all(cc_ctx* c) {
   c->allocs.clear();
   c->d_edges = c->d_rem = c->d_rem2 = nullptr;
   c->d_ids64 = c->d_uids = c->d_mix = nullptr;
+  c->d_gids = c->d_xid = c->d_out64 = nullptr;
+  c->d_xu32 = nullptr;
+  c->gids_cap = c->xid_cap = c->xu32_cap = c->out64_cap = 0;
+  c->gbase.clear();
   c->d_pi = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
   c->d_umin = c->d_umax = c->d_nlsegs = nullptr;
@@ -261,6 +276,35 @@ static inline cc_status scan_epoch_guard(cc_ctx* c) {
   return CC_OK;
 }
 
+// scan look-back flags for the tuple capacity and the id range (grown, never shrunk)
+static inline cc_status ensure_scan_tiles(cc_ctx* c) {
+  const uint64_t need = (c->cap + c->n) / 2048 + 4;
+  if (c->ss.flags && c->ss.max_tiles >= need) return CC_OK;
+  c->ss.max_tiles = need;
+  TRY(dalloc_t(c, &c->ss.flags, need));
+  CK(cudaMemsetAsync(c->ss.flags, 0, sizeof(uint64_t) * need, c->st));
+  return CC_OK;
+}
+// (re)allocate the tuple / sort buffers (d_w, d_q: `tuples` entries each) with the scan and
+// radix look-back state that scales with them; contents are not preserved
+static inline cc_status ensure_tuple_cap(cc_ctx* c, uint64_t tuples) {
+  if (tuples + 64 <= c->cap) return CC_OK;
+  const uint64_t cap = (tuples + 64 + 1023) & ~1023ull;
+  for (int i = 0; i < 2; i++) {
+    TRY(dalloc_t(c, &c->d_w[i], cap));
+    TRY(dalloc_t(c, &c->d_q[i], cap));
+  }
+  c->cap = cap;
+  TRY(dalloc_t(c, &c->d_lsegs, csr::long_seg_cap(cap)));
+  const uint64_t rt = cap / radix::TILE_MIN + 2;
+  if (rt > c->rws.max_tiles) {
+    c->rws.max_tiles = rt;
+    TRY(dalloc_t(c, &c->rws.lookback, rt * radix::RADIX));
+    CK(cudaMemsetAsync(c->rws.lookback, 0, sizeof(uint64_t) * rt * radix::RADIX, c->st));
+  }
+  return ensure_scan_tiles(c);
+}
+
 // ------------------------------------------------------------------------------ collectives
 // Thin wrappers over the caller's cc_comm (world_size > 1): synchronise the stream, call,
 // map a nonzero return to CC_ERR_COMM.  No-ops on one GPU.
@@ -353,3 +397,12 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local);
 
 // cc_run for world_size > 1 (cc_dist.cu).
 cc_status run_dist(cc_ctx* c, cc_mode mode);
+
+// n-sized buffers and the owned vertex block for id range n (cc_api.cu).
+cc_status alloc_vertex_buffers(cc_ctx* c, uint64_t n);
+
+// u64 ids with world_size > 1 (relabel_dist.cu): the distributed relabel of Alg. 2 line 4
+// (dense ids in id order over all ranks, edges rewritten as u32, n-sized buffers allocated),
+// and the collective label output of a rank's block as (original id, original label) pairs.
+cc_status dist_relabel(cc_ctx* c);
+cc_status dist_labels_u64(cc_ctx* c, uint64_t* ids, uint64_t* labels, int out_on_device);

@@ -124,6 +124,87 @@ def test_dist_matches_single_gpu_c2_sample():
     _check(run_ranks(_rank_run, 2, g.n, g.edges, ("auto",), 0), g.n, g.edges, ("auto",), trace=False)
 
 
+# ------------------------------------------------------------------ u64 ids over ranks
+def _u64_graph(seed, nv, m):
+    rng = np.random.default_rng(seed)
+    table = np.unique(rng.integers(0, 2**64 - 1, size=nv, dtype=np.uint64, endpoint=True))
+    table = np.concatenate([table, np.array([0, 2**64 - 1], dtype=np.uint64)])
+    idx = rng.integers(0, table.shape[0], size=(m, 2))
+    return table[idx]
+
+
+def _rank_run_u64(rank, world, edges, modes):
+    import torch
+    import paper_1607_06156_b200 as cc
+    torch.cuda.set_device(0)
+    comm = cc.TorchComm(device=torch.device("cuda", 0))
+    ctx = cc.CC(device=0, flags=cc.CC_FLAG_TRACE, comm=comm)
+    m = edges.shape[0]
+    a, b = m * rank // world, m * (rank + 1) // world
+    ctx.load(np.ascontiguousarray(edges[a:b]), 0, ids="u64")
+    out = {}
+    for mode in modes:
+        rep = ctx.run(mode)
+        ids, lab = ctx.labels_u64()
+        out[mode] = (ctx.block_range(), ids.copy(), lab.copy(), rep)
+    ctx.close()
+    return out
+
+
+def _check_u64(res, edges, modes, trace=True):
+    """Distributed relabel (SURVEY §8(e) 'distributed sort-unique + rank map'): the ranks'
+    blocks concatenate to the sorted distinct ids with the u64 union-find labels, and the SV
+    counters equal the transcription on the order-preserving dense relabel."""
+    ids_o, lab_o = oracle.uf_labels_u64(edges)
+    for mode in modes:
+        ids = np.concatenate([r[mode][1] for r in res])
+        lab = np.concatenate([r[mode][2] for r in res])
+        assert np.array_equal(ids, ids_o), mode
+        assert np.array_equal(lab, lab_o), mode
+        lo_hi = [r[mode][0] for r in res]
+        assert lo_hi[0][0] == 0 and lo_hi[-1][1] == ids_o.shape[0]
+        assert all(lo_hi[i][1] == lo_hi[i + 1][0] for i in range(len(lo_hi) - 1))
+        reps = [r[mode][3] for r in res]
+        assert all(rep["components"] == np.unique(lab_o).shape[0] for rep in reps)
+        assert all(rep["m_edges"] == edges.shape[0] for rep in reps)
+        if trace and mode == "sv":
+            dense, uniq = oracle.relabel_u64(edges)
+            _, tr = osv.sv_trace(uniq.shape[0], dense)
+            got = [(it["active_in"], it["partitions"], it["temps"], it["completed"], it["changed"],
+                    it["changed2"]) for it in reps[0]["iters"]]
+            assert got == [(d["A"], d["P"], d["T"], d["completed"], d["changed"], d["changed2"]) for d in tr]
+
+
+@pytest.mark.parametrize("world,seed,nv,m", [(2, 1, 50, 40), (3, 2, 3000, 5000), (2, 3, 200000, 300000),
+                                             (4, 4, 60000, 50000)])
+def test_dist_u64(world, seed, nv, m):
+    e = _u64_graph(seed, nv, m)
+    modes = ("sv", "auto")
+    _check_u64(run_ranks(_rank_run_u64, world, e, modes), e, modes)
+
+
+def test_dist_u64_c5_scaled():
+    """C5 (R-MAT U paths, u64 ids, edges sharded over ranks) at 1/4096 scale on 2 ranks:
+    distributed relabel -> gate (BFS route) -> BFS peel -> SV on the path remainder."""
+    g = graphgen.make("c5", 1 / 4096)
+    res = run_ranks(_rank_run_u64, 2, g.edges, ("auto",))
+    _check_u64(res, g.edges, ("auto",), trace=False)
+    assert all(r["auto"][3]["ran_bfs"] == 1 for r in res)
+
+
+def test_dist_u64_edge_cases():
+    # fewer edges than ranks; the same ids on every rank; extreme ids; skewed shares (one
+    # rank's ids all above the others')
+    e1 = np.array([[2**64 - 1, 0]], np.uint64)
+    _check_u64(run_ranks(_rank_run_u64, 3, e1, ("sv", "auto")), e1, ("sv", "auto"))
+    e2 = np.tile(np.array([[7, 9], [9, 11], [2**63, 7]], np.uint64), (6, 1))
+    _check_u64(run_ranks(_rank_run_u64, 3, e2, ("sv",)), e2, ("sv",))
+    lo = np.arange(0, 4000, dtype=np.uint64).reshape(-1, 2)
+    hi = (np.arange(0, 4000, dtype=np.uint64) + np.uint64(2**40)).reshape(-1, 2)
+    e3 = np.concatenate([lo, hi, [[5, 2**40 + 7]]]).astype(np.uint64)
+    _check_u64(run_ranks(_rank_run_u64, 2, e3, ("sv", "bfs+sv")), e3, ("sv", "bfs+sv"))
+
+
 def _nccl_world1(rank, world):
     """The NCCL forms of the TorchComm collectives (all_gather_into_tensor, uneven
     all_to_all_single, typed all_reduce) on device buffers, on a 1-rank NCCL group."""
