@@ -127,6 +127,10 @@ cc_status alloc_vertex_buffers(cc_ctx* c, uint64_t n) {
   TRY(dalloc_t(c, &c->d_segB, n + 64));
   TRY(dalloc_t(c, &c->d_umin, n + 1));
   TRY(dalloc_t(c, &c->d_umax, n + 1));
+  TRY(dalloc_t(c, &c->d_plist[0], n + 1));
+  TRY(dalloc_t(c, &c->d_plist[1], n + 1));
+  TRY(dalloc_t(c, &c->d_plcnt, 2));
+  TRY(dalloc_t(c, &c->d_nx, nw + 2));
   CK(cudaMemsetAsync(c->d_umin, 0xFF, sizeof(uint64_t) * (n + 1), c->st));
   CK(cudaMemsetAsync(c->d_umax, 0, sizeof(uint64_t) * (n + 1), c->st));
   return ensure_scan_tiles(c);
@@ -381,6 +385,14 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   CK(cudaMemsetAsync(PB, 0xFF, sizeof(uint32_t) * n4, c->st));
   CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nwp, c->st));
   CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nwp, c->st));
+  // slot scans after iteration 0 visit only L_i, a superset of the partition ids P_i built
+  // from the values of PB (lcur: L[lb] holds L_i; lprev: L[lb ^ 1] holds L_i-1)
+  uint32_t* NX = c->d_nx;
+  uint32_t* L[2] = {c->d_plist[0], c->d_plist[1]};
+  uint64_t* LC = c->d_plcnt;
+  int lb = 0;
+  bool lcur = false, lprev = false;
+  CK(cudaMemsetAsync(NX, 0, sizeof(uint32_t) * nwp, c->st));
   uint64_t len_live = len;  // live tuples of this rank (compaction decision)
   // exclusion of completed partitions (fig:loadbal variants)
   const bool excl = !(c->cfg.flags & CC_FLAG_NO_EXCLUDE);
@@ -415,7 +427,11 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       }
     }
     // ---- line 22 bookkeeping: |P_i|, completed, changed, temporaries
-    { Prof k(c, KF_SLOTS); csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all); k.end(8.0 * n4, 1); }
+    { Prof k(c, KF_SLOTS);
+      if (lcur) csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all, L[lb], LC + lb,
+                            lprev ? L[lb ^ 1] : nullptr, lprev ? LC + (lb ^ 1) : nullptr);
+      else csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all);
+      k.end(lcur ? 12.0 * (double)c->iters.back().partitions : 8.0 * n4, 1); }
     // ---- lines 17-21 (exclusion, p <- p_min), line 24 (+ temporaries), line 25 minima
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
@@ -424,22 +440,27 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
     // live tuples: this rank's (compaction) and the global count (convergence)
-    CK(cudaMemcpyAsync(c->d_ctr + sv::C_SURVIVORS, c->d_ctr + sv::C_OUT, sizeof(uint64_t),
-                       cudaMemcpyDeviceToDevice, c->st));
+    if (multi)
+      CK(cudaMemcpyAsync(c->d_ctr + sv::C_SURVIVORS, c->d_ctr + sv::C_OUT, sizeof(uint64_t),
+                         cudaMemcpyDeviceToDevice, c->st));
     if (multi) {
       if (sparse) TRY(comm_sparse_slots(c, PB, nullptr, n4));
       else TRY(comm_min_u32(c, PB, n4));
       TRY(comm_allreduce(c, c->d_ctr + sv::C_OUT, 1, CC_DT_I64, CC_OP_SUM));
     }
     { Prof k(c, KF_SLOTS);
-      csr::temps2(TB, n, PB, c->st);
-      csr::pstat2(PB, n, PA, NCP, TB, c->d_ctr, c->st);
-      k.end(8.0 * n4, 2); }
+      csr::pstat2(PB, n, PA, TB, c->d_ctr, c->st, NX, lcur ? L[lb] : nullptr, lcur ? LC + lb : nullptr);
+      csr::list_from_bits(NX, n, L[lb ^ 1], LC + (lb ^ 1), NCP, TB, c->st);
+      k.end(lcur ? 12.0 * (double)c->iters.back().partitions + n / 4.0 : 8.0 * n4 + n / 4.0, 2); }
+    lprev = lcur;
+    lcur = true;
+    lb ^= 1;
     c->launches += 6 + (have_long ? 4 : 0);
     CKL();
-    TRY(sync_read(c));
+    CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(uint64_t) * sv::C_NUM, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
     const uint64_t A1 = c->h_ctr[sv::C_OUT];
-    len_live = c->h_ctr[sv::C_SURVIVORS];
+    len_live = multi ? c->h_ctr[sv::C_SURVIVORS] : A1;
     cc_iter_stat s{};
     s.active_in = A;
     s.active_min = s.active_max = A;

@@ -58,15 +58,23 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
 // partition statistics after pass A (sets TB, clears PB); slot arrays padded to 4*ceil(n/4)
 // temps_all: a temporary for every partition, completed ones included (their tuples leave at
 // the end of the iteration or never)
+// list / lcnt (device): scan only the slots of the partition-id superset L_i (all slot writes
+// of iteration i land in P_i, a subset of L_i, and L_i+1 is a subset of L_i);
+// PB is then cleared over prev = L_i-1 (NULL: all of it).  list NULL: all n slots
 void pstat1(const uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
-            uint64_t* ctr, cudaStream_t st, bool temps_all = false);
+            uint64_t* ctr, cudaStream_t st, bool temps_all = false, const uint32_t* list = nullptr,
+            const uint64_t* lcnt = nullptr, const uint32_t* prev = nullptr, const uint64_t* pcnt = nullptr);
 // labels of the rows still in the array (no-exclusion variant)
 void final_labels(const uint32_t* R, const uint32_t* P, uint64_t L, uint32_t* label, cudaStream_t st);
-// temporaries' own contribution to PB
-void temps2(const uint32_t* TB, uint64_t n, uint32_t* PB, cudaStream_t st);
-// changed2 after pass B (clears PA, NCP, TB)
-void pstat2(const uint32_t* PB, uint64_t n, uint32_t* PA, uint32_t* NCP, uint32_t* TB, uint64_t* ctr,
-            cudaStream_t st);
+// after pass B: the temporaries' own element (PB[u] = min(PB[u], u) for TB(u)), changed2,
+// PA cleared; marks NX(PB[p]) for every written PB slot: the next iteration's partition ids
+// (list variant: over L_i)
+void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t* ctr, cudaStream_t st,
+            uint32_t* NX, const uint32_t* list = nullptr, const uint64_t* lcnt = nullptr);
+// list[0..*lcnt) = ids of the set bits of NX (bitmap of n bits, cleared on the way); clears
+// the NCP and TB bitmaps for the next iteration
+void list_from_bits(uint32_t* NX, uint64_t n, uint32_t* list, uint64_t* lcnt, uint32_t* NCP, uint32_t* TB,
+                    cudaStream_t st);
 // multi-GPU sparse slot exchange: touched slots as (p, value | NCP(p) << 31) entries (*cnt =
 // their number), and min / OR application of a list (entries with p = ~0 are padding)
 void extract_slots(const uint32_t* S, const uint32_t* BM, uint64_t n, uint2* out, uint64_t* cnt,

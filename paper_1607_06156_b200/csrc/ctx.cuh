@@ -58,6 +58,9 @@ struct cc_ctx {
   uint64_t cap = 0;
   uint32_t* d_segA = nullptr;
   uint32_t* d_segB = nullptr;
+  uint32_t* d_plist[2] = {nullptr, nullptr};  // csr engine: partition-id supersets L_i (slot scans)
+  uint64_t* d_plcnt = nullptr;                // their lengths
+  uint32_t* d_nx = nullptr;                   // bitmap of the next L (values of PB)
   uint64_t* d_umin = nullptr;  // csr engine: tagged partial row minima / maxima
   uint64_t* d_umax = nullptr;
   csr::LongSeg* d_lsegs = nullptr;  // csr engine: segments of rows longer than csr::LONG
@@ -164,6 +167,8 @@ static inline void dfree_all(cc_ctx* c) {
   c->gbase.clear();
   c->d_pi = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
+  c->d_plist[0] = c->d_plist[1] = c->d_nx = nullptr;
+  c->d_plcnt = nullptr;
   c->d_umin = c->d_umax = c->d_nlsegs = nullptr;
   c->d_garc = nullptr;
   c->d_gcur = nullptr;

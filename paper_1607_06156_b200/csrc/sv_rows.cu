@@ -517,6 +517,27 @@ __global__ void __launch_bounds__(RB) k_long2(const uint32_t* __restrict__ P,
 // --------------------------------------------------------------------------- slot scans
 // After pass A: |P_i|, completed, changed, T_i from PA/NCP; one temporary per surviving
 // partition marks TB(p_min) (line 22); PB is cleared for pass B.
+CC_DEVI void pstat1_one(uint32_t pid, uint32_t pm, bool ncp, int temps_all, uint32_t* TB, uint32_t& np,
+                        uint32_t& nc, uint32_t& ch, uint32_t& nt) {
+  np++;
+  ch += pm != pid;
+  const bool comp = pm == pid && !ncp;
+  nc += comp;
+  if (!comp || temps_all) {  // temps_all: completed partitions stay for this iteration
+    nt++;
+    const uint32_t b = 1u << (pm & 31);
+    if (!(*(volatile uint32_t*)&TB[pm >> 5] & b)) atomicOr(&TB[pm >> 5], b);
+  }
+}
+CC_DEVI void pstat1_flush(uint32_t np, uint32_t nc, uint32_t ch, uint32_t nt, unsigned long long* ctr) {
+  np = warp_sum(np); nc = warp_sum(nc); ch = warp_sum(ch); nt = warp_sum(nt);
+  if ((threadIdx.x & 31) == 0) {
+    if (np) atomicAdd(&ctr[sv::C_PARTITIONS], (unsigned long long)np);
+    if (nc) atomicAdd(&ctr[sv::C_COMPLETED], (unsigned long long)nc);
+    if (ch) atomicAdd(&ctr[sv::C_CHANGED], (unsigned long long)ch);
+    if (nt) atomicAdd(&ctr[sv::C_TEMPS], (unsigned long long)nt);
+  }
+}
 __global__ void __launch_bounds__(RB) k_pstat1(const uint32_t* __restrict__ PA,
                                                const uint32_t* __restrict__ NCP, uint64_t n4,
                                                uint32_t* TB, uint32_t* __restrict__ PB,
@@ -529,63 +550,135 @@ __global__ void __launch_bounds__(RB) k_pstat1(const uint32_t* __restrict__ PA,
     const uint32_t w = __ldg(&NCP[t >> 3]) >> (4 * (t & 7));
     const uint32_t v[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const uint32_t pm = v[j];
-      if (pm == INF) continue;
-      const uint32_t pid = (uint32_t)(4 * t + j);
-      np++;
-      ch += pm != pid;
-      const bool comp = pm == pid && !((w >> j) & 1u);
-      nc += comp;
-      if (!comp || temps_all) {  // temps_all: completed partitions stay for this iteration
-        nt++;
-        const uint32_t b = 1u << (pm & 31);
-        if (!(*(volatile uint32_t*)&TB[pm >> 5] & b)) atomicOr(&TB[pm >> 5], b);
-      }
-    }
+    for (int j = 0; j < 4; j++)
+      if (v[j] != INF) pstat1_one((uint32_t)(4 * t + j), v[j], (w >> j) & 1u, temps_all, TB, np, nc, ch, nt);
   }
-  np = warp_sum(np); nc = warp_sum(nc); ch = warp_sum(ch); nt = warp_sum(nt);
-  if ((threadIdx.x & 31) == 0) {
-    if (np) atomicAdd(&ctr[sv::C_PARTITIONS], (unsigned long long)np);
-    if (nc) atomicAdd(&ctr[sv::C_COMPLETED], (unsigned long long)nc);
-    if (ch) atomicAdd(&ctr[sv::C_CHANGED], (unsigned long long)ch);
-    if (nt) atomicAdd(&ctr[sv::C_TEMPS], (unsigned long long)nt);
+  pstat1_flush(np, nc, ch, nt, ctr);
+}
+// list form: statistics over L_i; PB is cleared over L_i-1 (its written keys lie in P_i-1)
+__global__ void __launch_bounds__(RB) k_pstat1_list(const uint32_t* __restrict__ PA,
+                                                    const uint32_t* __restrict__ NCP,
+                                                    const uint32_t* __restrict__ list,
+                                                    const unsigned long long* lcnt,
+                                                    const uint32_t* __restrict__ prev,
+                                                    const unsigned long long* pcnt, uint32_t* TB,
+                                                    uint32_t* __restrict__ PB, unsigned long long* ctr,
+                                                    int temps_all) {
+  uint32_t np = 0, nc = 0, ch = 0, nt = 0;
+  const uint64_t cp = *pcnt;
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cp; i += (uint64_t)gridDim.x * RB)
+    PB[prev[i]] = INF;
+  const uint64_t cnt = *lcnt;
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * RB) {
+    const uint32_t pid = list[i];
+    const uint32_t pm = PA[pid];
+    if (pm != INF) pstat1_one(pid, pm, tbit(NCP, pid), temps_all, TB, np, nc, ch, nt);
   }
+  pstat1_flush(np, nc, ch, nt, ctr);
 }
 
-// Temporaries <u,_,u>_tmp in PB(u) (pass 4): q = u_min'(u) <= u; the row part of u_min' was
-// pushed by pass B, the temporary's own element here.
-__global__ void __launch_bounds__(RB) k_temps2(const uint32_t* __restrict__ TB, uint64_t nw,
-                                               uint32_t* PB) {
-  for (uint64_t w = blockIdx.x * (uint64_t)RB + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * RB) {
-    uint32_t bits = TB[w];
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      const uint32_t u = (uint32_t)(w * 32 + b);
-      if (u < *(volatile uint32_t*)&PB[u]) atomicMin(&PB[u], u);
-    }
-  }
+// After pass B: the temporaries' own element (line 24: <u,_,u>_tmp is in PB(u) with
+// q = u_min'(u) <= u; the row part of u_min' was pushed by pass B) -- PB[u] = min(PB[u], u)
+// for TB(u) -- then changed2 from PB and PA cleared for the next iteration.  Every written PB
+// slot marks NX(PB[p]): the partition ids of the next iteration are values of PB (p <- PB[p]
+// in its pass A), so they form a subset of the marked ids.  NCP and TB are cleared by
+// k_list_from_bits, which runs after this kernel (TB is read here).
+CC_DEVI void mark(uint32_t* NX, uint32_t v) {
+  const uint32_t b = 1u << (v & 31);
+  if (!(*(volatile uint32_t*)&NX[v >> 5] & b)) atomicOr(&NX[v >> 5], b);
 }
-
-// After pass B: changed2 from PB; PA, NCP and TB are cleared for the next iteration.
-__global__ void __launch_bounds__(RB) k_pstat2(const uint32_t* __restrict__ PB, uint64_t n4,
-                                               uint32_t* __restrict__ PA, uint32_t* __restrict__ NCP,
-                                               uint32_t* __restrict__ TB, unsigned long long* ctr) {
+__global__ void __launch_bounds__(RB) k_pstat2(uint32_t* __restrict__ PB, uint64_t n4,
+                                               uint32_t* __restrict__ PA, const uint32_t* __restrict__ TB,
+                                               unsigned long long* ctr, uint32_t* NX) {
   uint32_t ch = 0;
   for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
-    const uint4 b = reinterpret_cast<const uint4*>(PB)[t];
+    uint4 b = reinterpret_cast<const uint4*>(PB)[t];
     reinterpret_cast<uint4*>(PA)[t] = make_uint4(INF, INF, INF, INF);
-    if ((t & 7) == 0) {
-      NCP[t >> 3] = 0u;
-      TB[t >> 3] = 0u;
+    const uint32_t tw = (TB[t >> 3] >> (4 * (t & 7))) & 15u;
+    if (tw) {
+      const uint32_t u0 = (uint32_t)(4 * t);
+      if (tw & 1u) b.x = min(b.x, u0);
+      if (tw & 2u) b.y = min(b.y, u0 + 1);
+      if (tw & 4u) b.z = min(b.z, u0 + 2);
+      if (tw & 8u) b.w = min(b.w, u0 + 3);
+      reinterpret_cast<uint4*>(PB)[t] = b;
     }
     const uint32_t v[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int j = 0; j < 4; j++) ch += v[j] != INF && v[j] != (uint32_t)(4 * t + j);
+    for (int j = 0; j < 4; j++)
+      if (v[j] != INF) {
+        ch += v[j] != (uint32_t)(4 * t + j);
+        mark(NX, v[j]);
+      }
   }
   ch = warp_sum(ch);
   if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
+}
+__global__ void __launch_bounds__(RB) k_pstat2_list(uint32_t* __restrict__ PB,
+                                                    const uint32_t* __restrict__ list,
+                                                    const unsigned long long* lcnt,
+                                                    uint32_t* __restrict__ PA, const uint32_t* __restrict__ TB,
+                                                    unsigned long long* ctr, uint32_t* NX) {
+  uint32_t ch = 0;
+  const uint64_t cnt = *lcnt;
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * RB) {
+    const uint32_t pid = list[i];
+    uint32_t b = PB[pid];
+    PA[pid] = INF;
+    if (((TB[pid >> 5] >> (pid & 31)) & 1u) && pid < b) PB[pid] = b = pid;
+    if (b != INF) {
+      ch += b != pid;
+      mark(NX, b);
+    }
+  }
+  ch = warp_sum(ch);
+  if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
+}
+
+// list of the set bits of NX (cleared): one block-wide scan per 256-word chunk, one atomic
+// per chunk with set bits
+__global__ void __launch_bounds__(RB) k_list_from_bits(uint32_t* NX, uint64_t nw, uint32_t* __restrict__ list,
+                                                       unsigned long long* lcnt, uint32_t* __restrict__ NCP,
+                                                       uint32_t* __restrict__ TB) {
+  __shared__ uint32_t s_w[RB / 32];
+  __shared__ unsigned long long s_base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint64_t w0 = blockIdx.x * (uint64_t)RB; w0 < nw; w0 += (uint64_t)gridDim.x * RB) {
+    const uint64_t w = w0 + threadIdx.x;
+    uint32_t bits = 0u;
+    if (w < nw) {
+      bits = NX[w];
+      if (bits) NX[w] = 0u;
+      NCP[w] = 0u;
+      TB[w] = 0u;
+    }
+    const uint32_t c = __popc(bits);
+    uint32_t x = c;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t acc = 0;
+      for (int i = 0; i < RB / 32; i++) {
+        const uint32_t t = s_w[i];
+        s_w[i] = acc;
+        acc += t;
+      }
+      s_base = acc ? atomicAdd(lcnt, (unsigned long long)acc) : 0ull;
+    }
+    __syncthreads();
+    uint64_t pos = s_base + s_w[wid] + x - c;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      list[pos++] = (uint32_t)(w * 32 + b);
+    }
+    __syncthreads();
+  }
 }
 
 // Without exclusion (fig:loadbal 'Naive') every row is still in the array at convergence:
@@ -720,25 +813,41 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
 }
 
 void pstat1(const uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
-            uint64_t* ctr, cudaStream_t st, bool temps_all) {
+            uint64_t* ctr, cudaStream_t st, bool temps_all, const uint32_t* list, const uint64_t* lcnt,
+            const uint32_t* prev, const uint64_t* pcnt) {
+  auto* c = reinterpret_cast<unsigned long long*>(ctr);
+  if (list) {
+    if (!prev) cudaMemsetAsync(PB, 0xFF, sizeof(uint32_t) * ((n + 3) / 4 * 4), st);
+    k_pstat1_list<<<148 * 8, RB, 0, st>>>(PA, NCP, list, reinterpret_cast<const unsigned long long*>(lcnt),
+                                          prev ? prev : list,
+                                          reinterpret_cast<const unsigned long long*>(prev ? pcnt : lcnt), TB,
+                                          PB, c, temps_all ? 1 : 0);
+    return;
+  }
   const uint64_t n4 = (n + 3) / 4;
   if (!n4) return;
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
-  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, reinterpret_cast<unsigned long long*>(ctr),
-                             temps_all ? 1 : 0);
+  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, c, temps_all ? 1 : 0);
 }
-void temps2(const uint32_t* TB, uint64_t n, uint32_t* PB, cudaStream_t st) {
-  const uint64_t nw = (n + 31) / 32;
-  if (!nw) return;
-  const unsigned g = (unsigned)std::min<uint64_t>((nw + RB - 1) / RB, 148 * 4);
-  k_temps2<<<g, RB, 0, st>>>(TB, nw, PB);
-}
-void pstat2(const uint32_t* PB, uint64_t n, uint32_t* PA, uint32_t* NCP, uint32_t* TB, uint64_t* ctr,
-            cudaStream_t st) {
+void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t* ctr, cudaStream_t st,
+            uint32_t* NX, const uint32_t* list, const uint64_t* lcnt) {
+  auto* c = reinterpret_cast<unsigned long long*>(ctr);
+  if (list) {
+    k_pstat2_list<<<148 * 8, RB, 0, st>>>(PB, list, reinterpret_cast<const unsigned long long*>(lcnt), PA, TB,
+                                          c, NX);
+    return;
+  }
   const uint64_t n4 = (n + 3) / 4;
   if (!n4) return;
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
-  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, NCP, TB, reinterpret_cast<unsigned long long*>(ctr));
+  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, TB, c, NX);
+}
+void list_from_bits(uint32_t* NX, uint64_t n, uint32_t* list, uint64_t* lcnt, uint32_t* NCP, uint32_t* TB,
+                    cudaStream_t st) {
+  cudaMemsetAsync(lcnt, 0, sizeof(uint64_t), st);
+  const uint64_t nw = (n + 31) / 32 + 2;  // the bitmaps' padding words too
+  const unsigned g = (unsigned)std::min<uint64_t>((nw + RB - 1) / RB, 148 * 8);
+  k_list_from_bits<<<g, RB, 0, st>>>(NX, nw, list, reinterpret_cast<unsigned long long*>(lcnt), NCP, TB);
 }
 
 }  // namespace csr
