@@ -428,9 +428,9 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     }
     // ---- line 22 bookkeeping: |P_i|, completed, changed, temporaries
     { Prof k(c, KF_SLOTS);
-      if (lcur) csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all, L[lb], LC + lb,
+      if (lcur) csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all, excl, L[lb], LC + lb,
                             lprev ? L[lb ^ 1] : nullptr, lprev ? LC + (lb ^ 1) : nullptr);
-      else csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all);
+      else csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all, excl);
       k.end(lcur ? 12.0 * (double)c->iters.back().partitions : 8.0 * n4, 1); }
     // ---- lines 17-21 (exclusion, p <- p_min), line 24 (+ temporaries), line 25 minima
     { Prof k(c, KF_ROWB);

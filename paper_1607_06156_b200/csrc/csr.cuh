@@ -61,8 +61,9 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
 // list / lcnt (device): scan only the slots of the partition-id superset L_i (all slot writes
 // of iteration i land in P_i, a subset of L_i, and L_i+1 is a subset of L_i);
 // PB is then cleared over prev = L_i-1 (NULL: all of it).  list NULL: all n slots
-void pstat1(const uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
-            uint64_t* ctr, cudaStream_t st, bool temps_all = false, const uint32_t* list = nullptr,
+// flag: completed partitions get bit 31 set in PA (pass B reads it in its relabel gather)
+void pstat1(uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
+            uint64_t* ctr, cudaStream_t st, bool temps_all, bool flag, const uint32_t* list = nullptr,
             const uint64_t* lcnt = nullptr, const uint32_t* prev = nullptr, const uint64_t* pcnt = nullptr);
 // labels of the rows still in the array (no-exclusion variant)
 void final_labels(const uint32_t* R, const uint32_t* P, uint64_t L, uint32_t* label, cudaStream_t st);

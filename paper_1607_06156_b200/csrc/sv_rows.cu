@@ -53,6 +53,9 @@ constexpr int RCACHE = 512;
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr uint32_t DEAD = 0xFFFFFFFFu;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
+// completed partition p (PA[p] = p and not NCP(p)): k_pstat1 sets this flag on PA[p] so that
+// pass B decides the exclusion from its one relabel gather (ids are < 2^30)
+constexpr uint32_t CBIT = 0x80000000u;
 
 CC_DEVI bool tbit(const uint32_t* bm, uint32_t i) { return (__ldg(&bm[i >> 5]) >> (i & 31)) & 1u; }
 
@@ -64,12 +67,14 @@ CC_DEVI void push_min(uint32_t* OUT, unsigned long long* s_pc, uint32_t p, uint3
   atomicMin(&OUT[p], q);  // result unused: compiles to a fire-and-forget reduction
   s_pc[h] = ((unsigned long long)p << 32) | q;
 }
-CC_DEVI void push_bit(uint32_t* BM, uint32_t* s_nc, uint32_t p) {
+// precheck (hot iterations, where many rows share one minimum): read the word first so a
+// set bit costs no atomic; otherwise a fire-and-forget atomic (no dependent load)
+CC_DEVI void push_bit(uint32_t* BM, uint32_t* s_nc, uint32_t p, bool precheck) {
   const uint32_t h = (p ^ (p >> 9)) & (RCACHE - 1);
   if (*(volatile uint32_t*)&s_nc[h] == p) return;
   s_nc[h] = p;
   const uint32_t b = 1u << (p & 31);
-  if (!(*(volatile uint32_t*)&BM[p >> 5] & b)) atomicOr(&BM[p >> 5], b);
+  if (!precheck || !(*(volatile uint32_t*)&BM[p >> 5] & b)) atomicOr(&BM[p >> 5], b);
 }
 CC_DEVI void set_bit(uint32_t* BM, uint32_t p) {
   const uint32_t b = 1u << (p & 31);
@@ -140,8 +145,8 @@ CC_DEVI uint32_t relabel(uint32_t pv, const uint32_t* __restrict__ MAP, const ui
   if (pv == DEAD) return DEAD;
   if (A) return MAP ? __ldg(&MAP[pv]) : pv;
   const uint32_t pm = __ldg(&MAP[pv]);
-  if (excl && pm == pv && !tbit(NCPr, pv)) return DEAD;
-  return pm;
+  if (excl && (pm & CBIT)) return DEAD;
+  return pm & ~CBIT;
 }
 
 }  // namespace
@@ -237,8 +242,12 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
         const bool fresh = p[j] != DEAD && (!A || MAP) && (j == 0 || p[j] != p[j - 1]);
-        m[j] = fresh ? __ldg(&MAP[p[j]]) : p[j];
-        if (!A && fresh && m[j] == p[j] && !tbit(NCPr, p[j])) cpl |= 1u << j;
+        uint32_t g = fresh ? __ldg(&MAP[p[j]]) : p[j];
+        if (!A && fresh) {
+          cpl |= (g >> 31) << j;  // CBIT: completed partition
+          g &= ~CBIT;
+        }
+        m[j] = g;
       }
 #pragma unroll
       for (int j = 1; j < RITEMS; j++)
@@ -397,7 +406,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
           // many non-PC rows share one minimum late in the run: filter through a block cache
           // and a read of the word before the atomic
           if (q != x && q != last_nc) {
-            push_bit(NCPw, s_nc, q);
+            push_bit(NCPw, s_nc, q, hot);
             last_nc = q;
           }
         } else if (tbit(TB, k[j])) {
@@ -517,7 +526,7 @@ __global__ void __launch_bounds__(RB) k_long2(const uint32_t* __restrict__ P,
 // --------------------------------------------------------------------------- slot scans
 // After pass A: |P_i|, completed, changed, T_i from PA/NCP; one temporary per surviving
 // partition marks TB(p_min) (line 22); PB is cleared for pass B.
-CC_DEVI void pstat1_one(uint32_t pid, uint32_t pm, bool ncp, int temps_all, uint32_t* TB, uint32_t& np,
+CC_DEVI bool pstat1_one(uint32_t pid, uint32_t pm, bool ncp, int temps_all, uint32_t* TB, uint32_t& np,
                         uint32_t& nc, uint32_t& ch, uint32_t& nt) {
   np++;
   ch += pm != pid;
@@ -528,6 +537,7 @@ CC_DEVI void pstat1_one(uint32_t pid, uint32_t pm, bool ncp, int temps_all, uint
     const uint32_t b = 1u << (pm & 31);
     if (!(*(volatile uint32_t*)&TB[pm >> 5] & b)) atomicOr(&TB[pm >> 5], b);
   }
+  return comp;
 }
 CC_DEVI void pstat1_flush(uint32_t np, uint32_t nc, uint32_t ch, uint32_t nt, unsigned long long* ctr) {
   np = warp_sum(np); nc = warp_sum(nc); ch = warp_sum(ch); nt = warp_sum(nt);
@@ -538,32 +548,38 @@ CC_DEVI void pstat1_flush(uint32_t np, uint32_t nc, uint32_t ch, uint32_t nt, un
     if (nt) atomicAdd(&ctr[sv::C_TEMPS], (unsigned long long)nt);
   }
 }
-__global__ void __launch_bounds__(RB) k_pstat1(const uint32_t* __restrict__ PA,
+// flag: mark completed partitions with CBIT in PA (pass B excludes them)
+__global__ void __launch_bounds__(RB) k_pstat1(uint32_t* __restrict__ PA,
                                                const uint32_t* __restrict__ NCP, uint64_t n4,
                                                uint32_t* TB, uint32_t* __restrict__ PB,
-                                               unsigned long long* ctr, int temps_all) {
+                                               unsigned long long* ctr, int temps_all, int flag) {
   uint32_t np = 0, nc = 0, ch = 0, nt = 0;
   for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
     const uint4 a = reinterpret_cast<const uint4*>(PA)[t];
     reinterpret_cast<uint4*>(PB)[t] = make_uint4(INF, INF, INF, INF);
     if ((a.x & a.y & a.z & a.w) == INF) continue;
     const uint32_t w = __ldg(&NCP[t >> 3]) >> (4 * (t & 7));
-    const uint32_t v[4] = {a.x, a.y, a.z, a.w};
+    uint32_t v[4] = {a.x, a.y, a.z, a.w};
+    uint32_t cm = 0;
 #pragma unroll
     for (int j = 0; j < 4; j++)
-      if (v[j] != INF) pstat1_one((uint32_t)(4 * t + j), v[j], (w >> j) & 1u, temps_all, TB, np, nc, ch, nt);
+      if (v[j] != INF && pstat1_one((uint32_t)(4 * t + j), v[j], (w >> j) & 1u, temps_all, TB, np, nc, ch, nt)) {
+        v[j] |= CBIT;
+        cm = 1;
+      }
+    if (cm && flag) reinterpret_cast<uint4*>(PA)[t] = make_uint4(v[0], v[1], v[2], v[3]);
   }
   pstat1_flush(np, nc, ch, nt, ctr);
 }
 // list form: statistics over L_i; PB is cleared over L_i-1 (its written keys lie in P_i-1)
-__global__ void __launch_bounds__(RB) k_pstat1_list(const uint32_t* __restrict__ PA,
+__global__ void __launch_bounds__(RB) k_pstat1_list(uint32_t* __restrict__ PA,
                                                     const uint32_t* __restrict__ NCP,
                                                     const uint32_t* __restrict__ list,
                                                     const unsigned long long* lcnt,
                                                     const uint32_t* __restrict__ prev,
                                                     const unsigned long long* pcnt, uint32_t* TB,
                                                     uint32_t* __restrict__ PB, unsigned long long* ctr,
-                                                    int temps_all) {
+                                                    int temps_all, int flag) {
   uint32_t np = 0, nc = 0, ch = 0, nt = 0;
   const uint64_t cp = *pcnt;
   for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cp; i += (uint64_t)gridDim.x * RB)
@@ -572,7 +588,8 @@ __global__ void __launch_bounds__(RB) k_pstat1_list(const uint32_t* __restrict__
   for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * RB) {
     const uint32_t pid = list[i];
     const uint32_t pm = PA[pid];
-    if (pm != INF) pstat1_one(pid, pm, tbit(NCP, pid), temps_all, TB, np, nc, ch, nt);
+    if (pm != INF && pstat1_one(pid, pm, tbit(NCP, pid), temps_all, TB, np, nc, ch, nt) && flag)
+      PA[pid] = pm | CBIT;
   }
   pstat1_flush(np, nc, ch, nt, ctr);
 }
@@ -812,22 +829,22 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
   }
 }
 
-void pstat1(const uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
-            uint64_t* ctr, cudaStream_t st, bool temps_all, const uint32_t* list, const uint64_t* lcnt,
-            const uint32_t* prev, const uint64_t* pcnt) {
+void pstat1(uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_t* PB,
+            uint64_t* ctr, cudaStream_t st, bool temps_all, bool flag, const uint32_t* list,
+            const uint64_t* lcnt, const uint32_t* prev, const uint64_t* pcnt) {
   auto* c = reinterpret_cast<unsigned long long*>(ctr);
   if (list) {
     if (!prev) cudaMemsetAsync(PB, 0xFF, sizeof(uint32_t) * ((n + 3) / 4 * 4), st);
     k_pstat1_list<<<148 * 8, RB, 0, st>>>(PA, NCP, list, reinterpret_cast<const unsigned long long*>(lcnt),
                                           prev ? prev : list,
                                           reinterpret_cast<const unsigned long long*>(prev ? pcnt : lcnt), TB,
-                                          PB, c, temps_all ? 1 : 0);
+                                          PB, c, temps_all ? 1 : 0, flag ? 1 : 0);
     return;
   }
   const uint64_t n4 = (n + 3) / 4;
   if (!n4) return;
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
-  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, c, temps_all ? 1 : 0);
+  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, c, temps_all ? 1 : 0, flag ? 1 : 0);
 }
 void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t* ctr, cudaStream_t st,
             uint32_t* NX, const uint32_t* list, const uint64_t* lcnt) {

@@ -1,13 +1,14 @@
 """Per CUDA source line: instructions executed and stall samples, from an ncu report.
-usage: python profiles/srclines.py <report.ncu-rep> <kernel-regex> [top]"""
+usage: python profiles/srclines.py <report.ncu-rep> <kernel-regex> [top] [launch-skip]"""
 import csv
 import subprocess
 import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"
 out = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                               "-k", "regex:" + kern, "--launch-count", "1"], text=True,
+                               "-k", "regex:" + kern, "--launch-skip", skip, "--launch-count", "1"], text=True,
                               stderr=subprocess.DEVNULL)
 rows = list(csv.reader(out.splitlines()))
 agg, fname, hdr = [], None, None
