@@ -391,7 +391,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   uint32_t* L[2] = {c->d_plist[0], c->d_plist[1]};
   uint64_t* LC = c->d_plcnt;
   int lb = 0;
-  bool lcur = false, lprev = false;
+  bool lcur = false, lprev = false, lexact = false;
   CK(cudaMemsetAsync(NX, 0, sizeof(uint32_t) * nwp, c->st));
   uint64_t len_live = len;  // live tuples of this rank (compaction decision)
   // exclusion of completed partitions (fig:loadbal variants)
@@ -411,7 +411,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     { Prof k(c, KF_ROWA);
       csr::rowpass(true, Rc, Pc, it ? Palt : nullptr, len, it ? PB : nullptr, nullptr, nullptr, PA,
                    NCP, c->d_label, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs,
-                   have_long, hot, c->d_ctr, c->st);
+                   have_long, hot, c->d_ctr, c->st, true, /*preset=*/lexact);
       k.end(8.0 * len + (it ? 4.0 * len : 0.0), 1 + (have_long ? 2 : 0)); }
     if (it) std::swap(Pc, Palt);
     // sparse exchange once few partitions remain: the entries all ranks touched (at most
@@ -449,9 +449,10 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       TRY(comm_allreduce(c, c->d_ctr + sv::C_OUT, 1, CC_DT_I64, CC_OP_SUM));
     }
     { Prof k(c, KF_SLOTS);
-      csr::pstat2(PB, n, PA, TB, c->d_ctr, c->st, NX, lcur ? L[lb] : nullptr, lcur ? LC + lb : nullptr);
-      csr::list_from_bits(NX, n, L[lb ^ 1], LC + (lb ^ 1), NCP, TB, c->st);
+      csr::pstat2(PB, n, PA, TB, c->d_ctr, c->st, NX, excl, lcur ? L[lb] : nullptr, lcur ? LC + lb : nullptr);
+      csr::list_from_bits(NX, n, L[lb ^ 1], LC + (lb ^ 1), NCP, TB, lcur ? PA : nullptr, c->st);
       k.end(lcur ? 12.0 * (double)c->iters.back().partitions + n / 4.0 : 8.0 * n4 + n / 4.0, 2); }
+    lexact = lcur;  // the list form of pstat2 marks P_i+1 exactly
     lprev = lcur;
     lcur = true;
     lb ^= 1;

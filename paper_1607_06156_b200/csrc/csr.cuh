@@ -54,7 +54,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
-             cudaStream_t st, bool excl = true);
+             cudaStream_t st, bool excl = true, bool preset = false);
 // partition statistics after pass A (sets TB, clears PB); slot arrays padded to 4*ceil(n/4)
 // temps_all: a temporary for every partition, completed ones included (their tuples leave at
 // the end of the iteration or never)
@@ -68,14 +68,15 @@ void pstat1(uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_
 // labels of the rows still in the array (no-exclusion variant)
 void final_labels(const uint32_t* R, const uint32_t* P, uint64_t L, uint32_t* label, cudaStream_t st);
 // after pass B: the temporaries' own element (PB[u] = min(PB[u], u) for TB(u)), changed2,
-// PA cleared; marks NX(PB[p]) for every written PB slot: the next iteration's partition ids
-// (list variant: over L_i)
+// PA cleared; marks in NX the next iteration's partition ids: list variant (over L_i) exactly,
+// { PB[PA[p]] : p not excluded }; all-slot variant a superset (every value of PB)
 void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t* ctr, cudaStream_t st,
-            uint32_t* NX, const uint32_t* list = nullptr, const uint64_t* lcnt = nullptr);
-// list[0..*lcnt) = ids of the set bits of NX (bitmap of n bits, cleared on the way); clears
-// the NCP and TB bitmaps for the next iteration
+            uint32_t* NX, bool excl, const uint32_t* list = nullptr, const uint64_t* lcnt = nullptr);
+// list[0..*lcnt) = ids of the set bits of NX (bitmap of n bits, cleared on the way); with PA
+// (exact list) each id gets PA[id] = id preset (pass A then skips updates q = p); clears the
+// NCP and TB bitmaps for the next iteration
 void list_from_bits(uint32_t* NX, uint64_t n, uint32_t* list, uint64_t* lcnt, uint32_t* NCP, uint32_t* TB,
-                    cudaStream_t st);
+                    uint32_t* PA, cudaStream_t st);
 // multi-GPU sparse slot exchange: touched slots as (p, value | NCP(p) << 31) entries (*cnt =
 // their number), and min / OR application of a list (entries with p = ~0 are padding)
 void extract_slots(const uint32_t* S, const uint32_t* BM, uint64_t n, uint2* out, uint64_t* cnt,

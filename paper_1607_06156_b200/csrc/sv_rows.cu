@@ -387,7 +387,9 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       if (k[j] == k[RITEMS - 1] && cout_k == k[RITEMS - 1]) { q = min(q, cout_m); if (A) x = max(x, cout_x); }
       if (k[j] == INF || k[j] == kfirst) continue;
       if (j == RITEMS - 1) qlast = q;
-      if (!hot) {
+      if ((hot & 2) && q == p[j]) {
+        // PA[p] was preset to p (p is a partition of this iteration): min(PA[p], p) = PA[p]
+      } else if (!(hot & 1)) {
         atomicMin(&OUT[p[j]], q);
       } else if (p[j] != last_p || q < last_q) {  // this thread's last update covers it
         const uint32_t h = (p[j] ^ (p[j] >> 10)) & (RAGG - 1);
@@ -428,7 +430,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     }
     __syncthreads();
   }
-  if (hot) {  // flush the block's aggregated slot updates
+  if (hot & 1) {  // flush the block's aggregated slot updates
     __syncthreads();
     for (int i = threadIdx.x; i < RAGG; i += PB)
       if (s_akey[i] != INF) atomicMin(&OUT[s_akey[i]], s_aval[i]);
@@ -596,20 +598,31 @@ __global__ void __launch_bounds__(RB) k_pstat1_list(uint32_t* __restrict__ PA,
 
 // After pass B: the temporaries' own element (line 24: <u,_,u>_tmp is in PB(u) with
 // q = u_min'(u) <= u; the row part of u_min' was pushed by pass B) -- PB[u] = min(PB[u], u)
-// for TB(u) -- then changed2 from PB and PA cleared for the next iteration.  Every written PB
-// slot marks NX(PB[p]): the partition ids of the next iteration are values of PB (p <- PB[p]
-// in its pass A), so they form a subset of the marked ids.  NCP and TB are cleared by
-// k_list_from_bits, which runs after this kernel (TB is read here).
+// for TB(u) -- then changed2 from PB and PA cleared for the next iteration.
+// The next iteration's partition ids, exactly: after pass B every live tuple of partition p
+// holds v = PA[p] (p not excluded), and the next pass A maps it to PB[v], so
+// P_i+1 = { PB[PA[p]] : p in P_i, p not excluded }; they are marked in NX.  NCP and TB are
+// cleared by k_list_from_bits, which runs after this kernel (TB is read here).
 CC_DEVI void mark(uint32_t* NX, uint32_t v) {
   const uint32_t b = 1u << (v & 31);
   if (!(*(volatile uint32_t*)&NX[v >> 5] & b)) atomicOr(&NX[v >> 5], b);
 }
+// PB[v] after the temporaries' fold (another thread may be folding slot v concurrently)
+CC_DEVI uint32_t pb_final(const uint32_t* PB, const uint32_t* TB, uint32_t v) {
+  const uint32_t b = PB[v];
+  return ((TB[v >> 5] >> (v & 31)) & 1u) ? min(b, v) : b;
+}
+CC_DEVI void mark_next(uint32_t* NX, const uint32_t* PB, const uint32_t* TB, uint32_t pa, int excl) {
+  if (pa == INF || (excl && (pa & CBIT))) return;
+  mark(NX, pb_final(PB, TB, pa & ~CBIT));
+}
 __global__ void __launch_bounds__(RB) k_pstat2(uint32_t* __restrict__ PB, uint64_t n4,
                                                uint32_t* __restrict__ PA, const uint32_t* __restrict__ TB,
-                                               unsigned long long* ctr, uint32_t* NX) {
+                                               unsigned long long* ctr, uint32_t* NX, int excl) {
   uint32_t ch = 0;
   for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
     uint4 b = reinterpret_cast<const uint4*>(PB)[t];
+    const uint4 a = reinterpret_cast<const uint4*>(PA)[t];
     reinterpret_cast<uint4*>(PA)[t] = make_uint4(INF, INF, INF, INF);
     const uint32_t tw = (TB[t >> 3] >> (4 * (t & 7))) & 15u;
     if (tw) {
@@ -621,12 +634,16 @@ __global__ void __launch_bounds__(RB) k_pstat2(uint32_t* __restrict__ PB, uint64
       reinterpret_cast<uint4*>(PB)[t] = b;
     }
     const uint32_t v[4] = {b.x, b.y, b.z, b.w};
+    // all-slot form (iteration 0, |P_i| ~ n): a superset of P_i+1, the values of PB, which
+    // needs no gather (the exact form costs one random PB read per partition)
 #pragma unroll
     for (int j = 0; j < 4; j++)
       if (v[j] != INF) {
         ch += v[j] != (uint32_t)(4 * t + j);
         mark(NX, v[j]);
       }
+    (void)a;
+    (void)excl;
   }
   ch = warp_sum(ch);
   if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
@@ -635,18 +652,17 @@ __global__ void __launch_bounds__(RB) k_pstat2_list(uint32_t* __restrict__ PB,
                                                     const uint32_t* __restrict__ list,
                                                     const unsigned long long* lcnt,
                                                     uint32_t* __restrict__ PA, const uint32_t* __restrict__ TB,
-                                                    unsigned long long* ctr, uint32_t* NX) {
+                                                    unsigned long long* ctr, uint32_t* NX, int excl) {
   uint32_t ch = 0;
   const uint64_t cnt = *lcnt;
   for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * RB) {
     const uint32_t pid = list[i];
     uint32_t b = PB[pid];
+    const uint32_t a = PA[pid];
     PA[pid] = INF;
     if (((TB[pid >> 5] >> (pid & 31)) & 1u) && pid < b) PB[pid] = b = pid;
-    if (b != INF) {
-      ch += b != pid;
-      mark(NX, b);
-    }
+    ch += b != INF && b != pid;
+    mark_next(NX, PB, TB, a, excl);
   }
   ch = warp_sum(ch);
   if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
@@ -656,7 +672,7 @@ __global__ void __launch_bounds__(RB) k_pstat2_list(uint32_t* __restrict__ PB,
 // per chunk with set bits
 __global__ void __launch_bounds__(RB) k_list_from_bits(uint32_t* NX, uint64_t nw, uint32_t* __restrict__ list,
                                                        unsigned long long* lcnt, uint32_t* __restrict__ NCP,
-                                                       uint32_t* __restrict__ TB) {
+                                                       uint32_t* __restrict__ TB, uint32_t* __restrict__ PA) {
   __shared__ uint32_t s_w[RB / 32];
   __shared__ unsigned long long s_base;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -689,10 +705,12 @@ __global__ void __launch_bounds__(RB) k_list_from_bits(uint32_t* NX, uint64_t nw
     }
     __syncthreads();
     uint64_t pos = s_base + s_w[wid] + x - c;
-    while (bits) {
+    while (bits) {  // exact list: each partition id p gets PA[p] = p (pass A skips q = p)
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
-      list[pos++] = (uint32_t)(w * 32 + b);
+      const uint32_t id = (uint32_t)(w * 32 + b);
+      list[pos++] = id;
+      if (PA) PA[id] = id;
     }
     __syncthreads();
   }
@@ -800,7 +818,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
-             cudaStream_t st, bool excl) {
+             cudaStream_t st, bool excl, bool preset) {
   if (!L) return;
   const uint64_t nt = row_tiles(L);
   auto* umin = reinterpret_cast<unsigned long long*>(UMIN);
@@ -812,7 +830,8 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
     static unsigned ga = 0;
     if (!ga) ga = persistent_grid((const void*)k_rowpass<true>, ~0ull);
     k_rowpass<true><<<(unsigned)std::min<uint64_t>(nt, ga), PB, 0, st>>>(
-        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0, excl ? 1 : 0);
+        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, (hot ? 1 : 0) | (preset ? 2 : 0),
+        excl ? 1 : 0);
     if (have_long) {
       k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
@@ -847,24 +866,24 @@ void pstat1(uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_
   k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, c, temps_all ? 1 : 0, flag ? 1 : 0);
 }
 void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t* ctr, cudaStream_t st,
-            uint32_t* NX, const uint32_t* list, const uint64_t* lcnt) {
+            uint32_t* NX, bool excl, const uint32_t* list, const uint64_t* lcnt) {
   auto* c = reinterpret_cast<unsigned long long*>(ctr);
   if (list) {
     k_pstat2_list<<<148 * 8, RB, 0, st>>>(PB, list, reinterpret_cast<const unsigned long long*>(lcnt), PA, TB,
-                                          c, NX);
+                                          c, NX, excl ? 1 : 0);
     return;
   }
   const uint64_t n4 = (n + 3) / 4;
   if (!n4) return;
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
-  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, TB, c, NX);
+  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, TB, c, NX, excl ? 1 : 0);
 }
 void list_from_bits(uint32_t* NX, uint64_t n, uint32_t* list, uint64_t* lcnt, uint32_t* NCP, uint32_t* TB,
-                    cudaStream_t st) {
+                    uint32_t* PA, cudaStream_t st) {
   cudaMemsetAsync(lcnt, 0, sizeof(uint64_t), st);
   const uint64_t nw = (n + 31) / 32 + 2;  // the bitmaps' padding words too
   const unsigned g = (unsigned)std::min<uint64_t>((nw + RB - 1) / RB, 148 * 8);
-  k_list_from_bits<<<g, RB, 0, st>>>(NX, nw, list, reinterpret_cast<unsigned long long*>(lcnt), NCP, TB);
+  k_list_from_bits<<<g, RB, 0, st>>>(NX, nw, list, reinterpret_cast<unsigned long long*>(lcnt), NCP, TB, PA);
 }
 
 }  // namespace csr
