@@ -387,8 +387,10 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       if (k[j] == k[RITEMS - 1] && cout_k == k[RITEMS - 1]) { q = min(q, cout_m); if (A) x = max(x, cout_x); }
       if (k[j] == INF || k[j] == kfirst) continue;
       if (j == RITEMS - 1) qlast = q;
-      if ((hot & 2) && q == p[j]) {
-        // PA[p] was preset to p (p is a partition of this iteration): min(PA[p], p) = PA[p]
+      if ((!A || (hot & 2)) && q == p[j]) {
+        // A: PA[p] was preset to p (p is a partition of this iteration).  B: every live value
+        // p is p_min of a surviving partition, so TB(p) holds and k_pstat2 applies the
+        // temporary's own min(PB[p], p).  Either way min(slot, p) changes nothing.
       } else if (!(hot & 1)) {
         atomicMin(&OUT[p[j]], q);
       } else if (p[j] != last_p || q < last_q) {  // this thread's last update covers it
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
             push_bit(NCPw, s_nc, q, hot);
             last_nc = q;
           }
-        } else if (tbit(TB, k[j])) {
+        } else if (q != k[j] && tbit(TB, k[j])) {  // q = r: k_pstat2's fold covers it
           atomicMin(&OUT[k[j]], q);
         }
       }
