@@ -65,15 +65,19 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
   const uint64_t v0 = tile * (B * SITEMS) + (uint64_t)threadIdx.x * SITEMS;
   uint32_t c[SITEMS];
   uint32_t sum = 0;
+  const bool full = v0 + SITEMS <= n;  // 8 vertices: two 16-byte loads, one bitmap byte
+  if (full) {
+    const uint4 a = reinterpret_cast<const uint4*>(deg + v0)[0];
+    const uint4 b = reinterpret_cast<const uint4*>(deg + v0)[1];
+    c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+  }
+  const uint32_t vb = vis ? (vis[v0 >> 5] >> (v0 & 31)) : 0u;
 #pragma unroll
   for (int k = 0; k < SITEMS; k++) {
     const uint64_t v = v0 + k;
-    uint32_t x = 0;
-    if (v < n) {
-      x = deg[v];
-      if (x && vis && ((vis[v >> 5] >> (v & 31)) & 1u)) x = 0;
-      if (x) x += 1;
-    }
+    uint32_t x = full ? c[k] : (v < n ? deg[v] : 0u);
+    if ((vb >> k) & 1u) x = 0;
+    if (x) x += 1;
     c[k] = x;
     sum += x;
   }
@@ -91,14 +95,24 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
     if (threadIdx.x == 0 && tot) atomicAdd(&garc[(tile * (B * SITEMS)) >> gshift], tot);
   }
   uint32_t run = (uint32_t)pref + excl;
+  uint32_t o[SITEMS];
 #pragma unroll
   for (int k = 0; k < SITEMS; k++) {
-    const uint64_t v = v0 + k;
-    if (v < n) {
-      off[v] = run;
-      cur[v] = run + 1;
-    }
+    o[k] = run;
     run += c[k];
+  }
+  if (full) {
+    reinterpret_cast<uint4*>(off + v0)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    reinterpret_cast<uint4*>(off + v0)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+    reinterpret_cast<uint4*>(cur + v0)[0] = make_uint4(o[0] + 1, o[1] + 1, o[2] + 1, o[3] + 1);
+    reinterpret_cast<uint4*>(cur + v0)[1] = make_uint4(o[4] + 1, o[5] + 1, o[6] + 1, o[7] + 1);
+  } else {
+#pragma unroll
+    for (int k = 0; k < SITEMS; k++)
+      if (v0 + k < n) {
+        off[v0 + k] = o[k];
+        cur[v0 + k] = o[k] + 1;
+      }
   }
   if (n > 0 && v0 <= n - 1 && n - 1 < v0 + SITEMS) {  // owner of the last vertex
     off[n] = run;
