@@ -840,7 +840,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
       k.end(8.0 * m + 8.0 * m + 16.0 * m + 16.0 * m + 4.0 * n, 4);
     } else {
       CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
-      graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st);
+      graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail, c->d_gctr + graph::G_NUM + 64);
       k.end(8.0 * m + 4.0 * n, 1);
     }
   }
@@ -905,16 +905,19 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     uint64_t mcur = m;
     int nb = 0;  // next scratch buffer
     bool last_compacted = false;
-    uint64_t visited = 1, levels = 0;
+    uint64_t visited = 1, levels = 0, front_arcs = 0;
     while (true) {
       CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
       CK(cudaMemsetAsync(c->d_gctr + graph::G_NEWVIS, 0, 2 * sizeof(uint64_t), c->st));
+      CK(cudaMemsetAsync(c->d_gctr + graph::G_FARCS, 0, sizeof(uint64_t), c->st));
       const bool root_level = levels == 0;
-      // compact once most present vertices are visited: the surviving edges are few
-      const bool compact = !root_level && 2 * visited > R.n_present;
+      // compact (keep only edges that can still matter) once most present vertices are
+      // visited, or when the frontier's arcs are a fifth of the current edge list: every edge
+      // at the frontier leaves, so the next level reads that much less
+      const bool compact = !root_level && (2 * visited > R.n_present || 5 * front_arcs >= 2 * mcur);
       Prof k(c, KF_BFS);
       graph::launch_bfs_level(root_level, compact, cur, mcur, (uint32_t)root, S, X, bufs[nb],
-                              c->d_gctr, c->st);
+                              c->d_gctr, c->d_deg, c->st);
       c->launches += 1;
       k.end(8.0 * (double)mcur + (compact ? 8.0 * (double)mcur / 8 : 0.0) + (double)n / 4, 1);
       CKL();
@@ -928,6 +931,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
       const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
       if (nv == 0) break;
       visited += nv;
+      front_arcs = c->h_gctr[graph::G_FARCS];
       levels++;
       graph::launch_bfs_advance(S, X, n, c->st);
       c->launches += 1;

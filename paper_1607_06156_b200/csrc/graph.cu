@@ -41,8 +41,37 @@ void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr,
 // edge list is streamed once per window and only endpoints inside it are counted, so the
 // random increments never reach DRAM.
 constexpr uint64_t DEG_WINDOW = 1ull << 24;
+// Hub vertices: on skewed graphs (R-MAT: the top id has ~0.1 % of all arc endpoints) every
+// increment of one hub serialises on one L2 address.  A 1/HUB_SAMPLE prefix of the (randomly
+// ordered) edge list is counted first, straight into deg; ids whose sample count reaches
+// HUB_MIN are hubs and are counted per block in a shared-memory table for the rest of the
+// list (one global add per hub per block at the end).  Exact either way: every endpoint is
+// counted once, in deg or in a block's table.
+constexpr uint64_t HUB_SAMPLE = 64;
+constexpr uint32_t HUB_MIN = 64;      // sampled count: degree ~ 4096 and up
+constexpr int HUB_CAP = 2048;         // hubs kept (more are counted globally)
+constexpr int HUB_TAB = 4096;         // shared-memory table slots (power of two)
+CC_DEVI uint32_t hub_hash(uint32_t v) { return (v * 2654435761u) >> 20; }  // 12 bits
+template <bool HUBS>
 __global__ void k_degree(const uint4* __restrict__ e2, uint64_t m, uint32_t* __restrict__ deg,
-                         uint32_t lo, uint32_t hi) {
+                         uint32_t lo, uint32_t hi, const uint32_t* __restrict__ hubs,
+                         const unsigned long long* nhubs) {
+  __shared__ uint32_t s_key[HUBS ? HUB_TAB : 1], s_cnt[HUBS ? HUB_TAB : 1];
+  if (HUBS) {
+    for (int i = threadIdx.x; i < HUB_TAB; i += BLOCK) {
+      s_key[i] = 0xFFFFFFFFu;
+      s_cnt[i] = 0;
+    }
+    __syncthreads();
+    const uint32_t nh = (uint32_t)min(*nhubs, (unsigned long long)HUB_CAP);
+    for (uint32_t i = threadIdx.x; i < nh; i += BLOCK) {  // linear probing, keys fixed
+      const uint32_t v = hubs[i];
+      if (v < lo || v >= hi) continue;
+      uint32_t h = hub_hash(v) & (HUB_TAB - 1);
+      while (atomicCAS(&s_key[h], 0xFFFFFFFFu, v) != 0xFFFFFFFFu) h = (h + 1) & (HUB_TAB - 1);
+    }
+    __syncthreads();
+  }
   const uint64_t npair = m >> 1;
   for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i <= npair;
        i += (uint64_t)gridDim.x * BLOCK) {
@@ -56,21 +85,87 @@ __global__ void k_degree(const uint4* __restrict__ e2, uint64_t m, uint32_t* __r
       v[0] = x.x; v[1] = x.y; cnt = 2;
     }
 #pragma unroll
-    for (int j = 0; j < 4; j++)
-      if (j < cnt && v[j] >= lo && v[j] < hi) atomicAdd(&deg[v[j]], 1u);
+    for (int j = 0; j < 4; j++) {
+      if (j >= cnt || v[j] < lo || v[j] >= hi) continue;
+      if (HUBS) {
+        uint32_t h = hub_hash(v[j]) & (HUB_TAB - 1), k;
+        while ((k = s_key[h]) != v[j] && k != 0xFFFFFFFFu) h = (h + 1) & (HUB_TAB - 1);
+        if (k == v[j]) {
+          atomicAdd(&s_cnt[h], 1u);
+          continue;
+        }
+      }
+      atomicAdd(&deg[v[j]], 1u);
+    }
+  }
+  if (HUBS) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < HUB_TAB; i += BLOCK)
+      if (s_cnt[i]) atomicAdd(&deg[s_key[i]], s_cnt[i]);
   }
 }
-void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st) {
+// histogram of floor(log2(sample count)) over ids with count >= HUB_MIN (picks the threshold
+// that keeps the hubs within HUB_CAP: the largest ones)
+__global__ void k_hub_hist(const uint32_t* __restrict__ deg, uint64_t n, unsigned long long* bins) {
+  __shared__ uint32_t s[32];
+  if (threadIdx.x < 32) s[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t v = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; v < n; v += (uint64_t)gridDim.x * BLOCK) {
+    const uint32_t d = deg[v];
+    if (d >= HUB_MIN) atomicAdd(&s[31 - __clz(d)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32 && s[threadIdx.x]) atomicAdd(&bins[threadIdx.x], (unsigned long long)s[threadIdx.x]);
+}
+// ids with sample count >= t -> hubs[0 .. *nhubs)
+__global__ void k_hubs(const uint32_t* __restrict__ deg, uint64_t n, uint32_t t, uint32_t* hubs,
+                       unsigned long long* nhubs) {
+  for (uint64_t v = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; v < n; v += (uint64_t)gridDim.x * BLOCK)
+    if (deg[v] >= t) {
+      const unsigned long long j = atomicAdd(nhubs, 1ull);
+      if (j < HUB_CAP) hubs[j] = (uint32_t)v;
+    }
+}
+void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
+                   uint32_t* hub_scratch, uint64_t* hub_count) {
+  // hub_count[0]: hub count; hub_count[8 .. 40): log2 histogram of the sample counts
   if (!m) return;
   static uint64_t window = 0;
   if (!window) {  // CC_DEG_WINDOW_LOG2: experiment hook for the counter window
     const char* e = getenv("CC_DEG_WINDOW_LOG2");
     window = e ? (1ull << atoi(e)) : DEG_WINDOW;
   }
+  auto* nh = reinterpret_cast<unsigned long long*>(hub_count);
+  // the hub table pays only on large edge lists (its sample must see the hubs)
+  const bool hubs = hub_scratch && m >= (1ull << 24);
+  uint64_t m0 = 0;
+  if (hubs) {
+    m0 = (m / HUB_SAMPLE) & ~1ull;  // even: the rest starts on a 16-byte boundary
+    k_degree<false><<<grid_for((m0 >> 1) + 1, 148 * 16), BLOCK, 0, st>>>(
+        reinterpret_cast<const uint4*>(edges), m0, deg, 0u, 0xFFFFFFFFu, nullptr, nullptr);
+    cudaMemsetAsync(hub_count, 0, sizeof(uint64_t) * 40, st);
+    k_hub_hist<<<grid_for(n, 148 * 8), BLOCK, 0, st>>>(deg, n, nh + 8);
+    uint64_t bins[32];
+    cudaMemcpyAsync(bins, hub_count + 8, sizeof(bins), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    uint32_t t = 0xFFFFFFFFu;  // smallest power of two whose ids fit the table
+    uint64_t above = 0;
+    for (int b = 31; b >= 0; b--) {
+      if (above + bins[b] > (uint64_t)HUB_CAP) break;
+      above += bins[b];
+      if (bins[b]) t = 1u << b;
+    }
+    if (above) k_hubs<<<grid_for(n, 148 * 8), BLOCK, 0, st>>>(deg, n, t, hub_scratch, nh);
+  }
   for (uint64_t lo = 0; lo < n; lo += window) {
     const uint64_t hi = std::min<uint64_t>(n, lo + window);
-    k_degree<<<grid_for((m >> 1) + 1, 148 * 16), BLOCK, 0, st>>>(
-        reinterpret_cast<const uint4*>(edges), m, deg, (uint32_t)lo, (uint32_t)hi);
+    const uint64_t mr = m - m0;
+    if (hubs)
+      k_degree<true><<<grid_for((mr >> 1) + 1, 148 * 8), BLOCK, 0, st>>>(
+          reinterpret_cast<const uint4*>(edges + m0), mr, deg, (uint32_t)lo, (uint32_t)hi, hub_scratch, nh);
+    else
+      k_degree<false><<<grid_for((mr >> 1) + 1, 148 * 16), BLOCK, 0, st>>>(
+          reinterpret_cast<const uint4*>(edges + m0), mr, deg, (uint32_t)lo, (uint32_t)hi, nullptr, nullptr);
   }
 }
 
@@ -149,10 +244,12 @@ template <bool ROOT, bool COMPACT>
 __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e, uint64_t m,
                                                      uint32_t root, uint32_t* S, uint32_t* next,
                                                      uint2* __restrict__ out,
-                                                     unsigned long long* gctr) {
+                                                     unsigned long long* gctr,
+                                                     const uint32_t* __restrict__ deg) {
   __shared__ uint32_t s_scan[BLOCK / 32 + 1];
   __shared__ unsigned long long s_base;
   uint32_t found = 0;
+  unsigned long long farcs = 0;
   const uint64_t stride = (uint64_t)gridDim.x * BLOCK * 2;
   const uint64_t iters = (m + stride - 1) / stride;
   for (uint64_t it = 0; it < iters; it++) {
@@ -171,13 +268,16 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
       if (j >= cnt) continue;
       const uint32_t a = x[j].x, b = x[j].y;
       if (ROOT) {
-        if (a == root) found += claim2(S, next, b);
-        if (b == root) found += claim2(S, next, a);
+        if (a == root && claim2(S, next, b)) { found++; farcs += __ldg(&deg[b]); }
+        if (b == root && claim2(S, next, a)) { found++; farcs += __ldg(&deg[a]); }
       } else {
         const uint32_t sa = st2(S, a), sb = st2(S, b);
-        if ((sa & 2u) && !(sb & 1u)) found += claim2(S, next, b);
-        if ((sb & 2u) && !(sa & 1u)) found += claim2(S, next, a);
-        keep[j] = !((sa & 1u) && (sb & 1u));
+        if ((sa & 2u) && !(sb & 1u) && claim2(S, next, b)) { found++; farcs += __ldg(&deg[b]); }
+        if ((sb & 2u) && !(sa & 1u) && claim2(S, next, a)) { found++; farcs += __ldg(&deg[a]); }
+        // after this level a frontier endpoint's neighbour is visited (by this or another
+        // edge): an edge whose endpoints are both visited then can no longer matter
+        const bool va = (sa & 1u) || (sb & 2u), vb = (sb & 1u) || (sa & 2u);
+        keep[j] = !(va && vb);
       }
     }
     if (COMPACT) {
@@ -193,7 +293,12 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
     }
   }
   found = warp_sum(found);
-  if ((threadIdx.x & 31) == 0 && found) atomicAdd(&gctr[G_NEWVIS], (unsigned long long)found);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) farcs += __shfl_xor_sync(0xffffffffu, farcs, o);
+  if ((threadIdx.x & 31) == 0 && found) {
+    atomicAdd(&gctr[G_NEWVIS], (unsigned long long)found);
+    atomicAdd(&gctr[G_FARCS], farcs);
+  }
 }
 // After a level: frontier bits <- next, visited bits already set by the claims.
 __global__ void k_bfs_advance(uint32_t* S, const uint32_t* __restrict__ next, uint64_t nw2) {
@@ -209,13 +314,14 @@ __global__ void k_bfs_advance(uint32_t* S, const uint32_t* __restrict__ next, ui
   }
 }
 void launch_bfs_level(bool root_level, bool compact, const uint2* edges, uint64_t m, uint32_t root,
-                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, cudaStream_t st) {
+                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, const uint32_t* deg,
+                      cudaStream_t st) {
   if (!m) return;
   const unsigned g = grid_for((m + 1) / 2, 148 * 8);
   auto* c = reinterpret_cast<unsigned long long*>(gctr);
-  if (root_level) k_bfs_level<true, false><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c);
-  else if (compact) k_bfs_level<false, true><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c);
-  else k_bfs_level<false, false><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c);
+  if (root_level) k_bfs_level<true, false><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c, deg);
+  else if (compact) k_bfs_level<false, true><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c, deg);
+  else k_bfs_level<false, false><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c, deg);
 }
 void launch_bfs_advance(uint32_t* S, const uint32_t* next, uint64_t n, cudaStream_t st) {
   const uint64_t nw2 = (n + 15) / 16;

@@ -17,19 +17,25 @@ enum GCtr : int {
   G_REMAIN,        // filter output cursor
   G_MINVIS,        // min visited id
   G_ERR,           // input validation flags
+  G_FARCS,         // BFS: arcs (full-graph degrees) of the vertices found in the current level
   G_NUM
 };
 
 void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr, cudaStream_t st);
-void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st);
+// deg[v] += arcs with source v (deg zeroed by the caller).  hub_scratch (>= 2048 u32) and
+// hub_count (40 device u64): per-block shared-memory counting of high-degree ids (NULL: off)
+void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
+                   uint32_t* hub_scratch = nullptr, uint64_t* hub_count = nullptr);
 // deg[0, n) are the degrees of ids base .. base+n-1 (base > 0: a rank's vertex block)
 void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* tail,
                      uint64_t* gctr, cudaStream_t st, uint64_t base = 0);
 // edge-streaming BFS level over 2-bit vertex state S (16 ids per word: bit0 visited, bit1
-// frontier); newly visited count in gctr[G_NEWVIS]; with `compact`, edges with an endpoint
-// unvisited at the start of the level are appended to `out` (count in gctr[G_REMAIN]).
+// frontier); newly visited count in gctr[G_NEWVIS] and their degree sum (deg) in
+// gctr[G_FARCS]; with `compact`, the edges that can still matter (an endpoint unvisited after
+// the level) are appended to `out` (count in gctr[G_REMAIN]).
 void launch_bfs_level(bool root_level, bool compact, const uint2* edges, uint64_t m, uint32_t root,
-                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, cudaStream_t st);
+                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, const uint32_t* deg,
+                      cudaStream_t st);
 void launch_bfs_advance(uint32_t* S, const uint32_t* next, uint64_t n, cudaStream_t st);
 void launch_filter(const uint2* edges, uint64_t m, const uint32_t* S, uint2* out,
                    uint64_t* gctr, cudaStream_t st);
