@@ -228,10 +228,12 @@ void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* 
 // list.  Vertex state is 2 bits (bit 0 visited, bit 1 in the current frontier), 16 ids per
 // word, so one random read per endpoint answers both questions; a frontier endpoint claims
 // its unvisited neighbour with atomicOr on the visited bit and marks it in `next`.
-// Level 1 (frontier = {root}) compares ids instead of reading state.  From the level at
-// which most vertices are visited, each level also compacts the edge list to the edges that
-// still have an endpoint unvisited at the start of the level: later levels and the filter
-// stream only those.  (edge-streaming bitmap BFS.)
+// Level 1 (frontier = {root}) compares ids instead of reading state.  From the level whose
+// frontier holds a fifth of the current arcs (or once most vertices are visited), each level
+// also compacts the edge list to the edges that can still matter -- an endpoint unvisited
+// after the level (a frontier endpoint's neighbour is visited by then, by this or another
+// edge) -- staged per warp in shared memory and written in runs, so later levels and the
+// filter stream only those.  (edge-streaming bitmap BFS.)
 CC_DEVI uint32_t st2(const uint32_t* S, uint32_t v) { return (S[v >> 4] >> (2 * (v & 15))) & 3u; }
 CC_DEVI bool claim2(uint32_t* S, uint32_t* next, uint32_t v) {
   const uint32_t m = 1u << (2 * (v & 15));
@@ -246,8 +248,21 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
                                                      uint2* __restrict__ out,
                                                      unsigned long long* gctr,
                                                      const uint32_t* __restrict__ deg) {
-  __shared__ uint32_t s_scan[BLOCK / 32 + 1];
-  __shared__ unsigned long long s_base;
+  // compaction: survivors are staged per warp in shared memory and flushed in runs (one
+  // global cursor atomic per run, coalesced stores)
+  constexpr int WBUF = COMPACT ? 256 : 1;
+  __shared__ uint2 s_buf[BLOCK / 32][WBUF];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t nbuf = 0;  // warp-uniform
+  auto flush = [&]() {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&gctr[G_REMAIN], (unsigned long long)nbuf);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    __syncwarp();
+    for (uint32_t i = lane; i < nbuf; i += 32) out[base + i] = s_buf[wid][i];
+    __syncwarp();
+    nbuf = 0;
+  };
   uint32_t found = 0;
   unsigned long long farcs = 0;
   const uint64_t stride = (uint64_t)gridDim.x * BLOCK * 2;
@@ -281,17 +296,17 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
       }
     }
     if (COMPACT) {
-      const uint32_t nk = (uint32_t)keep[0] + (uint32_t)keep[1];
-      uint32_t tot;
-      const uint32_t off = block_excl_scan<BLOCK>(nk, s_scan, &tot);
-      if (threadIdx.x == 0) s_base = tot ? atomicAdd(&gctr[G_REMAIN], (unsigned long long)tot) : 0ull;
-      __syncthreads();
-      uint2* dst = out + s_base + off;
-      if (keep[0]) *dst++ = x[0];
-      if (keep[1]) *dst = x[1];
-      __syncthreads();
+      const uint32_t lt = lanemask_lt();
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const uint32_t mk = __ballot_sync(0xffffffffu, keep[j]);
+        if (keep[j]) s_buf[wid][nbuf + __popc(mk & lt)] = x[j];
+        nbuf += __popc(mk);
+      }
+      if (nbuf > (uint32_t)(COMPACT ? WBUF - 64 : 0)) flush();
     }
   }
+  if (COMPACT && nbuf) flush();
   found = warp_sum(found);
 #pragma unroll
   for (int o = 16; o; o >>= 1) farcs += __shfl_xor_sync(0xffffffffu, farcs, o);
