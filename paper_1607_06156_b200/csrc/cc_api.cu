@@ -397,6 +397,9 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   // exclusion of completed partitions (fig:loadbal variants)
   const bool excl = !(c->cfg.flags & CC_FLAG_NO_EXCLUDE);
   const bool temps_all = !excl || (c->cfg.flags & CC_FLAG_NO_EARLY_EXCLUDE);
+  // pstat2 marks P_i+1 exactly (and PA is preset) unless completed partitions keep their
+  // temporaries while their tuples leave (CC_FLAG_NO_EARLY_EXCLUDE)
+  const bool exact_next = !(excl && temps_all);
   uint64_t local_in = A_local;
   for (uint32_t it = 0;; it++) {
     if (it >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
@@ -449,10 +452,10 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       TRY(comm_allreduce(c, c->d_ctr + sv::C_OUT, 1, CC_DT_I64, CC_OP_SUM));
     }
     { Prof k(c, KF_SLOTS);
-      csr::pstat2(PB, n, PA, TB, c->d_ctr, c->st, NX, excl, lcur ? L[lb] : nullptr, lcur ? LC + lb : nullptr);
-      csr::list_from_bits(NX, n, L[lb ^ 1], LC + (lb ^ 1), NCP, TB, lcur ? PA : nullptr, c->st);
+      csr::pstat2(PB, n, PA, TB, c->d_ctr, c->st, NX, lcur ? L[lb] : nullptr, lcur ? LC + lb : nullptr);
+      csr::list_from_bits(NX, n, L[lb ^ 1], LC + (lb ^ 1), NCP, TB, exact_next ? PA : nullptr, c->st);
       k.end(lcur ? 12.0 * (double)c->iters.back().partitions + n / 4.0 : 8.0 * n4 + n / 4.0, 2); }
-    lexact = lcur;  // the list form of pstat2 marks P_i+1 exactly
+    lexact = exact_next;
     lprev = lcur;
     lcur = true;
     lb ^= 1;

@@ -68,10 +68,10 @@ void pstat1(uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_
 // labels of the rows still in the array (no-exclusion variant)
 void final_labels(const uint32_t* R, const uint32_t* P, uint64_t L, uint32_t* label, cudaStream_t st);
 // after pass B: the temporaries' own element (PB[u] = min(PB[u], u) for TB(u)), changed2,
-// PA cleared; marks in NX the next iteration's partition ids: list variant (over L_i) exactly,
-// { PB[PA[p]] : p not excluded }; all-slot variant a superset (every value of PB)
+// PA cleared; marks in NX the next iteration's partition ids { PB[v] : TB(v) } (exact unless
+// CC_FLAG_NO_EARLY_EXCLUDE, where TB also holds completed partitions); list variant over L_i
 void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t* ctr, cudaStream_t st,
-            uint32_t* NX, bool excl, const uint32_t* list = nullptr, const uint64_t* lcnt = nullptr);
+            uint32_t* NX, const uint32_t* list = nullptr, const uint64_t* lcnt = nullptr);
 // list[0..*lcnt) = ids of the set bits of NX (bitmap of n bits, cleared on the way); with PA
 // (exact list) each id gets PA[id] = id preset (pass A then skips updates q = p); clears the
 // NCP and TB bitmaps for the next iteration

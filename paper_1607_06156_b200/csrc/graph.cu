@@ -137,7 +137,7 @@ void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cu
   }
   auto* nh = reinterpret_cast<unsigned long long*>(hub_count);
   // the hub table pays only on large edge lists (its sample must see the hubs)
-  const bool hubs = hub_scratch && m >= (1ull << 24);
+  const bool hubs = hub_scratch && m >= (1ull << 27);
   uint64_t m0 = 0;
   if (hubs) {
     m0 = (m / HUB_SAMPLE) & ~1ull;  // even: the rest starts on a 16-byte boundary

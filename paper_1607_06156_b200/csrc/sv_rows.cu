@@ -601,51 +601,34 @@ __global__ void __launch_bounds__(RB) k_pstat1_list(uint32_t* __restrict__ PA,
 // After pass B: the temporaries' own element (line 24: <u,_,u>_tmp is in PB(u) with
 // q = u_min'(u) <= u; the row part of u_min' was pushed by pass B) -- PB[u] = min(PB[u], u)
 // for TB(u) -- then changed2 from PB and PA cleared for the next iteration.
-// The next iteration's partition ids, exactly: after pass B every live tuple of partition p
-// holds v = PA[p] (p not excluded), and the next pass A maps it to PB[v], so
-// P_i+1 = { PB[PA[p]] : p in P_i, p not excluded }; they are marked in NX.  NCP and TB are
-// cleared by k_list_from_bits, which runs after this kernel (TB is read here).
+// The next iteration's partition ids: after pass B every live tuple of partition p holds
+// v = PA[p], and the next pass A maps it to PB[v].  The values v are exactly the temporaries'
+// ids TB (one per surviving partition; with CC_FLAG_NO_EARLY_EXCLUDE a superset, completed
+// partitions included), so P_i+1 = { PB[v] : TB(v) } is marked in NX from each slot's own
+// word -- no gather.  NCP and TB are cleared by k_list_from_bits, which runs after this kernel.
 CC_DEVI void mark(uint32_t* NX, uint32_t v) {
   const uint32_t b = 1u << (v & 31);
   if (!(*(volatile uint32_t*)&NX[v >> 5] & b)) atomicOr(&NX[v >> 5], b);
 }
-// PB[v] after the temporaries' fold (another thread may be folding slot v concurrently)
-CC_DEVI uint32_t pb_final(const uint32_t* PB, const uint32_t* TB, uint32_t v) {
-  const uint32_t b = PB[v];
-  return ((TB[v >> 5] >> (v & 31)) & 1u) ? min(b, v) : b;
-}
-CC_DEVI void mark_next(uint32_t* NX, const uint32_t* PB, const uint32_t* TB, uint32_t pa, int excl) {
-  if (pa == INF || (excl && (pa & CBIT))) return;
-  mark(NX, pb_final(PB, TB, pa & ~CBIT));
-}
 __global__ void __launch_bounds__(RB) k_pstat2(uint32_t* __restrict__ PB, uint64_t n4,
                                                uint32_t* __restrict__ PA, const uint32_t* __restrict__ TB,
-                                               unsigned long long* ctr, uint32_t* NX, int excl) {
+                                               unsigned long long* ctr, uint32_t* NX) {
   uint32_t ch = 0;
   for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
     uint4 b = reinterpret_cast<const uint4*>(PB)[t];
-    const uint4 a = reinterpret_cast<const uint4*>(PA)[t];
     reinterpret_cast<uint4*>(PA)[t] = make_uint4(INF, INF, INF, INF);
     const uint32_t tw = (TB[t >> 3] >> (4 * (t & 7))) & 15u;
     if (tw) {
       const uint32_t u0 = (uint32_t)(4 * t);
-      if (tw & 1u) b.x = min(b.x, u0);
-      if (tw & 2u) b.y = min(b.y, u0 + 1);
-      if (tw & 4u) b.z = min(b.z, u0 + 2);
-      if (tw & 8u) b.w = min(b.w, u0 + 3);
+      if (tw & 1u) { b.x = min(b.x, u0); mark(NX, b.x); }
+      if (tw & 2u) { b.y = min(b.y, u0 + 1); mark(NX, b.y); }
+      if (tw & 4u) { b.z = min(b.z, u0 + 2); mark(NX, b.z); }
+      if (tw & 8u) { b.w = min(b.w, u0 + 3); mark(NX, b.w); }
       reinterpret_cast<uint4*>(PB)[t] = b;
     }
     const uint32_t v[4] = {b.x, b.y, b.z, b.w};
-    // all-slot form (iteration 0, |P_i| ~ n): a superset of P_i+1, the values of PB, which
-    // needs no gather (the exact form costs one random PB read per partition)
 #pragma unroll
-    for (int j = 0; j < 4; j++)
-      if (v[j] != INF) {
-        ch += v[j] != (uint32_t)(4 * t + j);
-        mark(NX, v[j]);
-      }
-    (void)a;
-    (void)excl;
+    for (int j = 0; j < 4; j++) ch += v[j] != INF && v[j] != (uint32_t)(4 * t + j);
   }
   ch = warp_sum(ch);
   if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
@@ -654,17 +637,18 @@ __global__ void __launch_bounds__(RB) k_pstat2_list(uint32_t* __restrict__ PB,
                                                     const uint32_t* __restrict__ list,
                                                     const unsigned long long* lcnt,
                                                     uint32_t* __restrict__ PA, const uint32_t* __restrict__ TB,
-                                                    unsigned long long* ctr, uint32_t* NX, int excl) {
+                                                    unsigned long long* ctr, uint32_t* NX) {
   uint32_t ch = 0;
   const uint64_t cnt = *lcnt;
   for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * RB) {
     const uint32_t pid = list[i];
     uint32_t b = PB[pid];
-    const uint32_t a = PA[pid];
     PA[pid] = INF;
-    if (((TB[pid >> 5] >> (pid & 31)) & 1u) && pid < b) PB[pid] = b = pid;
+    if ((TB[pid >> 5] >> (pid & 31)) & 1u) {
+      if (pid < b) PB[pid] = b = pid;
+      mark(NX, b);
+    }
     ch += b != INF && b != pid;
-    mark_next(NX, PB, TB, a, excl);
   }
   ch = warp_sum(ch);
   if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
@@ -868,17 +852,17 @@ void pstat1(uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_
   k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, c, temps_all ? 1 : 0, flag ? 1 : 0);
 }
 void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t* ctr, cudaStream_t st,
-            uint32_t* NX, bool excl, const uint32_t* list, const uint64_t* lcnt) {
+            uint32_t* NX, const uint32_t* list, const uint64_t* lcnt) {
   auto* c = reinterpret_cast<unsigned long long*>(ctr);
   if (list) {
     k_pstat2_list<<<148 * 8, RB, 0, st>>>(PB, list, reinterpret_cast<const unsigned long long*>(lcnt), PA, TB,
-                                          c, NX, excl ? 1 : 0);
+                                          c, NX);
     return;
   }
   const uint64_t n4 = (n + 3) / 4;
   if (!n4) return;
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
-  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, TB, c, NX, excl ? 1 : 0);
+  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, TB, c, NX);
 }
 void list_from_bits(uint32_t* NX, uint64_t n, uint32_t* list, uint64_t* lcnt, uint32_t* NCP, uint32_t* TB,
                     uint32_t* PA, cudaStream_t st) {
