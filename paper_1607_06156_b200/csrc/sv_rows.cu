@@ -172,8 +172,12 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int hot, int excl) {
   constexpr int NW = PB / 32;
   // double-buffered tile staging: TMA brings tile i+2 while tile i is processed
-  __shared__ __align__(128) uint32_t s_r[2][PTILE];
-  __shared__ __align__(128) uint32_t s_in[2][PTILE];
+  // s_r: R[t0 - 4, t0) (the last one tells whether the tile starts inside a row), the tile,
+  // and the XT tuples past it (the first stretch of the last row's extension); s_in: the tile
+  // and the XT inputs past it.  Edge reads then cost no global round trip in the tile.
+  constexpr int RPRE = 4, XT = 32;
+  __shared__ __align__(128) uint32_t s_r[2][RPRE + PTILE + XT];
+  __shared__ __align__(128) uint32_t s_in[2][PTILE + XT];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_last[NW];
   __shared__ RunAgg s_wt[NW], s_wh[NW + 1];  // per warp: last run (prefix), first run (suffix)
@@ -196,11 +200,13 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     if (tl >= ntiles) return;
     const uint64_t a0 = (uint64_t)tl * PTILE;
     const uint32_t n = (uint32_t)(L - a0 < (uint64_t)PTILE ? L - a0 : (uint64_t)PTILE);
-    const uint32_t bytes = (n * 4 + 15) & ~15u;  // arrays are padded past L
+    const uint32_t pre = a0 > 0 ? RPRE : 0;
+    // arrays hold >= L + 64 entries: the XT past the end are in bounds (masked by i < L)
+    const uint32_t br = ((pre + n + XT) * 4 + 15) & ~15u, bp = ((n + XT) * 4 + 15) & ~15u;
     const uint64_t pol = l2_evict_first_policy();
-    mbar_expect_tx(&s_bar[b], 2 * bytes);
-    bulk_g2s(s_r[b], R + a0, bytes, &s_bar[b], pol);
-    bulk_g2s(s_in[b], Pin + a0, bytes, &s_bar[b], pol);
+    mbar_expect_tx(&s_bar[b], br + bp);
+    bulk_g2s(s_r[b] + (RPRE - pre), R + a0 - pre, br, &s_bar[b], pol);
+    bulk_g2s(s_in[b], Pin + a0, bp, &s_bar[b], pol);
   };
   if (threadIdx.x == 0) {
     mbar_init(&s_bar[0], 1);
@@ -219,13 +225,19 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     const uint64_t t0 = (uint64_t)tile * PTILE;
     const uint32_t tlen = (uint32_t)(L - t0 < (uint64_t)PTILE ? L - t0 : (uint64_t)PTILE);
     const uint64_t i0 = t0 + (uint64_t)threadIdx.x * RITEMS;
-    const uint32_t rprev = (threadIdx.x == 0 && t0 > 0) ? __ldg(&R[t0 - 1]) : INF;
     uint32_t r[RITEMS], p[RITEMS];
     mbar_wait(&s_bar[buf], (it >> 1) & 1);
+    const uint32_t rprev = (threadIdx.x == 0 && t0 > 0) ? s_r[buf][RPRE - 1] : INF;
+    // last warp: R and the relabelled P of tuple t0 + tlen + lane (its gather overlaps the tile)
+    uint32_t xr = INF, xm = DEAD;
+    if (wid == NW - 1 && t0 + tlen + lane < L) {
+      xr = s_r[buf][RPRE + tlen + lane];
+      xm = relabel<A>(s_in[buf][tlen + lane], MAP, NCPr, excl);
+    }
     {
       const uint32_t s0 = threadIdx.x * RITEMS;
-      const uint4 a = reinterpret_cast<const uint4*>(s_r[buf] + s0)[0];
-      const uint4 b = reinterpret_cast<const uint4*>(s_r[buf] + s0)[1];
+      const uint4 a = reinterpret_cast<const uint4*>(s_r[buf] + RPRE + s0)[0];
+      const uint4 b = reinterpret_cast<const uint4*>(s_r[buf] + RPRE + s0)[1];
       const uint4 c = reinterpret_cast<const uint4*>(s_in[buf] + s0)[0];
       const uint4 d = reinterpret_cast<const uint4*>(s_in[buf] + s0)[1];
       r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
@@ -339,17 +351,24 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       uint32_t emn = INF, emx = 0, ek = INF;
       const uint32_t klast = __shfl_sync(FULL, kt, 31);
       const uint64_t pos = t0 + tlen;
-      if (klast != INF && pos < L && __ldg(&R[pos]) == klast) {
+      if (klast != INF && __shfl_sync(FULL, xr, 0) == klast) {
         ek = klast;
-        for (uint64_t base = pos; base < pos + LONG; base += 32) {
-          const uint64_t i = base + lane;
-          const bool in = i < L && __ldg(&R[i]) == klast;
-          if (in) {
-            const uint32_t pv = relabel<A>(__ldg(&Pin[i]), MAP, NCPr, excl);  // live row: not DEAD
-            emn = min(emn, pv);
-            emx = max(emx, pv);
+        const bool in0 = xr == klast;  // the prefetched first 32 (live row: not DEAD)
+        if (in0) {
+          emn = xm;
+          emx = xm;
+        }
+        if (!__ballot_sync(FULL, !in0)) {
+          for (uint64_t base = pos + 32; base < pos + LONG; base += 32) {
+            const uint64_t i = base + lane;
+            const bool in = i < L && __ldg(&R[i]) == klast;
+            if (in) {
+              const uint32_t pv = relabel<A>(__ldg(&Pin[i]), MAP, NCPr, excl);
+              emn = min(emn, pv);
+              emx = max(emx, pv);
+            }
+            if (__ballot_sync(FULL, !in)) break;
           }
-          if (__ballot_sync(FULL, !in)) break;
         }
         emn = __reduce_min_sync(FULL, emn);
         emx = __reduce_max_sync(FULL, emx);
@@ -423,11 +442,15 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       const uint32_t q = __shfl_sync(FULL, qlast, 31);
       const uint32_t klast = s_wh[NW].key;
       const uint64_t pos = t0 + tlen;
-      for (uint64_t base = pos; base < pos + LONG; base += 32) {
-        const uint64_t i = base + lane;
-        const bool in = i < L && __ldg(&R[i]) == klast;
-        if (in) atomicMin(&OUT[relabel<A>(__ldg(&Pin[i]), MAP, NCPr, excl)], q);
-        if (__ballot_sync(FULL, !in)) break;
+      const bool in0 = xr == klast;
+      if (in0 && (q != xm || (A && !(hot & 2)))) atomicMin(&OUT[xm], q);  // q = p: see above
+      if (!__ballot_sync(FULL, !in0)) {
+        for (uint64_t base = pos + 32; base < pos + LONG; base += 32) {
+          const uint64_t i = base + lane;
+          const bool in = i < L && __ldg(&R[i]) == klast;
+          if (in) atomicMin(&OUT[relabel<A>(__ldg(&Pin[i]), MAP, NCPr, excl)], q);
+          if (__ballot_sync(FULL, !in)) break;
+        }
       }
     }
     __syncthreads();
