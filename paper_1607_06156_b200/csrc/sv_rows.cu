@@ -180,7 +180,10 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
   __shared__ __align__(128) uint32_t s_in[2][PTILE + XT];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ uint32_t s_last[NW];
-  __shared__ RunAgg s_wt[NW], s_wh[NW + 1];  // per warp: last run (prefix), first run (suffix)
+  // per warp: last run (prefix), first run (suffix); double-buffered by tile parity, so the
+  // next tile can write its aggregates while a slow warp still walks this tile's (the two
+  // barriers of the next tile separate a buffer's reuse) -- no end-of-tile barrier
+  __shared__ RunAgg s_wt2[2][NW], s_wh2[2][NW + 1];
   __shared__ uint32_t s_kfirst;
   // hot mode: per-block aggregation of slot updates (key claimed once per block, value
   // min-reduced in shared memory, flushed with one global atomic per key at the end)
@@ -344,6 +347,8 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     uint32_t cout_x = A ? __shfl_down_sync(FULL, hmx, 1) : 0u;
     if (lane == 0) cin_k = INF;
     if (lane == 31) cout_k = INF;
+    RunAgg* s_wt = s_wt2[buf];
+    RunAgg* s_wh = s_wh2[buf];
     if (lane == 31) s_wt[wid] = RunAgg{kt, tmn, tmx, 0u};
     if (lane == 0) s_wh[wid] = RunAgg{kh, hmn, hmx, 0u};
     // ---- extension of the tile's last run into the next tile (last warp)
@@ -453,7 +458,6 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
         }
       }
     }
-    __syncthreads();
   }
   if (hot & 1) {  // flush the block's aggregated slot updates
     __syncthreads();
