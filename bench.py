@@ -36,6 +36,7 @@ WORKLOADS = {
           "ids permuted (BASELINE configs[1])",
     "c3": "C3 road-like: 4096x4096 lattice, p=0.55, +1% diagonals, ids permuted (configs[2])",
     "c4": "C4 R-MAT scale 26, edge factor 16, a/b/c/d=.57/.19/.19/.05, ids permuted (configs[3])",
+    "c5": "C5 R-MAT scale 28 U 10 M geometric(mean 64) paths, u64 ids (configs[4]) at --scale",
 }
 
 
@@ -108,9 +109,14 @@ def dist_info():
     return ws, rk, lr
 
 
-def make_graph(cfg):
+def make_graph(cfg, scale=1.0):
     import graphgen
-    return graphgen.make(cfg, 1.0)
+    return graphgen.make(cfg, scale)
+
+
+def default_scale(cfg, ws):
+    """C5 (u64 ids) needs 8 GPUs at full size: one GPU runs 1/16 of it."""
+    return (1.0 / 16 if ws == 1 else 1.0) if cfg == "c5" else 1.0
 
 
 def shard(edges, rank, ws):
@@ -142,21 +148,23 @@ def run_reference(args):
     if rk != 0:
         return 0
     import oracle
-    g = make_graph(args.config)
+    scale = args.scale or default_scale(args.config, ws)
+    g = make_graph(args.config, scale)
     oracle.build()
+    run = (lambda: oracle.uf_labels_u64(g.edges)) if g.n == 0 else (lambda: oracle.uf_labels(g.n, g.edges))
     for _ in range(args.warmup):
-        oracle.uf_labels(g.n, g.edges)
+        run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.uf_labels(g.n, g.edges)
+        run()
     dt = time.perf_counter() - t0
     v = g.m * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "n": g.n, "m": g.m, "mode": "auto"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64" if g.n == 0 else "u32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "scale": scale, "n": g.n, "m": g.m, "mode": "auto"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"whole {args.config} graph per step (union-find, 1 thread)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -169,6 +177,14 @@ def cpu_baseline(g, budget_s=12.0):
     import oracle
     oracle.build()
     reps, t_used = 0, 0.0
+    if g.n == 0:  # u64 ids: the oracle (sort-unique + union-find) on a bounded prefix
+        e = g.edges[:min(g.m, 20_000_000)]
+        t0 = time.perf_counter()
+        oracle.uf_labels_u64(e)
+        t_used = time.perf_counter() - t0
+        return {"value": e.shape[0] / t_used, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"u64 union-find oracle (sort-unique + union-find) on the first "
+                          f"{e.shape[0]} edge records of the workload, {t_used:.1f} s, single thread"}
     t0 = time.perf_counter()
     while reps < 20 and t_used < budget_s:
         oracle.uf_labels(g.n, g.edges)
@@ -189,6 +205,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--regroup", default="csr", choices=["csr", "csrbfs", "direct", "sort"],
                     help="SV bucket regroup engine (DESIGN.md §5.3)")
+    ap.add_argument("--scale", type=float, default=None,
+                    help="fraction of the config's size (default 1; c5 on one GPU: 1/16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true",
@@ -217,14 +235,17 @@ def main():
     dev = torch.device("cuda", lr)
     stream = torch.cuda.current_stream(dev)
 
-    g = make_graph(args.config)
+    scale = args.scale or default_scale(args.config, ws)
+    g = make_graph(args.config, scale)
     n, m = g.n, g.m
+    u64 = n == 0  # C5: u64 ids, relabelled on the device (Alg. 2 line 4)
+    ids = "u64" if u64 else "u32"
     mine = shard(g.edges, rk, ws)
     flags = (0 if args.no_profile else cc.CC_FLAG_PROFILE) | cc.REGROUP_FLAGS[args.regroup]
     comm = cc.TorchComm(device=dev) if ws > 1 else None
     ctx = cc.CC(device=lr, stream=stream, flags=flags, comm=comm)
-    d_edges = torch.from_numpy(mine.view(np.int32)).to(dev)
-    ctx.load(d_edges, n)
+    d_edges = torch.from_numpy(mine.view(np.int64 if u64 else np.int32)).to(dev)
+    ctx.load(d_edges, n, ids=ids)
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     for _ in range(max(3, args.warmup)):
@@ -279,15 +300,18 @@ def main():
     # ---------------- e2e: host buffers through the public API (H2D + run + D2H)
     e2e = None
     if not args.no_e2e:
-        host = torch.from_numpy(mine.view(np.int32)).pin_memory()
+        host = torch.from_numpy(mine.view(np.int64 if u64 else np.int32)).pin_memory()
         lo, hi = ctx.block_range()
         hout = torch.empty(hi - lo, dtype=torch.int32).pin_memory()
-        hnp = host.numpy().view(np.uint32)
+        hnp = host.numpy().view(np.uint64 if u64 else np.uint32)
         onp = hout.numpy().view(np.uint32)
-        for _ in range(2):
-            ctx.load(hnp, n)
+
+        def e2e_step():
+            ctx.load(hnp, n, ids=ids)
             ctx.run(args.mode)
-            ctx.labels(onp)
+            return ctx.labels_u64() if u64 else ctx.labels(onp)
+        for _ in range(2):
+            e2e_step()
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
@@ -296,20 +320,23 @@ def main():
         ke = max(1, min(args.steps, 5))
         e0.record(stream)
         for _ in range(ke):
-            ctx.load(hnp, n)
-            ctx.run(args.mode)
-            ctx.labels(onp)
+            out_lab = e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
         if ws > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": m * ke / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(mine.nbytes), "d2h_bytes_per_step": int(4 * (hi - lo)),
-               "steps": ke}
+               "h2d_bytes_per_step": int(mine.nbytes),
+               "d2h_bytes_per_step": int((16 if u64 else 4) * (hi - lo)), "steps": ke}
         ok = None
         if rk == 0:
-            ok = bool(np.array_equal(onp, __import__("oracle").uf_labels(n, g.edges)[lo:hi]))
+            orc = __import__("oracle")
+            if not u64:
+                ok = bool(np.array_equal(onp, orc.uf_labels(n, g.edges)[lo:hi]))
+            elif ws == 1:  # (sorted distinct ids, labels) against the u64 oracle
+                want = orc.uf_labels_u64(g.edges)
+                ok = bool(np.array_equal(out_lab[0], want[0]) and np.array_equal(out_lab[1], want[1]))
 
     if rk == 0:
         peak, peak_src = peaks()
@@ -331,15 +358,16 @@ def main():
         if os.path.exists(tp):
             tr = json.load(open(tp)).get(f"{args.config}/{args.regroup}", {})
             traffic = tr.get(names[dom]) if dom is not None else None
-        path_bytes = alg_bytes(rep, n, m)
+        path_bytes = alg_bytes(rep, n if not u64 else rep["n_present"], m)
         step_s = ms_max / 1e3 / args.steps
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
             "ms_per_step_profiled": ms_prof / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "n": n, "m": m, "mode": args.mode,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u64" if u64 else "u32", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "scale": scale,
+                       "n": n if not u64 else int(rep["n_present"]), "m": m, "mode": args.mode,
                        "regroup": args.regroup,
                        "route": "bfs+sv" if rep["ran_bfs"] else "sv",
                        "sv_iterations": rep["sv_iterations"],
@@ -360,7 +388,8 @@ def main():
             "path_roofline": {"alg_bytes_per_step": path_bytes,
                               "frac": (path_bytes / (peak * 1e9)) / step_s,
                               "model": "SURVEY.md §8(d): 8m+8A0+sum(32A_i+48A_i+1+40T_i)+4n+4n_p"},
-            "stages_ms": {k: rep[k] for k in ("ms_prediction", "ms_bfs", "ms_filter", "ms_sv")},
+            "stages_ms": {k: rep[k] for k in ("ms_relabel", "ms_prediction", "ms_bfs", "ms_filter", "ms_sv",
+                                              "ms_finalize")},
             "sv_iters": [{"A": it["active_in"], "P": it["partitions"], "ms": round(it["ms"], 4)}
                          for it in rep["iters"]],
             "gpu_launches": launches,
