@@ -41,6 +41,10 @@ def main():
     for e in evs:
         rows.append((e.time_range.start, e.time_range.end, e.name[:60]))
     rows.sort()
+    if not rows:  # no CUPTI records (e.g. under ncu, which owns the profiling interface)
+        print("timeline: no kernel records")
+        ctx.close()
+        return
     t0, t1 = rows[0][0], rows[-1][1]
     busy = sum(b - a for a, b, _ in rows)
     gaps = [(rows[i + 1][0] - rows[i][1], rows[i][2], rows[i + 1][2]) for i in range(len(rows) - 1)]
