@@ -184,6 +184,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   if (w == CC_U64) {
     TRY(dalloc_t(c, &c->d_ids64, 2 * m + 1));
     TRY(dalloc_t(c, &c->d_uids, 2 * m + 1));
+    if (relabel::hash_slots(2 * m)) TRY(dalloc_t(c, &c->d_htab, relabel::hash_slots(2 * m) + 1));
     if (c->cfg.flags & CC_FLAG_PERMUTE_IDS) {
       TRY(dalloc_t(c, &c->d_mix, n + 1));
       TRY(dalloc_t(c, &c->d_pi, n + 1));
@@ -800,8 +801,12 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     TRY(scan_epoch_guard(c));
     uint64_t* total = c->d_gctr + graph::G_NUM + 1537;
     uint32_t* vals[2] = {c->d_q[0], c->d_q[1]};
-    relabel::run(c->d_ids64, 2 * m, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges),
-                 c->d_uids, total, c->st, &c->launches);
+    if (c->d_htab)
+      relabel::run_hash(c->d_ids64, 2 * m, c->d_htab, c->d_w, vals, c->rws, reinterpret_cast<uint32_t*>(c->d_edges),
+                        c->d_uids, total, c->d_gctr + graph::G_NUM + 1540, c->st, &c->launches);
+    else
+      relabel::run(c->d_ids64, 2 * m, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges),
+                   c->d_uids, total, c->st, &c->launches);
     CKL();
     CK(cudaMemcpyAsync(c->h_word, total, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));

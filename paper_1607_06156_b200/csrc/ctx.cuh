@@ -33,6 +33,7 @@ struct cc_ctx {
   uint2* d_rem2 = nullptr;
   uint64_t* d_ids64 = nullptr;  // u64 mode: loaded endpoints (2m)
   uint64_t* d_uids = nullptr;   // u64 mode: sorted distinct ids (rank -> id)
+  uint64_t* d_htab = nullptr;   // u64 mode: relabel hash table (relabel::hash_slots(2m) + 1)
   uint64_t* d_mix = nullptr;    // CC_FLAG_PERMUTE_IDS: mixed ids / their sorted copy
   uint32_t* d_pi = nullptr;     // CC_FLAG_PERMUTE_IDS: original rank -> permuted rank
   uint64_t n_alloc = 0;         // id bound the n-sized buffers were sized for
@@ -160,7 +161,7 @@ static inline void dfree_all(cc_ctx* c) {
   }
   c->allocs.clear();
   c->d_edges = c->d_rem = c->d_rem2 = nullptr;
-  c->d_ids64 = c->d_uids = c->d_mix = nullptr;
+  c->d_ids64 = c->d_uids = c->d_mix = c->d_htab = nullptr;
   c->d_gids = c->d_xid = c->d_out64 = nullptr;
   c->d_xu32 = nullptr;
   c->gids_cap = c->xid_cap = c->xu32_cap = c->out64_cap = 0;

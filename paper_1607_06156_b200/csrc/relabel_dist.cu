@@ -4,8 +4,9 @@
 // output of a rank's vertex block in original ids (SURVEY.md §8(e) "u64 relabel =
 // distributed sort-unique + rank map (two exchanges)").
 //
-//   1. local sort-unique of the rank's 2m endpoints (relabel::run): sorted distinct ids U
-//      and, per endpoint, its index in U;
+//   1. local sort-unique of the rank's 2m endpoints (relabel::run_hash: hash dedupe, then a
+//      radix sort of the distinct ids only): sorted distinct ids U and, per endpoint, its
+//      index in U;
 //   2. splitters: every rank contributes S regular samples of U weighted by |U|; the
 //      all-gathered samples give world-1 splitters (sample sort);
 //   3. U is cut at the splitters (binary search) and the runs go to their range owners by
@@ -141,8 +142,12 @@ cc_status dist_relabel(cc_ctx* c) {
   // 1. local sort-unique: U = c->d_uids[0..u), endpoint -> index in U in the u32 edge array
   TRY(scan_epoch_guard(c));
   CK(cudaMemsetAsync(total, 0, sizeof(uint64_t), c->st));
-  relabel::run(c->d_ids64, k, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges), c->d_uids,
-               total, c->st, &c->launches);
+  if (c->d_htab)
+    relabel::run_hash(c->d_ids64, k, c->d_htab, c->d_w, vals, c->rws, reinterpret_cast<uint32_t*>(c->d_edges),
+                      c->d_uids, total, c->d_gctr + graph::G_NUM + 1540, c->st, &c->launches);
+  else
+    relabel::run(c->d_ids64, k, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges), c->d_uids,
+                 total, c->st, &c->launches);
   CKL();
   uint64_t u = 0;
   CK(cudaMemcpyAsync(&u, total, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));

@@ -21,15 +21,18 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--mode", default="auto")
     ap.add_argument("--out", default="gpurun_out/timeline.json")
+    ap.add_argument("--scale", type=float, default=1.0)
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
     import graphgen
     import paper_1607_06156_b200 as cc
-    g = graphgen.make(args.config, 1.0)
+    g = graphgen.make(args.config, args.scale)
     dev = torch.device("cuda", 0)
     ctx = cc.CC(device=0)
-    ctx.load(torch.from_numpy(g.edges.view(np.int32)).to(dev), g.n)
+    u64 = g.n == 0
+    ctx.load(torch.from_numpy(g.edges.view(np.int64 if u64 else np.int32)).to(dev), g.n,
+             ids="u64" if u64 else "u32")
     for _ in range(3):
         ctx.run(args.mode)
     torch.cuda.synchronize()
