@@ -8,7 +8,7 @@ nproc >> gpurun_out/${TAG}_gpu.txt; lscpu | grep "Model name" >> gpurun_out/${TA
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
 timeout 1500 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/${TAG}_pytest_gpu.log
-for c in ${BENCH_CONFIGS:-c2 c4}; do
+for c in ${BENCH_CONFIGS:-c2 c4 c5}; do
   timeout 600 python bench.py --config $c > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err; echo "bench $c rc=$?"
 done
 CMD="python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
