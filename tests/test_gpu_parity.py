@@ -366,6 +366,35 @@ def test_u64_ids(cc, seed, nv, m):
     assert np.array_equal(lab, lab_o)
 
 
+@pytest.mark.parametrize("kind", ["matching", "path", "star_dups"])
+def test_u64_relabel_table_sizes(cc, request, kind):
+    """The hash relabel starts with a table for ~m/2 distinct ids and redoes
+    the insertion at full size on a long probe run: a perfect matching (every id distinct,
+    2m of them) and a long path (m + 1 distinct) force the retry; a star with repeated edges
+    stays in the small table.  Labels equal the u64 oracle's either way."""
+    if "[csr-" not in request.node.name:
+        pytest.skip("relabel is engine-independent")
+    rng = np.random.default_rng(17)
+    if kind == "matching":
+        ids = np.unique(rng.integers(0, 2**64 - 1, size=400_000, dtype=np.uint64, endpoint=True))
+        ids = rng.permutation(ids)[: (ids.shape[0] // 2) * 2]
+        e = ids.reshape(-1, 2)
+    elif kind == "path":
+        ids = rng.permutation(np.unique(rng.integers(0, 2**63, size=300_000, dtype=np.uint64)))
+        e = np.stack([ids[:-1], ids[1:]], 1)
+        e = e[rng.permutation(e.shape[0])]
+    else:
+        leaves = rng.integers(1, 2**40, size=5000, dtype=np.uint64)
+        e = np.stack([np.full(200_000, 2**64 - 1, np.uint64), leaves[rng.integers(0, 5000, 200_000)]], 1)
+    ids_o, lab_o = oracle.uf_labels_u64(e)
+    cc.load(e, 0, ids="u64")
+    rep = cc.run("auto")
+    ids, lab = cc.labels_u64()
+    assert np.array_equal(ids, ids_o)
+    assert np.array_equal(lab, lab_o)
+    assert rep["n_present"] == ids_o.shape[0]
+
+
 @pytest.mark.parametrize("scale", [1 / 4096, 1 / 256])
 def test_config_c5_scaled(cc, request, scale):
     """C5 structure (R-MAT U geometric paths, u64 ids = mix64 of dense indices, scrambled
