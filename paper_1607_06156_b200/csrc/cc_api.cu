@@ -408,14 +408,17 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     CK(cudaEventRecord(ev_it, c->st));
     seg_begin(c, &a);
     uint32_t* Rc = R[cb];
-    // few partitions per live tuple: slot updates repeat, filter them through the block caches
-    const bool hot = it > 0 && c->iters.back().partitions * 16 < len;
+    // few partitions per live tuple: slot updates repeat, filter them through the block caches.
+    // Thresholds measured on C2 (iterations with 490 k / 112 k / 16 k previous partitions):
+    // pass A gains from the block tables below ~1/512 partitions per tuple, pass B below 1/128.
+    const uint64_t prevp = it > 0 ? c->iters.back().partitions : ~0ull >> 12;
+    const bool hotA = it > 0 && prevp * 512 < len, hotB = it > 0 && prevp * 128 < len;
     CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_SURVIVORS + 1), c->st));
     // ---- lines 8-16 (+ line 25 relabel of the previous iteration)
     { Prof k(c, KF_ROWA);
       csr::rowpass(true, Rc, Pc, it ? Palt : nullptr, len, it ? PB : nullptr, nullptr, nullptr, PA,
                    NCP, c->d_label, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs,
-                   have_long, hot, c->d_ctr, c->st, true, /*preset=*/lexact);
+                   have_long, hotA, c->d_ctr, c->st, true, /*preset=*/lexact);
       k.end(8.0 * len + (it ? 4.0 * len : 0.0), 1 + (have_long ? 2 : 0)); }
     if (it) std::swap(Pc, Palt);
     // sparse exchange once few partitions remain: the entries all ranks touched (at most
@@ -439,7 +442,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     // ---- lines 17-21 (exclusion, p <- p_min), line 24 (+ temporaries), line 25 minima
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
-                   c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, hot, c->d_ctr, c->st,
+                   c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, hotB, c->d_ctr, c->st,
                    excl);
       k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
