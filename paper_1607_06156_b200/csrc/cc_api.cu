@@ -80,8 +80,12 @@ cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
   if (c->cfg.tau <= 0) c->cfg.tau = 0.05;
   c->st = (cudaStream_t)cfg->stream;
   if (cudaMallocHost(&c->h_ctr, sizeof(uint64_t) * (sv::C_NUM + graph::G_NUM + 8)) != cudaSuccess ||
+      cudaMallocHost(&c->h_ctr2, sizeof(uint64_t) * 2 * sv::C_NUM) != cudaSuccess ||
       cudaMallocHost(&c->h_hist, sizeof(uint32_t) * (graph::HIST_DENSE + graph::TAIL_CAP)) !=
           cudaSuccess) {
+    if (c->h_ctr) cudaFreeHost(c->h_ctr);
+    if (c->h_ctr2) cudaFreeHost(c->h_ctr2);
+    if (c->h_hist) cudaFreeHost(c->h_hist);
     delete c;
     return CC_ERR_NOMEM;
   }
@@ -98,6 +102,7 @@ cc_status cc_destroy(cc_ctx* c) {
   cudaStreamSynchronize(c->st);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
+  if (c->h_ctr2) cudaFreeHost(c->h_ctr2);
   if (c->h_hist) cudaFreeHost(c->h_hist);
   delete c;
   return CC_OK;
@@ -177,7 +182,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
     TRY(dalloc_t(c, &c->d_send, 2 * m + 1));
     TRY(dalloc_t(c, &c->d_cnt, 2 * world + world * world));
   }
-  TRY(dalloc_t(c, &c->d_ctr, sv::C_NUM));
+  TRY(dalloc_t(c, &c->d_ctr, 2 * sv::C_NUM));  // two alternating blocks (SV look-ahead)
   TRY(dalloc_t(c, &c->d_gctr, graph::G_NUM + 512 + 1024 + 8));  // + relabel scratch
   TRY(dalloc_t(c, &c->d_garc, 2048 + 8));
   TRY(dalloc_t(c, &c->d_gcur, 2048 + 8));
@@ -368,7 +373,6 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   const bool multi = c->cfg.world_size > 1;
   uint32_t* R[2] = {reinterpret_cast<uint32_t*>(c->d_w[0]), reinterpret_cast<uint32_t*>(c->d_w[1])};
   uint32_t* P[2] = {R[0] + c->cap, R[1] + c->cap};
-  cudaEvent_t a = nullptr;
   int cb = 0;  // buffer holding the tuple array
   const uint32_t max_iter = 2 * (uint32_t)c->kbits + 8;
   // slot arrays: PA (pass A minima), PB (pass B minima), NCP / TB bitmaps.  The slot scans
@@ -386,45 +390,55 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   CK(cudaMemsetAsync(PB, 0xFF, sizeof(uint32_t) * n4, c->st));
   CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nwp, c->st));
   CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nwp, c->st));
-  // slot scans after iteration 0 visit only L_i, a superset of the partition ids P_i built
-  // from the values of PB (lcur: L[lb] holds L_i; lprev: L[lb ^ 1] holds L_i-1)
+  // slot scans after iteration 0 visit only the partition list L_i (lcur: L[lb] holds L_i;
+  // lprev: L[lb ^ 1] holds L_i-1)
   uint32_t* NX = c->d_nx;
   uint32_t* L[2] = {c->d_plist[0], c->d_plist[1]};
   uint64_t* LC = c->d_plcnt;
   int lb = 0;
   bool lcur = false, lprev = false, lexact = false;
   CK(cudaMemsetAsync(NX, 0, sizeof(uint32_t) * nwp, c->st));
-  uint64_t len_live = len;  // live tuples of this rank (compaction decision)
   // exclusion of completed partitions (fig:loadbal variants)
   const bool excl = !(c->cfg.flags & CC_FLAG_NO_EXCLUDE);
   const bool temps_all = !excl || (c->cfg.flags & CC_FLAG_NO_EARLY_EXCLUDE);
   // pstat2 marks P_i+1 exactly (and PA is preset) unless completed partitions keep their
   // temporaries while their tuples leave (CC_FLAG_NO_EARLY_EXCLUDE)
   const bool exact_next = !(excl && temps_all);
-  uint64_t local_in = A_local;
-  for (uint32_t it = 0;; it++) {
-    if (it >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
+  // Look-ahead (one GPU, with exclusion): iteration i+1 is enqueued before the host reads
+  // iteration i's counters, so the host round trip overlaps device work.  Its row passes pick
+  // the hot variant, or nothing at all once iteration i left no live tuple, from those
+  // counters on the device; counters alternate between two blocks.  Compaction (rare) is a
+  // synchronisation point.  Several ranks, or no exclusion, run step by step.
+  const bool ahead = !multi && excl;
+  uint64_t* CTR[2] = {c->d_ctr, c->d_ctr + sv::C_NUM};
+  cudaEvent_t ev_read[2] = {ev_get(c), ev_get(c)};
+  // hot thresholds measured on C2 (iterations with 490 k / 112 k / 16 k previous partitions):
+  // pass A gains from the block tables below 1/512 partitions per live tuple, pass B below 1/128
+  constexpr int HOT_A = 9, HOT_B = 7;
+  uint32_t next_enq = 0;
+  auto enqueue = [&](uint32_t it) -> cc_status {
     cudaEvent_t ev_it = ev_get(c);
     CK(cudaEventRecord(ev_it, c->st));
+    c->it_ev.push_back(ev_it);
+    cudaEvent_t a = nullptr;
     seg_begin(c, &a);
+    uint64_t* ctr = CTR[it & 1];
+    const uint64_t* prevctr = it ? CTR[(it - 1) & 1] : nullptr;
+    // the last known partition count (byte models; the sparse exchange of several ranks, which
+    // run step by step so it is the previous iteration's)
+    const uint64_t prevp = c->iters.empty() ? n : c->iters.back().partitions;
     uint32_t* Rc = R[cb];
-    // few partitions per live tuple: slot updates repeat, filter them through the block caches.
-    // Thresholds measured on C2 (iterations with 490 k / 112 k / 16 k previous partitions):
-    // pass A gains from the block tables below ~1/512 partitions per tuple, pass B below 1/128.
-    const uint64_t prevp = it > 0 ? c->iters.back().partitions : ~0ull >> 12;
-    const bool hotA = it > 0 && prevp * 512 < len, hotB = it > 0 && prevp * 128 < len;
-    CK(cudaMemsetAsync(c->d_ctr, 0, sizeof(uint64_t) * (sv::C_SURVIVORS + 1), c->st));
+    CK(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * (sv::C_SURVIVORS + 1), c->st));
     // ---- lines 8-16 (+ line 25 relabel of the previous iteration)
     { Prof k(c, KF_ROWA);
       csr::rowpass(true, Rc, Pc, it ? Palt : nullptr, len, it ? PB : nullptr, nullptr, nullptr, PA,
                    NCP, c->d_label, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs,
-                   have_long, hotA, c->d_ctr, c->st, true, /*preset=*/lexact);
+                   have_long, false, ctr, c->st, true, /*preset=*/lexact, prevctr, HOT_A);
       k.end(8.0 * len + (it ? 4.0 * len : 0.0), 1 + (have_long ? 2 : 0)); }
     if (it) std::swap(Pc, Palt);
     // sparse exchange once few partitions remain: the entries all ranks touched (at most
     // |P_i-1| per rank) cost less than the dense n-slot reduction
-    const bool sparse = multi && it > 0 &&
-                        c->iters.back().partitions * (uint64_t)c->cfg.world_size * 2 < n4;
+    const bool sparse = multi && it > 0 && prevp * (uint64_t)c->cfg.world_size * 2 < n4;
     if (multi) {  // partition minima and 'not completed' flags over all ranks
       if (sparse) {
         TRY(comm_sparse_slots(c, PA, NCP, n4));
@@ -435,48 +449,67 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     }
     // ---- line 22 bookkeeping: |P_i|, completed, changed, temporaries
     { Prof k(c, KF_SLOTS);
-      if (lcur) csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all, excl, L[lb], LC + lb,
+      if (lcur) csr::pstat1(PA, NCP, n, TB, PB, ctr, c->st, temps_all, excl, L[lb], LC + lb,
                             lprev ? L[lb ^ 1] : nullptr, lprev ? LC + (lb ^ 1) : nullptr);
-      else csr::pstat1(PA, NCP, n, TB, PB, c->d_ctr, c->st, temps_all, excl);
-      k.end(lcur ? 12.0 * (double)c->iters.back().partitions : 8.0 * n4, 1); }
+      else csr::pstat1(PA, NCP, n, TB, PB, ctr, c->st, temps_all, excl);
+      k.end(lcur ? 12.0 * (double)prevp : 8.0 * n4, 1); }
     // ---- lines 17-21 (exclusion, p <- p_min), line 24 (+ temporaries), line 25 minima
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
-                   c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, hotB, c->d_ctr, c->st,
-                   excl);
+                   c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, false, ctr, c->st,
+                   excl, false, prevctr, HOT_B);
       k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
     // live tuples: this rank's (compaction) and the global count (convergence)
-    if (multi)
-      CK(cudaMemcpyAsync(c->d_ctr + sv::C_SURVIVORS, c->d_ctr + sv::C_OUT, sizeof(uint64_t),
-                         cudaMemcpyDeviceToDevice, c->st));
     if (multi) {
+      CK(cudaMemcpyAsync(ctr + sv::C_SURVIVORS, ctr + sv::C_OUT, sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                         c->st));
       if (sparse) TRY(comm_sparse_slots(c, PB, nullptr, n4));
       else TRY(comm_min_u32(c, PB, n4));
-      TRY(comm_allreduce(c, c->d_ctr + sv::C_OUT, 1, CC_DT_I64, CC_OP_SUM));
+      TRY(comm_allreduce(c, ctr + sv::C_OUT, 1, CC_DT_I64, CC_OP_SUM));
     }
     { Prof k(c, KF_SLOTS);
-      csr::pstat2(PB, n, PA, TB, c->d_ctr, c->st, NX, lcur ? L[lb] : nullptr, lcur ? LC + lb : nullptr);
+      csr::pstat2(PB, n, PA, TB, ctr, c->st, NX, lcur ? L[lb] : nullptr, lcur ? LC + lb : nullptr);
       csr::list_from_bits(NX, n, L[lb ^ 1], LC + (lb ^ 1), NCP, TB, exact_next ? PA : nullptr, c->st);
-      k.end(lcur ? 12.0 * (double)c->iters.back().partitions + n / 4.0 : 8.0 * n4 + n / 4.0, 2); }
+      k.end(lcur ? 12.0 * (double)prevp + n / 4.0 : 8.0 * n4 + n / 4.0, 2); }
     lexact = exact_next;
     lprev = lcur;
     lcur = true;
     lb ^= 1;
-    c->launches += 6 + (have_long ? 4 : 0);
+    c->launches += 6 + (have_long ? 4 : 0) + (it && ahead ? 2 : 0);
     CKL();
-    CK(cudaMemcpyAsync(c->h_ctr, c->d_ctr, sizeof(uint64_t) * sv::C_NUM, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    const uint64_t A1 = c->h_ctr[sv::C_OUT];
-    len_live = multi ? c->h_ctr[sv::C_SURVIVORS] : A1;
+    CK(cudaMemcpyAsync(c->h_ctr2 + (it & 1) * sv::C_NUM, ctr, sizeof(uint64_t) * sv::C_NUM,
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaEventRecord(ev_read[it & 1], c->st));
+    seg_end(c, a, 20.0 * len + 16.0 * n4, 8);
+    next_enq = it + 1;
+    return CC_OK;
+  };
+  // byte-model bookkeeping of the last enqueued iteration, undone if it turns out to be a
+  // look-ahead that had nothing to do (its kernels returned at once)
+  struct Snap { size_t nev; double bytes; uint64_t launches; } snap[KF_N];
+  auto take_snap = [&]() {
+    for (int f = 0; f < KF_N; f++) snap[f] = {c->kst[f].ev.size(), c->kst[f].bytes, c->kst[f].launches};
+  };
+  uint64_t local_in = A_local;
+  bool pending_compact = false;
+  TRY(enqueue(0));
+  for (uint32_t it = 0;; it++) {
+    if (ahead && !pending_compact && next_enq == it + 1 && it + 1 < max_iter) {
+      take_snap();
+      TRY(enqueue(it + 1));
+    }
+    CK(cudaEventSynchronize(ev_read[it & 1]));
+    const uint64_t* h = c->h_ctr2 + (it & 1) * sv::C_NUM;
+    const uint64_t A1 = h[sv::C_OUT];
+    const uint64_t len_live = multi ? h[sv::C_SURVIVORS] : A1;
     cc_iter_stat s{};
     s.active_in = A;
-    s.active_min = s.active_max = A;
-    s.partitions = c->h_ctr[sv::C_PARTITIONS];
-    s.completed = c->h_ctr[sv::C_COMPLETED];
-    s.changed = c->h_ctr[sv::C_CHANGED];
-    s.temps = c->h_ctr[sv::C_TEMPS];
-    s.changed2 = c->h_ctr[sv::C_CHANGED2];
+    s.partitions = h[sv::C_PARTITIONS];
+    s.completed = h[sv::C_COMPLETED];
+    s.changed = h[sv::C_CHANGED];
+    s.temps = h[sv::C_TEMPS];
+    s.changed2 = h[sv::C_CHANGED2];
     s.active_min = s.active_max = local_in;
     if (multi) {  // per-rank load (fig:loadbal): min and max of the live tuples over ranks
       uint64_t* mm = c->d_gcur + 2050;
@@ -492,8 +525,6 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     }
     local_in = len_live;
     c->iters.push_back(s);
-    c->it_ev.push_back(ev_it);
-    seg_end(c, a, 20.0 * len + 16.0 * n4, 8);
     if (!excl) {
       // 'Naive': nothing leaves; the partition passes decide convergence
       if (s.changed == 0 && s.changed2 == 0) {
@@ -501,15 +532,24 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
         c->launches += 1;
         break;
       }
-      A = A1;
-      continue;
+    } else if (A1 == 0) {
+      if (next_enq == it + 2)  // a look-ahead iteration is in flight: it returns at once
+        for (int f = 0; f < KF_N; f++) {
+          c->kst[f].ev.resize(snap[f].nev);
+          c->kst[f].bytes = snap[f].bytes;
+          c->kst[f].launches = snap[f].launches;
+        }
+      break;
     }
-    if (A1 == 0) break;
+    if (it + 1 >= max_iter) return fail(c, CC_ERR_NOCONV, "SV did not converge in %u iterations", max_iter);
     // dead rows of completed partitions are squeezed out once they are a third of the array
-    // (the paper's 'swapped to the end of the local array', sec:distSVOpt1)
-    if (3 * (len - len_live) > len) {
+    // (the paper's 'swapped to the end of the local array', sec:distSVOpt1); with the next
+    // iteration already in flight, after it (its counts are exact then)
+    const bool want = 3 * (len - len_live) > len;
+    if (pending_compact || (want && next_enq == it + 1)) {
+      pending_compact = false;
       TRY(scan_epoch_guard(c));
-      { Prof k(c, KF_COMPACT); csr::compact(Rc, Pc, len, R[cb ^ 1], P[cb ^ 1], c->ss, c->st);
+      { Prof k(c, KF_COMPACT); csr::compact(R[cb], Pc, len, R[cb ^ 1], P[cb ^ 1], c->ss, c->st);
         k.end(8.0 * len + 8.0 * len_live, 1); }
       c->launches += 1;
       cb ^= 1;
@@ -517,9 +557,13 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       Pc = P[cb];
       Palt = c->d_q[0];
       if (have_long) csr::longlist(R[cb], Pc, len, c->d_deg, c->d_lsegs, c->d_nlsegs, c->st);
+    } else if (want) {
+      pending_compact = true;
     }
     A = A1;
+    if (next_enq == it + 1) TRY(enqueue(it + 1));
   }
+  CK(cudaStreamSynchronize(c->st));
   return CC_OK;
 }
 

@@ -54,7 +54,10 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
-             cudaStream_t st, bool excl = true, bool preset = false);
+             cudaStream_t st, bool excl = true, bool preset = false, const uint64_t* prevctr = nullptr,
+             int hot_shift = 0);
+// prevctr (device, the previous iteration's sv counters): the pass returns at once when it
+// left no live tuple, and is hot when |P_prev| << hot_shift < L (overrides `hot`)
 // partition statistics after pass A (sets TB, clears PB); slot arrays padded to 4*ceil(n/4)
 // temps_all: a temporary for every partition, completed ones included (their tuples leave at
 // the end of the iteration or never)

@@ -83,6 +83,7 @@ struct cc_ctx {
   uint64_t* d_ctr = nullptr;   // sv counters
   uint64_t* d_gctr = nullptr;  // graph counters
   uint64_t* h_ctr = nullptr;   // pinned mirrors
+  uint64_t* h_ctr2 = nullptr;  // pinned: the two alternating SV counter blocks (look-ahead)
   uint64_t* h_gctr = nullptr;
   uint32_t* h_hist = nullptr;  // pinned histogram staging
   uint32_t* h_word = nullptr;

@@ -164,12 +164,17 @@ CC_DEVI uint32_t relabel(uint32_t pv, const uint32_t* __restrict__ MAP, const ui
 struct RunAgg {
   uint32_t key, mn, mx, pad;
 };
-template <bool A>
+template <bool A, bool HOT>
 __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     const uint32_t* __restrict__ R, const uint32_t* __restrict__ Pin, uint32_t* __restrict__ Pout,
     uint64_t L, uint32_t ntiles, const uint32_t* __restrict__ MAP,
     const uint32_t* __restrict__ NCPr, const uint32_t* __restrict__ TB, uint32_t* OUT,
-    uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int hot, int excl) {
+    uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int preset, int excl,
+    const unsigned long long* __restrict__ prevctr, int hot_shift) {
+  // With prevctr both variants are launched and the previous iteration's counters pick one on
+  // the device (so the host can enqueue this pass before reading them): nothing left ->
+  // neither runs; few partitions per live tuple -> the HOT variant.
+  if (prevctr && (prevctr[sv::C_OUT] == 0 || ((prevctr[sv::C_PARTITIONS] << hot_shift) < L) != HOT)) return;
   constexpr int NW = PB / 32;
   // double-buffered tile staging: TMA brings tile i+2 while tile i is processed
   // s_r: R[t0 - 4, t0) (the last one tells whether the tile starts inside a row), the tile,
@@ -411,11 +416,11 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       if (k[j] == k[RITEMS - 1] && cout_k == k[RITEMS - 1]) { q = min(q, cout_m); if (A) x = max(x, cout_x); }
       if (k[j] == INF || k[j] == kfirst) continue;
       if (j == RITEMS - 1) qlast = q;
-      if ((!A || (hot & 2)) && q == p[j]) {
+      if ((!A || preset) && q == p[j]) {
         // A: PA[p] was preset to p (p is a partition of this iteration).  B: every live value
         // p is p_min of a surviving partition, so TB(p) holds and k_pstat2 applies the
         // temporary's own min(PB[p], p).  Either way min(slot, p) changes nothing.
-      } else if (!(hot & 1)) {
+      } else if (!HOT) {
         atomicMin(&OUT[p[j]], q);
       } else if (p[j] != last_p || q < last_q) {  // this thread's last update covers it
         const uint32_t h = (p[j] ^ (p[j] >> 10)) & (RAGG - 1);
@@ -434,7 +439,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
           // many non-PC rows share one minimum late in the run: filter through a block cache
           // and a read of the word before the atomic
           if (q != x && q != last_nc) {
-            push_bit(NCPw, s_nc, q, hot);
+            push_bit(NCPw, s_nc, q, HOT);
             last_nc = q;
           }
         } else if (q != k[j] && tbit(TB, k[j])) {  // q = r: k_pstat2's fold covers it
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       const uint32_t klast = s_wh[NW].key;
       const uint64_t pos = t0 + tlen;
       const bool in0 = xr == klast;
-      if (in0 && (q != xm || (A && !(hot & 2)))) atomicMin(&OUT[xm], q);  // q = p: see above
+      if (in0 && (q != xm || (A && !preset))) atomicMin(&OUT[xm], q);  // q = p: see above
       if (!__ballot_sync(FULL, !in0)) {
         for (uint64_t base = pos + 32; base < pos + LONG; base += 32) {
           const uint64_t i = base + lane;
@@ -459,7 +464,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       }
     }
   }
-  if (hot & 1) {  // flush the block's aggregated slot updates
+  if (HOT) {  // flush the block's aggregated slot updates
     __syncthreads();
     for (int i = threadIdx.x; i < RAGG; i += PB)
       if (s_akey[i] != INF) atomicMin(&OUT[s_akey[i]], s_aval[i]);
@@ -806,12 +811,23 @@ void or_parts(const uint32_t* parts, uint64_t words, int world, uint32_t* out, c
                                                                                             world, out);
 }
 
-static unsigned persistent_grid(const void* fn, uint64_t ntiles) {
+static unsigned persistent_grid(const void* fn) {
   int ps = 0, sms = 148, dev = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, fn, PB, 0);
   if (ps < 1) ps = 1;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ntiles, (uint64_t)sms * ps));
+  return (unsigned)(sms * ps);
+}
+template <bool A, bool HOT>
+static void launch_rowpass(const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L, uint64_t nt,
+                           const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
+                           uint32_t* NCPw, uint32_t* label, unsigned long long* c, int preset, int excl,
+                           const uint64_t* prevctr, int hot_shift, cudaStream_t st) {
+  static unsigned grid = 0;
+  if (!grid) grid = persistent_grid((const void*)k_rowpass<A, HOT>);
+  k_rowpass<A, HOT><<<(unsigned)std::min<uint64_t>(nt, grid), PB, 0, st>>>(
+      R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
+      reinterpret_cast<const unsigned long long*>(prevctr), hot_shift);
 }
 
 uint64_t row_tiles(uint64_t L) { return (L + PTILE - 1) / PTILE; }
@@ -831,7 +847,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
-             cudaStream_t st, bool excl, bool preset) {
+             cudaStream_t st, bool excl, bool preset, const uint64_t* prevctr, int hot_shift) {
   if (!L) return;
   const uint64_t nt = row_tiles(L);
   auto* umin = reinterpret_cast<unsigned long long*>(UMIN);
@@ -839,21 +855,22 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
   auto* ns = reinterpret_cast<const unsigned long long*>(nsegs);
   auto* c = reinterpret_cast<unsigned long long*>(ctr);
   const uint32_t* Pv = Pout ? Pout : Pin;  // relabelled values, for the long-row kernels
+  // with prevctr both variants go in and the device picks (see k_rowpass)
+  const int pre = preset ? 1 : 0, ex = excl ? 1 : 0;
   if (passA) {
-    static unsigned ga = 0;
-    if (!ga) ga = persistent_grid((const void*)k_rowpass<true>, ~0ull);
-    k_rowpass<true><<<(unsigned)std::min<uint64_t>(nt, ga), PB, 0, st>>>(
-        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, (hot ? 1 : 0) | (preset ? 2 : 0),
-        excl ? 1 : 0);
+    if (prevctr || hot)
+      launch_rowpass<true, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr, hot_shift, st);
+    if (prevctr || !hot)
+      launch_rowpass<true, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr, hot_shift, st);
     if (have_long) {
       k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
     }
   } else {
-    static unsigned gb = 0;
-    if (!gb) gb = persistent_grid((const void*)k_rowpass<false>, ~0ull);
-    k_rowpass<false><<<(unsigned)std::min<uint64_t>(nt, gb), PB, 0, st>>>(
-        R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, hot ? 1 : 0, excl ? 1 : 0);
+    if (prevctr || hot)
+      launch_rowpass<false, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr, hot_shift, st);
+    if (prevctr || !hot)
+      launch_rowpass<false, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr, hot_shift, st);
     if (have_long) {
       k_long1<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
