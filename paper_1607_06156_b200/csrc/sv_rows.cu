@@ -139,11 +139,11 @@ CC_DEVI void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
 }
 
 // relabel of one input value: A -> MAP (NULL: identity); B -> PA[p], or DEAD if p completed
-template <bool A>
+template <bool A, bool REL = true>
 CC_DEVI uint32_t relabel(uint32_t pv, const uint32_t* __restrict__ MAP, const uint32_t* __restrict__ NCPr,
                          int excl) {
   if (pv == DEAD) return DEAD;
-  if (A) return MAP ? __ldg(&MAP[pv]) : pv;
+  if (A) return REL ? __ldg(&MAP[pv]) : pv;
   const uint32_t pm = __ldg(&MAP[pv]);
   if (excl && (pm & CBIT)) return DEAD;
   return pm & ~CBIT;
@@ -164,7 +164,8 @@ CC_DEVI uint32_t relabel(uint32_t pv, const uint32_t* __restrict__ MAP, const ui
 struct RunAgg {
   uint32_t key, mn, mx, pad;
 };
-template <bool A, bool HOT>
+// REL: pass A relabels through MAP = PB (every iteration but the first) and writes Pout
+template <bool A, bool HOT, bool REL>
 __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     const uint32_t* __restrict__ R, const uint32_t* __restrict__ Pin, uint32_t* __restrict__ Pout,
     uint64_t L, uint32_t ntiles, const uint32_t* __restrict__ MAP,
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     uint32_t xr = INF, xm = DEAD;
     if (wid == NW - 1 && t0 + tlen + lane < L) {
       xr = s_r[buf][RPRE + tlen + lane];
-      xm = relabel<A>(s_in[buf][tlen + lane], MAP, NCPr, excl);
+      xm = relabel<A, REL>(s_in[buf][tlen + lane], MAP, NCPr, excl);
     }
     {
       const uint32_t s0 = threadIdx.x * RITEMS;
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       uint32_t m[RITEMS], cpl = 0;
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
-        const bool fresh = p[j] != DEAD && (!A || MAP) && (j == 0 || p[j] != p[j - 1]);
+        const bool fresh = p[j] != DEAD && (!A || REL) && (j == 0 || p[j] != p[j - 1]);
         uint32_t g = fresh ? __ldg(&MAP[p[j]]) : p[j];
         if (!A && fresh) {
           cpl |= (g >> 31) << j;  // CBIT: completed partition
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       }
 #pragma unroll
       for (int j = 1; j < RITEMS; j++)
-        if (p[j] != DEAD && (!A || MAP) && p[j] == p[j - 1]) {
+        if (p[j] != DEAD && (!A || REL) && p[j] == p[j - 1]) {
           m[j] = m[j - 1];
           cpl |= ((cpl >> (j - 1)) & 1u) << j;
         }
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) p[j] = m[j];
     }
-    if (Pout) store8(Pout, i0, L, p);
+    if (!A || REL) store8(Pout, i0, L, p);
     // keys: dead tuples and long rows (k_long1/k_long2) take no part
     uint32_t k[RITEMS];
 #pragma unroll
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
             const uint64_t i = base + lane;
             const bool in = i < L && __ldg(&R[i]) == klast;
             if (in) {
-              const uint32_t pv = relabel<A>(__ldg(&Pin[i]), MAP, NCPr, excl);
+              const uint32_t pv = relabel<A, REL>(__ldg(&Pin[i]), MAP, NCPr, excl);
               emn = min(emn, pv);
               emx = max(emx, pv);
             }
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
         for (uint64_t base = pos + 32; base < pos + LONG; base += 32) {
           const uint64_t i = base + lane;
           const bool in = i < L && __ldg(&R[i]) == klast;
-          if (in) atomicMin(&OUT[relabel<A>(__ldg(&Pin[i]), MAP, NCPr, excl)], q);
+          if (in) atomicMin(&OUT[relabel<A, REL>(__ldg(&Pin[i]), MAP, NCPr, excl)], q);
           if (__ballot_sync(FULL, !in)) break;
         }
       }
@@ -818,14 +819,14 @@ static unsigned persistent_grid(const void* fn) {
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return (unsigned)(sms * ps);
 }
-template <bool A, bool HOT>
+template <bool A, bool HOT, bool REL>
 static void launch_rowpass(const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L, uint64_t nt,
                            const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
                            uint32_t* NCPw, uint32_t* label, unsigned long long* c, int preset, int excl,
                            const uint64_t* prevctr, int hot_shift, cudaStream_t st) {
   static unsigned grid = 0;
-  if (!grid) grid = persistent_grid((const void*)k_rowpass<A, HOT>);
-  k_rowpass<A, HOT><<<(unsigned)std::min<uint64_t>(nt, grid), PB, 0, st>>>(
+  if (!grid) grid = persistent_grid((const void*)k_rowpass<A, HOT, REL>);
+  k_rowpass<A, HOT, REL><<<(unsigned)std::min<uint64_t>(nt, grid), PB, 0, st>>>(
       R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
       reinterpret_cast<const unsigned long long*>(prevctr), hot_shift);
 }
@@ -857,20 +858,31 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
   const uint32_t* Pv = Pout ? Pout : Pin;  // relabelled values, for the long-row kernels
   // with prevctr both variants go in and the device picks (see k_rowpass)
   const int pre = preset ? 1 : 0, ex = excl ? 1 : 0;
-  if (passA) {
+  if (passA && !MAP) {  // the first iteration: identity relabel, no P written, never hot
+    launch_rowpass<true, false, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
+                                       hot_shift, st);
+    if (have_long) {
+      k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
+      k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
+    }
+  } else if (passA) {
     if (prevctr || hot)
-      launch_rowpass<true, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr, hot_shift, st);
+      launch_rowpass<true, true, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
+                                       hot_shift, st);
     if (prevctr || !hot)
-      launch_rowpass<true, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr, hot_shift, st);
+      launch_rowpass<true, false, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
+                                        hot_shift, st);
     if (have_long) {
       k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
     }
   } else {
     if (prevctr || hot)
-      launch_rowpass<false, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr, hot_shift, st);
+      launch_rowpass<false, true, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
+                                        hot_shift, st);
     if (prevctr || !hot)
-      launch_rowpass<false, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr, hot_shift, st);
+      launch_rowpass<false, false, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
+                                         hot_shift, st);
     if (have_long) {
       k_long1<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);

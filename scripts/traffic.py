@@ -29,7 +29,7 @@ def main():
     tl = os.path.join(ROOT, "gpurun_out", f"traffic_tl_{args.config}.json")
     subprocess.check_call([sys.executable, os.path.join(ROOT, "scripts", "timeline.py"), "--config", args.config,
                            "--out", tl], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
-    per_run = sum(1 for o in json.load(open(tl))["ops"] if "k_rowpass" in o[2])
+    per_run = sum(1 for o in json.load(open(tl))["ops"] if "k_rowpass" in o[2])  # both variants
     out = subprocess.check_output(
         ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
          "--clock-control", "none", "--csv", "-k", "regex:k_rowpass", "-s", str(3 * per_run), "-c", str(per_run),
@@ -38,9 +38,17 @@ def main():
     rows = [r for r in csv.reader(io.StringIO(out[out.index('"ID"'):]))]
     hdr = rows[0]
     acc = {}
+    busy = set()  # launches that did the pass (the variant the device did not pick returns at once)
     for r in rows[1:]:
         d = dict(zip(hdr, r))
-        if d.get("Metric Name") not in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        if d.get("Metric Name") == "gpu__time_duration.sum":
+            us = float(d["Metric Value"].replace(",", "")) * {"nsecond": 1e-3, "usecond": 1.0,
+                                                             "msecond": 1e3}.get(d["Metric Unit"], 1.0)
+            if us > 20.0:
+                busy.add(d["ID"])
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") not in ("dram__bytes_read.sum", "dram__bytes_write.sum") or d["ID"] not in busy:
             continue
         kn = d["Kernel Name"]
         fam = FAM["true" if ("k_rowpass<true" in kn or "k_rowpass<1" in kn) else "false"]
