@@ -56,8 +56,10 @@ def main():
         key = (fam, d["ID"])
         acc[key] = acc.get(key, 0.0) + v
     res = {}
-    for (fam, _), v in acc.items():
+    for (fam, i), v in acc.items():
         res.setdefault(fam, []).append(v)
+    with open(os.path.join(ROOT, "gpurun_out", f"traffic_{args.config}.csv"), "w") as f:
+        f.write(out[out.index('"ID"'):])
     data = json.load(open(args.out)) if os.path.exists(args.out) else {}
     data[f"{args.config}/csr"] = {f: sum(v) / len(v) for f, v in res.items()}
     data["_source"] = ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every k_rowpass launch "
