@@ -164,8 +164,9 @@ CC_DEVI uint32_t relabel(uint32_t pv, const uint32_t* __restrict__ MAP, const ui
 struct RunAgg {
   uint32_t key, mn, mx, pad;
 };
-// REL: pass A relabels through MAP = PB (every iteration but the first) and writes Pout
-template <bool A, bool HOT, bool REL>
+// REL: pass A relabels through MAP = PB (every iteration but the first) and writes Pout.
+// X: pass A -- PA is preset (updates q = p are skipped); pass B -- completed partitions leave.
+template <bool A, bool HOT, bool REL, bool X>
 __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     const uint32_t* __restrict__ R, const uint32_t* __restrict__ Pin, uint32_t* __restrict__ Pout,
     uint64_t L, uint32_t ntiles, const uint32_t* __restrict__ MAP,
@@ -176,6 +177,10 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
   // the device (so the host can enqueue this pass before reading them): nothing left ->
   // neither runs; few partitions per live tuple -> the HOT variant.
   if (prevctr && (prevctr[sv::C_OUT] == 0 || ((prevctr[sv::C_PARTITIONS] << hot_shift) < L) != HOT)) return;
+  constexpr bool PRESET = A && X;
+  constexpr int EXCL = (A || X) ? 1 : 0;  // (pass A's relabel ignores it)
+  (void)preset;
+  (void)excl;
   constexpr int NW = PB / 32;
   // double-buffered tile staging: TMA brings tile i+2 while tile i is processed
   // s_r: R[t0 - 4, t0) (the last one tells whether the tile starts inside a row), the tile,
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     uint32_t xr = INF, xm = DEAD;
     if (wid == NW - 1 && t0 + tlen + lane < L) {
       xr = s_r[buf][RPRE + tlen + lane];
-      xm = relabel<A, REL>(s_in[buf][tlen + lane], MAP, NCPr, excl);
+      xm = relabel<A, REL>(s_in[buf][tlen + lane], MAP, NCPr, EXCL);
     }
     {
       const uint32_t s0 = threadIdx.x * RITEMS;
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       if (!A) {
 #pragma unroll
         for (int j = 0; j < RITEMS; j++) {
-          if (excl && p[j] != DEAD && ((cpl >> j) & 1u)) {
+          if (EXCL && p[j] != DEAD && ((cpl >> j) & 1u)) {
             // completed partition: the whole row leaves, its vertex is labelled p
             if (j == 0 || r[j - 1] != r[j]) label[r[j] & ~R_LONG] = p[j];
             m[j] = DEAD;
@@ -374,7 +379,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
             const uint64_t i = base + lane;
             const bool in = i < L && __ldg(&R[i]) == klast;
             if (in) {
-              const uint32_t pv = relabel<A, REL>(__ldg(&Pin[i]), MAP, NCPr, excl);
+              const uint32_t pv = relabel<A, REL>(__ldg(&Pin[i]), MAP, NCPr, EXCL);
               emn = min(emn, pv);
               emx = max(emx, pv);
             }
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       if (k[j] == k[RITEMS - 1] && cout_k == k[RITEMS - 1]) { q = min(q, cout_m); if (A) x = max(x, cout_x); }
       if (k[j] == INF || k[j] == kfirst) continue;
       if (j == RITEMS - 1) qlast = q;
-      if ((!A || preset) && q == p[j]) {
+      if ((!A || PRESET) && q == p[j]) {
         // A: PA[p] was preset to p (p is a partition of this iteration).  B: every live value
         // p is p_min of a surviving partition, so TB(p) holds and k_pstat2 applies the
         // temporary's own min(PB[p], p).  Either way min(slot, p) changes nothing.
@@ -454,12 +459,12 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       const uint32_t klast = s_wh[NW].key;
       const uint64_t pos = t0 + tlen;
       const bool in0 = xr == klast;
-      if (in0 && (q != xm || (A && !preset))) atomicMin(&OUT[xm], q);  // q = p: see above
+      if (in0 && (q != xm || (A && !PRESET))) atomicMin(&OUT[xm], q);  // q = p: see above
       if (!__ballot_sync(FULL, !in0)) {
         for (uint64_t base = pos + 32; base < pos + LONG; base += 32) {
           const uint64_t i = base + lane;
           const bool in = i < L && __ldg(&R[i]) == klast;
-          if (in) atomicMin(&OUT[relabel<A, REL>(__ldg(&Pin[i]), MAP, NCPr, excl)], q);
+          if (in) atomicMin(&OUT[relabel<A, REL>(__ldg(&Pin[i]), MAP, NCPr, EXCL)], q);
           if (__ballot_sync(FULL, !in)) break;
         }
       }
@@ -819,16 +824,29 @@ static unsigned persistent_grid(const void* fn) {
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return (unsigned)(sms * ps);
 }
+template <bool A, bool HOT, bool REL, bool X>
+static void launch_rowpass_x(const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L, uint64_t nt,
+                           const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
+                           uint32_t* NCPw, uint32_t* label, unsigned long long* c, int preset, int excl,
+                           const uint64_t* prevctr, int hot_shift, cudaStream_t st) {
+  static unsigned grid = 0;
+  if (!grid) grid = persistent_grid((const void*)k_rowpass<A, HOT, REL, X>);
+  k_rowpass<A, HOT, REL, X><<<(unsigned)std::min<uint64_t>(nt, grid), PB, 0, st>>>(
+      R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
+      reinterpret_cast<const unsigned long long*>(prevctr), hot_shift);
+}
+
 template <bool A, bool HOT, bool REL>
 static void launch_rowpass(const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L, uint64_t nt,
                            const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
                            uint32_t* NCPw, uint32_t* label, unsigned long long* c, int preset, int excl,
                            const uint64_t* prevctr, int hot_shift, cudaStream_t st) {
-  static unsigned grid = 0;
-  if (!grid) grid = persistent_grid((const void*)k_rowpass<A, HOT, REL>);
-  k_rowpass<A, HOT, REL><<<(unsigned)std::min<uint64_t>(nt, grid), PB, 0, st>>>(
-      R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
-      reinterpret_cast<const unsigned long long*>(prevctr), hot_shift);
+  if (A ? preset : excl)
+    launch_rowpass_x<A, HOT, REL, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
+                                        prevctr, hot_shift, st);
+  else
+    launch_rowpass_x<A, HOT, REL, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
+                                         prevctr, hot_shift, st);
 }
 
 uint64_t row_tiles(uint64_t L) { return (L + PTILE - 1) / PTILE; }
