@@ -24,7 +24,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "traffic.json"))
+    ap.add_argument("--from-csv", default=None, help="recompute from a CSV an earlier run saved")
     args = ap.parse_args()
+    if args.from_csv:
+        return summarize(open(args.from_csv).read(), args)
     # launches of one cc_run: count them in a plain run first
     tl = os.path.join(ROOT, "gpurun_out", f"traffic_tl_{args.config}.json")
     subprocess.check_call([sys.executable, os.path.join(ROOT, "scripts", "timeline.py"), "--config", args.config,
@@ -35,6 +38,12 @@ def main():
          "--clock-control", "none", "--csv", "-k", "regex:k_rowpass", "-s", str(3 * per_run), "-c", str(per_run),
          sys.executable, os.path.join(ROOT, "scripts", "timeline.py"), "--config", args.config, "--out", tl],
         text=True, stderr=subprocess.DEVNULL)
+    with open(os.path.join(ROOT, "gpurun_out", f"traffic_{args.config}.csv"), "w") as f:
+        f.write(out[out.index('"ID"'):])
+    summarize(out, args)
+
+
+def summarize(out, args):
     rows = [r for r in csv.reader(io.StringIO(out[out.index('"ID"'):]))]
     hdr = rows[0]
     acc = {}
@@ -42,8 +51,8 @@ def main():
     for r in rows[1:]:
         d = dict(zip(hdr, r))
         if d.get("Metric Name") == "gpu__time_duration.sum":
-            us = float(d["Metric Value"].replace(",", "")) * {"nsecond": 1e-3, "usecond": 1.0,
-                                                             "msecond": 1e3}.get(d["Metric Unit"], 1.0)
+            us = float(d["Metric Value"].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
+                                                             "msecond": 1e3, "ms": 1e3}.get(d["Metric Unit"], 1.0)
             if us > 20.0:
                 busy.add(d["ID"])
     for r in rows[1:]:
@@ -58,8 +67,6 @@ def main():
     res = {}
     for (fam, i), v in acc.items():
         res.setdefault(fam, []).append(v)
-    with open(os.path.join(ROOT, "gpurun_out", f"traffic_{args.config}.csv"), "w") as f:
-        f.write(out[out.index('"ID"'):])
     data = json.load(open(args.out)) if os.path.exists(args.out) else {}
     data[f"{args.config}/csr"] = {f: sum(v) / len(v) for f, v in res.items()}
     data["_source"] = ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every k_rowpass launch "
