@@ -213,7 +213,7 @@ enum KFam { KF_RADIX = 0, KF_SVITER, KF_BFS, KF_ROWA, KF_ROWB, KF_SLOTS, KF_CSR,
 static const char* const kKfNames[KF_N] = {
     "k_hist+k_onesweep (radix regroup)", "SV iteration (all bucket passes)", "k_bfs_level",
     "k_rowpass<A> +k_long1/2 (Alg.1 lines 8-16)", "k_rowpass<B> +k_long1/2 (Alg.1 lines 17-25)",
-    "k_pstat1/k_temps2/k_pstat2 (partition slot scans)",
+    "k_pstat1/k_pstat2/k_list_from_bits (partition slot scans)",
     "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)", "prediction (k_degree, k_deg_hist)",
     "k_compact (ordered exclusion of completed rows)"};
 
