@@ -219,17 +219,17 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
     if (dmax >= graph::HIST_DENSE) {
       const uint64_t mytail = c->h_gctr[graph::G_TAIL];
       if (mytail > TAILX) return fail(c, CC_ERR_INVALID, "more than %u degrees >= 2^20 on one rank", TAILX);
-      const uint64_t need = (uint64_t)world * (TAILX + 1);
+      // scratch: everyone's lists [0, world (TAILX + 1)), then my own (count, entries)
+      const uint64_t need = (uint64_t)(world + 1) * (TAILX + 1);
       if (!c->d_gath || c->gath_cap < need) {
         TRY(dalloc_t(c, &c->d_gath, need));
         c->gath_cap = need;
       }
-      uint32_t* stage = c->d_gath + (uint64_t)world * TAILX;  // my count, then my entries
+      uint32_t* gathered = c->d_gath;
+      uint32_t* stage = c->d_gath + (uint64_t)world * (TAILX + 1);
       uint32_t nt32 = (uint32_t)mytail;
       CK(cudaMemcpyAsync(stage, &nt32, sizeof(uint32_t), cudaMemcpyHostToDevice, c->st));
       CK(cudaMemcpyAsync(stage + 1, c->d_tail, sizeof(uint32_t) * TAILX, cudaMemcpyDeviceToDevice, c->st));
-      uint32_t* gathered = nullptr;
-      TRY(dalloc_t(c, &gathered, (uint64_t)world * (TAILX + 1)));
       TRY(comm_allgather(c, stage, gathered, sizeof(uint32_t) * (TAILX + 1)));
       std::vector<uint32_t> h((size_t)world * (TAILX + 1)), merged;
       CK(cudaMemcpyAsync(h.data(), gathered, sizeof(uint32_t) * h.size(), cudaMemcpyDeviceToHost, c->st));

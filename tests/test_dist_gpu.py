@@ -102,6 +102,22 @@ def test_dist_edge_cases():
     _check(run_ranks(_rank_run, 3, 40, e2, ("sv", "auto"), 0), 40, e2, ("sv", "auto"))
 
 
+def test_dist_degree_tail():
+    """A degree >= 2^20 (beyond the dense histogram bins) on a rank: the tail lists of all
+    ranks are gathered for the gate (cc_dist.cu); route, max degree and labels as on one GPU."""
+    leaves = (1 << 20) + 5
+    n = leaves + 100
+    rng = np.random.default_rng(3)
+    star = np.stack([np.full(leaves, 7, np.uint32), np.arange(100, 100 + leaves, dtype=np.uint32)], 1)
+    other = rng.integers(0, 100, size=(300, 2)).astype(np.uint32)
+    e = np.concatenate([star, other])[rng.permutation(leaves + 300)]
+    res = run_ranks(_rank_run, 2, n, e, ("auto",), 0)
+    _check(res, n, e, ("auto",), trace=False)
+    deg = np.bincount(e.ravel(), minlength=n) + np.bincount(e[e[:, 0] == e[:, 1], 0], minlength=n)
+    for r in res:
+        assert r["auto"][3]["max_degree"] == int(deg.max())
+
+
 def test_dist_exclusion_variants():
     """fig:loadbal variants on 2 ranks: same trace as the transcription with that choice."""
     import paper_1607_06156_b200 as cc
