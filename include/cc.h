@@ -126,7 +126,9 @@ typedef struct {
   uint64_t changed;    /* #{p : p_min != p} at the first partition pass        */
   uint64_t changed2;   /* same count at the second partition pass             */
   uint64_t active_min; /* live tuples entering the iteration on the least / most loaded */
-  uint64_t active_max; /* rank (fig:loadbal); = active_in on one GPU        */
+  uint64_t active_max; /* rank (fig:loadbal); = active_in on one GPU.  With
+                          several ranks they are reduced only under CC_FLAG_TRACE (two
+                          extra all-reduces per iteration); otherwise this rank's count */
   double ms;           /* device time of the iteration                                 */
 } cc_iter_stat;
 

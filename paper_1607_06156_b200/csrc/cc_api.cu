@@ -511,7 +511,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     s.temps = h[sv::C_TEMPS];
     s.changed2 = h[sv::C_CHANGED2];
     s.active_min = s.active_max = local_in;
-    if (multi) {  // per-rank load (fig:loadbal): min and max of the live tuples over ranks
+    if (multi && (c->cfg.flags & CC_FLAG_TRACE)) {  // per-rank load (fig:loadbal): min / max over ranks
       uint64_t* mm = c->d_gcur + 2050;
       const uint64_t v2[2] = {local_in, local_in};
       CK(cudaMemcpyAsync(mm, v2, sizeof(v2), cudaMemcpyHostToDevice, c->st));
