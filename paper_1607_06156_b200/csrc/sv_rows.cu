@@ -314,12 +314,22 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     // ---- thread-local scans; the temporary <r,_,r> of line 22 joins VB(r) at the row head
     uint32_t v[RITEMS];
     uint32_t heads = 0;
+    // B: the thread's row heads are consecutive ids, almost always inside one TB word
+    uint32_t tbi = INF, tbw = 0;
 #pragma unroll
     for (int j = 0; j < RITEMS; j++) {
       const uint32_t pk = j ? k[j - 1] : prevk;
       const bool h = k[j] != INF && k[j] != pk;
       heads |= (uint32_t)h << j;
-      v[j] = (!A && h && tbit(TB, k[j])) ? min(p[j], k[j]) : p[j];
+      bool t = false;
+      if (!A && h) {
+        if ((k[j] >> 5) != tbi) {
+          tbi = k[j] >> 5;
+          tbw = __ldg(&TB[tbi]);
+        }
+        t = (tbw >> (k[j] & 31)) & 1u;
+      }
+      v[j] = t ? min(p[j], k[j]) : p[j];
     }
     uint32_t fmn[RITEMS], fmx[RITEMS], bmn[RITEMS], bmx[RITEMS];
     fmn[0] = v[0]; fmx[0] = p[0];
