@@ -171,6 +171,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   const uint64_t world = (uint64_t)c->cfg.world_size;
   TRY(dalloc_t(c, &c->d_edges, m + 1));
   TRY(dalloc_t(c, &c->d_hist, graph::HIST_DENSE));
+  TRY(dalloc_t(c, &c->d_hpairs, graph::HIST_DENSE));
   TRY(dalloc_t(c, &c->d_tail, graph::TAIL_CAP));
   for (int i = 0; i < 2; i++) {
     TRY(dalloc_t(c, &c->d_w[i], c->cap));
@@ -679,14 +680,24 @@ cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs_ou
     const uint64_t dmax = R.max_degree;
     const uint64_t dense_n = std::min<uint64_t>(dmax + 1, graph::HIST_DENSE);
     const uint64_t tail_n = std::min<uint64_t>(c->h_gctr[graph::G_TAIL], graph::TAIL_CAP);
-    CK(cudaMemcpyAsync(c->h_hist, c->d_hist, sizeof(uint32_t) * dense_n, cudaMemcpyDeviceToHost, c->st));
+    // only the non-empty bins cross PCIe (C4: ~2 k of 2^20)
+    uint64_t* npairs = c->d_gctr + graph::G_NUM + 1544 - 1;
+    graph::launch_hist_pairs(c->d_hist, dense_n, c->d_hpairs, npairs, c->st);
+    c->launches += 1;
+    uint64_t np = 0;
+    CK(cudaMemcpyAsync(&np, npairs, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
     if (tail_n)
       CK(cudaMemcpyAsync(c->h_hist + graph::HIST_DENSE, c->d_tail, sizeof(uint32_t) * tail_n,
                          cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    std::vector<uint2> pairs(np);
+    if (np) {
+      CK(cudaMemcpyAsync(pairs.data(), c->d_hpairs, sizeof(uint2) * np, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+    }
+    std::sort(pairs.begin(), pairs.end(), [](const uint2& a, const uint2& b) { return a.x < b.x; });
     gate::Hist h;
-    for (uint64_t d = 1; d < dense_n; d++)
-      if (c->h_hist[d]) h.push_back({d, c->h_hist[d]});
+    for (const uint2& pr : pairs) h.push_back({pr.x, pr.y});
     if (tail_n) {
       std::vector<uint32_t> t(c->h_hist + graph::HIST_DENSE, c->h_hist + graph::HIST_DENSE + tail_n);
       std::sort(t.begin(), t.end());

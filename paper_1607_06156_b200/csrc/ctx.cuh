@@ -51,6 +51,7 @@ struct cc_ctx {
   uint32_t* d_label = nullptr;
   uint32_t* d_deg = nullptr;
   uint32_t* d_hist = nullptr;
+  uint2* d_hpairs = nullptr;    // non-empty histogram bins (degree, count) for the host gate
   uint32_t* d_tail = nullptr;
   uint32_t* d_bm[3] = {nullptr, nullptr, nullptr};  // visited, frontier, next
   uint32_t* d_sbm[3] = {nullptr, nullptr, nullptr}; // direct SV: notpc, ncp, head
@@ -169,6 +170,7 @@ static inline void dfree_all(cc_ctx* c) {
   c->gbase.clear();
   c->d_pi = nullptr;
   c->d_label = c->d_deg = c->d_hist = c->d_tail = c->d_segA = c->d_segB = nullptr;
+  c->d_hpairs = nullptr;
   c->d_plist[0] = c->d_plist[1] = c->d_nx = nullptr;
   c->d_plcnt = nullptr;
   c->d_umin = c->d_umax = c->d_nlsegs = nullptr;

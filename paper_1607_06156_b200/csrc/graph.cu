@@ -216,6 +216,25 @@ __global__ void __launch_bounds__(BLOCK) k_deg_hist(const uint32_t* __restrict__
     if (best) atomicMax(&gctr[G_MAXKEY], best);
   }
 }
+// non-empty dense bins as (degree, count) pairs (unordered): only these reach the host
+__global__ void k_hist_pairs(const uint32_t* __restrict__ hist, uint64_t nb, uint2* __restrict__ out,
+                             unsigned long long* cnt) {
+  for (uint64_t b0 = blockIdx.x * (uint64_t)BLOCK; b0 < nb; b0 += (uint64_t)gridDim.x * BLOCK) {
+    const uint64_t d = b0 + threadIdx.x;
+    const uint32_t c = (d < nb && d > 0) ? hist[d] : 0u;
+    const uint32_t mask = __ballot_sync(0xffffffffu, c != 0);
+    if (!mask) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(cnt, (unsigned long long)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (c) out[base + __popc(mask & ((1u << lane) - 1u))] = make_uint2((uint32_t)d, c);
+  }
+}
+void launch_hist_pairs(const uint32_t* hist, uint64_t nb, uint2* out, uint64_t* cnt, cudaStream_t st) {
+  cudaMemsetAsync(cnt, 0, sizeof(uint64_t), st);
+  if (nb) k_hist_pairs<<<grid_for(nb, 148 * 4), BLOCK, 0, st>>>(hist, nb, out, reinterpret_cast<unsigned long long*>(cnt));
+}
 void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* tail,
                      uint64_t* gctr, cudaStream_t st, uint64_t base) {
   if (!n) return;

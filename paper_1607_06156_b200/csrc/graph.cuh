@@ -27,6 +27,8 @@ void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr,
 void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
                    uint32_t* hub_scratch = nullptr, uint64_t* hub_count = nullptr);
 // deg[0, n) are the degrees of ids base .. base+n-1 (base > 0: a rank's vertex block)
+// the non-empty bins of hist[1, nb) as (degree, count) pairs into out, *cnt of them (unordered)
+void launch_hist_pairs(const uint32_t* hist, uint64_t nb, uint2* out, uint64_t* cnt, cudaStream_t st);
 void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* tail,
                      uint64_t* gctr, cudaStream_t st, uint64_t base = 0);
 // edge-streaming BFS level over 2-bit vertex state S (16 ids per word: bit0 visited, bit1
