@@ -49,7 +49,7 @@ static unsigned grid(uint64_t work, unsigned per_block, unsigned cap) {
 // cnt[v] = |VB_0(v)| = deg(v) + 1 for present v (the vertex tuple <v,_,v> + one tuple per
 // arc into v), 0 otherwise.  Exclusive scan -> off[v]; cur[v] = off[v] + 1 is the next
 // free slot for arcs.  Tile = B*8 vertices, single pass with decoupled look-back.
-constexpr int SITEMS = 8;
+constexpr int SITEMS = 16;  // vertices per thread of k_rows (tiles of 4096: half the look-back chain of 8)
 __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
                                             const uint32_t* __restrict__ vis, uint64_t n,
                                             uint32_t* __restrict__ off, uint32_t* __restrict__ cur,
@@ -65,11 +65,13 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
   const uint64_t v0 = tile * (B * SITEMS) + (uint64_t)threadIdx.x * SITEMS;
   uint32_t c[SITEMS];
   uint32_t sum = 0;
-  const bool full = v0 + SITEMS <= n;  // 8 vertices: two 16-byte loads, one bitmap byte
+  const bool full = v0 + SITEMS <= n;  // 16-byte loads; the vertices' bits in one bitmap word
   if (full) {
-    const uint4 a = reinterpret_cast<const uint4*>(deg + v0)[0];
-    const uint4 b = reinterpret_cast<const uint4*>(deg + v0)[1];
-    c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+#pragma unroll
+    for (int q = 0; q < SITEMS / 4; q++) {
+      const uint4 a = reinterpret_cast<const uint4*>(deg + v0)[q];
+      c[4 * q] = a.x; c[4 * q + 1] = a.y; c[4 * q + 2] = a.z; c[4 * q + 3] = a.w;
+    }
   }
   const uint32_t vb = vis ? (vis[v0 >> 5] >> (v0 & 31)) : 0u;
 #pragma unroll
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
   const uint32_t excl = block_excl_scan<B>(sum, s_scan, &tot);
   const uint64_t pref = scan::tile_prefix(flags, tile, tot, epoch, &s_pref);
   // arcs of this tile (tuples minus vertex tuples) for the CSR bucket pass; a tile of
-  // B*SITEMS = 2^11 vertices lies inside one group of 2^gshift vertices (gshift >= 11)
+  // B*SITEMS = 2^12 vertices lies inside one group of 2^gshift vertices (gshift >= 12)
   if (count_groups) {
     uint32_t nv = 0;
 #pragma unroll
@@ -102,10 +104,12 @@ __global__ void __launch_bounds__(B) k_rows(const uint32_t* __restrict__ deg,
     run += c[k];
   }
   if (full) {
-    reinterpret_cast<uint4*>(off + v0)[0] = make_uint4(o[0], o[1], o[2], o[3]);
-    reinterpret_cast<uint4*>(off + v0)[1] = make_uint4(o[4], o[5], o[6], o[7]);
-    reinterpret_cast<uint4*>(cur + v0)[0] = make_uint4(o[0] + 1, o[1] + 1, o[2] + 1, o[3] + 1);
-    reinterpret_cast<uint4*>(cur + v0)[1] = make_uint4(o[4] + 1, o[5] + 1, o[6] + 1, o[7] + 1);
+#pragma unroll
+    for (int q = 0; q < SITEMS / 4; q++) {
+      reinterpret_cast<uint4*>(off + v0)[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      reinterpret_cast<uint4*>(cur + v0)[q] =
+          make_uint4(o[4 * q] + 1, o[4 * q + 1] + 1, o[4 * q + 2] + 1, o[4 * q + 3] + 1);
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < SITEMS; k++)
@@ -479,14 +483,14 @@ int group_shift(uint64_t n, uint64_t tuples) {
   int lg = 0;  // log2 G: about 2M tuples per group
   while (lg < 10 && (tuples >> (21 + lg)) > 0) lg++;
   int gs = kb - lg;
-  return gs < 11 ? 11 : gs;
+  return gs < 12 ? 12 : gs;  // a k_rows tile (2^12 vertices) lies inside one group
 }
 
 int group_shift_full(uint64_t n) {
   int kb = 0;
   while ((1ull << kb) < n) kb++;
   if (kb > 26) return -1;  // more than MAXG groups of 2^15 ids: use graph::launch_degree
-  return kb - 11 < 11 ? 11 : kb - 11;
+  return kb - 11 < 12 ? 12 : kb - 11;
 }
 
 void build(const uint2* edges, uint64_t m, const uint32_t* deg, const uint32_t* vis, uint64_t n,
