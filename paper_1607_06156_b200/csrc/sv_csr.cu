@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(B) k_place(const uint32_t* __restrict__ off, u
   const uint64_t s = blockIdx.x, v0 = s << SUBG;
   const uint32_t cnt = (uint32_t)min((uint64_t)1 << SUBG, n - v0);
   const uint32_t base0 = off[v0], T = off[v0 + cnt] - base0;
+  if (T == 0) return;  // no rows here (e.g. the small remainder after a BFS peel)
   const bool staged = T <= (uint32_t)PLACE_CAP;  // else rows are written in place
   if (threadIdx.x == 0) s_nlong = 0;
   for (uint32_t l = threadIdx.x; l <= cnt; l += B) s_off[l] = off[v0 + l] - base0;
