@@ -24,16 +24,21 @@
 // be completed-but-for-this-row; NCP(m) is the paper's "not all tuples potentially
 // completed" for exactly the partitions where it decides.
 //
-// Work split.  A block stages a 2048-tuple tile (8 per thread) in shared memory after the
-// relabel; thread t owns the rows whose head lies in its 8-tuple slice and walks each of them
-// (into the next tile through global memory when the row crosses the tile edge), so every
-// row is reduced and applied by exactly one thread with no cross-thread combine.  Rows longer
-// than LONG tuples (hubs) would serialise a warp; they are listed once per compaction as
-// segments of at most LSEG tuples and handled by warps in two small kernels (segment partials
-// into epoch-tagged 64-bit slots whose newer tags always win the atomic, then the apply).
-// Partition slots PA/PB are n-sized u32 arrays that stay resident in L2; each block filters
-// its slot updates through a shared-memory cache of values it has already pushed (slots only
-// decrease), so a partition shared by millions of tuples costs one atomic per block.
+// Work split.  A persistent block stages 2048-tuple tiles (8 per thread) in shared memory by
+// TMA, together with R[t0-4, t0) and the 32 tuples past the tile; run minima are branch-free
+// segmented scans (thread, warp, block), and a row that continues past the tile edge is
+// finished by the tile that holds its head (the last warp reads the extension), so every row
+// is reduced and applied by exactly one block.  Rows longer than LONG tuples (hubs) are
+// listed once per compaction as segments of at most LSEG tuples and handled by warps in two
+// small kernels (segment partials into epoch-tagged 64-bit slots whose newer tags always win
+// the atomic, then the apply).  Partition slots PA/PB are n-sized u32 arrays; only slots of
+// the iteration's partition list are ever written (k_pstat1/k_pstat2/k_list_from_bits keep
+// them clean), updates q = p are skipped (PA preset / k_pstat2's temporary fold), and in hot
+// iterations (few partitions per live tuple) each block min-reduces its updates in a
+// shared-memory table first.  Every pass is compiled per (pass, hot, relabel, preset/
+// exclusion) so each variant carries only its own code and shared memory; with the previous
+// iteration's counters (prevctr) both hot variants are launched and the device runs one,
+// which lets the host enqueue the next iteration before reading the counters.
 #include <algorithm>
 
 #include "csr.cuh"
