@@ -17,3 +17,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 $CMD > gpurun_out/${TAG}_plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k "regex:${NCU_KERNELS:-k_rowpass|k_pstat1|k_place|k_bucket2}" -s ${NCU_SKIP:-60} -c ${NCU_COUNT:-8} \
   -o gpurun_out/${TAG}_full_c2 $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
+# kernel timelines (CUPTI), DRAM traffic per row-pass launch, L2 request rates
+python scripts/timeline.py --out gpurun_out/${TAG}_tl_c2.json > /dev/null 2>&1
+python scripts/timeline.py --config c4 --out gpurun_out/${TAG}_tl_c4.json > /dev/null 2>&1
+python scripts/traffic.py > gpurun_out/${TAG}_traffic.log 2>&1; cp profiles/traffic.json gpurun_out/${TAG}_traffic.json
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_requests_op_red.sum,lts__t_requests_op_red_lookup_hit.sum,lts__t_requests_op_atom.sum,lts__t_requests_op_read.sum,lts__t_sectors_op_read.sum"
+ncu --metrics $M --clock-control none --csv -k 'regex:k_rowpass' -s 84 -c 28 python scripts/timeline.py --out gpurun_out/l2x.json > gpurun_out/${TAG}_l2_c2.csv 2>/dev/null
+echo "extras done"
