@@ -459,9 +459,9 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
         if (A) {
           // many non-PC rows share one minimum late in the run: filter through a block cache
           // and a read of the word before the atomic
-          if (q != x && q != last_nc) {
+          if (q != x && (HOT || q != last_nc)) {  // hot: the block cache filters repeats
             push_bit(NCPw, s_nc, q, HOT);
-            last_nc = q;
+            if (!HOT) last_nc = q;
           }
         } else if (q != k[j] && tbit(TB, k[j])) {  // q = r: k_pstat2's fold covers it
           atomicMin(&OUT[k[j]], q);
