@@ -196,6 +196,23 @@ cc_status cc_labels_u32(cc_ctx* ctx, uint32_t* out, uint64_t cap, uint64_t* coun
 cc_status cc_labels_u64(cc_ctx* ctx, uint64_t* ids, uint64_t* labels, uint64_t cap,
                         uint64_t* count, int out_on_device);
 
+/* The degree distribution D of the last cc_run (Alg. 2 line 2): the
+ * non-empty bins (d, D[d]), d >= 1 ascending, with D[d] = #{v : deg(v) = d} and deg(v) = arcs
+ * with source v (a self-loop counts 2) -- exactly the input the power-law
+ * gate (line 3) was fitted on.  Summed over all ranks when world_size > 1.  `degrees` and
+ * `counts` (host) have room for `cap` bins; *count receives the bin count.  CC_ERR_STATE if the
+ * last cc_run did not build it (it does in CC_MODE_AUTO or under CC_FLAG_TRACE);
+ * CC_ERR_INVALID if cap is smaller. */
+cc_status cc_degree_histogram(cc_ctx* ctx, uint64_t* degrees, uint64_t* counts, uint64_t cap,
+                              uint64_t* count);
+
+/* deg(v) for every id v in [0, n) (Alg. 2 line 2; same kernels and dispatch as the prediction
+ * stage of cc_run) into `out` (room for `cap`, host or device per out_on_device); *count = n.
+ * u32 graphs on one GPU (CC_ERR_INVALID otherwise); CC_ERR_STATE before cc_load_edges.  Uses
+ * the context's tuple scratch: labels of an earlier cc_run are invalidated (CC_ERR_STATE from
+ * cc_labels_* until the next cc_run). */
+cc_status cc_degrees_u32(cc_ctx* ctx, uint32_t* out, uint64_t cap, uint64_t* count, int out_on_device);
+
 /* Multi-GPU (world_size > 1): rank k owns the vertex block [k*B, min((k+1)*B, n)) with
  * B = 32*ceil(n / (32*world_size)) -- its CSR rows (owner-computes) and its
  * labels.  Writes the block of this rank (lo = 0, hi = n on one GPU). */

@@ -87,6 +87,7 @@ class cc_report(ctypes.Structure):
 
 EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
            "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_radix_sort_pairs",
+           "cc_degree_histogram", "cc_degrees_u32",
            "cc_set_profiling", "cc_last_launch_count",
            "cc_kernel_stats",
            "cc_kernel_name", "cc_destroy", "cc_status_string", "cc_last_error"]
@@ -110,6 +111,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_labels_u64.argtypes = [P, P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     lib.cc_labels_device.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_uint64)]
     lib.cc_block_range.argtypes = [P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+    lib.cc_degree_histogram.argtypes = [P, P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+    lib.cc_degrees_u32.argtypes = [P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     lib.cc_bfs_eccentricity.argtypes = [P, P, ctypes.c_uint32, P]
     lib.cc_radix_sort_pairs.argtypes = [P, P, P, P, ctypes.c_uint64, ctypes.c_int, P]
     lib.cc_radix_sort_pairs.restype = ctypes.c_int
@@ -124,7 +127,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_kernel_name.argtypes = [ctypes.c_int]
     for f in ("cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
               "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_kernel_stats",
-              "cc_destroy"):
+              "cc_destroy", "cc_degree_histogram", "cc_degrees_u32"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -285,12 +288,17 @@ def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=Non
 
 
 def cc_load_edges(ctx, pairs, n_vertices, ids="u32"):
-    """pairs: (m,2) uint32 numpy array (host) or torch CUDA tensor (device)."""
-    if ids != "u32":
-        w = CC_U64
-    else:
-        w = CC_U32
+    """pairs: (m,2) array of ids -- numpy (host; converted to uint32 / uint64) or a torch CUDA
+    tensor (device; 4-byte elements for ids='u32', 8-byte for 'u64', passed as is)."""
+    if ids not in ("u32", "u64"):
+        raise ValueError(f"ids must be 'u32' or 'u64', not {ids!r}")
+    w = CC_U32 if ids == "u32" else CC_U64
     if hasattr(pairs, "is_cuda") and pairs.is_cuda:
+        if pairs.dim() != 2 or pairs.shape[1] != 2:
+            raise ValueError(f"device edge tensor must have shape (m, 2), not {tuple(pairs.shape)}")
+        want = 4 if w == CC_U32 else 8
+        if pairs.element_size() != want or pairs.is_floating_point():
+            raise ValueError(f"ids={ids!r} needs {want}-byte integer elements, got {pairs.dtype}")
         t = pairs.contiguous()
         m = t.shape[0]
         _check(ctx, lib().cc_load_edges(ctx, w, ctypes.c_void_p(t.data_ptr()), m, n_vertices, 1))
@@ -322,9 +330,13 @@ def cc_labels_u32(ctx, out=None):
     if out is None:
         out = np.empty(n, dtype=np.uint32)
     if hasattr(out, "is_cuda") and out.is_cuda:
+        if out.element_size() != 4 or out.is_floating_point() or not out.is_contiguous():
+            raise ValueError(f"label output must be a contiguous 4-byte integer tensor, got {out.dtype}")
         _check(ctx, lib().cc_labels_u32(ctx, ctypes.c_void_p(out.data_ptr()), out.numel(),
                                         ctypes.byref(cnt), 1))
     else:
+        if out.dtype.itemsize != 4 or out.dtype.kind not in "iu" or not out.flags.c_contiguous:
+            raise ValueError(f"label output must be a contiguous 4-byte integer array, got {out.dtype}")
         _check(ctx, lib().cc_labels_u32(ctx, out.ctypes.data_as(ctypes.c_void_p), out.shape[0],
                                         ctypes.byref(cnt), 0))
     return out
@@ -340,6 +352,27 @@ def cc_labels_u64(ctx):
     _check(ctx, lib().cc_labels_u64(ctx, ids.ctypes.data_as(ctypes.c_void_p),
                                     lab.ctypes.data_as(ctypes.c_void_p), n, ctypes.byref(cnt), 0))
     return ids, lab
+
+
+def cc_degree_histogram(ctx):
+    """The degree distribution the gate consumed in the last cc_run: (degrees, counts) numpy
+    uint64 arrays of the non-empty bins, ascending."""
+    cnt = ctypes.c_uint64()
+    lib().cc_degree_histogram(ctx, None, None, 0, ctypes.byref(cnt))  # query the bin count
+    nb = cnt.value
+    d = np.zeros(nb, dtype=np.uint64)
+    c = np.zeros(nb, dtype=np.uint64)
+    _check(ctx, lib().cc_degree_histogram(ctx, d.ctypes.data_as(ctypes.c_void_p),
+                                          c.ctypes.data_as(ctypes.c_void_p), nb, ctypes.byref(cnt)))
+    return d, c
+
+
+def cc_degrees_u32(ctx, n):
+    """deg(v) for v in [0, n) as a numpy uint32 array (the prediction-stage count)."""
+    out = np.empty(n, dtype=np.uint32)
+    cnt = ctypes.c_uint64()
+    _check(ctx, lib().cc_degrees_u32(ctx, out.ctypes.data_as(ctypes.c_void_p), n, ctypes.byref(cnt), 0))
+    return out
 
 
 def cc_block_range(ctx):
@@ -420,6 +453,12 @@ class CC:
 
     def block_range(self):
         return cc_block_range(self.ctx)
+
+    def degree_histogram(self):
+        return cc_degree_histogram(self.ctx)
+
+    def degrees(self, n):
+        return cc_degrees_u32(self.ctx, n)
 
     def labels_u64(self):
         return cc_labels_u64(self.ctx)

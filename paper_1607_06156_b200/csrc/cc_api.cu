@@ -670,6 +670,8 @@ static cc_status run_sv(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint
 cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs_out, uint64_t* root) {
   cc_report& R = c->rep;
   TRY(sync_read(c));
+  c->dhist.clear();
+  c->dhist_valid = want_hist;  // an all-isolated graph has the empty distribution
   R.n_present = c->h_gctr[graph::G_NPRESENT];
   const uint64_t maxkey = c->h_gctr[graph::G_MAXKEY];
   R.max_degree = maxkey >> 32;
@@ -708,6 +710,8 @@ cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs_ou
         i = j;
       }
     }
+    c->dhist = h;
+    c->dhist_valid = true;
     gate::LsFit g = gate::fit_ls(h);
     R.ls_alpha = g.alpha;
     R.ls_r2 = g.r2;
@@ -906,7 +910,9 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
       k.end(8.0 * m + 8.0 * m + 16.0 * m + 16.0 * m + 4.0 * n, 4);
     } else {
       CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
-      graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail, c->d_gctr + graph::G_NUM + 64);
+      // scratch: tuple buffer 1 (8 cap >= 16m + 16n bytes) is free until the SV / CSR stages
+      graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail, c->d_gctr + graph::G_NUM + 64,
+                           c->d_w[1], sizeof(uint64_t) * c->cap, c->d_garc);
       k.end(8.0 * m + 4.0 * n, 1);
     }
   }
@@ -1115,6 +1121,44 @@ extern "C" cc_status cc_labels_u64(cc_ctx* c, uint64_t* ids, uint64_t* labels, u
     CK(cudaMemcpyAsync(ids, c->d_uids, sizeof(uint64_t) * c->n, k, c->st));
     CK(cudaMemcpyAsync(labels, tmp, sizeof(uint64_t) * c->n, k, c->st));
   }
+  CK(cudaStreamSynchronize(c->st));
+  return CC_OK;
+}
+
+extern "C" cc_status cc_degree_histogram(cc_ctx* c, uint64_t* degrees, uint64_t* counts, uint64_t cap,
+                                         uint64_t* count) {
+  if (!c) return CC_ERR_INVALID;
+  if (!c->ran || !c->dhist_valid)
+    return fail(c, CC_ERR_STATE, "no degree distribution: cc_run(AUTO) or CC_FLAG_TRACE first");
+  const uint64_t nb = c->dhist.size();
+  if (count) *count = nb;
+  if (!degrees || !counts || cap < nb) return fail(c, CC_ERR_INVALID, "output buffers too small");
+  for (uint64_t i = 0; i < nb; i++) {
+    degrees[i] = c->dhist[i].first;
+    counts[i] = c->dhist[i].second;
+  }
+  return CC_OK;
+}
+
+extern "C" cc_status cc_degrees_u32(cc_ctx* c, uint32_t* out, uint64_t cap, uint64_t* count,
+                                    int out_on_device) {
+  if (!c) return CC_ERR_INVALID;
+  if (!c->loaded) return fail(c, CC_ERR_STATE, "cc_degrees_u32 before cc_load_edges");
+  if (c->idw != CC_U32 || multi_gpu(c))
+    return fail(c, CC_ERR_INVALID, "cc_degrees_u32: u32 ids on one GPU only");
+  const uint64_t n = c->n, m = c->m;
+  if (count) *count = n;
+  if (!out || cap < n) return fail(c, CC_ERR_INVALID, "output buffer too small");
+  CK(cudaSetDevice(c->cfg.device));
+  // the prediction stage's count (Alg. 2 line 2), same kernels and dispatch as cc_run
+  CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
+  graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail, c->d_gctr + graph::G_NUM + 64,
+                       c->d_w[1], sizeof(uint64_t) * c->cap, c->d_garc);
+  CKL();
+  c->ran = false;  // tuple buffer 1 was scratch: labels need a new cc_run
+  if (n)
+    CK(cudaMemcpyAsync(out, c->d_deg, sizeof(uint32_t) * n,
+                       out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   return CC_OK;
 }

@@ -92,6 +92,8 @@ struct cc_ctx {
   scan::State ss;
   std::vector<std::pair<void*, size_t>> allocs;
   // report
+  std::vector<std::pair<uint64_t, uint64_t>> dhist;  // gate input of the last cc_run: (degree, count)
+  bool dhist_valid = false;
   std::vector<cc_iter_stat> iters;
   cc_report rep{};
   uint64_t launches = 0;

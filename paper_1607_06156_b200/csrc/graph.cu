@@ -104,6 +104,8 @@ __global__ void k_degree(const uint4* __restrict__ e2, uint64_t m, uint32_t* __r
       if (s_cnt[i]) atomicAdd(&deg[s_key[i]], s_cnt[i]);
   }
 }
+bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, void* scratch,
+                         uint64_t scratch_bytes, uint32_t* cursor, cudaStream_t st);
 // histogram of floor(log2(sample count)) over ids with count >= HUB_MIN (picks the threshold
 // that keeps the hubs within HUB_CAP: the largest ones)
 __global__ void k_hub_hist(const uint32_t* __restrict__ deg, uint64_t n, unsigned long long* bins) {
@@ -127,9 +129,18 @@ __global__ void k_hubs(const uint32_t* __restrict__ deg, uint64_t n, uint32_t t,
     }
 }
 void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
-                   uint32_t* hub_scratch, uint64_t* hub_count) {
+                   uint32_t* hub_scratch, uint64_t* hub_count, void* radix_scratch,
+                   uint64_t radix_bytes, uint32_t* radix_cursor) {
   // hub_count[0]: hub count; hub_count[8 .. 40): log2 histogram of the sample counts
   if (!m) return;
+  {
+    // bucketed shared-memory count (default for n >= 2^20); CC_DEG_ALGO=radix|window forces one
+    const char* e = getenv("CC_DEG_ALGO");
+    const bool force_radix = e && e[0] == 'r', force_window = e && e[0] == 'w';
+    if (radix_scratch && !force_window && (force_radix || n >= (1ull << 20)) &&
+        launch_degree_radix(edges, m, n, deg, radix_scratch, radix_bytes, radix_cursor, st))
+      return;
+  }
   static uint64_t window = 0;
   if (!window) {  // CC_DEG_WINDOW_LOG2: experiment hook for the counter window
     const char* e = getenv("CC_DEG_WINDOW_LOG2");
@@ -167,6 +178,185 @@ void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cu
       k_degree<false><<<grid_for((mr >> 1) + 1, 148 * 16), BLOCK, 0, st>>>(
           reinterpret_cast<const uint4*>(edges + m0), mr, deg, (uint32_t)lo, (uint32_t)hi, nullptr, nullptr);
   }
+}
+
+// ---------------------------------------------------------------- degrees, bucketed
+// The same count with shared-memory counters instead of L2 increments.  A random 4-byte
+// increment costs one L2 request whichever way it is issued (the L2-resident ceiling measured
+// by scripts/micro/l2_peaks.cu is ~195 G/s on this B200), while a shared-memory atomicAdd at a
+// random slot runs at ~1.45 T/s.  So the endpoints are first bucketed by id >> 15 (<= 2048
+// buckets of 2^15 ids: the counters of one bucket fill 128 KB of shared memory), then each
+// bucket is counted by one block in shared memory:
+//   k_deg_part  : streams the edge list once; every endpoint claims a slot in its bucket's
+//                 32-entry shared-memory staging row (shared atomic); after each round of
+//                 8192 endpoints the rows holding >= 16 entries are written out as whole
+//                 32-byte sectors (u16: the id's low 15 bits) to the bucket's region, whose
+//                 cursor is one global atomic per sector.  A staging row that is full, or a
+//                 region that is full (capacity 2x the mean bucket), sends the endpoint
+//                 straight to deg with an L2 increment: exact on any degree distribution,
+//                 only slower on a pathological one.
+//   k_deg_count : one block per (bucket, slice of 2^21 entries) counts its entries in
+//                 shared memory and adds the counts to deg (plain read-add-write when the
+//                 bucket is one slice, an L2 increment per non-zero counter otherwise).
+// Traffic: 8m (edges) + 4m (u16 entries out) + 4m (in) + 8n (deg read + write) bytes, against
+// 8m per 2^24-id window (4 windows on C4) for the L2-increment count above.  Ids beyond 2^26
+// are handled in super-windows of 2^26 ids (one edge-list pass each).
+constexpr int DR_SPAN = 15;                       // ids per bucket: 2^15
+constexpr uint32_t DR_NB = 2048;                  // buckets per super-window (2^26 ids)
+constexpr int DR_CAP = 32;                        // staging entries per bucket (u16)
+constexpr int DR_THREADS = 1024;
+constexpr int DR_VEC = 2;                         // uint4 (two edges) per thread per round
+constexpr uint64_t DR_SLICE = 1ull << 21;         // entries per counting block
+__global__ void __launch_bounds__(DR_THREADS, 1)
+k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo, uint32_t nbk,
+           uint16_t* __restrict__ region, uint32_t C, uint32_t* __restrict__ cursor,
+           uint32_t* __restrict__ deg) {
+  extern __shared__ __align__(16) uint8_t dr_smem[];
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(dr_smem);                        // [DR_NB]
+  uint16_t* s_buf = reinterpret_cast<uint16_t*>(dr_smem + DR_NB * sizeof(uint32_t));  // [DR_NB][DR_CAP]
+  for (uint32_t b = threadIdx.x; b < DR_NB; b += DR_THREADS) s_cnt[b] = 0;
+  __syncthreads();
+  const uint64_t npair = m >> 1;  // uint4 = two edges
+  const uint64_t per_round = (uint64_t)DR_THREADS * DR_VEC;
+  const uint64_t rounds = (npair + 1 + per_round - 1) / per_round;  // +1: the odd last edge
+  const uint32_t span_end = nbk << DR_SPAN;
+  auto insert = [&](uint32_t v) {
+    const uint32_t x = v - lo;
+    if (x >= span_end) return;
+    const uint32_t b = x >> DR_SPAN;
+    const uint32_t slot = atomicAdd(&s_cnt[b], 1u);
+    if (slot < DR_CAP) s_buf[b * DR_CAP + slot] = (uint16_t)(x & ((1u << DR_SPAN) - 1));
+    else atomicAdd(&deg[v], 1u);  // staging row full this round
+  };
+  for (uint64_t r = blockIdx.x; r < rounds; r += gridDim.x) {
+    const uint64_t i0 = r * per_round + threadIdx.x;
+    uint4 x[DR_VEC];
+    bool ok[DR_VEC];
+#pragma unroll
+    for (int j = 0; j < DR_VEC; j++) {
+      const uint64_t i = i0 + (uint64_t)j * DR_THREADS;
+      ok[j] = i < npair;
+      if (ok[j]) x[j] = ldg_stream(&e2[i]);
+    }
+#pragma unroll
+    for (int j = 0; j < DR_VEC; j++)
+      if (ok[j]) {
+        insert(x[j].x); insert(x[j].y); insert(x[j].z); insert(x[j].w);
+      }
+#pragma unroll
+    for (int j = 0; j < DR_VEC; j++)
+      if ((m & 1) && i0 + (uint64_t)j * DR_THREADS == npair) {  // last edge of an odd-length list
+        const uint2 t = reinterpret_cast<const uint2*>(e2)[m - 1];
+        insert(t.x); insert(t.y);
+      }
+    __syncthreads();
+    // write out whole 16-entry (32-byte) groups of every staging row
+    for (uint32_t b = threadIdx.x; b < DR_NB; b += DR_THREADS) {
+      const uint32_t c = min(s_cnt[b], (uint32_t)DR_CAP);
+      if (c < 16) {
+        s_cnt[b] = c;
+        continue;
+      }
+      const uint32_t nf = c & ~15u;  // 16 or 32
+      uint4* row = reinterpret_cast<uint4*>(s_buf + b * DR_CAP);
+      const uint32_t pos = atomicAdd(&cursor[b], nf);
+      const uint32_t fit = pos >= C ? 0u : min(nf, C - pos);  // multiple of 16
+      uint4* dst = reinterpret_cast<uint4*>(region + (uint64_t)b * C + pos);
+      for (uint32_t k = 0; k < fit / 8; k++) dst[k] = row[k];
+      for (uint32_t k = fit; k < nf; k++)  // region full: count directly
+        atomicAdd(&deg[lo + (b << DR_SPAN) + s_buf[b * DR_CAP + k]], 1u);
+      if (nf == 16) {  // keep the remaining c - 16 (< 16) entries at the row start
+        row[0] = row[2];
+        row[1] = row[3];
+      }
+      s_cnt[b] = c - nf;
+    }
+    __syncthreads();
+  }
+  // staged leftovers (< 16 per bucket): count directly
+  for (uint32_t b = threadIdx.x; b < DR_NB; b += DR_THREADS) {
+    const uint32_t c = s_cnt[b];
+    for (uint32_t k = 0; k < c; k++) atomicAdd(&deg[lo + (b << DR_SPAN) + s_buf[b * DR_CAP + k]], 1u);
+  }
+}
+__global__ void __launch_bounds__(DR_THREADS, 1)
+k_deg_count(const uint16_t* __restrict__ region, uint32_t C, const uint32_t* __restrict__ cursor,
+            uint32_t nbk, uint32_t lo, uint64_t n, uint32_t* __restrict__ deg) {
+  extern __shared__ __align__(16) uint8_t dr_smem[];
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(dr_smem);  // [2^DR_SPAN]
+  const uint32_t b = blockIdx.x % nbk, s = blockIdx.x / nbk;
+  const uint64_t fill = min(cursor[b], C);
+  const uint64_t e0 = (uint64_t)s * DR_SLICE;
+  if (e0 >= fill) return;
+  const uint64_t e1 = min(fill, e0 + DR_SLICE);
+  for (uint32_t i = threadIdx.x; i < (1u << DR_SPAN); i += DR_THREADS) s_cnt[i] = 0;
+  __syncthreads();
+  // entries of one bucket: 16-byte vectors (8 u16), fill is a multiple of 16
+  const uint4* src = reinterpret_cast<const uint4*>(region + (uint64_t)b * C + e0);
+  const uint32_t nv = (uint32_t)((e1 - e0) >> 3);
+  constexpr int U = 4;
+  for (uint32_t k0 = threadIdx.x; k0 < nv; k0 += DR_THREADS * U) {
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (k0 + u * DR_THREADS < nv) x[u] = ldg_stream(src + k0 + u * DR_THREADS);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (k0 + u * DR_THREADS < nv) {
+        const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+          atomicAdd(&s_cnt[w[h] & 0xFFFFu], 1u);
+          atomicAdd(&s_cnt[w[h] >> 16], 1u);
+        }
+      }
+  }
+  __syncthreads();
+  const bool single = fill <= DR_SLICE;
+  const uint64_t base = (uint64_t)lo + ((uint64_t)b << DR_SPAN);
+  for (uint32_t i = threadIdx.x; i < (1u << DR_SPAN); i += DR_THREADS) {
+    const uint32_t c = s_cnt[i];
+    if (!c || base + i >= n) continue;
+    if (single) deg[base + i] += c;
+    else atomicAdd(&deg[base + i], c);
+  }
+}
+uint64_t degree_radix_scratch(uint64_t m, uint64_t n) {
+  // bytes of region scratch launch_degree_radix needs (u16 entries)
+  const uint64_t nb_all = (n + (1u << DR_SPAN) - 1) >> DR_SPAN;
+  const uint64_t nbk = std::min<uint64_t>(nb_all, DR_NB);
+  const uint64_t mean = nb_all ? (2 * m + nb_all - 1) / nb_all : 0;
+  const uint64_t C = ((2 * mean + 1024) + 31) & ~31ull;
+  return nbk * C * sizeof(uint16_t);
+}
+bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, void* scratch,
+                         uint64_t scratch_bytes, uint32_t* cursor, cudaStream_t st) {
+  if (!m || !n) return true;
+  const uint64_t nb_all = (n + (1u << DR_SPAN) - 1) >> DR_SPAN;
+  const uint64_t nbk = std::min<uint64_t>(nb_all, DR_NB);
+  const uint64_t mean = (2 * m + nb_all - 1) / nb_all;
+  const uint64_t C = ((2 * mean + 1024) + 31) & ~31ull;
+  if (C >= (1ull << 31) || nbk * C * sizeof(uint16_t) > scratch_bytes) return false;
+  static bool attr = false;
+  const int smem_part = DR_NB * sizeof(uint32_t) + DR_NB * DR_CAP * sizeof(uint16_t);
+  const int smem_count = (1 << DR_SPAN) * sizeof(uint32_t);
+  if (!attr) {
+    cudaFuncSetAttribute(k_deg_part, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_part);
+    cudaFuncSetAttribute(k_deg_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_count);
+    attr = true;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const uint64_t slices = (C + DR_SLICE - 1) / DR_SLICE;
+  for (uint64_t lo = 0; lo < n; lo += (uint64_t)DR_NB << DR_SPAN) {
+    const uint32_t nb = (uint32_t)std::min<uint64_t>(DR_NB, (n - lo + (1u << DR_SPAN) - 1) >> DR_SPAN);
+    cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * DR_NB, st);
+    k_deg_part<<<sms, DR_THREADS, smem_part, st>>>(reinterpret_cast<const uint4*>(edges), m, (uint32_t)lo, nb,
+                                                   reinterpret_cast<uint16_t*>(scratch), (uint32_t)C, cursor, deg);
+    k_deg_count<<<(unsigned)(nb * slices), DR_THREADS, smem_count, st>>>(
+        reinterpret_cast<const uint16_t*>(scratch), (uint32_t)C, cursor, nb, (uint32_t)lo, n, deg);
+  }
+  return true;
 }
 
 // Degree distribution D[d] = #{v : deg(v) = d}, d >= 1 (C10), plus n_present and the
