@@ -184,126 +184,215 @@ void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cu
 // The same count with shared-memory counters instead of L2 increments.  A random 4-byte
 // increment costs one L2 request whichever way it is issued (the L2-resident ceiling measured
 // by scripts/micro/l2_peaks.cu is ~195 G/s on this B200), while a shared-memory atomicAdd at a
-// random slot runs at ~1.45 T/s.  So the endpoints are first bucketed by id >> 15 (<= 2048
-// buckets of 2^15 ids: the counters of one bucket fill 128 KB of shared memory), then each
-// bucket is counted by one block in shared memory:
-//   k_deg_part  : streams the edge list once; every endpoint claims a slot in its bucket's
-//                 32-entry shared-memory staging row (shared atomic); after each round of
-//                 8192 endpoints the rows holding >= 16 entries are written out as whole
-//                 32-byte sectors (u16: the id's low 15 bits) to the bucket's region, whose
-//                 cursor is one global atomic per sector.  A staging row that is full, or a
-//                 region that is full (capacity 2x the mean bucket), sends the endpoint
-//                 straight to deg with an L2 increment: exact on any degree distribution,
-//                 only slower on a pathological one.
-//   k_deg_count : one block per (bucket, slice of 2^21 entries) counts its entries in
-//                 shared memory and adds the counts to deg (plain read-add-write when the
-//                 bucket is one slice, an L2 increment per non-zero counter otherwise).
+// random slot runs at ~1.45 T/s (scripts/micro/smem_atomics.cu).  So the endpoints are first
+// bucketed by id >> 15 (<= 2048 buckets of 2^15 ids: the counters of one bucket fill 128 KB of
+// shared memory), then each bucket is counted by one block in shared memory:
+//   k_deg_part  : one block per SM streams its share of the edge list (two register sets in
+//                 turn keep the next round's 16-byte loads in flight); every endpoint claims a
+//                 slot in its bucket's 32-entry shared-memory ring (one shared atomic); after
+//                 each round of 8192 endpoints every ring holding >= 16 entries writes one
+//                 32-byte group (u16: the id's low 15 bits) to its bucket's region in HBM.  The
+//                 region is shared by all blocks (so only ~2048 lines are ever partly written
+//                 and the L2 writes whole lines back), and its cursor is reserved one group
+//                 ahead: the thread owning a bucket holds the position of its next group in a
+//                 register, so the global atomic's latency is never waited for.  A full ring or
+//                 region sends the endpoint straight to deg with an L2 increment: exact on any
+//                 degree distribution, only slower on a pathological one.
+//   k_deg_order : buckets by decreasing size (the heaviest are counted first: a hub's bucket
+//                 is long and its same-address shared atomics serialise).
+//   k_deg_count : one block per bucket counts its region in shared memory and adds to deg.
 // Traffic: 8m (edges) + 4m (u16 entries out) + 4m (in) + 8n (deg read + write) bytes, against
 // 8m per 2^24-id window (4 windows on C4) for the L2-increment count above.  Ids beyond 2^26
 // are handled in super-windows of 2^26 ids (one edge-list pass each).
 constexpr int DR_SPAN = 15;                       // ids per bucket: 2^15
 constexpr uint32_t DR_NB = 2048;                  // buckets per super-window (2^26 ids)
-constexpr int DR_CAP = 32;                        // staging entries per bucket (u16)
+constexpr int DR_CAP = 32;                        // ring entries per bucket (u16, 64 B)
 constexpr int DR_THREADS = 1024;
 constexpr int DR_VEC = 2;                         // uint4 (two edges) per thread per round
-constexpr uint64_t DR_SLICE = 1ull << 21;         // entries per counting block
+constexpr uint16_t DR_PAD = 0x8000;               // padding entry (counted into a dummy slot)
+static_assert(DR_NB == 2 * DR_THREADS, "each k_deg_part thread owns two buckets");
+constexpr uint32_t DR_Q = 1024;                   // entries per bucket per epoch of the region layout
+struct DegRadix {
+  uint16_t* reg;    // bucket regions, epoch-interleaved: entry pos of bucket b at dr_addr(b, pos)
+  uint32_t* cur;    // [DR_NB] region cursors (entries reserved)
+  uint32_t* order;  // [DR_NB] buckets by decreasing size
+  uint32_t C;       // region capacity per bucket (entries, a multiple of DR_Q)
+  uint32_t nbk;     // buckets of this super-window
+};
+// Epoch e holds entries [e*DR_Q, (e+1)*DR_Q) of every bucket, side by side: the buckets fill
+// at similar rates, so the blocks' scattered group writes stay within a few MB of address
+// space (TLB reach).  One region per bucket, each in its own pages, made the writes 2x slower
+// (scripts/micro/deg_part_phases.cu).
+CC_DEVI uint64_t dr_addr(const DegRadix& R, uint32_t b, uint32_t pos) {
+  return ((uint64_t)(pos / DR_Q) * R.nbk + b) * DR_Q + (pos % DR_Q);
+}
+// Ring of bucket b: DR_CAP u16 slots (four 16-byte chunks, chunk index XOR-swizzled by bits 1-2
+// of b so that rows 64 bytes apart do not share banks) and one packed word
+// W[b] = (written-out << 16) | claimed, both renormalised to < 64 at every write-out.
+CC_DEVI uint32_t dr_phys(uint32_t b, uint32_t pos) { return (pos & 31u) ^ ((b << 2) & 24u); }
+template <bool FULL>  // FULL: every id is in this super-window (lo = 0, n <= 2^26): no range test
 __global__ void __launch_bounds__(DR_THREADS, 1)
-k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo, uint32_t nbk,
-           uint16_t* __restrict__ region, uint32_t C, uint32_t* __restrict__ cursor,
+k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo_arg, uint32_t nbk, DegRadix R,
            uint32_t* __restrict__ deg) {
-  extern __shared__ __align__(16) uint8_t dr_smem[];
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(dr_smem);                        // [DR_NB]
-  uint16_t* s_buf = reinterpret_cast<uint16_t*>(dr_smem + DR_NB * sizeof(uint32_t));  // [DR_NB][DR_CAP]
-  for (uint32_t b = threadIdx.x; b < DR_NB; b += DR_THREADS) s_cnt[b] = 0;
+  extern __shared__ __align__(16) uint32_t dsm[];
+  uint32_t* s_w = dsm;                                          // [DR_NB]
+  uint16_t* s_row = reinterpret_cast<uint16_t*>(dsm + DR_NB);  // [DR_NB][DR_CAP]
+  const uint32_t lo = FULL ? 0u : lo_arg;
+  for (uint32_t b = threadIdx.x; b < DR_NB; b += DR_THREADS) s_w[b] = 0;
+  // this thread's buckets and the region position of their next 16-entry group
+  const uint32_t ob[2] = {threadIdx.x, threadIdx.x + DR_THREADS};
+  uint32_t opos[2];
+#pragma unroll
+  for (int i = 0; i < 2; i++) opos[i] = ob[i] < nbk ? atomicAdd(&R.cur[ob[i]], 16u) : 0xFFFFFFFFu;
   __syncthreads();
+  const uint32_t G = gridDim.x, k = blockIdx.x;
   const uint64_t npair = m >> 1;  // uint4 = two edges
-  const uint64_t per_round = (uint64_t)DR_THREADS * DR_VEC;
-  const uint64_t rounds = (npair + 1 + per_round - 1) / per_round;  // +1: the odd last edge
+  constexpr uint32_t PER_ROUND = DR_THREADS * DR_VEC;
+  const uint32_t rounds = (uint32_t)((npair + PER_ROUND - 1) / PER_ROUND);
+  const uint32_t full_rounds = (uint32_t)(npair / PER_ROUND);  // rounds with every slot valid
   const uint32_t span_end = nbk << DR_SPAN;
-  auto insert = [&](uint32_t v) {
-    const uint32_t x = v - lo;
-    if (x >= span_end) return;
-    const uint32_t b = x >> DR_SPAN;
-    const uint32_t slot = atomicAdd(&s_cnt[b], 1u);
-    if (slot < DR_CAP) s_buf[b * DR_CAP + slot] = (uint16_t)(x & ((1u << DR_SPAN) - 1));
-    else atomicAdd(&deg[v], 1u);  // staging row full this round
+  constexpr uint32_t LOWMASK = (1u << DR_SPAN) - 1;
+  auto claim_store = [&](const uint32_t (&v)[4], int nv) {
+    uint32_t old[4];
+#pragma unroll
+    for (int h = 0; h < 4; h++)  // the slot claims in flight together, then the stores
+      old[h] = (h < nv && (FULL || v[h] < span_end)) ? atomicAdd(&s_w[v[h] >> DR_SPAN], 1u) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      if (old[h] == 0xFFFFFFFFu) continue;
+      const uint32_t b = v[h] >> DR_SPAN, w = old[h] & 0xFFFFu;
+      if (w - (old[h] >> 16) < DR_CAP) s_row[b * DR_CAP + dr_phys(b, w)] = (uint16_t)(v[h] & LOWMASK);
+      else atomicAdd(&deg[v[h] + lo], 1u);  // ring full this round
+    }
   };
-  for (uint64_t r = blockIdx.x; r < rounds; r += gridDim.x) {
-    const uint64_t i0 = r * per_round + threadIdx.x;
-    uint4 x[DR_VEC];
-    bool ok[DR_VEC];
+  if ((m & 1) && k == 0 && threadIdx.x == 0) {  // the last edge of an odd-length list
+    const uint2 t = reinterpret_cast<const uint2*>(e2)[m - 1];
+    const uint32_t v[4] = {t.x - lo, t.y - lo, 0u, 0u};
+    claim_store(v, 2);
+  }
+  auto load = [&](uint4 (&x)[DR_VEC], uint32_t r) {
+    const uint4* p = e2 + (uint64_t)r * PER_ROUND + threadIdx.x;
+    if (r < full_rounds) {
+#pragma unroll
+      for (int j = 0; j < DR_VEC; j++) x[j] = ldg_stream(p + j * DR_THREADS);
+    } else if (r < rounds) {
+#pragma unroll
+      for (int j = 0; j < DR_VEC; j++)
+        if ((uint64_t)r * PER_ROUND + threadIdx.x + j * DR_THREADS < npair) x[j] = ldg_stream(p + j * DR_THREADS);
+    }
+  };
+  auto insert_round = [&](const uint4 (&x)[DR_VEC], uint32_t r) {
 #pragma unroll
     for (int j = 0; j < DR_VEC; j++) {
-      const uint64_t i = i0 + (uint64_t)j * DR_THREADS;
-      ok[j] = i < npair;
-      if (ok[j]) x[j] = ldg_stream(&e2[i]);
+      if (r >= full_rounds && (uint64_t)r * PER_ROUND + threadIdx.x + j * DR_THREADS >= npair) continue;
+      const uint32_t v[4] = {x[j].x - lo, x[j].y - lo, x[j].z - lo, x[j].w - lo};
+      claim_store(v, 4);
     }
+  };
+  // one group of 16 entries of bucket b (in registers) to its reserved region position
+  auto put_group = [&](uint32_t b, uint32_t pos, const uint4& r0, const uint4& r1) {
+    if (pos < R.C) {  // C and pos are multiples of 16
+      uint4* dst = reinterpret_cast<uint4*>(R.reg + dr_addr(R, b, pos));
+      dst[0] = r0;
+      dst[1] = r1;
+    } else {  // region full: count directly
+      const uint32_t wv[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      const uint32_t bs = lo + (b << DR_SPAN);
 #pragma unroll
-    for (int j = 0; j < DR_VEC; j++)
-      if (ok[j]) {
-        insert(x[j].x); insert(x[j].y); insert(x[j].z); insert(x[j].w);
+      for (int h = 0; h < 8; h++) {
+        if ((wv[h] & 0xFFFFu) != DR_PAD) atomicAdd(&deg[bs + (wv[h] & 0xFFFFu)], 1u);
+        if ((wv[h] >> 16) != DR_PAD) atomicAdd(&deg[bs + (wv[h] >> 16)], 1u);
       }
+    }
+  };
+  // write out one 16-entry group of each of this thread's rings holding one
+  auto flush = [&]() {
 #pragma unroll
-    for (int j = 0; j < DR_VEC; j++)
-      if ((m & 1) && i0 + (uint64_t)j * DR_THREADS == npair) {  // last edge of an odd-length list
-        const uint2 t = reinterpret_cast<const uint2*>(e2)[m - 1];
-        insert(t.x); insert(t.y);
-      }
+    for (int i = 0; i < 2; i++) {
+      const uint32_t b = ob[i];
+      const uint32_t wd = s_w[b];
+      uint32_t w = wd & 0xFFFFu, f = wd >> 16;
+      if (w - f < 16) continue;
+      if (w - f > DR_CAP) w = f + DR_CAP;  // claims past the ring went to deg directly
+      const uint32_t c0 = f & 16u;         // logical chunks c0/8, c0/8 + 1
+      const uint4* row = reinterpret_cast<const uint4*>(s_row + b * DR_CAP);
+      const uint4 r0 = row[dr_phys(b, c0) >> 3], r1 = row[dr_phys(b, c0 + 8) >> 3];
+      f += 16;
+      const uint32_t base = f & ~31u;
+      s_w[b] = ((f - base) << 16) | (w - base);
+      put_group(b, opos[i], r0, r1);
+      opos[i] = atomicAdd(&R.cur[b], 16u);  // the next group's position, needed rounds later
+    }
+  };
+  uint4 xa[DR_VEC], xb[DR_VEC];
+  load(xa, k);
+  for (uint32_t r = k; r < rounds; r += 2 * G) {
+    load(xb, r + G);
+    insert_round(xa, r);
     __syncthreads();
-    // write out whole 16-entry (32-byte) groups of every staging row
-    for (uint32_t b = threadIdx.x; b < DR_NB; b += DR_THREADS) {
-      const uint32_t c = min(s_cnt[b], (uint32_t)DR_CAP);
-      if (c < 16) {
-        s_cnt[b] = c;
-        continue;
-      }
-      const uint32_t nf = c & ~15u;  // 16 or 32
-      uint4* row = reinterpret_cast<uint4*>(s_buf + b * DR_CAP);
-      const uint32_t pos = atomicAdd(&cursor[b], nf);
-      const uint32_t fit = pos >= C ? 0u : min(nf, C - pos);  // multiple of 16
-      uint4* dst = reinterpret_cast<uint4*>(region + (uint64_t)b * C + pos);
-      for (uint32_t k = 0; k < fit / 8; k++) dst[k] = row[k];
-      for (uint32_t k = fit; k < nf; k++)  // region full: count directly
-        atomicAdd(&deg[lo + (b << DR_SPAN) + s_buf[b * DR_CAP + k]], 1u);
-      if (nf == 16) {  // keep the remaining c - 16 (< 16) entries at the row start
-        row[0] = row[2];
-        row[1] = row[3];
-      }
-      s_cnt[b] = c - nf;
-    }
+    flush();
+    __syncthreads();
+    if (r + G >= rounds) break;
+    load(xa, r + 2 * G);
+    insert_round(xb, r + G);
+    __syncthreads();
+    flush();
     __syncthreads();
   }
-  // staged leftovers (< 16 per bucket): count directly
-  for (uint32_t b = threadIdx.x; b < DR_NB; b += DR_THREADS) {
-    const uint32_t c = s_cnt[b];
-    for (uint32_t k = 0; k < c; k++) atomicAdd(&deg[lo + (b << DR_SPAN) + s_buf[b * DR_CAP + k]], 1u);
+  // the ring leftovers (<= 16 per bucket) fill the reserved group, padded with DR_PAD
+#pragma unroll
+  for (int i = 0; i < 2; i++) {
+    const uint32_t b = ob[i];
+    if (b >= nbk) continue;
+    const uint32_t wd = s_w[b];
+    const uint32_t w = wd & 0xFFFFu, f = wd >> 16;
+    uint32_t e[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++)
+      e[q] = (f + q < w) ? s_row[b * DR_CAP + dr_phys(b, f + q)] : DR_PAD;
+    uint4 r0, r1;
+    r0.x = e[0] | (e[1] << 16); r0.y = e[2] | (e[3] << 16); r0.z = e[4] | (e[5] << 16); r0.w = e[6] | (e[7] << 16);
+    r1.x = e[8] | (e[9] << 16); r1.y = e[10] | (e[11] << 16); r1.z = e[12] | (e[13] << 16); r1.w = e[14] | (e[15] << 16);
+    put_group(b, opos[i], r0, r1);
+  }
+}
+// order[rank] = bucket, by decreasing entry count (ties: smaller bucket first); one block
+__global__ void __launch_bounds__(1024) k_deg_order(DegRadix R, uint32_t nbk) {
+  __shared__ uint32_t s_size[DR_NB];
+  for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) s_size[b] = min(R.cur[b], R.C);
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) {
+    const uint32_t sb = s_size[b];
+    uint32_t rank = 0;
+    for (uint32_t o = 0; o < nbk; o++) {
+      const uint32_t so = s_size[o];
+      rank += (so > sb) | ((so == sb) & (o < b));
+    }
+    R.order[rank] = b;
   }
 }
 __global__ void __launch_bounds__(DR_THREADS, 1)
-k_deg_count(const uint16_t* __restrict__ region, uint32_t C, const uint32_t* __restrict__ cursor,
-            uint32_t nbk, uint32_t lo, uint64_t n, uint32_t* __restrict__ deg) {
-  extern __shared__ __align__(16) uint8_t dr_smem[];
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(dr_smem);  // [2^DR_SPAN]
-  const uint32_t b = blockIdx.x % nbk, s = blockIdx.x / nbk;
-  const uint64_t fill = min(cursor[b], C);
-  const uint64_t e0 = (uint64_t)s * DR_SLICE;
-  if (e0 >= fill) return;
-  const uint64_t e1 = min(fill, e0 + DR_SLICE);
-  for (uint32_t i = threadIdx.x; i < (1u << DR_SPAN); i += DR_THREADS) s_cnt[i] = 0;
+k_deg_count(DegRadix R, uint32_t lo, uint64_t n, uint32_t* __restrict__ deg) {
+  extern __shared__ __align__(16) uint32_t dsm[];
+  uint32_t* s_cnt = dsm;  // [2^DR_SPAN + 1]: slot 2^DR_SPAN absorbs DR_PAD
+  const uint32_t b = R.order[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i <= (1u << DR_SPAN); i += DR_THREADS) s_cnt[i] = 0;
   __syncthreads();
-  // entries of one bucket: 16-byte vectors (8 u16), fill is a multiple of 16
-  const uint4* src = reinterpret_cast<const uint4*>(region + (uint64_t)b * C + e0);
-  const uint32_t nv = (uint32_t)((e1 - e0) >> 3);
-  constexpr int U = 4;
-  for (uint32_t k0 = threadIdx.x; k0 < nv; k0 += DR_THREADS * U) {
-    uint4 x[U];
+  // one warp per epoch chunk of this bucket (DR_Q entries = 128 vectors of 16 bytes)
+  const uint32_t fill = min(R.cur[b], R.C);
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint32_t e = wid; e * DR_Q < fill; e += DR_THREADS / 32) {
+    const uint4* src = reinterpret_cast<const uint4*>(R.reg + dr_addr(R, b, e * DR_Q));
+    const uint32_t nv = min(DR_Q, fill - e * DR_Q) >> 3;  // a multiple of 2 (groups of 16)
+    constexpr int U = DR_Q / 8 / 32;  // 4 vectors per lane
+    uint4 v[U];
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (k0 + u * DR_THREADS < nv) x[u] = ldg_stream(src + k0 + u * DR_THREADS);
+      if (lane + u * 32 < nv) v[u] = ldg_stream(src + lane + u * 32);
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (k0 + u * DR_THREADS < nv) {
-        const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+      if (lane + u * 32 < nv) {
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
         for (int h = 0; h < 4; h++) {
           atomicAdd(&s_cnt[w[h] & 0xFFFFu], 1u);
@@ -312,49 +401,74 @@ k_deg_count(const uint16_t* __restrict__ region, uint32_t C, const uint32_t* __r
       }
   }
   __syncthreads();
-  const bool single = fill <= DR_SLICE;
   const uint64_t base = (uint64_t)lo + ((uint64_t)b << DR_SPAN);
   for (uint32_t i = threadIdx.x; i < (1u << DR_SPAN); i += DR_THREADS) {
     const uint32_t c = s_cnt[i];
-    if (!c || base + i >= n) continue;
-    if (single) deg[base + i] += c;
-    else atomicAdd(&deg[base + i], c);
+    if (c && base + i < n) deg[base + i] += c;  // one block per bucket: plain add
   }
 }
-uint64_t degree_radix_scratch(uint64_t m, uint64_t n) {
-  // bytes of region scratch launch_degree_radix needs (u16 entries)
+static bool deg_radix_plan(uint64_t m, uint64_t n, uint64_t scratch_bytes, uint64_t* nbk, uint64_t* C) {
   const uint64_t nb_all = (n + (1u << DR_SPAN) - 1) >> DR_SPAN;
-  const uint64_t nbk = std::min<uint64_t>(nb_all, DR_NB);
-  const uint64_t mean = nb_all ? (2 * m + nb_all - 1) / nb_all : 0;
-  const uint64_t C = ((2 * mean + 1024) + 31) & ~31ull;
-  return nbk * C * sizeof(uint16_t);
+  *nbk = std::min<uint64_t>(nb_all, DR_NB);
+  const uint64_t mean = (2 * m + nb_all - 1) / nb_all;  // entries per bucket
+  // 4x the mean (R-MAT 26: the heaviest bucket holds ~2.6x), less if the scratch is short; plus
+  // the groups reserved ahead and padded (one per bucket per block)
+  const uint64_t head = 256 + sizeof(uint32_t) * 2 * DR_NB;
+  const uint64_t fit = scratch_bytes > head ? (scratch_bytes - head) / (*nbk * sizeof(uint16_t)) : 0;
+  uint64_t c = std::min<uint64_t>(4 * mean + 16 * 160 * 2, fit);
+  c = c / DR_Q * DR_Q;
+  *C = c;
+  return c >= 2 * mean && c < (1ull << 31);
 }
-bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, void* scratch,
-                         uint64_t scratch_bytes, uint32_t* cursor, cudaStream_t st) {
-  if (!m || !n) return true;
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+uint64_t degree_radix_scratch(uint64_t m, uint64_t n) {
   const uint64_t nb_all = (n + (1u << DR_SPAN) - 1) >> DR_SPAN;
   const uint64_t nbk = std::min<uint64_t>(nb_all, DR_NB);
   const uint64_t mean = (2 * m + nb_all - 1) / nb_all;
-  const uint64_t C = ((2 * mean + 1024) + 31) & ~31ull;
-  if (C >= (1ull << 31) || nbk * C * sizeof(uint16_t) > scratch_bytes) return false;
+  return 256 + sizeof(uint32_t) * 2 * DR_NB + nbk * sizeof(uint16_t) * (4 * mean + 16 * 160 * 2);
+}
+bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, void* scratch,
+                         uint64_t scratch_bytes, uint32_t* /*cursor*/, cudaStream_t st) {
+  if (!m || !n) return true;
+  uint64_t nbk, C;
+  if (!deg_radix_plan(m, n, scratch_bytes, &nbk, &C)) return false;
+  uint8_t* p = reinterpret_cast<uint8_t*>(scratch);
+  DegRadix R;
+  R.C = (uint32_t)C;
+  R.nbk = (uint32_t)nbk;
+  R.cur = reinterpret_cast<uint32_t*>(p);
+  R.order = R.cur + DR_NB;
+  R.reg = reinterpret_cast<uint16_t*>(p + 256 + sizeof(uint32_t) * 2 * DR_NB);
   static bool attr = false;
   const int smem_part = DR_NB * sizeof(uint32_t) + DR_NB * DR_CAP * sizeof(uint16_t);
-  const int smem_count = (1 << DR_SPAN) * sizeof(uint32_t);
+  const int smem_count = ((1 << DR_SPAN) + 1) * sizeof(uint32_t);
   if (!attr) {
-    cudaFuncSetAttribute(k_deg_part, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_part);
+    cudaFuncSetAttribute(k_deg_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_part);
+    cudaFuncSetAttribute(k_deg_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_part);
     cudaFuncSetAttribute(k_deg_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_count);
     attr = true;
   }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const uint64_t slices = (C + DR_SLICE - 1) / DR_SLICE;
+  const int G = sm_count();
   for (uint64_t lo = 0; lo < n; lo += (uint64_t)DR_NB << DR_SPAN) {
     const uint32_t nb = (uint32_t)std::min<uint64_t>(DR_NB, (n - lo + (1u << DR_SPAN) - 1) >> DR_SPAN);
-    cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * DR_NB, st);
-    k_deg_part<<<sms, DR_THREADS, smem_part, st>>>(reinterpret_cast<const uint4*>(edges), m, (uint32_t)lo, nb,
-                                                   reinterpret_cast<uint16_t*>(scratch), (uint32_t)C, cursor, deg);
-    k_deg_count<<<(unsigned)(nb * slices), DR_THREADS, smem_count, st>>>(
-        reinterpret_cast<const uint16_t*>(scratch), (uint32_t)C, cursor, nb, (uint32_t)lo, n, deg);
+    R.nbk = nb;
+    cudaMemsetAsync(R.cur, 0, sizeof(uint32_t) * DR_NB, st);
+    if (lo == 0 && n <= ((uint64_t)DR_NB << DR_SPAN))
+      k_deg_part<true><<<G, DR_THREADS, smem_part, st>>>(reinterpret_cast<const uint4*>(edges), m, 0u, nb, R, deg);
+    else
+      k_deg_part<false><<<G, DR_THREADS, smem_part, st>>>(reinterpret_cast<const uint4*>(edges), m, (uint32_t)lo,
+                                                          nb, R, deg);
+    k_deg_order<<<1, 1024, 0, st>>>(R, nb);
+    k_deg_count<<<nb, DR_THREADS, smem_count, st>>>(R, (uint32_t)lo, n, deg);
   }
   return true;
 }
@@ -363,6 +477,7 @@ bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* d
 // (max degree, smallest argmax) key used for the BFS root (C13).  Shared-memory bins for
 // small degrees (where all the mass is), global bins up to 2^20, a tail list beyond.
 constexpr int SBINS = 2048;
+constexpr int HLOC = 8;  // degrees 1..HLOC are counted in registers (most ids; no atomics)
 __global__ void __launch_bounds__(BLOCK) k_deg_hist(const uint32_t* __restrict__ deg, uint64_t n,
                                                     uint32_t* __restrict__ hist,
                                                     uint32_t* __restrict__ tail,
@@ -370,27 +485,37 @@ __global__ void __launch_bounds__(BLOCK) k_deg_hist(const uint32_t* __restrict__
   __shared__ uint32_t sh[SBINS];
   for (int i = threadIdx.x; i < SBINS; i += BLOCK) sh[i] = 0;
   __syncthreads();
-  uint32_t npres = 0;
+  uint32_t npres = 0, loc[HLOC];
+#pragma unroll
+  for (int j = 0; j < HLOC; j++) loc[j] = 0;
   unsigned long long best = 0;
-  const uint32_t lt = lanemask_lt();
-  for (uint64_t base = blockIdx.x * (uint64_t)BLOCK; base < n; base += (uint64_t)gridDim.x * BLOCK) {
-    uint64_t v = base + threadIdx.x;
-    uint32_t d = v < n ? deg[v] : 0u;
-    if (d) {
-      npres++;
-      unsigned long long key = ((unsigned long long)d << 32) | (0xFFFFFFFFu - (uint32_t)(v + id0));
-      best = key > best ? key : best;
+  auto add = [&](uint32_t d, uint64_t v) {
+    if (!d) return;
+    npres++;
+    const unsigned long long key = ((unsigned long long)d << 32) | (0xFFFFFFFFu - (uint32_t)(v + id0));
+    best = key > best ? key : best;
+    if (d <= HLOC) {
+#pragma unroll
+      for (int j = 0; j < HLOC; j++) loc[j] += (d == (uint32_t)j + 1);
+    } else if (d < SBINS) {
+      atomicAdd(&sh[d], 1u);
+    } else if (d < HIST_DENSE) {
+      atomicAdd(&hist[d], 1u);
+    } else {
+      const unsigned long long pos = atomicAdd(&gctr[G_TAIL], 1ull);
+      if (pos < TAIL_CAP) tail[pos] = d;
     }
-    uint32_t bin = (d && d < SBINS) ? d : (SBINS + (threadIdx.x & 31));
-    uint32_t peers = __match_any_sync(0xffffffffu, bin);
-    if (bin < SBINS && (peers & lt) == 0) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
-    if (d >= SBINS) {
-      if (d < HIST_DENSE) atomicAdd(&hist[d], 1u);
-      else {
-        unsigned long long pos = atomicAdd(&gctr[G_TAIL], 1ull);
-        if (pos < TAIL_CAP) tail[pos] = d;
-      }
-    }
+  };
+  const uint64_t n4 = n >> 2;  // 16-byte loads (deg is 16-byte aligned)
+  for (uint64_t q = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; q < n4; q += (uint64_t)gridDim.x * BLOCK) {
+    const uint4 d = reinterpret_cast<const uint4*>(deg)[q];
+    add(d.x, 4 * q); add(d.y, 4 * q + 1); add(d.z, 4 * q + 2); add(d.w, 4 * q + 3);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) add(deg[4 * n4 + threadIdx.x], 4 * n4 + threadIdx.x);
+#pragma unroll
+  for (int j = 0; j < HLOC; j++) {
+    const uint32_t t = warp_sum(loc[j]);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(&sh[j + 1], t);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < SBINS; i += BLOCK)

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--mode", default="auto")
     ap.add_argument("--out", default="gpurun_out/timeline.json")
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--op", default="run", choices=["run", "degrees"],
+                    help="degrees: only the prediction-stage degree count (cc_degrees_u32)")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -33,11 +35,12 @@ def main():
     u64 = g.n == 0
     ctx.load(torch.from_numpy(g.edges.view(np.int64 if u64 else np.int32)).to(dev), g.n,
              ids="u64" if u64 else "u32")
+    op = (lambda: ctx.run(args.mode)) if args.op == "run" else (lambda: ctx.degrees(g.n))
     for _ in range(3):
-        ctx.run(args.mode)
+        op()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        ctx.run(args.mode)
+        op()
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
     rows = []
