@@ -1,17 +1,19 @@
 #!/usr/bin/env python
 """Benchmark: undirected edges/s to final component labels (BASELINE.json metric).
 
-One step = one cc_run(mode=auto) -- the whole hot path of Alg. 2 (degree distribution,
-gate, optional BFS peel + filter, edge-tuple SV to convergence) -- on the BASELINE.json
-workload configs[1] (C2, de Bruijn-like, ~16.1 M vertices / ~16.9 M edges), with the edge
-list already resident in HBM.  See DESIGN.md §6 for the byte models behind `roofline`.
+One step = one cc_run(mode=auto) -- the whole hot path of Alg. 2 (degree distribution, power-law
+gate, BFS peel + filter when the gate says scale-free, edge-tuple SV to convergence on the rest)
+-- with the edge list already resident in HBM (profiling starts after the edges
+are loaded).  The default workload is BASELINE.json configs[3] (C4: R-MAT scale 26, 1.07 G
+edges), the largest config that fits one GPU (C5 needs several).  See
+DESIGN.md §6 for the byte and access models behind `roofline`, `kernels` and `path_roofline`.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--mode auto]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--mode auto]
   python bench.py --impl reference ...      # the CPU oracle, timed on the host cores
 
 N > 1 (torchrun, one process per GPU): the same workload sharded over the ranks -- rank k
 loads block k of the edge list, the library regroups arcs to vertex-block owners and combines
-partition slots over NCCL (cc_comm over torch.distributed) -- strong scaling.
+partition slots over NCCL -- strong scaling.
 """
 from __future__ import annotations
 
@@ -35,9 +37,12 @@ WORKLOADS = {
     "c2": "C2 de Bruijn-like: 50,000 geometric(mean 320) paths + 5% bubbles + 0.5% joins, "
           "ids permuted (BASELINE configs[1])",
     "c3": "C3 road-like: 4096x4096 lattice, p=0.55, +1% diagonals, ids permuted (configs[2])",
-    "c4": "C4 R-MAT scale 26, edge factor 16, a/b/c/d=.57/.19/.19/.05, ids permuted (configs[3])",
+    "c4": "C4 R-MAT scale 26, edge factor 16, a/b/c/d=.57/.19/.19/.05, ids permuted (BASELINE configs[3])",
     "c5": "C5 R-MAT scale 28 U 10 M geometric(mean 64) paths, u64 ids (configs[4]) at --scale",
 }
+# the CPU reference arm's bounded sample per step (edges): the first REF_SAMPLE[c] edge records
+# of the config (C4's are i.i.d., so a prefix is a uniform sample), same id range
+REF_SAMPLE = {"c4": 1 << 25}
 
 
 def peaks():
@@ -46,6 +51,34 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def micro_peaks():
+    """Measured request-rate ceilings on this B200 (scripts/micro/l2_peaks.cu, smem_atomics.cu;
+    profiles/r02/micro_peaks.json): the denominators of the access-bound roofline fractions."""
+    p = os.path.join(ROOT, "profiles", "r02", "micro_peaks.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+def host_info():
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    mem = None
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                mem = round(int(ln.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "cpu_model": model,
+            "ram_gib": mem}
 
 
 class Clocks:
@@ -144,17 +177,30 @@ def alg_bytes(rep, n, m):
     return b
 
 
+def oracle_threads():
+    return 1  # oracle/uf.c is a single-threaded union-find
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle (union-find, oracle/uf.c), as it stands."""
+    """--impl reference: the CPU oracle (union-find, oracle/uf.c) as it stands, on the host cores.
+    Each step is a bounded sample of the workload (REF_SAMPLE: a prefix of the edge list with the
+    same id range; the whole graph for the small configs), so the K + W steps take a few minutes."""
     ws, rk, _ = dist_info()
     if rk != 0:
         return 0
+    import graphgen
     import oracle
     scale = args.scale or default_scale(args.config, ws)
-    g = make_graph(args.config, scale)
+    if args.config in REF_SAMPLE and scale == 1.0:
+        g = graphgen.make_prefix(args.config, REF_SAMPLE[args.config])
+        sample = (f"first {g.m:,} edge records of {args.config} (of {16 << 26:,}; i.i.d. R-MAT edges, "
+                  f"n = {g.n:,}), union-find, 1 thread, per step")
+    else:
+        g = make_graph(args.config, scale)
+        sample = f"whole {args.config} graph (scale {scale}) per step (union-find, 1 thread)"
     oracle.build()
     run = (lambda: oracle.uf_labels_u64(g.edges)) if g.n == 0 else (lambda: oracle.uf_labels(g.n, g.edges))
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -163,12 +209,13 @@ def run_reference(args):
     v = g.m * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u64" if g.n == 0 else "u32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "scale": scale, "n": g.n, "m": g.m, "mode": "auto"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"whole {args.config} graph per step (union-find, 1 thread)"},
+        "config": {"workload": WORKLOADS[args.config], "scale": scale, "n": g.n, "m_per_step": g.m,
+                   "mode": "auto"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
+                         "sample": sample, "host": host_info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -179,22 +226,33 @@ def cpu_baseline(g, budget_s=12.0):
     import oracle
     oracle.build()
     reps, t_used = 0, 0.0
+    host = host_info()
     if g.n == 0:  # u64 ids: the oracle (sort-unique + union-find) on a bounded prefix
         e = g.edges[:min(g.m, 20_000_000)]
         t0 = time.perf_counter()
         oracle.uf_labels_u64(e)
         t_used = time.perf_counter() - t0
-        return {"value": e.shape[0] / t_used, "unit": UNIT, "cores": 1, "kind": "oracle",
+        return {"value": e.shape[0] / t_used, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
                 "sample": f"u64 union-find oracle (sort-unique + union-find) on the first "
-                          f"{e.shape[0]} edge records of the workload, {t_used:.1f} s, single thread"}
+                          f"{e.shape[0]} edge records of the workload, {t_used:.1f} s, single thread",
+                "host": host}
     t0 = time.perf_counter()
     while reps < 20 and t_used < budget_s:
         oracle.uf_labels(g.n, g.edges)
         reps += 1
         t_used = time.perf_counter() - t0
-    return {"value": g.m * reps / t_used, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": g.m * reps / t_used, "unit": UNIT, "cores": oracle_threads(), "kind": "oracle",
             "sample": f"union-find oracle on the whole workload graph, {reps} repetition(s), "
-                      f"{t_used:.1f} s, single thread"}
+                      f"{t_used:.1f} s, single thread", "host": host}
+
+
+def traffic_for(config, regroup):
+    """ncu DRAM bytes per cc_run by kernel family (profiles/traffic.json, scripts/traffic.py)."""
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(tp):
+        return {}, None
+    d = json.load(open(tp))
+    return d.get(f"{config}/{regroup}", {}), d.get("_source")
 
 
 def main():
@@ -202,11 +260,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="auto", choices=["auto", "sv", "bfs+sv"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--regroup", default="csr", choices=["csr", "csrbfs", "direct", "sort"],
-                    help="SV bucket regroup engine (DESIGN.md §5.3)")
+                    help="SV bucket regroup engine (DESIGN.md §5.2)")
     ap.add_argument("--scale", type=float, default=None,
                     help="fraction of the config's size (default 1; c5 on one GPU: 1/16)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -250,7 +308,8 @@ def main():
     ctx.load(d_edges, n, ids=ids)
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    for _ in range(max(3, args.warmup)):
+    warmup = max(3, args.warmup)
+    for _ in range(warmup):
         rep = ctx.run(args.mode)
     torch.cuda.synchronize()
     if ws > 1:
@@ -258,7 +317,7 @@ def main():
     clocks = Clocks(lr)
     clocks.start()
     names = cc.kernel_families()
-    fam = {i: [0.0, 0.0, 0] for i in range(len(names))}
+    fam = {i: {"ms": 0.0, "bytes": 0.0, "launches": 0, "ops": 0.0, "ops_unit": ""} for i in range(len(names))}
     launches = 0
 
     def timed_steps(profiled):
@@ -276,9 +335,9 @@ def main():
             if profiled:
                 for f in fam:
                     s = ctx.kernel_stats(f)
-                    fam[f][0] += s["ms"]
-                    fam[f][1] += s["bytes"]
-                    fam[f][2] += s["launches"]
+                    for key in ("ms", "bytes", "launches", "ops"):
+                        fam[f][key] += s[key]
+                    fam[f]["ops_unit"] = s["ops_unit"]
             else:
                 launches += ctx.launches()
         torch.cuda.synchronize()
@@ -300,7 +359,7 @@ def main():
     value = m * args.steps / (ms_max / 1e3)
 
     # ---------------- e2e: host buffers through the public API (H2D + run + D2H)
-    e2e = None
+    e2e, ok = None, None
     if not args.no_e2e:
         host = torch.from_numpy(mine.view(np.int64 if u64 else np.int32)).pin_memory()
         lo, hi = ctx.block_range()
@@ -330,8 +389,8 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": m * ke / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(mine.nbytes),
-               "d2h_bytes_per_step": int((16 if u64 else 4) * (hi - lo)), "steps": ke}
-        ok = None
+               "d2h_bytes_per_step": int((16 if u64 else 4) * (hi - lo)), "steps": ke,
+               "path": "cc_load_edges(pinned host pairs) + cc_run + cc_labels (pinned host out)"}
         if rk == 0:
             orc = __import__("oracle")
             if not u64:
@@ -342,54 +401,92 @@ def main():
 
     if rk == 0:
         peak, peak_src = peaks()
+        mp = micro_peaks()
+        traffic, traffic_src = traffic_for(args.config, args.regroup)
+        K = args.steps
         # dominant kernel: the single-kernel family with the largest device time in the timed
         # region (family 1 is the whole-iteration aggregate, excluded)
-        leaf = [i for i in fam if i != 1 and fam[i][0] > 0]
-        dom = max(leaf, key=lambda i: fam[i][0]) if leaf else None
-        kernels = {names[i]: {"ms_per_step": fam[i][0] / args.steps,
-                              "alg_GBps": (fam[i][1] / (fam[i][0] / 1e3)) / 1e9 if fam[i][0] else None,
-                              "launches_per_step": fam[i][2] / args.steps}
-                   for i in fam if fam[i][0] > 0}
+        leaf = [i for i in fam if i != 1 and fam[i]["ms"] > 0]
+        dom = max(leaf, key=lambda i: fam[i]["ms"]) if leaf else None
+        ops_peak = {"random 4-byte L2 reads (2 per edge of the level)": ("l2_random_read_Gops", "L2"),
+                    "shared-memory atomics (2 per arc: bucket claim + count)": ("smem_atomic_Gops", "SMEM")}
+        kernels = {}
+        for i in fam:
+            f = fam[i]
+            if f["ms"] <= 0:
+                continue
+            row = {"ms_per_step": f["ms"] / K,
+                   "alg_GBps": (f["bytes"] / (f["ms"] / 1e3)) / 1e9,
+                   "hbm_frac": (f["bytes"] / (f["ms"] / 1e3)) / 1e9 / peak,
+                   "launches_per_step": f["launches"] / K,
+                   "share_of_step": f["ms"] / ms_prof if ms_prof else None}
+            tr = traffic.get(names[i])
+            if tr:
+                row["dram_bytes_per_step_ncu"] = tr
+                row["dram_GBps"] = tr / (f["ms"] / K / 1e3) / 1e9
+                row["dram_frac"] = row["dram_GBps"] / peak
+            if f["ops"] > 0:
+                pk = ops_peak.get(f["ops_unit"])
+                row["ops_unit"] = f["ops_unit"]
+                row["Gops_per_s"] = f["ops"] / (f["ms"] / 1e3) / 1e9
+                if pk and mp.get(pk[0]):
+                    row["ops_peak_Gops"] = mp[pk[0]]
+                    row["ops_frac"] = row["Gops_per_s"] / mp[pk[0]]
+            kernels[names[i]] = row
+        roof = {"bound": "hbm", "kernel": None}
         if dom is not None:
-            d_ms, d_bytes, d_launches = fam[dom]
-            achieved = (d_bytes / (d_ms / 1e3)) / 1e9
-        else:
-            d_ms, d_bytes, d_launches, achieved = 0.0, 0.0, 0, None
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            tr = json.load(open(tp)).get(f"{args.config}/{args.regroup}", {})
-            traffic = tr.get(names[dom]) if dom is not None else None
+            f = fam[dom]
+            achieved = (f["bytes"] / (f["ms"] / 1e3)) / 1e9
+            kr = kernels[names[dom]]
+            roof = {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak,
+                    "traffic": (traffic.get(names[dom]) / (f["launches"] / K)) if traffic.get(names[dom]) else None,
+                    "traffic_unit": "ncu dram bytes read+written per launch (profiles/traffic.json)",
+                    "peak_source": peak_src,
+                    "alg_bytes_per_launch": f["bytes"] / f["launches"] if f["launches"] else None,
+                    "ms_per_launch": f["ms"] / f["launches"] if f["launches"] else None,
+                    "share_of_step": f["ms"] / ms_prof if ms_prof else None,
+                    "timing": "CUDA events around each launch on the library stream, in a second pass "
+                              "of the same K steps (ms_per_step_profiled)",
+                    "launches_per_step": f["launches"] / K}
+            if "ops_frac" in kr:
+                # what actually bounds it: the random-access request rate, against the measured
+                # ceiling of the same access pattern on this GPU
+                roof["access_bound"] = {"unit": kr["ops_unit"], "achieved_Gops": kr["Gops_per_s"],
+                                        "peak_Gops": kr["ops_peak_Gops"], "frac": kr["ops_frac"],
+                                        "peak_source": mp.get("source")}
+            if "dram_GBps" in kr:
+                roof["dram_GBps_live"] = kr["dram_GBps"]
+                roof["dram_frac"] = kr["dram_frac"]
         path_bytes = alg_bytes(rep, n if not u64 else rep["n_present"], m)
-        step_s = ms_max / 1e3 / args.steps
+        step_s = ms_max / 1e3 / K
+        dram_step = sum(v for k, v in traffic.items()) if traffic else None
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
-            "ms_per_step_profiled": ms_prof / args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
+            "warmup": warmup, "ms_per_step": ms_max / K,
+            "ms_per_step_profiled": ms_prof / K,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u64" if u64 else "u32", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "scale": scale,
                        "n": n if not u64 else int(rep["n_present"]), "m": m, "mode": args.mode,
                        "regroup": args.regroup,
                        "route": "bfs+sv" if rep["ran_bfs"] else "sv",
+                       "bfs_levels": rep["bfs_levels"], "remainder_edges": rep["remainder_edges"],
                        "sv_iterations": rep["sv_iterations"],
-                       "l2": "flushed between timed steps (256 MiB write, outside step events)",
+                       "l2": ("inputs larger than L2 (edge list %.1f GB) and a 256 MiB write between "
+                              "timed steps, outside the step's events" % (mine.nbytes / 1e9)),
                        "parallelism": (f"{ws} ranks: edge blocks, vertex-block owners, NCCL slot "
                                        "exchange" if ws > 1 else "1 GPU")},
-            "roofline": {"bound": "hbm", "kernel": names[dom] if dom is not None else None,
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "alg_bytes_per_launch": (d_bytes / d_launches) if d_launches else None,
-                         "ms_per_launch": (d_ms / d_launches) if d_launches else None,
-                         "share_of_step": (d_ms / ms_prof) if ms_prof else None,
-                         "timing": "CUDA events around each launch on the library stream, in a "
-                                   "second pass of the same K steps (ms_per_step_profiled)",
-                         "launches_per_step": d_launches / args.steps},
+            "roofline": roof,
             "kernels": kernels,
             "path_roofline": {"alg_bytes_per_step": path_bytes,
                               "frac": (path_bytes / (peak * 1e9)) / step_s,
-                              "model": "SURVEY.md §8(d): 8m+8A0+sum(32A_i+48A_i+1+40T_i)+4n+4n_p"},
+                              "model": "SURVEY.md §8(d): 8m+8A0+sum(32A_i+48A_i+1+40T_i)+4n+4n_p, BFS route "
+                                       "+32m+20n; the bytes a sort-based regroup would move, not what this "
+                                       "design moves: read as 'equivalent to that design at X of peak'"},
+            "dram_path": ({"ncu_bytes_per_step": dram_step, "GBps": dram_step / step_s / 1e9,
+                           "frac": dram_step / step_s / 1e9 / peak, "source": traffic_src}
+                          if dram_step else None),
             "stages_ms": {k: rep[k] for k in ("ms_relabel", "ms_prediction", "ms_bfs", "ms_filter", "ms_sv",
                                               "ms_finalize")},
             "sv_iters": [{"A": it["active_in"], "P": it["partitions"], "ms": round(it["ms"], 4)}
@@ -397,7 +494,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,
-            "e2e_labels_match_oracle": ok if e2e else None,
+            "e2e_labels_match_oracle": ok,
         }
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(g)

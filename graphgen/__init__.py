@@ -109,8 +109,11 @@ def grid(seed: int, side: int, keep_p: float, n_diag: int):
 
 
 def rmat(seed: int, scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19,
-         permute_ids: bool = True) -> np.ndarray:
-    m = edge_factor << scale
+         permute_ids: bool = True, m: int | None = None) -> np.ndarray:
+    """R-MAT edges 0 .. m-1 (default m = edge_factor << scale).  Edge e is a pure function of
+    (seed, e) and the id permutation depends only on the scale, so a smaller m draws exactly
+    the first m edges of the full list (a uniform sample: R-MAT edges are i.i.d.)."""
+    m = (edge_factor << scale) if m is None else int(m)
     ta, tab, tabc = int(a * 2**32), int((a + b) * 2**32), int((a + b + c) * 2**32)
     out = np.empty((m, 2), dtype=np.uint32)
     _L().gg_rmat(seed, scale, m, ta, tab, tabc, int(permute_ids), _ptr(out))
@@ -175,6 +178,15 @@ def make(config: str, scale: float = 1.0, seed: int | None = None) -> Graph:
         return Graph("c5", 0, union_u64(s, a, 1 << sc, b), dict(rmat_scale=sc, n_paths=npaths,
                                                                   scale=scale))
     raise KeyError(config)
+
+
+def make_prefix(config: str, m_prefix: int) -> Graph:
+    """The first ``m_prefix`` edge records of a full-size R-MAT config (c4), same id range:
+    the bounded sample the CPU reference arm of bench.py times per step."""
+    if config != "c4":
+        raise KeyError("prefix samples are drawn for the R-MAT config c4 only")
+    s = BASE_SEED + 4
+    return Graph("c4", 1 << 26, rmat(s, 26, 16, m=m_prefix), dict(rmat_scale=26, m_prefix=m_prefix))
 
 
 def rmat_scale_graph(scale: int, seed: int | None = None) -> Graph:

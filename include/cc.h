@@ -253,6 +253,11 @@ uint64_t cc_last_launch_count(const cc_ctx* ctx);
 cc_status cc_kernel_stats(const cc_ctx* ctx, int which, double* ms, double* bytes,
                           uint64_t* launches);
 const char* cc_kernel_name(int which);
+/* The random accesses family `which` made in the last cc_run under CC_FLAG_PROFILE (its
+ * algorithmic count, e.g. 2 L2 reads per edge of a BFS level, 2 shared-memory atomics per arc
+ * of the bucketed degree count) and their unit ("" if the family is not access-bound), for a
+ * request-rate roofline beside the bytes of cc_kernel_stats.  CC_ERR_INVALID for a bad index. */
+cc_status cc_kernel_ops(const cc_ctx* ctx, int which, double* ops, const char** unit);
 
 cc_status cc_destroy(cc_ctx* ctx);
 

@@ -89,7 +89,7 @@ EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", 
            "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_radix_sort_pairs",
            "cc_degree_histogram", "cc_degrees_u32",
            "cc_set_profiling", "cc_last_launch_count",
-           "cc_kernel_stats",
+           "cc_kernel_stats", "cc_kernel_ops",
            "cc_kernel_name", "cc_destroy", "cc_status_string", "cc_last_error"]
 
 
@@ -122,6 +122,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_last_launch_count.argtypes = [P]
     lib.cc_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
+    lib.cc_kernel_ops.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_char_p)]
+    lib.cc_kernel_ops.restype = ctypes.c_int
     lib.cc_destroy.argtypes = [P]
     lib.cc_kernel_name.restype = ctypes.c_char_p
     lib.cc_kernel_name.argtypes = [ctypes.c_int]
@@ -415,7 +417,10 @@ def cc_radix_sort_pairs(keys, vals, tmp_keys, tmp_vals, key_bits=64, stream=None
 def cc_kernel_stats(ctx, which):
     ms, by, ln = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
     _check(ctx, lib().cc_kernel_stats(ctx, which, ctypes.byref(ms), ctypes.byref(by), ctypes.byref(ln)))
-    return dict(ms=ms.value, bytes=by.value, launches=ln.value)
+    ops, unit = ctypes.c_double(), ctypes.c_char_p()
+    _check(ctx, lib().cc_kernel_ops(ctx, which, ctypes.byref(ops), ctypes.byref(unit)))
+    return dict(ms=ms.value, bytes=by.value, launches=ln.value, ops=ops.value,
+                ops_unit=(unit.value or b"").decode())
 
 
 def kernel_families():

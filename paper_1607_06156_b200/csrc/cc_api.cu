@@ -911,14 +911,23 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     } else {
       CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
       // scratch: tuple buffer 1 (8 cap >= 16m + 16n bytes) is free until the SV / CSR stages
-      graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail, c->d_gctr + graph::G_NUM + 64,
-                           c->d_w[1], sizeof(uint64_t) * c->cap, c->d_garc);
-      k.end(8.0 * m + 4.0 * n, 1);
+      const int algo = graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail,
+                                            c->d_gctr + graph::G_NUM + 64, c->d_w[1],
+                                            sizeof(uint64_t) * c->cap, c->d_garc);
+      // bucketed: edges read, u16 entries written and read, deg read + written; 2 shared
+      // atomics per arc.  L2 windows: the edge list once per 2^24-id window, 1 L2 add per arc
+      const double nwin = (double)((n + (1ull << 24) - 1) >> 24);
+      if (algo == 1) k.end(8.0 * m + 4.0 * m + 4.0 * m + 8.0 * n, 3, 4.0 * m);
+      else k.end(8.0 * m * (nwin > 0 ? nwin : 1) + 4.0 * n, 1, 0.0);
     }
   }
   const bool want_hist = (mode == CC_MODE_AUTO) || (c->cfg.flags & CC_FLAG_TRACE);
   if (want_hist) CK(cudaMemsetAsync(c->d_hist, 0, sizeof(uint32_t) * graph::HIST_DENSE, c->st));
-  graph::launch_deg_hist(c->d_deg, n, c->d_hist, c->d_tail, c->d_gctr, c->st);
+  {
+    Prof k(c, KF_HIST);
+    graph::launch_deg_hist(c->d_deg, n, c->d_hist, c->d_tail, c->d_gctr, c->st);
+    k.end(4.0 * n, 1);
+  }
   c->launches += 3;
   CKL();
   bool run_bfs = false;
@@ -991,7 +1000,8 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
       graph::launch_bfs_level(root_level, compact, cur, mcur, (uint32_t)root, S, X, bufs[nb],
                               c->d_gctr, c->d_deg, c->st);
       c->launches += 1;
-      k.end(8.0 * (double)mcur + (compact ? 8.0 * (double)mcur / 8 : 0.0) + (double)n / 4, 1);
+      k.end(8.0 * (double)mcur + (compact ? 8.0 * (double)mcur / 8 : 0.0) + (double)n / 4, 1,
+            root_level ? 0.0 : 2.0 * (double)mcur);
       CKL();
       TRY(sync_read(c));
       last_compacted = compact;
@@ -1185,6 +1195,13 @@ extern "C" cc_status cc_kernel_stats(const cc_ctx* c, int which, double* ms, dou
   if (ms) *ms = c->kst[which].ms;
   if (bytes) *bytes = c->kst[which].bytes;
   if (launches) *launches = c->kst[which].launches;
+  return CC_OK;
+}
+
+extern "C" cc_status cc_kernel_ops(const cc_ctx* c, int which, double* ops, const char** unit) {
+  if (!c || which < 0 || which >= KF_N) return CC_ERR_INVALID;
+  if (ops) *ops = c->kst[which].ops;
+  if (unit) *unit = kKfOps[which];
   return CC_OK;
 }
 

@@ -103,7 +103,7 @@ struct cc_ctx {
   std::vector<cudaEvent_t> it_ev;  // SV iteration start events
   struct KStat {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-    double bytes = 0, ms = 0;
+    double bytes = 0, ms = 0, ops = 0;
     uint64_t launches = 0;
   } kst[16];
 };
@@ -213,13 +213,19 @@ static inline bool profiling(const cc_ctx* c) { return (c->cfg.flags & CC_FLAG_P
 
 // kernel families timed under CC_FLAG_PROFILE (cc_kernel_stats / cc_kernel_name)
 enum KFam { KF_RADIX = 0, KF_SVITER, KF_BFS, KF_ROWA, KF_ROWB, KF_SLOTS, KF_CSR, KF_PREDICT,
-            KF_COMPACT, KF_N };
+            KF_COMPACT, KF_HIST, KF_N };
 static const char* const kKfNames[KF_N] = {
     "k_hist+k_onesweep (radix regroup)", "SV iteration (all bucket passes)", "k_bfs_level",
     "k_rowpass<A> +k_long1/2 (Alg.1 lines 8-16)", "k_rowpass<B> +k_long1/2 (Alg.1 lines 17-25)",
     "k_pstat1/k_pstat2/k_list_from_bits (partition slot scans)",
-    "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)", "prediction (k_degree, k_deg_hist)",
-    "k_compact (ordered exclusion of completed rows)"};
+    "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)",
+    "degree count (k_deg_part, k_deg_order, k_deg_count)",
+    "k_compact (ordered exclusion of completed rows)",
+    "degree distribution (k_deg_hist, k_hist_pairs)"};
+// unit of the per-family `ops` count (cc_kernel_ops): the random accesses that bound the family
+static const char* const kKfOps[KF_N] = {
+    "", "", "random 4-byte L2 reads (2 per edge of the level)", "", "", "", "",
+    "shared-memory atomics (2 per arc: bucket claim + count)", "", ""};
 
 struct Prof {
   cc_ctx* c;
@@ -228,13 +234,14 @@ struct Prof {
   Prof(cc_ctx* c_, int f_) : c(c_), f(f_) {
     if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
   }
-  void end(double bytes, uint64_t nl) {
+  void end(double bytes, uint64_t nl, double ops = 0) {
     if (!profiling(c)) return;
     cudaEvent_t b = ev_get(c);
     cudaEventRecord(b, c->st);
     c->kst[f].ev.push_back({a, b});
     c->kst[f].bytes += bytes;
     c->kst[f].launches += nl;
+    c->kst[f].ops += ops;
   }
 };
 

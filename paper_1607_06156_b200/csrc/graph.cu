@@ -128,18 +128,18 @@ __global__ void k_hubs(const uint32_t* __restrict__ deg, uint64_t n, uint32_t t,
       if (j < HUB_CAP) hubs[j] = (uint32_t)v;
     }
 }
-void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
-                   uint32_t* hub_scratch, uint64_t* hub_count, void* radix_scratch,
-                   uint64_t radix_bytes, uint32_t* radix_cursor) {
+int launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
+                  uint32_t* hub_scratch, uint64_t* hub_count, void* radix_scratch,
+                  uint64_t radix_bytes, uint32_t* radix_cursor) {
   // hub_count[0]: hub count; hub_count[8 .. 40): log2 histogram of the sample counts
-  if (!m) return;
+  if (!m) return 0;
   {
     // bucketed shared-memory count (default for n >= 2^20); CC_DEG_ALGO=radix|window forces one
     const char* e = getenv("CC_DEG_ALGO");
     const bool force_radix = e && e[0] == 'r', force_window = e && e[0] == 'w';
     if (radix_scratch && !force_window && (force_radix || n >= (1ull << 20)) &&
         launch_degree_radix(edges, m, n, deg, radix_scratch, radix_bytes, radix_cursor, st))
-      return;
+      return 1;
   }
   static uint64_t window = 0;
   if (!window) {  // CC_DEG_WINDOW_LOG2: experiment hook for the counter window
@@ -178,6 +178,7 @@ void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cu
       k_degree<false><<<grid_for((mr >> 1) + 1, 148 * 16), BLOCK, 0, st>>>(
           reinterpret_cast<const uint4*>(edges + m0), mr, deg, (uint32_t)lo, (uint32_t)hi, nullptr, nullptr);
   }
+  return 0;
 }
 
 // ---------------------------------------------------------------- degrees, bucketed

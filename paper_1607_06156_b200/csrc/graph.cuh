@@ -27,10 +27,11 @@ void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr,
 // radix_scratch (>= degree_radix_scratch(m, n) bytes) and radix_cursor (2048 u32): the
 // bucketed shared-memory count (graph.cu), used when n >= 2^20 (CC_DEG_ALGO=radix|window
 // forces one); otherwise, or when the scratch is too small, L2 increments in id windows.
-void launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
-                   uint32_t* hub_scratch = nullptr, uint64_t* hub_count = nullptr,
-                   void* radix_scratch = nullptr, uint64_t radix_bytes = 0,
-                   uint32_t* radix_cursor = nullptr);
+// returns 1 if the bucketed count ran, 0 for the L2-window increments
+int launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
+                  uint32_t* hub_scratch = nullptr, uint64_t* hub_count = nullptr,
+                  void* radix_scratch = nullptr, uint64_t radix_bytes = 0,
+                  uint32_t* radix_cursor = nullptr);
 uint64_t degree_radix_scratch(uint64_t m, uint64_t n);
 // deg[0, n) are the degrees of ids base .. base+n-1 (base > 0: a rank's vertex block)
 // the non-empty bins of hist[1, nb) as (degree, count) pairs into out, *cnt of them (unordered)
