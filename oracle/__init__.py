@@ -92,3 +92,15 @@ def relabel_u64(edges: np.ndarray):
 
 def components_from_labels(labels: np.ndarray) -> int:
     return int(np.count_nonzero(labels == np.arange(labels.shape[0], dtype=labels.dtype)))
+
+
+def component_size_histogram(labels: np.ndarray) -> dict:
+    """{component size: number of components of that size} from min-id labels (the
+    north-star invariant 'component-size histogram'; a component = the ids sharing a label,
+    PAPER.md:28)."""
+    lab = np.asarray(labels, dtype=np.int64)
+    if lab.shape[0] == 0:
+        return {}
+    _, sizes = np.unique(lab, return_counts=True)
+    s, c = np.unique(sizes, return_counts=True)
+    return {int(a): int(b) for a, b in zip(s, c)}

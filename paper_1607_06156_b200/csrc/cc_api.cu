@@ -91,6 +91,14 @@ cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
   }
   c->h_gctr = c->h_ctr + sv::C_NUM;
   c->h_word = reinterpret_cast<uint32_t*>(c->h_gctr + graph::G_NUM);
+  if (cudaMalloc(&c->d_agree, 2 * sizeof(uint64_t)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeHost(c->h_ctr);
+    cudaFreeHost(c->h_ctr2);
+    cudaFreeHost(c->h_hist);
+    delete c;
+    return CC_ERR_NOMEM;
+  }
   *out = c;
   return CC_OK;
 }
@@ -104,6 +112,7 @@ cc_status cc_destroy(cc_ctx* c) {
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   if (c->h_ctr2) cudaFreeHost(c->h_ctr2);
   if (c->h_hist) cudaFreeHost(c->h_hist);
+  if (c->d_agree) cudaFree(c->d_agree);
   delete c;
   return CC_OK;
 }
@@ -141,22 +150,9 @@ cc_status alloc_vertex_buffers(cc_ctx* c, uint64_t n) {
   return ensure_scan_tiles(c);
 }
 
-extern "C" {
-
-cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint64_t n, int on_dev) {
-  if (!c) return CC_ERR_INVALID;
-  if (m && !pairs) return fail(c, CC_ERR_INVALID, "pairs is NULL");
-  if (w != CC_U32 && w != CC_U64) return fail(c, CC_ERR_INVALID, "bad id width %d", (int)w);
-  // u64 ids over several ranks: the global id count is known only after the distributed
-  // relabel in cc_run, which then allocates the n-sized buffers (relabel_dist.cu)
-  const bool dist64 = w == CC_U64 && c->cfg.world_size > 1;
-  if (dist64 && (c->cfg.flags & CC_FLAG_PERMUTE_IDS))
-    return fail(c, CC_ERR_INVALID, "CC_FLAG_PERMUTE_IDS is single-GPU in this build");
-  if (w == CC_U64) {
-    if (n != 0) return fail(c, CC_ERR_INVALID, "u64 ids: n_vertices must be 0");
-    n = std::min<uint64_t>(2 * m, 1ull << 30);  // bound on distinct ids (checked in cc_run)
-  }
-  if (n > (1ull << 30)) return fail(c, CC_ERR_INVALID, "n_vertices %llu > 2^30", (unsigned long long)n);
+// Device buffers of a load (local: a rank's own m); the caller agrees on the outcome over
+// the ranks, so a rank that cannot allocate never leaves the others in a collective.
+static cc_status load_buffers(cc_ctx* c, cc_idw w, uint64_t m, uint64_t n, bool dist64) {
   if (2 * m + 2 * n >= (1ull << 32))
     return fail(c, CC_ERR_INVALID, "tuple count 2m+2n exceeds 2^32 on one GPU");
   CK(cudaSetDevice(c->cfg.device));
@@ -204,6 +200,26 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   CK(cudaMemsetAsync(c->rws.lookback, 0, sizeof(uint64_t) * c->rws.max_tiles * radix::RADIX, c->st));
   if (!dist64) TRY(alloc_vertex_buffers(c, n));
   else TRY(ensure_scan_tiles(c));
+  return CC_OK;
+}
+
+extern "C" {
+
+cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint64_t n, int on_dev) {
+  if (!c) return CC_ERR_INVALID;
+  if (m && !pairs) return fail(c, CC_ERR_INVALID, "pairs is NULL");
+  if (w != CC_U32 && w != CC_U64) return fail(c, CC_ERR_INVALID, "bad id width %d", (int)w);
+  // u64 ids over several ranks: the global id count is known only after the distributed
+  // relabel in cc_run, which then allocates the n-sized buffers (relabel_dist.cu)
+  const bool dist64 = w == CC_U64 && c->cfg.world_size > 1;
+  if (dist64 && (c->cfg.flags & CC_FLAG_PERMUTE_IDS))
+    return fail(c, CC_ERR_INVALID, "CC_FLAG_PERMUTE_IDS is single-GPU in this build");
+  if (w == CC_U64) {
+    if (n != 0) return fail(c, CC_ERR_INVALID, "u64 ids: n_vertices must be 0");
+    n = std::min<uint64_t>(2 * m, 1ull << 30);  // bound on distinct ids (checked in cc_run)
+  }
+  if (n > (1ull << 30)) return fail(c, CC_ERR_INVALID, "n_vertices %llu > 2^30", (unsigned long long)n);
+  TRY(comm_agree(c, load_buffers(c, w, m, n, dist64)));
   if (w == CC_U64) {
     if (m)
       CK(cudaMemcpyAsync(c->d_ids64, pairs, 2 * m * sizeof(uint64_t),

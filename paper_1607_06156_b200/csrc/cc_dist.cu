@@ -189,12 +189,22 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
     rb[k] = allc[(size_t)k * world + rank] * sizeof(uint2);
     na += allc[(size_t)k * world + rank];
   }
-  if (!c->d_recv || c->recv_cap < na + 1) {
-    TRY(dalloc_t(c, &c->d_recv, na + 1));
-    c->recv_cap = na + 1;
+  {
+    // the owned rows' tuples (received arcs + one vertex tuple per owned id) are indexed by
+    // 32-bit CSR offsets (csr::build, k_bfs_up): a skewed rank must not wrap them.  Every
+    // local failure before the next collective is agreed on by all ranks (comm_agree).
+    cc_status s = CC_OK;
+    if (na + (hi - lo) + 64 >= (1ull << 32))
+      s = fail(c, CC_ERR_INVALID, "rank %d owns %llu arcs + %llu ids: more than 2^32 tuples", rank,
+               (unsigned long long)na, (unsigned long long)(hi - lo));
+    if (s == CC_OK && (!c->d_recv || c->recv_cap < na + 1)) {
+      s = dalloc_t(c, &c->d_recv, na + 1);
+      if (s == CC_OK) c->recv_cap = na + 1;
+    }
+    TRY(comm_agree(c, s));
   }
   TRY(comm_alltoallv(c, c->d_send, sb.data(), c->d_recv, rb.data()));
-  TRY(ensure_tuple_cap(c, na + (hi - lo)));
+  TRY(comm_agree(c, ensure_tuple_cap(c, na + (hi - lo))));
   c->launches += 2;
 
   // ------------------------------------------------ prediction (Alg. 2 lines 2-3)
@@ -218,13 +228,15 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
     // degrees beyond the dense bins: gather every rank's short tail list
     if (dmax >= graph::HIST_DENSE) {
       const uint64_t mytail = c->h_gctr[graph::G_TAIL];
-      if (mytail > TAILX) return fail(c, CC_ERR_INVALID, "more than %u degrees >= 2^20 on one rank", TAILX);
+      cc_status s = CC_OK;
+      if (mytail > TAILX) s = fail(c, CC_ERR_INVALID, "more than %u degrees >= 2^20 on one rank", TAILX);
       // scratch: everyone's lists [0, world (TAILX + 1)), then my own (count, entries)
       const uint64_t need = (uint64_t)(world + 1) * (TAILX + 1);
-      if (!c->d_gath || c->gath_cap < need) {
-        TRY(dalloc_t(c, &c->d_gath, need));
-        c->gath_cap = need;
+      if (s == CC_OK && (!c->d_gath || c->gath_cap < need)) {
+        s = dalloc_t(c, &c->d_gath, need);
+        if (s == CC_OK) c->gath_cap = need;
       }
+      TRY(comm_agree(c, s));
       uint32_t* gathered = c->d_gath;
       uint32_t* stage = c->d_gath + (uint64_t)world * (TAILX + 1);
       uint32_t nt32 = (uint32_t)mytail;
@@ -265,7 +277,7 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
   CKL();
   TRY(sync_read(c));
   const uint64_t len = c->h_ctr[sv::C_VT_OUT];  // tuples of owned rows
-  if (len > c->cap) return fail(c, CC_ERR_INVALID, "tuple count exceeds capacity");
+  TRY(comm_agree(c, len > c->cap ? fail(c, CC_ERR_INVALID, "tuple count exceeds capacity") : CC_OK));
   csr::fill(c->d_recv, na, off, cur, n, len, Rt, Pt, garc, gshift, gcur,
             reinterpret_cast<uint2*>(c->d_w[1]), c->d_segB, nlong, c->st, /*directed=*/true);
   c->launches += 6;

@@ -81,6 +81,7 @@ struct cc_ctx {
   uint64_t xsend_cap = 0, xrecv_cap = 0;
   uint32_t* d_garc = nullptr;  // CSR vertex-group scratch: arcs per group (<= 2048 groups)
   uint64_t* d_gcur = nullptr;  // group cursors [0, 2048), long-row count at [2048]
+  uint64_t* d_agree = nullptr; // comm_agree word (cudaMalloc at cc_init, outside `allocs`)
   uint64_t* d_ctr = nullptr;   // sv counters
   uint64_t* d_gctr = nullptr;  // graph counters
   uint64_t* h_ctr = nullptr;   // pinned mirrors
@@ -350,6 +351,22 @@ static inline cc_status comm_alltoallv(cc_ctx* c, const void* send, const uint64
     return fail(c, CC_ERR_COMM, "alltoallv failed");
   return CC_OK;
 }
+// Failure agreement: every rank contributes its local status (MAX over ranks), so a rank
+// that fails locally (allocation, capacity, input checks) never leaves the others blocked in
+// the next collective -- all ranks return a failure together (CC_ERR_COMM on the ranks that
+// were fine, naming the failing status).  Costs one 8-byte all-reduce and a stream sync.
+static inline cc_status comm_agree(cc_ctx* c, cc_status mine) {
+  if (!multi_gpu(c)) return mine;
+  uint64_t* w = c->d_agree;
+  uint64_t v = (uint64_t)mine;
+  CK(cudaMemcpyAsync(w, &v, sizeof(uint64_t), cudaMemcpyHostToDevice, c->st));
+  TRY(comm_allreduce(c, w, 1, CC_DT_I64, CC_OP_MAX));
+  CK(cudaMemcpyAsync(&v, w, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (v == (uint64_t)CC_OK) return CC_OK;
+  if (mine != CC_OK) return mine;  // this rank's own error text is already in c->err
+  return fail(c, CC_ERR_COMM, "another rank failed with status %llu", (unsigned long long)v);
+}
 // min over ranks of u32 slots (INF = 0xFFFFFFFF): flip the sign bit so that the signed order of
 // the exchanged int32 equals the unsigned order, reduce, flip back
 static inline cc_status comm_min_u32(cc_ctx* c, uint32_t* a, uint64_t count) {
@@ -365,8 +382,9 @@ static inline cc_status comm_or_bits(cc_ctx* c, uint32_t* bm, uint64_t words) {
   if (!multi_gpu(c)) return CC_OK;
   const uint64_t need = words * (uint64_t)c->cfg.world_size;
   if (!c->d_gath || c->gath_cap < need) {
-    TRY(dalloc_t(c, &c->d_gath, need));
-    c->gath_cap = need;
+    cc_status s = dalloc_t(c, &c->d_gath, need);
+    if (s == CC_OK) c->gath_cap = need;
+    TRY(comm_agree(c, s));
   }
   TRY(comm_allgather(c, bm, c->d_gath, words * sizeof(uint32_t)));
   csr::or_parts(c->d_gath, words, c->cfg.world_size, bm, c->st);
@@ -382,8 +400,9 @@ static inline cc_status comm_sparse_slots(cc_ctx* c, uint32_t* S, uint32_t* BM, 
   if (!multi_gpu(c)) return CC_OK;
   const uint64_t world = (uint64_t)c->cfg.world_size;
   if (!c->d_xsend || c->xsend_cap < count + 1) {
-    TRY(dalloc_t(c, &c->d_xsend, count + 1));
-    c->xsend_cap = count + 1;
+    cc_status s = dalloc_t(c, &c->d_xsend, count + 1);
+    if (s == CC_OK) c->xsend_cap = count + 1;
+    TRY(comm_agree(c, s));
   }
   uint64_t* cnt = c->d_gcur + 2052;  // [2052]: my entries, [2053]: max over ranks
   csr::extract_slots(S, BM, count, c->d_xsend, cnt, c->st);
@@ -397,8 +416,9 @@ static inline cc_status comm_sparse_slots(cc_ctx* c, uint32_t* S, uint32_t* BM, 
   if (pad > mine)  // padding entries (slot ~0) up to the common length
     CK(cudaMemsetAsync(c->d_xsend + mine, 0xFF, sizeof(uint2) * (pad - mine), c->st));
   if (!c->d_xrecv || c->xrecv_cap < world * pad + 1) {
-    TRY(dalloc_t(c, &c->d_xrecv, world * pad + 1));
-    c->xrecv_cap = world * pad + 1;
+    cc_status s = dalloc_t(c, &c->d_xrecv, world * pad + 1);
+    if (s == CC_OK) c->xrecv_cap = world * pad + 1;
+    TRY(comm_agree(c, s));
   }
   TRY(comm_allgather(c, c->d_xsend, c->d_xrecv, pad * sizeof(uint2)));
   csr::apply_slots(c->d_xrecv, world * pad, S, BM, c->st);

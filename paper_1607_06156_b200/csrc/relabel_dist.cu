@@ -80,12 +80,16 @@ __global__ void k_scatter(const uint64_t* __restrict__ x, const uint32_t* __rest
 
 using namespace cc::rdist;
 
+// grow-once scratch; the outcome is agreed on by all ranks (comm_agree), since every call
+// site is followed by a collective that a rank which failed here would never enter
 template <typename T>
 static cc_status grow(cc_ctx* c, T** p, uint64_t* cap, uint64_t need) {
-  if (*p && *cap >= need) return CC_OK;
-  TRY(dalloc_t(c, p, need));
-  *cap = need;
-  return CC_OK;
+  cc_status s = CC_OK;
+  if (!*p || *cap < need) {
+    s = dalloc_t(c, p, need);
+    if (s == CC_OK) *cap = need;
+  }
+  return comm_agree(c, s);
 }
 
 // counts[j] of this rank -> everyone's; returns what each rank sends to this one

@@ -61,7 +61,7 @@ def _check(res, n, edges, modes, trace=True):
     return want
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_dist_c1(world):
     g = graphgen.make("c1", 0.5)
     modes = ("sv", "auto", "bfs+sv")

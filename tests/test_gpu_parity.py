@@ -221,22 +221,82 @@ def test_config_trace_parity(cc, cfg, scale):
     assert norm(trace_of(rep)) == norm(tr)
 
 
+def _golden_trace(cfg):
+    """Full-size SV trace written by tests/golden/make_traces.py (oracle.sv.sv_trace only)."""
+    p = os.path.join(ROOT, "tests", "golden", f"trace_{cfg}.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    g = graphgen.make(cfg)
+    assert (d["n"], d["m"]) == (g.n, g.m), "golden trace was written for another graph"
+    return d["trace"]
+
+
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
 def test_config_full_labels(cc, cfg):
-    """Full BASELINE.json sizes, the launch configuration bench.py times (mode=auto)."""
+    """Full BASELINE.json sizes, the launch configuration bench.py times (mode=auto), plus
+    the two hard-coded routes of fig:dynamic: labels bit-exact in every mode, the
+    mode=sv trace equal to the oracle's full-size golden trace counter by counter, and the
+    forced BFS (root, visited set size, levels, remainder) equal to oracle.bfs."""
     g = graphgen.make(cfg)
     want = oracle.uf_labels(g.n, g.edges).astype(np.int64)
-    for mode in ("auto", "sv"):
+    golden = _golden_trace(cfg)
+    assert golden is not None or cfg != "c1"
+    deg, _ = odeg.degree_distribution(g.n, g.edges)
+    root = obfs.bfs_root(deg)
+    vis, levels = obfs.bfs(g.n, g.edges, root)
+    for mode in ("auto", "sv", "bfs+sv"):
         lab, rep = run(cc, g.n, g.edges, mode)
         assert np.array_equal(lab, want), mode
-        assert rep["ran_bfs"] == (1 if mode == "bfs+sv" else 0)
+        assert oracle.component_size_histogram(lab) == oracle.component_size_histogram(want)
+        if mode == "auto":
+            assert rep["ran_bfs"] == 0  # bounded-degree configs: the gate says SV
+        if mode == "sv" and golden is not None:
+            assert norm(trace_of(rep)) == norm(golden), mode
+        if mode == "bfs+sv":
+            assert rep["ran_bfs"] == 1
+            assert rep["bfs_root"] == root
+            assert rep["bfs_visited"] == int(vis.sum())
+            assert rep["bfs_levels"] == levels
+            assert rep["remainder_edges"] == int(obfs.filter_edges(g.edges, vis).shape[0])
         # trace invariants at any size (C5, P:197): T = P - completed; A non-increasing
         its = rep["iters"]
         for i, it in enumerate(its):
             assert it["temps"] == it["partitions"] - it["completed"]
             if i:
                 assert it["active_in"] <= its[i - 1]["active_in"]
-        assert its[-1]["changed"] == 0
+        assert not its or its[-1]["changed"] == 0
+
+
+@pytest.mark.parametrize("graph", ["c1", "c2s", "rmat14", "rmat18"])
+@pytest.mark.parametrize("tau", [0.05, 0.2, 1.0])
+def test_gate_ks_decision(graph, tau):
+    """CC_FLAG_GATE_KS: the route is the paper's K-S < tau decision,
+    identical to the oracle's (oracle.hybrid with gate='ks'); labels bit-exact."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_06156_b200 as ccmod
+    if graph == "c1":
+        g = graphgen.make("c1")
+    elif graph == "c2s":
+        g = graphgen.make("c2", 0.05)
+    else:
+        g = graphgen.rmat_scale_graph(int(graph[4:]))
+    _, hist = odeg.degree_distribution(g.n, g.edges)
+    ks = odeg.ks_powerlaw(hist)
+    if ks["ks"] == ks["ks"]:
+        assert abs(ks["ks"] - tau) > 1e-6, "tau too close to the statistic for a stable decision"
+    want_bfs = bool(ks["ks"] == ks["ks"] and ks["ks"] < tau)
+    ctx = ccmod.CC(device=0, flags=ccmod.CC_FLAG_GATE_KS, tau=tau)
+    try:
+        lab, rep = run(ctx, g.n, g.edges, "auto")
+    finally:
+        ctx.close()
+    assert bool(rep["ran_bfs"]) == want_bfs
+    assert np.array_equal(lab, oracle.uf_labels(g.n, g.edges).astype(np.int64))
+    if graph == "rmat18" and tau == 0.05:
+        assert not want_bfs  # SURVEY §0.3: K-S does not call the synthetic R-MAT a power law
 
 
 def test_rmat_bfs_route(cc):

@@ -100,6 +100,47 @@ def test_uf_vs_scipy_and_invariants(seed):
     assert oracle.components_from_labels(lab) == nc
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_uf_component_size_histogram_vs_scipy(seed):
+    """Component-size histogram (north-star invariant) against scipy's component sizes."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(100, 5000))
+    e = graphgen.er(seed + 11, n, int(rng.integers(0, n)))
+    h = oracle.component_size_histogram(oracle.uf_labels(n, e))
+    g = sp.coo_matrix((np.ones(e.shape[0]), (e[:, 0].astype(np.int64), e[:, 1].astype(np.int64))),
+                      shape=(n, n))
+    _, comp = connected_components(g, directed=False)
+    s, c = np.unique(np.bincount(comp), return_counts=True)
+    assert h == {int(a): int(b) for a, b in zip(s, c)}
+    assert sum(k * v for k, v in h.items()) == n
+
+
+def test_uf_component_size_histogram_closed_form():
+    """Closed forms: disjoint cliques of sizes 1..12 (each size three times), paths of
+    lengths 1..40 and a star, ids scrambled by a random permutation; the histogram is known
+    by construction, independent of any labelling."""
+    rng = np.random.default_rng(7)
+    sizes, edges, base = [], [], 0
+    for k in list(range(1, 13)) * 3:
+        edges += [(base + a, base + b) for a, b in itertools.combinations(range(k), 2)]
+        sizes.append(k)
+        base += k
+    for k in range(1, 41):
+        edges += [(base + i, base + i + 1) for i in range(k - 1)]
+        sizes.append(k)
+        base += k
+    edges += [(base, base + i) for i in range(1, 500)]
+    sizes.append(500)
+    base += 500
+    perm = rng.permutation(base)
+    e = perm[np.array(edges, dtype=np.int64)].astype(np.uint32)
+    e = e[rng.permutation(e.shape[0])]
+    want = {}
+    for k in sizes:
+        want[k] = want.get(k, 0) + 1
+    assert oracle.component_size_histogram(oracle.uf_labels(base, e)) == want
+
+
 def test_uf_rejects_out_of_range():
     with pytest.raises(ValueError):
         oracle.uf_labels(3, np.array([[0, 3]], dtype=np.uint32))
