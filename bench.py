@@ -302,7 +302,12 @@ def main():
     ids = "u64" if u64 else "u32"
     mine = shard(g.edges, rk, ws)
     flags = (0 if args.no_profile else cc.CC_FLAG_PROFILE) | cc.REGROUP_FLAGS[args.regroup]
-    comm = cc.TorchComm(device=dev) if ws > 1 else None
+    # N > 1: the library owns an NCCL communicator (cfg.nccl_id, include/cc.h) and enqueues
+    # every exchange on its stream; the process group only broadcasts the NCCL id.  gloo (one
+    # shared GPU, correctness runs) goes through the cc_comm callbacks instead.
+    comm = None
+    if ws > 1:
+        comm = cc.NcclGroup.from_process_group() if backend == "nccl" else cc.TorchComm(device=dev)
     ctx = cc.CC(device=lr, stream=stream, flags=flags, comm=comm)
     d_edges = torch.from_numpy(mine.view(np.int64 if u64 else np.int32)).to(dev)
     ctx.load(d_edges, n, ids=ids)
@@ -475,8 +480,8 @@ def main():
                        "sv_iterations": rep["sv_iterations"],
                        "l2": ("inputs larger than L2 (edge list %.1f GB) and a 256 MiB write between "
                               "timed steps, outside the step's events" % (mine.nbytes / 1e9)),
-                       "parallelism": (f"{ws} ranks: edge blocks, vertex-block owners, NCCL slot "
-                                       "exchange" if ws > 1 else "1 GPU")},
+                       "parallelism": (f"{ws} ranks: edge blocks, vertex-block owners, library-owned "
+                                       f"NCCL exchange ({backend})" if ws > 1 else "1 GPU")},
             "roofline": roof,
             "kernels": kernels,
             "path_roofline": {"alg_bytes_per_step": path_bytes,

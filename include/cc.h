@@ -81,8 +81,18 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
                                         direction-optimising (top-down / bottom-up) BFS on the
                                         CSR rows instead of the edge-streaming BFS            */
 
-/* ---- multi-GPU exchange (world_size > 1).  The library runs one process per GPU; the
- * caller supplies the collectives (e.g. torch.distributed over NCCL, NVLink/NVSwitch).  Every
+/* ---- multi-GPU exchange (world_size > 1).  The library runs one process per GPU.  Two ways
+ * to connect the ranks:
+ *  (1) library-owned NCCL: rank 0 calls cc_get_unique_id, the caller
+ *      broadcasts the 128 bytes (e.g. torch.distributed.broadcast_object_list), and every
+ *      rank passes them as cfg.nccl_id.  cc_init then creates an NCCL communicator
+ *      (ncclCommInitRank; collective: all ranks must be inside cc_init together) and every
+ *      exchange is an NCCL call enqueued on cfg.stream -- no host synchronisation per
+ *      collective, no callback into the caller.  libnccl.so.2 is loaded at run time (the
+ *      copy already in the process if any; CC_NCCL_LIB=path overrides).  world_size == 1
+ *      with nccl_id runs the sharded driver on a 1-rank communicator (tests).
+ *  (2) caller callbacks (cfg.comm, below; used when nccl_id is NULL), e.g.
+ *      torch.distributed over gloo in the CPU-side tests.  Every
  * callback is entered with all earlier work on `stream` complete and must return 0 only once
  * its result is in place in the (device) buffers; nonzero -> CC_ERR_COMM.  All ranks call the
  * same sequence of collectives (SPMD).  Element types follow cc_dtype; the library maps its
@@ -115,7 +125,16 @@ typedef struct {
   double tau;          /* K-S threshold for CC_FLAG_GATE_KS; <= 0 => 0.05*/
   uint64_t seed;       /* reserved (deterministic run; no randomness is drawn)         */
   uint32_t flags;      /* CC_FLAG_*                                                    */
+  const void* nccl_id; /* CC_UNIQUE_ID_BYTES from cc_get_unique_id (rank 0, broadcast), or
+                          NULL.  Non-NULL: library-owned NCCL communicator (cfg.comm ignored) */
 } cc_config;
+
+#define CC_UNIQUE_ID_BYTES 128
+
+/* 128-byte NCCL unique id for cfg.nccl_id (call on rank 0 only, broadcast the bytes to the
+ * other ranks).  CC_ERR_COMM if libnccl cannot be loaded or fails (cc_last_error(NULL) is
+ * not available: the reason is written to `why` when non-NULL, up to why_len bytes). */
+cc_status cc_get_unique_id(void* out128, char* why, size_t why_len);
 
 /* One SV iteration (counters of SURVEY.md §8(c) "Trace oracle"). */
 typedef struct {
@@ -152,8 +171,9 @@ typedef struct {
 const char* cc_version(void);
 
 /* Create a context on cfg->device.  cfg is copied.  Returns CC_ERR_INVALID for a NULL
- * argument, a bad rank / world_size, or world_size > 1 without cfg->comm; CC_ERR_CUDA if the
- * device cannot be used.  In multi-GPU contexts (world_size > 1) cc_load_edges,
+ * argument, a bad rank / world_size, or world_size > 1 with neither cfg->nccl_id nor
+ * cfg->comm; CC_ERR_CUDA if the device cannot be used; CC_ERR_COMM if the NCCL communicator
+ * cannot be created (collective with nccl_id: every rank calls cc_init).  In multi-GPU contexts (world_size > 1) cc_load_edges,
  * cc_run are collective (every rank calls them, each with its own block of edges). */
 cc_status cc_init(const cc_config* cfg, cc_ctx** out);
 

@@ -59,7 +59,8 @@ class cc_config(ctypes.Structure):
                 ("world_size", ctypes.c_int), ("comm", ctypes.POINTER(cc_comm)),
                 ("alloc", ALLOC_FN), ("free", FREE_FN),
                 ("alloc_user", ctypes.c_void_p), ("tau", ctypes.c_double),
-                ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32)]
+                ("seed", ctypes.c_uint64), ("flags", ctypes.c_uint32),
+                ("nccl_id", ctypes.c_void_p)]
 
 
 class cc_iter_stat(ctypes.Structure):
@@ -85,7 +86,7 @@ class cc_report(ctypes.Structure):
                 ("n_iters", ctypes.c_uint32)]
 
 
-EXPORTS = ["cc_version", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
+EXPORTS = ["cc_version", "cc_get_unique_id", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
            "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_radix_sort_pairs",
            "cc_degree_histogram", "cc_degrees_u32",
            "cc_set_profiling", "cc_last_launch_count",
@@ -105,6 +106,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_last_error.restype = ctypes.c_char_p
     lib.cc_last_error.argtypes = [P]
     lib.cc_init.argtypes = [ctypes.POINTER(cc_config), ctypes.POINTER(P)]
+    lib.cc_get_unique_id.argtypes = [P, P, ctypes.c_size_t]
     lib.cc_load_edges.argtypes = [P, ctypes.c_int, P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]
     lib.cc_run.argtypes = [P, ctypes.c_int, ctypes.POINTER(cc_report)]
     lib.cc_labels_u32.argtypes = [P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
@@ -249,12 +251,51 @@ class TorchComm:
             return 1
 
 
+class NcclGroup:
+    """Library-owned NCCL communicator (include/cc.h cfg.nccl_id): rank 0 draws the 128-byte
+    id with cc_get_unique_id and torch.distributed broadcasts it (the only use of the process
+    group); cc_init then builds the communicator and every exchange is an NCCL call on the
+    library's stream.  ``NcclGroup.single()`` is a 1-rank communicator (the sharded driver on
+    one GPU, for tests)."""
+
+    def __init__(self, rank, world, uid: bytes):
+        if len(uid) != CC_UNIQUE_ID_BYTES:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self.rank, self.world, self.uid = rank, world, bytes(uid)
+        self._buf = ctypes.create_string_buffer(self.uid, CC_UNIQUE_ID_BYTES)
+
+    @classmethod
+    def from_process_group(cls, group=None):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cc_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+        return cls(rank, world, obj[0])
+
+    @classmethod
+    def single(cls):
+        return cls(0, 1, cc_get_unique_id())
+
+
+CC_UNIQUE_ID_BYTES = 128
+
+
+def cc_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(CC_UNIQUE_ID_BYTES)
+    why = ctypes.create_string_buffer(512)
+    st = lib().cc_get_unique_id(buf, why, 512)
+    if st != CC_OK:
+        raise CCError(st, why.value.decode(errors="replace"))
+    return buf.raw
+
+
 # ------------------------------------------------------------------ C-ABI-named wrappers
-def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=None):
+def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=None, alloc_limit=None):
     """Create a context.  ``stream``: a torch.cuda.Stream or raw cudaStream_t int (default:
     torch's current stream).  ``torch_alloc``: route device allocations through PyTorch's
-    caching allocator.  ``comm``: a :class:`TorchComm` for a multi-GPU (world_size > 1)
-    context; rank and world size are taken from it."""
+    caching allocator.  ``comm``: a :class:`NcclGroup` (library-owned NCCL) or a
+    :class:`TorchComm` (callbacks) for a multi-GPU context; rank and world size are taken
+    from it.  ``alloc_limit`` (tests): allocations above this many bytes fail (NOMEM)."""
     import torch
     if stream is None:
         stream = torch.cuda.current_stream(device)
@@ -264,7 +305,9 @@ def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=Non
     cfg.stream = sptr
     cfg.rank = comm.rank if comm else 0
     cfg.world_size = comm.world if comm else 1
-    if comm:
+    if isinstance(comm, NcclGroup):
+        cfg.nccl_id = ctypes.cast(comm._buf, ctypes.c_void_p)
+    elif comm:
         cfg.comm = ctypes.pointer(comm.struct)
     cfg.tau = tau
     cfg.flags = flags
@@ -273,6 +316,8 @@ def cc_init(device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=Non
         dev = device
 
         def _alloc(nbytes, st, user):
+            if alloc_limit is not None and nbytes > alloc_limit:
+                return None
             try:
                 return torch.cuda.caching_allocator_alloc(int(nbytes), dev, st or 0)
             except Exception:  # OOM -> NULL -> CC_ERR_NOMEM
@@ -440,8 +485,9 @@ def cc_destroy(ctx):
 class CC:
     """Convenience wrapper: ``CC().load(edges, n).run('auto')`` then ``.labels()``."""
 
-    def __init__(self, device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=None):
-        self.ctx, self._keep = cc_init(device, stream, flags, tau, torch_alloc, comm)
+    def __init__(self, device=0, stream=None, flags=0, tau=0.05, torch_alloc=True, comm=None,
+                 alloc_limit=None):
+        self.ctx, self._keep = cc_init(device, stream, flags, tau, torch_alloc, comm, alloc_limit)
 
     def load(self, pairs, n_vertices, ids="u32"):
         cc_load_edges(self.ctx, pairs, n_vertices, ids)

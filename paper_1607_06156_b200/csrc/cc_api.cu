@@ -61,13 +61,23 @@ cc_status cc_set_profiling(cc_ctx* c, int on) {
   return CC_OK;
 }
 
+cc_status cc_get_unique_id(void* out128, char* why, size_t why_len) {
+  if (!out128) return CC_ERR_INVALID;
+  std::string e;
+  if (nccl::unique_id(out128, &e)) {
+    if (why && why_len) std::snprintf(why, why_len, "%s", e.c_str());
+    return CC_ERR_COMM;
+  }
+  return CC_OK;
+}
+
 cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
   if (!cfg || !out) return CC_ERR_INVALID;
   *out = nullptr;
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return CC_ERR_INVALID;
-  if (cfg->world_size > 1 && (!cfg->comm || !cfg->comm->allreduce || !cfg->comm->allgather ||
-                              !cfg->comm->alltoallv))
-    return CC_ERR_INVALID;  // multi-GPU contexts need the caller's collectives
+  if (cfg->world_size > 1 && !cfg->nccl_id &&
+      (!cfg->comm || !cfg->comm->allreduce || !cfg->comm->allgather || !cfg->comm->alltoallv))
+    return CC_ERR_INVALID;  // multi-GPU contexts need NCCL or the caller's collectives
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
     cudaGetLastError();
@@ -78,6 +88,15 @@ cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
   cc_ctx* c = new cc_ctx();
   c->cfg = *cfg;
   if (c->cfg.tau <= 0) c->cfg.tau = 0.05;
+  if (cfg->nccl_id) {
+    std::string e;
+    if (nccl::init(&c->nccl, cfg->nccl_id, cfg->world_size, cfg->rank, cfg->device, &e)) {
+      std::fprintf(stderr, "cc_init: %s\n", e.c_str());
+      delete c;
+      return CC_ERR_COMM;
+    }
+  }
+  c->dist = cfg->world_size > 1 || c->nccl != nullptr;
   c->st = (cudaStream_t)cfg->stream;
   if (cudaMallocHost(&c->h_ctr, sizeof(uint64_t) * (sv::C_NUM + graph::G_NUM + 8)) != cudaSuccess ||
       cudaMallocHost(&c->h_ctr2, sizeof(uint64_t) * 2 * sv::C_NUM) != cudaSuccess ||
@@ -86,6 +105,7 @@ cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
     if (c->h_ctr) cudaFreeHost(c->h_ctr);
     if (c->h_ctr2) cudaFreeHost(c->h_ctr2);
     if (c->h_hist) cudaFreeHost(c->h_hist);
+    if (c->nccl) nccl::destroy(c->nccl);
     delete c;
     return CC_ERR_NOMEM;
   }
@@ -96,6 +116,7 @@ cc_status cc_init(const cc_config* cfg, cc_ctx** out) {
     cudaFreeHost(c->h_ctr);
     cudaFreeHost(c->h_ctr2);
     cudaFreeHost(c->h_hist);
+    if (c->nccl) nccl::destroy(c->nccl);
     delete c;
     return CC_ERR_NOMEM;
   }
@@ -113,6 +134,7 @@ cc_status cc_destroy(cc_ctx* c) {
   if (c->h_ctr2) cudaFreeHost(c->h_ctr2);
   if (c->h_hist) cudaFreeHost(c->h_hist);
   if (c->d_agree) cudaFree(c->d_agree);
+  if (c->nccl) nccl::destroy(c->nccl);
   delete c;
   return CC_OK;
 }
@@ -175,7 +197,7 @@ static cc_status load_buffers(cc_ctx* c, cc_idw w, uint64_t m, uint64_t n, bool 
   }
   TRY(dalloc_t(c, &c->d_lsegs, csr::long_seg_cap(c->cap)));
   TRY(dalloc_t(c, &c->d_nlsegs, 2));
-  if (world > 1) {
+  if (multi_gpu(c)) {
     TRY(dalloc_t(c, &c->d_send, 2 * m + 1));
     TRY(dalloc_t(c, &c->d_cnt, 2 * world + world * world));
   }
@@ -211,7 +233,7 @@ cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint
   if (w != CC_U32 && w != CC_U64) return fail(c, CC_ERR_INVALID, "bad id width %d", (int)w);
   // u64 ids over several ranks: the global id count is known only after the distributed
   // relabel in cc_run, which then allocates the n-sized buffers (relabel_dist.cu)
-  const bool dist64 = w == CC_U64 && c->cfg.world_size > 1;
+  const bool dist64 = w == CC_U64 && multi_gpu(c);
   if (dist64 && (c->cfg.flags & CC_FLAG_PERMUTE_IDS))
     return fail(c, CC_ERR_INVALID, "CC_FLAG_PERMUTE_IDS is single-GPU in this build");
   if (w == CC_U64) {
@@ -387,7 +409,7 @@ static cc_status run_sv_csr(cc_ctx* c, const uint2* edges, uint64_t m_sv, const 
 cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   const uint64_t n = c->n;
   const uint64_t nw = (n + 31) / 32;
-  const bool multi = c->cfg.world_size > 1;
+  const bool multi = multi_gpu(c);
   uint32_t* R[2] = {reinterpret_cast<uint32_t*>(c->d_w[0]), reinterpret_cast<uint32_t*>(c->d_w[1])};
   uint32_t* P[2] = {R[0] + c->cap, R[1] + c->cap};
   int cb = 0;  // buffer holding the tuple array

@@ -12,6 +12,7 @@
 #include "../../include/cc.h"
 #include "csr.cuh"
 #include "graph.cuh"
+#include "nccl_comm.h"
 #include "radix.cuh"
 #include "scan.cuh"
 #include "sv.cuh"
@@ -21,6 +22,8 @@ using namespace cc;
 struct cc_ctx {
   cc_config cfg{};
   cudaStream_t st = nullptr;
+  void* nccl = nullptr;  // library-owned ncclComm_t (cfg.nccl_id), else the cfg.comm callbacks
+  bool dist = false;     // sharded driver: world_size > 1, or a 1-rank NCCL communicator
   std::string err;
   // graph
   bool loaded = false, ran = false;
@@ -325,11 +328,18 @@ static inline cc_status ensure_tuple_cap(cc_ctx* c, uint64_t tuples) {
 }
 
 // ------------------------------------------------------------------------------ collectives
-// Thin wrappers over the caller's cc_comm (world_size > 1): synchronise the stream, call,
-// map a nonzero return to CC_ERR_COMM.  No-ops on one GPU.
-static inline bool multi_gpu(const cc_ctx* c) { return c->cfg.world_size > 1; }
+// Library-owned NCCL (cfg.nccl_id): enqueued on the library stream, ordered by the device,
+// no host synchronisation.  Caller callbacks (cfg.comm): synchronise the stream, call, map a
+// nonzero return to CC_ERR_COMM.  No-ops on one GPU.
+static inline bool multi_gpu(const cc_ctx* c) { return c->dist; }
 static inline cc_status comm_allreduce(cc_ctx* c, void* buf, uint64_t count, int dt, int op) {
   if (!multi_gpu(c)) return CC_OK;
+  if (c->nccl) {
+    std::string e;
+    if (nccl::allreduce(c->nccl, buf, count, dt, op, c->st, &e))
+      return fail(c, CC_ERR_COMM, "allreduce(count=%llu): %s", (unsigned long long)count, e.c_str());
+    return CC_OK;
+  }
   CK(cudaStreamSynchronize(c->st));
   if (c->cfg.comm->allreduce(c->cfg.comm->user, buf, count, dt, op, (void*)c->st) != 0)
     return fail(c, CC_ERR_COMM, "allreduce(count=%llu, dtype=%d, op=%d) failed",
@@ -338,6 +348,12 @@ static inline cc_status comm_allreduce(cc_ctx* c, void* buf, uint64_t count, int
 }
 static inline cc_status comm_allgather(cc_ctx* c, const void* send, void* recv, uint64_t bytes) {
   if (!multi_gpu(c)) return CC_OK;
+  if (c->nccl) {
+    std::string e;
+    if (nccl::allgather(c->nccl, send, recv, bytes, c->st, &e))
+      return fail(c, CC_ERR_COMM, "allgather(%llu bytes): %s", (unsigned long long)bytes, e.c_str());
+    return CC_OK;
+  }
   CK(cudaStreamSynchronize(c->st));
   if (c->cfg.comm->allgather(c->cfg.comm->user, send, recv, bytes, (void*)c->st) != 0)
     return fail(c, CC_ERR_COMM, "allgather(%llu bytes) failed", (unsigned long long)bytes);
@@ -346,6 +362,12 @@ static inline cc_status comm_allgather(cc_ctx* c, const void* send, void* recv, 
 static inline cc_status comm_alltoallv(cc_ctx* c, const void* send, const uint64_t* sb, void* recv,
                                        const uint64_t* rb) {
   if (!multi_gpu(c)) return CC_OK;
+  if (c->nccl) {
+    std::string e;
+    if (nccl::alltoallv(c->nccl, c->cfg.world_size, send, sb, recv, rb, c->st, &e))
+      return fail(c, CC_ERR_COMM, "alltoallv: %s", e.c_str());
+    return CC_OK;
+  }
   CK(cudaStreamSynchronize(c->st));
   if (c->cfg.comm->alltoallv(c->cfg.comm->user, send, sb, recv, rb, (void*)c->st) != 0)
     return fail(c, CC_ERR_COMM, "alltoallv failed");
@@ -371,6 +393,7 @@ static inline cc_status comm_agree(cc_ctx* c, cc_status mine) {
 // the exchanged int32 equals the unsigned order, reduce, flip back
 static inline cc_status comm_min_u32(cc_ctx* c, uint32_t* a, uint64_t count) {
   if (!multi_gpu(c)) return CC_OK;
+  if (c->nccl) return comm_allreduce(c, a, count, nccl::DT_U32, CC_OP_MIN);  // NCCL has u32 MIN
   csr::flip_sign(a, count, c->st);
   TRY(comm_allreduce(c, a, count, CC_DT_I32, CC_OP_MIN));
   csr::flip_sign(a, count, c->st);

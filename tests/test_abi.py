@@ -86,3 +86,16 @@ def test_bench_reference_arm_prints_contract_line():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_unique_id_host_only(lib):
+    """cc_get_unique_id: 128 bytes from the NCCL the library loads at run time
+    (no GPU needed); NULL output is rejected with a status."""
+    import paper_1607_06156_b200 as cc
+    assert lib.cc_get_unique_id(None, None, 0) == 1
+    try:
+        a = cc.cc_get_unique_id()
+    except cc.CCError as e:  # no usable NCCL / network interface in this container
+        pytest.skip(str(e))
+    assert isinstance(a, bytes) and len(a) == cc.CC_UNIQUE_ID_BYTES
+    assert a != cc.cc_get_unique_id()

@@ -255,3 +255,92 @@ def test_torchcomm_nccl_world1():
     assert res[1] == [1, 2]
     assert res[2] == list(range(12))
     assert res[3] == [100 + i for i in range(8)]
+
+
+# ------------------------------------------------------------------ library-owned NCCL
+def _nccl_own_world1(rank, world, cases):
+    """cfg.nccl_id at world 1: the sharded driver (owner regroup, prediction reductions,
+    bottom-up BFS, slot exchanges, u64 distributed relabel) on a 1-rank NCCL communicator
+    created by the library, every collective an NCCL call on the library stream."""
+    import torch
+    import paper_1607_06156_b200 as cc
+    torch.cuda.set_device(0)
+    grp = cc.NcclGroup.single()
+    ctx = cc.CC(device=0, flags=cc.CC_FLAG_TRACE, comm=grp)
+    out = []
+    try:
+        for kind, n, e, modes in cases:
+            if kind == "u32":
+                ctx.load(e, n)
+                for mode in modes:
+                    rep = ctx.run(mode)
+                    out.append((kind, mode, ctx.labels().copy(), rep))
+            else:
+                ctx.load(e, 0, ids="u64")
+                for mode in modes:
+                    rep = ctx.run(mode)
+                    out.append((kind, mode, ctx.labels_u64(), rep))
+    finally:
+        ctx.close()
+    return out
+
+
+def test_nccl_owned_world1():
+    g1 = graphgen.make("c1", 0.5)
+    g2 = graphgen.rmat_scale_graph(14)
+    rng = np.random.default_rng(9)
+    ids = rng.integers(0, 2**63, size=3000, dtype=np.uint64)
+    e64 = ids[rng.integers(0, 3000, size=(5000, 2))]
+    cases = [("u32", g1.n, g1.edges, ("sv", "bfs+sv")), ("u32", g2.n, g2.edges, ("auto", "sv")),
+             ("u64", 0, e64, ("sv",))]
+    res = run_ranks(_nccl_own_world1, 1, cases)[0]
+    k = 0
+    for kind, n, e, modes in cases:
+        for mode in modes:
+            _, mode_got, lab, rep = res[k]
+            k += 1
+            assert mode_got == mode
+            if kind == "u32":
+                assert np.array_equal(lab, oracle.uf_labels(n, e)), mode
+                if mode == "sv":
+                    _, tr = osv.sv_trace(n, e)
+                    got = [dict(A=it["active_in"], P=it["partitions"], T=it["temps"],
+                                completed=it["completed"], changed=it["changed"], changed2=it["changed2"])
+                           for it in rep["iters"]]
+                    assert [{a: int(b) for a, b in d.items()} for d in got] == \
+                        [{a: int(d[a]) for a in ("A", "P", "T", "completed", "changed", "changed2")} for d in tr]
+                if mode == "auto":
+                    assert rep["ran_bfs"] == 1
+            else:
+                want = oracle.uf_labels_u64(e)
+                assert np.array_equal(lab[0], want[0]) and np.array_equal(lab[1], want[1])
+
+
+# ------------------------------------------------------------------ failure agreement
+def _rank_fail(rank, world, n, edges, limit_rank, limit):
+    import torch
+    import paper_1607_06156_b200 as cc
+    torch.cuda.set_device(0)
+    comm = cc.TorchComm(device=torch.device("cuda", 0))
+    ctx = cc.CC(device=0, comm=comm, alloc_limit=limit if rank == limit_rank else None)
+    m = edges.shape[0]
+    a, b = m * rank // world, m * (rank + 1) // world
+    try:
+        ctx.load(np.ascontiguousarray(edges[a:b]), n)
+        ctx.run("sv")
+        return ("ok", None)
+    except cc.CCError as e:
+        return ("err", e.status)
+    finally:
+        ctx.close()
+
+
+def test_dist_failure_agreement():
+    """A local failure on one rank (an allocation the allocator refuses) is agreed on by every
+    rank before the next collective: all ranks raise (the failing rank NOMEM, the others
+    COMM), none is left blocked in a collective (collective error paths)."""
+    import paper_1607_06156_b200 as cc
+    g = graphgen.make("c1", 0.5)
+    res = run_ranks(_rank_fail, 2, g.n, g.edges, 1, 1 << 16, timeout=120)
+    assert res[1] == ("err", cc.CC_ERR_NOMEM)
+    assert res[0] == ("err", cc.CC_ERR_COMM)
