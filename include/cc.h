@@ -77,6 +77,8 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
 #define CC_FLAG_REGROUP_SORT 0x8u
 #define CC_FLAG_REGROUP_DIRECT 0x20u
 #define CC_FLAG_PROFILE 0x10u        /* CUDA-event timing of kernel families (cc_kernel_stats) */
+#define CC_FLAG_NO_COLLAPSE 0x200u   /* csr engine: never collapse potentially-completed rows
+                                        to one tuple (ablation; DESIGN.md §5.2 row collapse) */
 #define CC_FLAG_BFS_CSR 0x40u        /* csr engine: degrees from the bucketed CSR build and a
                                         direction-optimising (top-down / bottom-up) BFS on the
                                         CSR rows instead of the edge-streaming BFS            */

@@ -32,6 +32,7 @@ CC_FLAG_PROFILE = 0x10
 CC_FLAG_BFS_CSR = 0x40
 CC_FLAG_NO_EXCLUDE = 0x80
 CC_FLAG_PERMUTE_IDS = 0x100
+CC_FLAG_NO_COLLAPSE = 0x200
 EXCLUSION_FLAGS = {"early": 0, "end": CC_FLAG_NO_EARLY_EXCLUDE, "none": CC_FLAG_NO_EXCLUDE}
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -167,6 +168,7 @@ cc_status alloc_vertex_buffers(cc_ctx* c, uint64_t n) {
   TRY(dalloc_t(c, &c->d_plist[1], n + 1));
   TRY(dalloc_t(c, &c->d_plcnt, 2));
   TRY(dalloc_t(c, &c->d_nx, nw + 2));
+  TRY(dalloc_t(c, &c->d_hw, n + 1));
   CK(cudaMemsetAsync(c->d_umin, 0xFF, sizeof(uint64_t) * (n + 1), c->st));
   CK(cudaMemsetAsync(c->d_umax, 0, sizeof(uint64_t) * (n + 1), c->st));
   return ensure_scan_tiles(c);
@@ -455,6 +457,17 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   // pass A gains from the block tables below 1/512 partitions per live tuple, pass B below 1/128
   constexpr int HOT_A = 9, HOT_B = 7;
   uint32_t next_enq = 0;
+  // Row collapse (one GPU, paper exclusion): once partitions are large, most rows are PC and
+  // stay PC; collapse() folds each to its head tuple, so later passes stream ~one tuple per
+  // vertex.  hidden = folded tuples of the rows still live (A_i = live tuples + hidden).
+  const bool can_collapse = !multi && excl && !temps_all && !(c->cfg.flags & CC_FLAG_NO_COLLAPSE);
+  bool collapse_ok = can_collapse, hw_ready = false, pending_collapse = false;
+  uint64_t hidden = 0;
+  uint32_t last_collapse = 0;
+  // CC_COLLAPSE_FORCE=1 (tests): collapse after every iteration from the first, at any size
+  const char* cf = getenv("CC_COLLAPSE_FORCE");
+  const bool collapse_force = cf && cf[0] == '1';
+  const uint64_t COLLAPSE_MIN_LEN = collapse_force ? 0 : (1ull << 16);
   auto enqueue = [&](uint32_t it) -> cc_status {
     cudaEvent_t ev_it = ev_get(c);
     CK(cudaEventRecord(ev_it, c->st));
@@ -496,7 +509,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
                    c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, false, ctr, c->st,
-                   excl, false, prevctr, HOT_B);
+                   excl, false, prevctr, HOT_B, hw_ready ? c->d_hw : nullptr);
       k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
     // live tuples: this rank's (compaction) and the global count (convergence)
@@ -542,6 +555,11 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     const uint64_t* h = c->h_ctr2 + (it & 1) * sv::C_NUM;
     const uint64_t A1 = h[sv::C_OUT];
     const uint64_t len_live = multi ? h[sv::C_SURVIVORS] : A1;
+    if (hw_ready) {
+      if (h[sv::C_HIDDEN_DEAD] > hidden)
+        return fail(c, CC_ERR_INVALID, "internal: collapsed-row count underflow");
+      hidden -= h[sv::C_HIDDEN_DEAD];
+    }
     cc_iter_stat s{};
     s.active_in = A;
     s.partitions = h[sv::C_PARTITIONS];
@@ -562,7 +580,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       s.active_min = r2[0];
       s.active_max = r2[1];
     }
-    local_in = len_live;
+    local_in = multi ? len_live : A1 + hidden;
     c->iters.push_back(s);
     if (!excl) {
       // 'Naive': nothing leaves; the partition passes decide convergence
@@ -572,6 +590,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
         break;
       }
     } else if (A1 == 0) {
+      if (hidden) return fail(c, CC_ERR_INVALID, "internal: collapsed rows left at convergence");
       if (next_enq == it + 2)  // a look-ahead iteration is in flight: it returns at once
         for (int f = 0; f < KF_N; f++) {
           c->kst[f].ev.resize(snap[f].nev);
@@ -584,22 +603,52 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     // dead rows of completed partitions are squeezed out once they are a third of the array
     // (the paper's 'swapped to the end of the local array', sec:distSVOpt1); with the next
     // iteration already in flight, after it (its counts are exact then)
-    const bool want = 3 * (len - len_live) > len;
+    // collapse once an average partition spans many tuples (then almost every row is PC),
+    // at most every other iteration, and not again after one that folded little
+    const bool want_collapse =
+        collapse_force ? can_collapse && len_live > 0
+                       : collapse_ok && it >= 1 && it >= last_collapse + 2 && len_live >= COLLAPSE_MIN_LEN &&
+                             s.partitions * 16 < len_live;
+    const bool want = 3 * (len - len_live) > len || want_collapse;
     if (pending_compact || (want && next_enq == it + 1)) {
-      pending_compact = false;
+      const bool do_collapse = pending_collapse || want_collapse;
+      pending_compact = pending_collapse = false;
       TRY(scan_epoch_guard(c));
-      { Prof k(c, KF_COMPACT); csr::compact(R[cb], Pc, len, R[cb ^ 1], P[cb ^ 1], c->ss, c->st);
-        k.end(8.0 * len + 8.0 * len_live, 1); }
+      if (do_collapse) {
+        if (!hw_ready) {
+          CK(cudaMemsetAsync(c->d_hw, 0, sizeof(uint32_t) * n, c->st));
+          hw_ready = true;
+        }
+        uint64_t* hc = c->d_gcur + 2054;  // [2054]: folded tuples, [2055]: output length
+        CK(cudaMemsetAsync(hc, 0, sizeof(uint64_t), c->st));
+        { Prof k(c, KF_COMPACT);
+          csr::collapse(R[cb], Pc, len, R[cb ^ 1], P[cb ^ 1], c->d_hw, hc, hc + 1, c->ss, c->st);
+          k.end(8.0 * len + 8.0 * len_live, 1); }
+        uint64_t hv[2] = {0, 0};
+        CK(cudaMemcpyAsync(hv, hc, sizeof(hv), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        hidden += hv[0];
+        if (hv[1] + hv[0] != len_live)
+          return fail(c, CC_ERR_INVALID, "internal: collapse kept %llu + folded %llu of %llu live tuples",
+                      (unsigned long long)hv[1], (unsigned long long)hv[0], (unsigned long long)len_live);
+        collapse_ok = hv[0] * 8 >= len_live;  // folded >= 1/8: worth trying again later
+        last_collapse = it;
+        len = hv[1];
+      } else {
+        { Prof k(c, KF_COMPACT); csr::compact(R[cb], Pc, len, R[cb ^ 1], P[cb ^ 1], c->ss, c->st);
+          k.end(8.0 * len + 8.0 * len_live, 1); }
+        len = len_live;
+      }
       c->launches += 1;
       cb ^= 1;
-      len = len_live;
       Pc = P[cb];
       Palt = c->d_q[0];
       if (have_long) csr::longlist(R[cb], Pc, len, c->d_deg, c->d_lsegs, c->d_nlsegs, c->st);
     } else if (want) {
       pending_compact = true;
+      pending_collapse = want_collapse;
     }
-    A = A1;
+    A = A1 + hidden;
     if (next_enq == it + 1) TRY(enqueue(it + 1));
   }
   CK(cudaStreamSynchronize(c->st));

@@ -55,7 +55,9 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
              cudaStream_t st, bool excl = true, bool preset = false, const uint64_t* prevctr = nullptr,
-             int hot_shift = 0);
+             int hot_shift = 0, const uint32_t* HW = nullptr);
+// HW (pass B, row collapse): HW[r] = tuples folded into row r by collapse(); a row that leaves
+// adds them to ctr[C_HIDDEN_DEAD] (NULL before the first collapse of a run)
 // prevctr (device, the previous iteration's sv counters): the pass returns at once when it
 // left no live tuple, and is hot when |P_prev| << hot_shift < L (overrides `hot`)
 // partition statistics after pass A (sets TB, clears PB); slot arrays padded to 4*ceil(n/4)
@@ -88,6 +90,14 @@ void apply_slots(const uint2* in, uint64_t count, uint32_t* S, uint32_t* BM, cud
 // multi-GPU slot exchange helpers: a[i] ^= 0x80000000; out[i] = OR_k parts[k*words + i]
 void flip_sign(uint32_t* a, uint64_t n, cudaStream_t st);
 void or_parts(const uint32_t* parts, uint64_t words, int world, uint32_t* out, cudaStream_t st);
+// ordered compaction that also collapses every potentially-completed row (all live p equal,
+// PAPER.md:150-155) that lies inside one compaction tile and is not a long row to its head
+// tuple: such a row stays PC for good (one relabel maps its equal values to one value), so its
+// other tuples repeat the head's bucket updates (min is idempotent).  HW[r] += the tuples
+// folded into row r, *hidden += their total, *out_len = the output length.  Partition sets,
+// completion, temporaries and every trace counter are unchanged; A_i = live + hidden.
+void collapse(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2, uint32_t* HW,
+              uint64_t* hidden, uint64_t* out_len, scan::State& ss, cudaStream_t st);
 // ordered compaction of live tuples (R order kept); output count = live count
 void compact(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2,
              scan::State& ss, cudaStream_t st);

@@ -66,6 +66,7 @@ struct cc_ctx {
   uint32_t* d_plist[2] = {nullptr, nullptr};  // csr engine: partition-id supersets L_i (slot scans)
   uint64_t* d_plcnt = nullptr;                // their lengths
   uint32_t* d_nx = nullptr;                   // bitmap of the next L (values of PB)
+  uint32_t* d_hw = nullptr;                   // csr engine: tuples folded into each row (collapse)
   uint64_t* d_umin = nullptr;  // csr engine: tagged partial row minima / maxima
   uint64_t* d_umax = nullptr;
   csr::LongSeg* d_lsegs = nullptr;  // csr engine: segments of rows longer than csr::LONG

@@ -13,6 +13,7 @@ enum Ctr : int {
   C_CHANGED,        // p_min != p at pass 2
   C_TEMPS,          // temporaries emitted
   C_CHANGED2,       // p_min != p at pass 4
+  C_HIDDEN_DEAD,    // csr engine: collapsed tuples of the rows that left in pass B (row collapse)
   C_SURVIVORS,      // non-temporary tuples kept
   C_VT_OUT,         // vertex-tuple cursor (init)
   C_ERR,            // error flags (range)

@@ -477,6 +477,132 @@ __global__ void __launch_bounds__(B) k_compact(const uint32_t* __restrict__ R,
   }
 }
 
+// ===================================================================== row collapse
+// Ordered compaction that also folds every collapsible row to its head tuple (csr.cuh
+// collapse()).  A row is collapsible when it lies inside this tile (it neither continues from
+// the previous tile nor into the next), is not a long row (k_long1/k_long2 own those, and
+// their segment list is built from the degrees) and all its p are equal (PC).  Dead rows
+// (completed partitions) leave whole, as in k_compact.
+__global__ void __launch_bounds__(B) k_collapse(const uint32_t* __restrict__ R,
+                                                const uint32_t* __restrict__ P, uint64_t A,
+                                                uint32_t* __restrict__ R2, uint32_t* __restrict__ P2,
+                                                uint32_t* __restrict__ HW, unsigned long long* hidden,
+                                                unsigned long long* out_len, uint64_t ntiles,
+                                                uint64_t* flags, uint32_t* ticket, uint32_t epoch) {
+  __shared__ uint32_t s_scan[B / 32 + 1];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_pref;
+  __shared__ uint32_t s_r[CTILE], s_p[CTILE];
+  __shared__ uint32_t s_bad[CTILE], s_cnt[CTILE];  // per row head (local index)
+  __shared__ uint32_t s_wmax[B / 32];
+  __shared__ unsigned long long s_hid;
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(ticket, 1u);
+    s_hid = 0;
+  }
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t t0 = tile * CTILE;
+  const uint32_t x0 = threadIdx.x * CITEMS;
+  const uint32_t rbefore = t0 > 0 ? R[t0 - 1] : 0xFFFFFFFFu;           // uniform loads
+  const uint32_t rafter = t0 + CTILE < A ? R[t0 + CTILE] : 0xFFFFFFFFu;
+  uint32_t r[CITEMS], p[CITEMS];
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++) {
+    const uint64_t i = t0 + x0 + k;
+    r[k] = i < A ? R[i] : 0xFFFFFFFEu;  // past the end: a key no row has
+    p[k] = i < A ? P[i] : DEAD;
+    s_r[x0 + k] = r[k];
+    s_p[x0 + k] = p[k];
+    s_bad[x0 + k] = 0;
+    s_cnt[x0 + k] = 0;
+  }
+  __syncthreads();
+  // head position (+1) of the row holding each item: block-wide inclusive max scan of the
+  // heads (0 = the row started in the previous tile)
+  uint32_t hh[CITEMS];
+  uint32_t run = 0;
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++) {
+    const uint32_t x = x0 + k;
+    const uint32_t rp = x ? s_r[x - 1] : rbefore;
+    if (rp != r[k]) run = x + 1;
+    hh[k] = run;
+  }
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t v = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v = max(v, y);
+    }
+    if (lane == 31) s_wmax[wid] = v;
+    __syncthreads();
+    uint32_t carry = __shfl_up_sync(0xffffffffu, v, 1);
+    if (lane == 0) carry = 0;
+    for (int w = 0; w < wid; w++) carry = max(carry, s_wmax[w]);
+#pragma unroll
+    for (int k = 0; k < CITEMS; k++) {
+      if (hh[k]) break;  // items before the thread's first head take the carry
+      hh[k] = carry;
+    }
+  }
+  // a row is not collapsible if it is long, has two different p, or reaches the next tile
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++) {
+    const uint32_t x = x0 + k;
+    if (!hh[k] || p[k] == DEAD) continue;
+    const uint32_t h = hh[k] - 1;
+    bool bad = (r[k] & R_LONG) != 0;
+    if (x != h && s_p[x - 1] != p[k]) bad = true;
+    if (x == CTILE - 1 && rafter == r[k]) bad = true;
+    if (bad) s_bad[h] = 1;
+  }
+  __syncthreads();
+  uint32_t keep = 0, cnt = 0;
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++) {
+    const uint32_t x = x0 + k;
+    bool kp = p[k] != DEAD;
+    if (kp && hh[k] && x != hh[k] - 1 && !s_bad[hh[k] - 1]) {
+      kp = false;
+      atomicAdd(&s_cnt[hh[k] - 1], 1u);
+    }
+    keep |= (uint32_t)kp << k;
+    cnt += kp;
+  }
+  __syncthreads();
+  // heads of collapsed rows record the folded tuples (a row lies in one tile: plain add)
+  unsigned long long hid = 0;
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++) {
+    const uint32_t x = x0 + k;
+    if (hh[k] == x + 1 && s_cnt[x]) {
+      HW[r[k]] += s_cnt[x];
+      hid += s_cnt[x];
+    }
+  }
+  hid = warp_sum(hid);
+  if ((threadIdx.x & 31) == 0 && hid) atomicAdd(&s_hid, hid);
+  uint32_t tot;
+  const uint32_t excl = block_excl_scan<B>(cnt, s_scan, &tot);
+  const uint64_t pref = scan::tile_prefix(flags, tile, tot, epoch, &s_pref);
+  uint32_t o = excl;
+#pragma unroll
+  for (int k = 0; k < CITEMS; k++)
+    if ((keep >> k) & 1u) { s_r[o] = r[k]; s_p[o] = p[k]; o++; }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < tot; i += B) {
+    R2[pref + i] = s_r[i];
+    P2[pref + i] = s_p[i];
+  }
+  if (threadIdx.x == 0) {
+    if (s_hid) atomicAdd(hidden, s_hid);
+    if (tile == ntiles - 1) *out_len = pref + tot;
+  }
+}
+
 // ===================================================================== launchers
 int group_shift(uint64_t n, uint64_t tuples) {
   int kb = 0;
@@ -579,6 +705,16 @@ void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, ui
   else k_bucket<false><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp);
   const uint64_t na = directed ? m : 2 * m;
   k_scatter<<<grid((na + XITEMS - 1) / XITEMS, B, 148 * 8), B, 0, st>>>(tmp, na, cur, P);
+}
+void collapse(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2, uint32_t* HW,
+              uint64_t* hidden, uint64_t* out_len, scan::State& ss, cudaStream_t st) {
+  cudaMemsetAsync(out_len, 0, sizeof(uint64_t), st);
+  if (!A) return;
+  cudaMemsetAsync(ss.ticket, 0, sizeof(uint32_t), st);
+  const uint64_t tiles = (A + CTILE - 1) / CTILE;
+  k_collapse<<<(unsigned)tiles, B, 0, st>>>(R, P, A, R2, P2, HW, reinterpret_cast<unsigned long long*>(hidden),
+                                            reinterpret_cast<unsigned long long*>(out_len), tiles, ss.flags,
+                                            ss.ticket, ++ss.epoch);
 }
 void compact(const uint32_t* R, const uint32_t* P, uint64_t A, uint32_t* R2, uint32_t* P2,
              scan::State& ss, cudaStream_t st) {

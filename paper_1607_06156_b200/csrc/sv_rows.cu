@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     uint64_t L, uint32_t ntiles, const uint32_t* __restrict__ MAP,
     const uint32_t* __restrict__ NCPr, const uint32_t* __restrict__ TB, uint32_t* OUT,
     uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int preset, int excl,
-    const unsigned long long* __restrict__ prevctr, int hot_shift) {
+    const unsigned long long* __restrict__ prevctr, int hot_shift, const uint32_t* __restrict__ HW) {
   // With prevctr both variants are launched and the previous iteration's counters pick one on
   // the device (so the host can enqueue this pass before reading them): nothing left ->
   // neither runs; few partitions per live tuple -> the HOT variant.
@@ -206,6 +206,9 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
   constexpr int RAGG = 1024;
   __shared__ uint32_t s_akey[RAGG], s_aval[RAGG];
   __shared__ uint32_t s_nc[A ? RCACHE : 1];
+  // B with row collapse: tuples the collapse folded into the rows that leave in this pass
+  __shared__ unsigned long long s_hid;
+  if (!A && threadIdx.x == 0) s_hid = 0;
   for (int i = threadIdx.x; i < RAGG; i += PB) {
     s_akey[i] = INF;
     s_aval[i] = INF;
@@ -291,7 +294,14 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
         for (int j = 0; j < RITEMS; j++) {
           if (EXCL && p[j] != DEAD && ((cpl >> j) & 1u)) {
             // completed partition: the whole row leaves, its vertex is labelled p
-            if (j == 0 || r[j - 1] != r[j]) label[r[j] & ~R_LONG] = p[j];
+            if (j == 0 || r[j - 1] != r[j]) {
+              label[r[j] & ~R_LONG] = p[j];
+              // a collapsed row is one tuple (its own head); other rows have HW = 0
+              if (HW) {
+                const uint32_t w = __ldg(&HW[r[j] & ~R_LONG]);
+                if (w) atomicAdd(&s_hid, (unsigned long long)w);
+              }
+            }
             m[j] = DEAD;
           }
           live += m[j] != DEAD;
@@ -493,6 +503,10 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
   if (!A) {
     live = warp_sum(live);
     if (lane == 0 && live) atomicAdd(&ctr[sv::C_OUT], (unsigned long long)live);
+    if (HW) {
+      __syncthreads();
+      if (threadIdx.x == 0 && s_hid) atomicAdd(&ctr[sv::C_HIDDEN_DEAD], s_hid);
+    }
   }
 }
 
@@ -843,25 +857,25 @@ template <bool A, bool HOT, bool REL, bool X>
 static void launch_rowpass_x(const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L, uint64_t nt,
                            const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
                            uint32_t* NCPw, uint32_t* label, unsigned long long* c, int preset, int excl,
-                           const uint64_t* prevctr, int hot_shift, cudaStream_t st) {
+                           const uint64_t* prevctr, int hot_shift, cudaStream_t st, const uint32_t* HW) {
   static unsigned grid = 0;
   if (!grid) grid = persistent_grid((const void*)k_rowpass<A, HOT, REL, X>);
   k_rowpass<A, HOT, REL, X><<<(unsigned)std::min<uint64_t>(nt, grid), PB, 0, st>>>(
       R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
-      reinterpret_cast<const unsigned long long*>(prevctr), hot_shift);
+      reinterpret_cast<const unsigned long long*>(prevctr), hot_shift, HW);
 }
 
 template <bool A, bool HOT, bool REL>
 static void launch_rowpass(const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L, uint64_t nt,
                            const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
                            uint32_t* NCPw, uint32_t* label, unsigned long long* c, int preset, int excl,
-                           const uint64_t* prevctr, int hot_shift, cudaStream_t st) {
+                           const uint64_t* prevctr, int hot_shift, cudaStream_t st, const uint32_t* HW) {
   if (A ? preset : excl)
     launch_rowpass_x<A, HOT, REL, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
-                                        prevctr, hot_shift, st);
+                                        prevctr, hot_shift, st, HW);
   else
     launch_rowpass_x<A, HOT, REL, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
-                                         prevctr, hot_shift, st);
+                                         prevctr, hot_shift, st, HW);
 }
 
 uint64_t row_tiles(uint64_t L) { return (L + PTILE - 1) / PTILE; }
@@ -881,7 +895,8 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
-             cudaStream_t st, bool excl, bool preset, const uint64_t* prevctr, int hot_shift) {
+             cudaStream_t st, bool excl, bool preset, const uint64_t* prevctr, int hot_shift,
+             const uint32_t* HW) {
   if (!L) return;
   const uint64_t nt = row_tiles(L);
   auto* umin = reinterpret_cast<unsigned long long*>(UMIN);
@@ -893,7 +908,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
   const int pre = preset ? 1 : 0, ex = excl ? 1 : 0;
   if (passA && !MAP) {  // the first iteration: identity relabel, no P written, never hot
     launch_rowpass<true, false, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                       hot_shift, st);
+                                       hot_shift, st, passA ? nullptr : HW);
     if (have_long) {
       k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
@@ -901,10 +916,10 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
   } else if (passA) {
     if (prevctr || hot)
       launch_rowpass<true, true, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                       hot_shift, st);
+                                       hot_shift, st, passA ? nullptr : HW);
     if (prevctr || !hot)
       launch_rowpass<true, false, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                        hot_shift, st);
+                                        hot_shift, st, passA ? nullptr : HW);
     if (have_long) {
       k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
@@ -912,10 +927,10 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
   } else {
     if (prevctr || hot)
       launch_rowpass<false, true, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                        hot_shift, st);
+                                        hot_shift, st, passA ? nullptr : HW);
     if (prevctr || !hot)
       launch_rowpass<false, false, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                         hot_shift, st);
+                                         hot_shift, st, passA ? nullptr : HW);
     if (have_long) {
       k_long1<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);

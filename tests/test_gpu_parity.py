@@ -179,6 +179,64 @@ def test_row_lengths_straddle_tiles(cc, seed):
     assert norm(trace_of(rep)) == norm(tr)
 
 
+@pytest.mark.parametrize("graph", ["straddle0", "straddle1", "er", "c1", "path", "rmat12"])
+def test_row_collapse_forced(graph, monkeypatch):
+    """Row collapse after every iteration from the first, at any size
+    (CC_COLLAPSE_FORCE=1): rows straddling collapse tiles (2048) and row-pass tiles, long rows
+    (never collapsed), every tile edge.  Labels and every counter of every iteration (A_i =
+    live + folded tuples) equal the Alg. 1 transcription, and equal a run with
+    CC_FLAG_NO_COLLAPSE."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_06156_b200 as ccmod
+    rng = np.random.default_rng(5)
+    if graph.startswith("straddle"):
+        seed = int(graph[-1])
+        r2 = np.random.default_rng(91 + seed)
+        sizes = [1, 2, 3, 31, 33, 255, 256, 257, 258, 1000, 2046, 2047, 2048, 2049, 2050, 4097] * 3
+        sizes += list(r2.integers(1, 300, size=300))
+        n = int(sum(sizes) + 500)
+        perm = r2.permutation(n).astype(np.uint32)
+        parts, nxt = [], 0
+        for s_ in r2.permutation(np.array(sizes)):
+            parts.append(np.stack([np.full(int(s_) - 1, perm[nxt], np.uint32), perm[nxt + 1:nxt + int(s_)]], 1))
+            nxt += int(s_)
+        joins = r2.choice(perm[:nxt], size=(len(sizes) // 3, 2)).astype(np.uint32)
+        e = np.concatenate(parts + [joins]).astype(np.uint32)
+    elif graph == "er":
+        n = 30000
+        e = graphgen.er(17, n, 24000)
+    elif graph == "c1":
+        g = graphgen.make("c1")
+        n, e = g.n, g.edges
+    elif graph == "path":
+        n = 100000
+        perm = rng.permutation(n).astype(np.uint32)
+        e = np.stack([perm[:-1], perm[1:]], 1)
+    else:
+        g = graphgen.rmat_scale_graph(12)
+        n, e = g.n, g.edges
+    want, tr = osv.sv_trace(n, e)
+    ctx = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE)
+    ref = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE | ccmod.CC_FLAG_NO_COLLAPSE)
+    try:
+        monkeypatch.setenv("CC_COLLAPSE_FORCE", "1")
+        for mode in ("sv", "auto"):
+            lab, rep = run(ctx, n, e, mode)
+            assert np.array_equal(lab, oracle.uf_labels(n, e).astype(np.int64)), mode
+            if mode == "sv":
+                assert np.array_equal(lab, want)
+                assert norm(trace_of(rep)) == norm(tr)
+        monkeypatch.delenv("CC_COLLAPSE_FORCE")
+        lab2, rep2 = run(ref, n, e, "sv")
+        assert np.array_equal(lab2, want)
+        assert norm(trace_of(rep2)) == norm(tr)
+    finally:
+        ctx.close()
+        ref.close()
+
+
 @pytest.mark.parametrize("exclusion", ["end", "none"])
 def test_exclusion_variants_trace(exclusion):
     """The paper's exclusion timings (SURVEY C4, sec:distSVOpt1 P:220-225) and the
