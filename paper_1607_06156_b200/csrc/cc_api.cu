@@ -560,6 +560,9 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
         return fail(c, CC_ERR_INVALID, "internal: collapsed-row count underflow");
       hidden -= h[sv::C_HIDDEN_DEAD];
     }
+    // A_i+1: this iteration's survivors (counted before any collapse below folds them) plus
+    // the tuples folded by earlier collapses into rows still live
+    const uint64_t A_next = A1 + hidden;
     cc_iter_stat s{};
     s.active_in = A;
     s.partitions = h[sv::C_PARTITIONS];
@@ -648,7 +651,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       pending_compact = true;
       pending_collapse = want_collapse;
     }
-    A = A1 + hidden;
+    A = A_next;
     if (next_enq == it + 1) TRY(enqueue(it + 1));
   }
   CK(cudaStreamSynchronize(c->st));

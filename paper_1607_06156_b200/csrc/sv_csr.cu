@@ -492,8 +492,10 @@ __global__ void __launch_bounds__(B) k_collapse(const uint32_t* __restrict__ R,
   __shared__ uint32_t s_scan[B / 32 + 1];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_pref;
-  __shared__ uint32_t s_r[CTILE], s_p[CTILE];
-  __shared__ uint32_t s_bad[CTILE], s_cnt[CTILE];  // per row head (local index)
+  __shared__ __align__(16) uint32_t s_r[CTILE];
+  __shared__ __align__(16) uint32_t s_p[CTILE];
+  __shared__ __align__(16) uint32_t s_bad[CTILE];  // per row head (local index)
+  __shared__ __align__(16) uint32_t s_cnt[CTILE];
   __shared__ uint32_t s_wmax[B / 32];
   __shared__ unsigned long long s_hid;
   if (threadIdx.x == 0) {
@@ -507,16 +509,30 @@ __global__ void __launch_bounds__(B) k_collapse(const uint32_t* __restrict__ R,
   const uint32_t rbefore = t0 > 0 ? R[t0 - 1] : 0xFFFFFFFFu;           // uniform loads
   const uint32_t rafter = t0 + CTILE < A ? R[t0 + CTILE] : 0xFFFFFFFFu;
   uint32_t r[CITEMS], p[CITEMS];
+  static_assert(CITEMS == 8, "two 16-byte vectors per thread");
+  if (t0 + x0 + CITEMS <= A) {  // arrays are 16-byte aligned at tile offsets (CTILE * 4 bytes)
+    const uint4 a = ldg_stream(reinterpret_cast<const uint4*>(R + t0 + x0));
+    const uint4 b = ldg_stream(reinterpret_cast<const uint4*>(R + t0 + x0) + 1);
+    const uint4 c = ldg_stream(reinterpret_cast<const uint4*>(P + t0 + x0));
+    const uint4 d = ldg_stream(reinterpret_cast<const uint4*>(P + t0 + x0) + 1);
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+    p[0] = c.x; p[1] = c.y; p[2] = c.z; p[3] = c.w; p[4] = d.x; p[5] = d.y; p[6] = d.z; p[7] = d.w;
+  } else {
 #pragma unroll
-  for (int k = 0; k < CITEMS; k++) {
-    const uint64_t i = t0 + x0 + k;
-    r[k] = i < A ? R[i] : 0xFFFFFFFEu;  // past the end: a key no row has
-    p[k] = i < A ? P[i] : DEAD;
-    s_r[x0 + k] = r[k];
-    s_p[x0 + k] = p[k];
-    s_bad[x0 + k] = 0;
-    s_cnt[x0 + k] = 0;
+    for (int k = 0; k < CITEMS; k++) {
+      const uint64_t i = t0 + x0 + k;
+      r[k] = i < A ? R[i] : 0xFFFFFFFEu;  // past the end: a key no row has
+      p[k] = i < A ? P[i] : DEAD;
+    }
   }
+  reinterpret_cast<uint4*>(s_r + x0)[0] = make_uint4(r[0], r[1], r[2], r[3]);
+  reinterpret_cast<uint4*>(s_r + x0)[1] = make_uint4(r[4], r[5], r[6], r[7]);
+  reinterpret_cast<uint4*>(s_p + x0)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+  reinterpret_cast<uint4*>(s_p + x0)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+  reinterpret_cast<uint4*>(s_bad + x0)[0] = make_uint4(0, 0, 0, 0);
+  reinterpret_cast<uint4*>(s_bad + x0)[1] = make_uint4(0, 0, 0, 0);
+  reinterpret_cast<uint4*>(s_cnt + x0)[0] = make_uint4(0, 0, 0, 0);
+  reinterpret_cast<uint4*>(s_cnt + x0)[1] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   // head position (+1) of the row holding each item: block-wide inclusive max scan of the
   // heads (0 = the row started in the previous tile)

@@ -206,9 +206,6 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
   constexpr int RAGG = 1024;
   __shared__ uint32_t s_akey[RAGG], s_aval[RAGG];
   __shared__ uint32_t s_nc[A ? RCACHE : 1];
-  // B with row collapse: tuples the collapse folded into the rows that leave in this pass
-  __shared__ unsigned long long s_hid;
-  if (!A && threadIdx.x == 0) s_hid = 0;
   for (int i = threadIdx.x; i < RAGG; i += PB) {
     s_akey[i] = INF;
     s_aval[i] = INF;
@@ -241,6 +238,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     issue(blockIdx.x + gridDim.x, 1);
   }
   uint32_t live = 0;
+  uint32_t hid = 0;  // B with row collapse: folded tuples of the rows that leave (HW)
   uint32_t it = 0;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
     const int buf = it & 1;
@@ -297,10 +295,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
             if (j == 0 || r[j - 1] != r[j]) {
               label[r[j] & ~R_LONG] = p[j];
               // a collapsed row is one tuple (its own head); other rows have HW = 0
-              if (HW) {
-                const uint32_t w = __ldg(&HW[r[j] & ~R_LONG]);
-                if (w) atomicAdd(&s_hid, (unsigned long long)w);
-              }
+              if (HW) hid += __ldg(&HW[r[j] & ~R_LONG]);
             }
             m[j] = DEAD;
           }
@@ -504,8 +499,8 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     live = warp_sum(live);
     if (lane == 0 && live) atomicAdd(&ctr[sv::C_OUT], (unsigned long long)live);
     if (HW) {
-      __syncthreads();
-      if (threadIdx.x == 0 && s_hid) atomicAdd(&ctr[sv::C_HIDDEN_DEAD], s_hid);
+      hid = warp_sum(hid);
+      if (lane == 0 && hid) atomicAdd(&ctr[sv::C_HIDDEN_DEAD], (unsigned long long)hid);
     }
   }
 }
