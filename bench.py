@@ -148,10 +148,12 @@ def make_graph(cfg, scale=1.0):
 
 
 def default_scale(cfg, ws):
-    """C5 (u64 ids, 4.9 G edges) needs 8 GPUs at full size, and every rank
-    here draws the whole edge list on the host before taking its block (79 GB at full size):
-    the default is 1/16 of it at any N; --scale 1 asks for the full config."""
-    return 1.0 / 16 if cfg == "c5" else 1.0
+    """C5 (u64 ids, 4.9 G edges, 79 GB of records) needs 8 GPUs at full size (SURVEY §8
+    table): full size at N = 8 (each rank draws its own block, graphgen.make_block), 1/16 of
+    it below; --scale overrides."""
+    if cfg != "c5":
+        return 1.0
+    return 1.0 if ws >= 8 else 1.0 / 16
 
 
 def shard(edges, rank, ws):
@@ -296,11 +298,19 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     scale = args.scale or default_scale(args.config, ws)
-    g = make_graph(args.config, scale)
-    n, m = g.n, g.m
+    if ws > 1 and args.config == "c5":
+        # each rank draws only its own block of records (graphgen.make_block): at full size
+        # the whole C5 list is 79 GB of host memory
+        import graphgen
+        g = graphgen.make_block(args.config, scale, rk, ws)
+        n, m = g.n, int(g.params["m_total"])
+        mine = g.edges
+    else:
+        g = make_graph(args.config, scale)
+        n, m = g.n, g.m
+        mine = shard(g.edges, rk, ws)
     u64 = n == 0  # C5: u64 ids, relabelled on the device (Alg. 2 line 4)
     ids = "u64" if u64 else "u32"
-    mine = shard(g.edges, rk, ws)
     flags = (0 if args.no_profile else cc.CC_FLAG_PROFILE) | cc.REGROUP_FLAGS[args.regroup]
     # N > 1: the library owns an NCCL communicator (cfg.nccl_id, include/cc.h) and enqueues
     # every exchange on its stream; the process group only broadcasts the NCCL id.  gloo (one

@@ -53,6 +53,8 @@ def _L():
         lib.gg_union_u64.argtypes = [u64, p32, u64, u64, p32, u64, p32]
         lib.gg_mix64_value.restype = u64
         lib.gg_mix64_value.argtypes = [u64]
+        lib.gg_c5_block.argtypes = [u64, u64, u32, u64, u32, u32, u32, p32, u64, u64, u64, p32]
+        lib.gg_c5_block.restype = i32
         for f in (lib.gg_blocks, lib.gg_er, lib.gg_paths, lib.gg_grid, lib.gg_rmat, lib.gg_union_u64):
             f.restype = i32
         _lib = lib
@@ -178,6 +180,32 @@ def make(config: str, scale: float = 1.0, seed: int | None = None) -> Graph:
         return Graph("c5", 0, union_u64(s, a, 1 << sc, b), dict(rmat_scale=sc, n_paths=npaths,
                                                                   scale=scale))
     raise KeyError(config)
+
+
+def make_block(config: str, scale: float, rank: int, world: int) -> Graph:
+    """Rank ``rank``'s block (PAPER.md:205 block distribution: records [m*rank/world,
+    m*(rank+1)/world)) of ``make(config, scale)``, drawn without the other ranks' records.
+    C5: the R-MAT part is drawn edge by edge inside the block (gen.c gg_c5_block); only the
+    path part (~1/8 of the records) is drawn whole.  Other configs: drawn whole and sliced.
+    ``Graph.params['m_total']`` is the whole list's length."""
+    if config != "c5":
+        g = make(config, scale)
+        m = g.m
+        e = np.ascontiguousarray(g.edges[m * rank // world:m * (rank + 1) // world])
+        return Graph(config, g.n, e, dict(g.params, m_total=m, rank=rank, world=world))
+    s = BASE_SEED + 5
+    sc = max(4, 28 + int(round(np.log2(scale))) if scale != 1.0 else 28)
+    npaths = max(1, int(10_000_000 * scale))
+    _, b = paths(s + 100, npaths, 64.0, 0, 0)
+    b = np.ascontiguousarray(b, dtype=np.uint32)
+    ma = 16 << sc
+    m = ma + b.shape[0]
+    i0, i1 = m * rank // world, m * (rank + 1) // world
+    out = np.empty((i1 - i0, 2), dtype=np.uint64)
+    a, ab, abc = int(0.57 * 2**32), int((0.57 + 0.19) * 2**32), int((0.57 + 0.19 + 0.19) * 2**32)
+    _L().gg_c5_block(s, s, sc, ma, a, ab, abc, _ptr(b), b.shape[0], i0, i1, _ptr(out))
+    return Graph("c5", 0, out, dict(rmat_scale=sc, n_paths=npaths, scale=scale, m_total=m, rank=rank,
+                                    world=world))
 
 
 def make_prefix(config: str, m_prefix: int) -> Graph:

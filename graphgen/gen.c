@@ -280,3 +280,40 @@ int gg_union_u64(uint64_t seed, const uint32_t* a, uint64_t ma, uint64_t na, con
   }
   return 0;
 }
+
+/* C5, one rank's block of the output: edge records [i0, i1) of gg_union_u64's list over the
+ * R-MAT part (scale `scale`, ma edges, thresholds as gg_rmat, ids permuted) and the path part
+ * b (mb pairs) -- R-MAT edges are drawn on the fly (each is a pure function of (seed, j)),
+ * so a rank never holds the other ranks' R-MAT edges.  Identical to the same rows of
+ * gg_union_u64(seed, rmat(...), 2^scale, b).                                              */
+int gg_c5_block(uint64_t seed, uint64_t rseed, uint32_t scale, uint64_t ma, uint32_t ta, uint32_t tab,
+                uint32_t tabc, const uint32_t* b, uint64_t mb, uint64_t i0, uint64_t i1, uint64_t* out) {
+  const uint64_t m = ma + mb, na = 1ULL << scale;
+  gg_perm pe, pid;
+  perm_init(&pe, m ? m : 1, seed, 9);
+  perm_init(&pid, na, rseed, 1001);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = (int64_t)i0; i < (int64_t)i1; i++) {
+    uint64_t j = perm_apply(&pe, (uint64_t)i);
+    uint64_t u = 0, v = 0;
+    if (j < ma) {
+      for (uint32_t l = 0; l < scale; l += 2) {
+        uint64_t r = gg_rand(rseed, 30, j * 32 + l / 2);
+        for (int h = 0; h < 2 && l + h < scale; h++) {
+          uint32_t x = (uint32_t)(h ? (r >> 32) : r);
+          uint32_t ub = (x >= tab), vb = (x >= ta && x < tab) || (x >= tabc);
+          u = (u << 1) | ub; v = (v << 1) | vb;
+        }
+      }
+      u = perm_apply(&pid, u);
+      v = perm_apply(&pid, v);
+    } else {
+      j -= ma;
+      u = na + b[2 * j];
+      v = na + b[2 * j + 1];
+    }
+    out[2 * (i - i0)] = gg_mix64(u);
+    out[2 * (i - i0) + 1] = gg_mix64(v);
+  }
+  return 0;
+}

@@ -210,7 +210,11 @@ static cc_status load_buffers(cc_ctx* c, cc_idw w, uint64_t m, uint64_t n, bool 
   if (w == CC_U64) {
     TRY(dalloc_t(c, &c->d_ids64, 2 * m + 1));
     TRY(dalloc_t(c, &c->d_uids, 2 * m + 1));
-    if (relabel::hash_slots(2 * m)) TRY(dalloc_t(c, &c->d_htab, relabel::hash_slots(2 * m) + 1));
+    c->htab_slots = 0;
+    if (relabel::hash_slots(2 * m)) {
+      c->htab_slots = relabel::hash_first_slots(2 * m) + 1;
+      TRY(dalloc_t(c, &c->d_htab, c->htab_slots));
+    }
     if (c->cfg.flags & CC_FLAG_PERMUTE_IDS) {
       TRY(dalloc_t(c, &c->d_mix, n + 1));
       TRY(dalloc_t(c, &c->d_pi, n + 1));
@@ -954,8 +958,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     uint64_t* total = c->d_gctr + graph::G_NUM + 1537;
     uint32_t* vals[2] = {c->d_q[0], c->d_q[1]};
     if (c->d_htab)
-      relabel::run_hash(c->d_ids64, 2 * m, c->d_htab, c->d_w, vals, c->rws, reinterpret_cast<uint32_t*>(c->d_edges),
-                        c->d_uids, total, c->d_gctr + graph::G_NUM + 1540, c->st, &c->launches);
+      TRY(relabel_hash(c, 2 * m, total));
     else
       relabel::run(c->d_ids64, 2 * m, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges),
                    c->d_uids, total, c->st, &c->launches);

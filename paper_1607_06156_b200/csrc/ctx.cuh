@@ -14,6 +14,7 @@
 #include "graph.cuh"
 #include "nccl_comm.h"
 #include "radix.cuh"
+#include "relabel.cuh"
 #include "scan.cuh"
 #include "sv.cuh"
 
@@ -36,7 +37,8 @@ struct cc_ctx {
   uint2* d_rem2 = nullptr;
   uint64_t* d_ids64 = nullptr;  // u64 mode: loaded endpoints (2m)
   uint64_t* d_uids = nullptr;   // u64 mode: sorted distinct ids (rank -> id)
-  uint64_t* d_htab = nullptr;   // u64 mode: relabel hash table (relabel::hash_slots(2m) + 1)
+  uint64_t* d_htab = nullptr;   // u64 mode: relabel hash table (first-attempt size, grown on overflow)
+  uint64_t htab_slots = 0;
   uint64_t* d_mix = nullptr;    // CC_FLAG_PERMUTE_IDS: mixed ids / their sorted copy
   uint32_t* d_pi = nullptr;     // CC_FLAG_PERMUTE_IDS: original rank -> permuted rank
   uint64_t n_alloc = 0;         // id bound the n-sized buffers were sized for
@@ -447,6 +449,24 @@ static inline cc_status comm_sparse_slots(cc_ctx* c, uint32_t* S, uint32_t* BM, 
   TRY(comm_allgather(c, c->d_xsend, c->d_xrecv, pad * sizeof(uint2)));
   csr::apply_slots(c->d_xrecv, world * pad, S, BM, c->st);
   c->launches += 2;
+  return CC_OK;
+}
+
+// u64 relabel through the hash table (relabel::run_hash), growing the table to the full size
+// only if the first, small attempt overflowed (no 2m-sized table at load)
+static inline cc_status relabel_hash(cc_ctx* c, uint64_t k, uint64_t* total) {
+  uint32_t* vals[2] = {c->d_q[0], c->d_q[1]};
+  uint64_t* scratch = c->d_gctr + graph::G_NUM + 1540;
+  int r = relabel::run_hash(c->d_ids64, k, c->d_htab, c->htab_slots, false, c->d_w, vals, c->rws,
+                            reinterpret_cast<uint32_t*>(c->d_edges), c->d_uids, total, scratch, c->st, &c->launches);
+  if (r == 1) {
+    const uint64_t need = relabel::hash_slots(k) + 1;
+    TRY(dalloc_t(c, &c->d_htab, need));
+    c->htab_slots = need;
+    r = relabel::run_hash(c->d_ids64, k, c->d_htab, c->htab_slots, true, c->d_w, vals, c->rws,
+                          reinterpret_cast<uint32_t*>(c->d_edges), c->d_uids, total, scratch, c->st, &c->launches);
+  }
+  if (r) return fail(c, CC_ERR_INVALID, "internal: relabel hash table");
   return CC_OK;
 }
 

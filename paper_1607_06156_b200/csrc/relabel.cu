@@ -186,16 +186,24 @@ uint64_t hash_slots(uint64_t k) {
   return k * 10 > cap * 9 ? 0 : cap;
 }
 
-cc_status_t run_hash(const uint64_t* ids, uint64_t k, uint64_t* table, uint64_t* keys[2], uint32_t* vals[2],
-                     radix::Workspace& rws, uint32_t* dense, uint64_t* uids, uint64_t* total, uint64_t* scratch,
-                     cudaStream_t st, uint64_t* launches) {
-  if (!k) return 0;
-  // The table starts sized for k/8 distinct ids at load 1/2 (graphs repeat each id about
-  // degree times; C5: 2m / |V| ~ 13): its scan, its memset and the random probes then stay
-  // within a small region.  A probe run past MAX_PROBE retries once at the full size.
+uint64_t hash_first_slots(uint64_t k) {
   const uint64_t full = hash_slots(k);
   uint64_t cap = 1024;
   while (cap < k / 4 && cap < full) cap <<= 1;
+  return cap;
+}
+
+cc_status_t run_hash(const uint64_t* ids, uint64_t k, uint64_t* table, uint64_t table_slots, bool start_full,
+                     uint64_t* keys[2], uint32_t* vals[2], radix::Workspace& rws, uint32_t* dense, uint64_t* uids,
+                     uint64_t* total, uint64_t* scratch, cudaStream_t st, uint64_t* launches) {
+  if (!k) return 0;
+  // The table starts sized for k/8 distinct ids at load 1/2 (graphs repeat each id about
+  // degree times; C5: 2m / |V| ~ 13): its scan, its memset and the random probes then stay
+  // within a small region.  A probe run past MAX_PROBE retries once at the full size, in a
+  // table the caller grows only then (return 1).
+  const uint64_t full = hash_slots(k);
+  uint64_t cap = start_full ? full : hash_first_slots(k);
+  if (cap + 1 > table_slots) return 1;
   auto* cnt = reinterpret_cast<unsigned long long*>(scratch);  // [0] count, [1] id ~0 seen, [2] overflow
   while (true) {
     cudaMemsetAsync(table, 0xFF, sizeof(uint64_t) * (cap + 1), st);
@@ -209,6 +217,7 @@ cc_status_t run_hash(const uint64_t* ids, uint64_t k, uint64_t* table, uint64_t*
     cudaStreamSynchronize(st);
     if (!ovf) break;
     cap = full;
+    if (cap + 1 > table_slots) return 1;
   }
   k_hcompact<<<grid(cap, 148 * 16), B, 0, st>>>(table, cap, keys[0], vals[0], cnt, cnt + 1);
   uint64_t d = 0;

@@ -147,8 +147,7 @@ cc_status dist_relabel(cc_ctx* c) {
   TRY(scan_epoch_guard(c));
   CK(cudaMemsetAsync(total, 0, sizeof(uint64_t), c->st));
   if (c->d_htab)
-    relabel::run_hash(c->d_ids64, k, c->d_htab, c->d_w, vals, c->rws, reinterpret_cast<uint32_t*>(c->d_edges),
-                      c->d_uids, total, c->d_gctr + graph::G_NUM + 1540, c->st, &c->launches);
+    TRY(comm_agree(c, relabel_hash(c, k, total)));  // a rank may grow its table (local failure)
   else
     relabel::run(c->d_ids64, k, c->d_w, vals, c->rws, c->ss, reinterpret_cast<uint32_t*>(c->d_edges), c->d_uids,
                  total, c->st, &c->launches);

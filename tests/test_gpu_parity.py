@@ -434,6 +434,18 @@ def test_config_c4_full(cc, request):
     root = rep["bfs_root"]
     assert rep["bfs_visited"] == int(np.count_nonzero(want == want[root]))
     assert rep["max_degree"] == int(np.bincount(g.edges.reshape(-1), minlength=g.n).max())
+    # the hard-coded SV route (fig:dynamic 'never BFS') on 2.18 G tuples, whose
+    # 67 M-slot partition arrays exceed L2: labels bit-identical, trace invariants
+    rep = cc.run("sv")
+    assert rep["ran_bfs"] == 0
+    assert np.array_equal(cc.labels(), want)
+    assert oracle.component_size_histogram(cc.labels()) == oracle.component_size_histogram(want)
+    its = rep["iters"]
+    assert its[0]["active_in"] == 2 * g.m + int(np.count_nonzero(np.bincount(g.edges.reshape(-1), minlength=g.n)))
+    for i, it in enumerate(its):
+        assert it["temps"] == it["partitions"] - it["completed"]
+        if i:
+            assert it["active_in"] <= its[i - 1]["active_in"]
 
 
 def test_degree_counts_large_id_range(cc, request):

@@ -457,3 +457,13 @@ def test_c5_generator_is_a_relabelled_union():
     assert np.array_equal(np.sort(g.edges.reshape(-1)), np.sort(mixed.reshape(-1)))
     sample = np.arange(20000, dtype=np.uint64)
     assert len({graphgen.mix64(int(x)) for x in sample}) == sample.shape[0]
+
+
+def test_graphgen_c5_blocks_concatenate():
+    """Per-rank C5 generation (graphgen.make_block, bench.py at N > 1) draws exactly the rows
+    of the whole list that the block distribution gives each rank."""
+    g = graphgen.make("c5", 1 / 4096)
+    for world in (2, 3, 8):
+        parts = [graphgen.make_block("c5", 1 / 4096, r, world) for r in range(world)]
+        assert all(p.params["m_total"] == g.m for p in parts)
+        assert np.array_equal(np.concatenate([p.edges for p in parts]), g.edges)
