@@ -167,6 +167,9 @@ typedef struct {
   double ms_total, ms_prediction, ms_relabel, ms_bfs, ms_filter, ms_sv, ms_finalize;
   const cc_iter_stat* iters;          /* sv_iterations entries (CC_FLAG_TRACE)          */
   uint32_t n_iters;
+  int bfs_spec_root;                  /* 1: the BFS root's level ran inside the degree
+                                         pass on a guessed root that proved exact (large
+                                         lists); labels are unaffected  */
 } cc_report;
 
 /* Library version string. */

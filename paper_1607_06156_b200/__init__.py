@@ -84,7 +84,8 @@ class cc_report(ctypes.Structure):
                 ("ms_relabel", ctypes.c_double), ("ms_bfs", ctypes.c_double),
                 ("ms_filter", ctypes.c_double), ("ms_sv", ctypes.c_double),
                 ("ms_finalize", ctypes.c_double), ("iters", ctypes.POINTER(cc_iter_stat)),
-                ("n_iters", ctypes.c_uint32)]
+                ("n_iters", ctypes.c_uint32),
+                ("bfs_spec_root", ctypes.c_int)]
 
 
 EXPORTS = ["cc_version", "cc_get_unique_id", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",

@@ -459,7 +459,13 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   cudaEvent_t ev_read[2] = {ev_get(c), ev_get(c)};
   // hot thresholds measured on C2 (iterations with 490 k / 112 k / 16 k previous partitions):
   // pass A gains from the block tables below 1/512 partitions per live tuple, pass B below 1/128
-  constexpr int HOT_A = 9, HOT_B = 7;
+  // CC_HOT_SEL=1: select on the slot targets of this iteration instead (|P_i| for pass A, the
+  // distinct p_min targets for pass B; csr.cuh rowpass), thresholds $CC_HOT_A / $CC_HOT_B
+  const char* hs = getenv("CC_HOT_SEL");
+  const bool hot_cur = hs && hs[0] == '1';
+  const char* ha = getenv("CC_HOT_A");
+  const char* hb = getenv("CC_HOT_B");
+  const int HOT_A = ha ? atoi(ha) : 9, HOT_B = hb ? atoi(hb) : 7;
   uint32_t next_enq = 0;
   // Row collapse (one GPU, paper exclusion): once partitions are large, most rows are PC and
   // stay PC; collapse() folds each to its head tuple, so later passes stream ~one tuple per
@@ -489,7 +495,8 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     { Prof k(c, KF_ROWA);
       csr::rowpass(true, Rc, Pc, it ? Palt : nullptr, len, it ? PB : nullptr, nullptr, nullptr, PA,
                    NCP, c->d_label, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs,
-                   have_long, false, ctr, c->st, true, /*preset=*/lexact, prevctr, HOT_A);
+                   have_long, false, ctr, c->st, true, /*preset=*/lexact, prevctr, HOT_A, nullptr,
+                   hot_cur && lcur ? LC + lb : nullptr, 0);
       k.end(8.0 * len + (it ? 4.0 * len : 0.0), 1 + (have_long ? 2 : 0)); }
     if (it) std::swap(Pc, Palt);
     // sparse exchange once few partitions remain: the entries all ranks touched (at most
@@ -513,7 +520,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
                    c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, false, ctr, c->st,
-                   excl, false, prevctr, HOT_B, hw_ready ? c->d_hw : nullptr);
+                   excl, false, prevctr, HOT_B, hw_ready ? c->d_hw : nullptr, hot_cur ? ctr : nullptr, 1);
       k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
     // live tuples: this rank's (compaction) and the global count (convergence)
@@ -825,6 +832,98 @@ cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs_ou
   return CC_OK;
 }
 
+// Edge-streaming BFS peel (Alg. 2 lines 7-11) from `root`
+// over this rank's edge list c->d_edges.  With world_size > 1 the 2-bit state is replicated
+// and each level's found bitmap is OR-ed over ranks before it is counted, so every rank takes
+// the same levels; the edge lists stay where they were loaded.  spec_ok: level 1 already ran
+// inside the degree pass (graph.cu k_deg_sample).  Out: the remainder E \ {(u,v) | u in VI}
+// of this rank's edges (*rem, *m_rem), the visited bitmap in c->d_bm[0], labels of VI written,
+// rep.bfs_visited / bfs_levels set; *e_bfs recorded after the labels.
+cc_status bfs_stream(cc_ctx* c, uint64_t root, bool spec_ok, const uint2** rem, uint64_t* m_rem,
+                     cudaEvent_t* e_bfs) {
+  cc_report& R = c->rep;
+  const uint64_t n = c->n, m = c->m;
+  const uint64_t nw = (n + 31) / 32;
+  uint32_t *V = c->d_bm[0], *S = c->d_bm[1], *X = c->d_bm[2];
+  if (!c->d_rem) TRY(comm_agree(c, dalloc_t(c, &c->d_rem, m + 1)));
+  if (!c->d_rem2) TRY(comm_agree(c, dalloc_t(c, &c->d_rem2, m + 1)));
+  uint2* bufs[2] = {c->d_rem, c->d_rem2};
+  if (!spec_ok) {
+    CK(cudaMemsetAsync(S, 0, sizeof(uint32_t) * 2 * nw, c->st));
+    c->h_word[0] = 1u << (2 * (root & 15));
+    CK(cudaMemcpyAsync(S + root / 16, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
+  }
+  const uint2* cur = c->d_edges;
+  uint64_t mcur = m;
+  int nb = 0;  // next scratch buffer
+  bool last_compacted = false;
+  uint64_t visited = 1, levels = 0, front_arcs = 0;
+  bool spec_pending = spec_ok;
+  while (true) {
+    const bool root_level = levels == 0;
+    bool compact = false;
+    if (!spec_pending) {
+      CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
+      // compact (keep only edges that can still matter) once most present vertices are
+      // visited, or when the frontier's arcs are a fifth of the current edge list: every edge
+      // at the frontier leaves, so the next level reads that much less (a local decision:
+      // each rank compacts its own list)
+      compact = !root_level && (2 * visited > R.n_present || 5 * front_arcs >= 2 * mcur);
+      CK(cudaMemsetAsync(c->d_gctr + graph::G_REMAIN, 0, sizeof(uint64_t), c->st));
+      Prof k(c, KF_BFS);
+      graph::launch_bfs_level(root_level, compact, cur, mcur, (uint32_t)root, S, X, bufs[nb], c->d_gctr, c->st);
+      c->launches += 1;
+      k.end(8.0 * (double)mcur + (compact ? 8.0 * (double)mcur / 8 : 0.0) + (double)n / 4, 1,
+            root_level ? 0.0 : 2.0 * (double)mcur);
+    }
+    spec_pending = false;
+    // the level's found ids (OR over ranks: every rank's edges found some) and their arcs
+    TRY(comm_or_bits(c, X, nw));
+    CK(cudaMemsetAsync(c->d_gctr + graph::G_NEWVIS, 0, sizeof(uint64_t), c->st));
+    CK(cudaMemsetAsync(c->d_gctr + graph::G_FARCS, 0, sizeof(uint64_t), c->st));
+    graph::launch_farcs(X, n, c->d_deg, c->d_gctr + graph::G_NEWVIS, c->d_gctr + graph::G_FARCS, c->st);
+    c->launches += 1;
+    CKL();
+    TRY(sync_read(c));
+    last_compacted = compact;
+    if (compact) {
+      cur = bufs[nb];
+      mcur = c->h_gctr[graph::G_REMAIN];
+      nb ^= 1;
+    }
+    const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
+    if (nv == 0) break;
+    visited += nv;
+    front_arcs = c->h_gctr[graph::G_FARCS];
+    levels++;
+    graph::launch_bfs_advance(S, X, n, c->st);
+    c->launches += 1;
+  }
+  R.bfs_visited = visited;
+  R.bfs_levels = levels;
+  graph::launch_vis_bits(S, n, V, c->st);
+  graph::launch_min_visited(V, n, c->d_gctr, c->st);
+  graph::launch_bfs_labels(V, n, c->d_label, c->d_gctr, c->st);
+  c->launches += 3;
+  *e_bfs = ev_get(c);
+  CK(cudaEventRecord(*e_bfs, c->st));
+  if (last_compacted) {
+    // a level that discovers nothing leaves no edge with exactly one visited endpoint:
+    // its survivors are exactly E \ {(u,v) | u in VI}
+    *m_rem = mcur;
+    *rem = cur;
+  } else {
+    CK(cudaMemsetAsync(c->d_gctr + graph::G_REMAIN, 0, sizeof(uint64_t), c->st));
+    graph::launch_filter(cur, mcur, S, bufs[nb], c->d_gctr, c->st);
+    c->launches += 1;
+    CKL();
+    TRY(sync_read(c));
+    *m_rem = c->h_gctr[graph::G_REMAIN];
+    *rem = bufs[nb];
+  }
+  return CC_OK;
+}
+
 // CSR rows of the whole graph from the bucketed arcs (csr::bucket_degrees already ran with
 // the same gsf): offsets in c->d_q[0], tuples in buffer 0.  *A = tuple count.
 static cc_status build_full_rows(cc_ctx* c, int gsf, uint64_t* A_out) {
@@ -996,6 +1095,16 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
   CK(cudaMemsetAsync(c->d_gctr + graph::G_MINVIS, 0xFF, sizeof(uint64_t), c->st));
   sv::launch_init_labels(c->d_label, n, c->st);
+  // speculative root level (graph.cu k_deg_sample): on large lists the degree pass also runs
+  // the BFS level of a root guessed from a prefix; kept below if the guess is the root
+  bool spec_ran = false;
+  const bool spec_want = gsf < 0 && mode != CC_MODE_SV && m >= graph::spec_min_edges();
+  graph::SpecLevel spec{c->d_bm[1], c->d_bm[2], c->d_gctr};
+  if (spec_want) {
+    const uint64_t nw = (n + 31) / 32;
+    CK(cudaMemsetAsync(spec.S, 0, sizeof(uint32_t) * 2 * nw, c->st));
+    CK(cudaMemsetAsync(spec.next, 0, sizeof(uint32_t) * nw, c->st));
+  }
   {
     Prof k(c, KF_PREDICT);
     if (gsf >= 0) {
@@ -1004,9 +1113,13 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
     } else {
       CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
       // scratch: tuple buffer 1 (8 cap >= 16m + 16n bytes) is free until the SV / CSR stages
-      const int algo = graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail,
-                                            c->d_gctr + graph::G_NUM + 64, c->d_w[1],
-                                            sizeof(uint64_t) * c->cap, c->d_garc);
+      const int ret = graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail,
+                                           c->d_gctr + graph::G_NUM + 64, c->d_w[1],
+                                           sizeof(uint64_t) * c->cap, c->d_garc,
+                                           spec_want ? &spec : nullptr);
+      const int algo = ret & 1;
+      spec_ran = (ret & 2) != 0;
+      if (spec_ran) c->launches += 3;
       // bucketed: edges read, u16 entries written and read, deg read + written; 2 shared
       // atomics per arc.  L2 windows: the edge list once per 2^24-id window, 1 L2 add per arc
       const double nwin = (double)((n + (1ull << 24) - 1) >> 24);
@@ -1067,74 +1180,14 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   } else if (run_bfs) {
     R.ran_bfs = 1;
     R.bfs_root = root;
-    const uint64_t nw = (n + 31) / 32;
-    uint32_t *V = c->d_bm[0], *S = c->d_bm[1], *X = c->d_bm[2];
-    if (!c->d_rem) TRY(dalloc_t(c, &c->d_rem, m + 1));
-    if (!c->d_rem2) TRY(dalloc_t(c, &c->d_rem2, m + 1));
-    uint2* bufs[2] = {c->d_rem, c->d_rem2};
-    CK(cudaMemsetAsync(S, 0, sizeof(uint32_t) * 2 * nw, c->st));
-    c->h_word[0] = 1u << (2 * (root & 15));
-    CK(cudaMemcpyAsync(S + root / 16, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
-    const uint2* cur = c->d_edges;
-    uint64_t mcur = m;
-    int nb = 0;  // next scratch buffer
-    bool last_compacted = false;
-    uint64_t visited = 1, levels = 0, front_arcs = 0;
-    while (true) {
-      CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
-      CK(cudaMemsetAsync(c->d_gctr + graph::G_NEWVIS, 0, 2 * sizeof(uint64_t), c->st));
-      CK(cudaMemsetAsync(c->d_gctr + graph::G_FARCS, 0, sizeof(uint64_t), c->st));
-      const bool root_level = levels == 0;
-      // compact (keep only edges that can still matter) once most present vertices are
-      // visited, or when the frontier's arcs are a fifth of the current edge list: every edge
-      // at the frontier leaves, so the next level reads that much less
-      const bool compact = !root_level && (2 * visited > R.n_present || 5 * front_arcs >= 2 * mcur);
-      Prof k(c, KF_BFS);
-      graph::launch_bfs_level(root_level, compact, cur, mcur, (uint32_t)root, S, X, bufs[nb],
-                              c->d_gctr, c->d_deg, c->st);
-      c->launches += 1;
-      k.end(8.0 * (double)mcur + (compact ? 8.0 * (double)mcur / 8 : 0.0) + (double)n / 4, 1,
-            root_level ? 0.0 : 2.0 * (double)mcur);
-      CKL();
-      TRY(sync_read(c));
-      last_compacted = compact;
-      if (compact) {
-        cur = bufs[nb];
-        mcur = c->h_gctr[graph::G_REMAIN];
-        nb ^= 1;
-      }
-      const uint64_t nv = c->h_gctr[graph::G_NEWVIS];
-      if (nv == 0) break;
-      visited += nv;
-      front_arcs = c->h_gctr[graph::G_FARCS];
-      levels++;
-      graph::launch_bfs_advance(S, X, n, c->st);
-      c->launches += 1;
-    }
-    R.bfs_visited = visited;
-    R.bfs_levels = levels;
-    graph::launch_vis_bits(S, n, V, c->st);
-    graph::launch_min_visited(V, n, c->d_gctr, c->st);
-    graph::launch_bfs_labels(V, n, c->d_label, c->d_gctr, c->st);
-    c->launches += 3;
-    e_bfs = ev_get(c);
-    CK(cudaEventRecord(e_bfs, c->st));
-    if (last_compacted) {
-      // a level that discovers nothing leaves no edge with exactly one visited endpoint:
-      // its survivors are exactly E \ {(u,v) | u in VI}
-      m_sv = mcur;
-      sv_edges = cur;
-    } else {
-      CK(cudaMemsetAsync(c->d_gctr + graph::G_REMAIN, 0, sizeof(uint64_t), c->st));
-      graph::launch_filter(cur, mcur, S, bufs[nb], c->d_gctr, c->st);
-      c->launches += 1;
-      CKL();
-      TRY(sync_read(c));
-      m_sv = c->h_gctr[graph::G_REMAIN];
-      sv_edges = bufs[nb];
-    }
+    // the speculative level is the root's level iff the guess is the root (same id: the
+    // claims are then exactly those level 1 makes)
+    const uint64_t guess = c->h_gctr[graph::G_GUESS];
+    const bool spec_ok = spec_ran && guess && (uint64_t)(0xFFFFFFFFu - (uint32_t)guess) == root;
+    R.bfs_spec_root = spec_ok ? 1 : 0;
+    TRY(bfs_stream(c, root, spec_ok, &sv_edges, &m_sv, &e_bfs));
     R.remainder_edges = m_sv;
-    vis = V;
+    vis = c->d_bm[0];
     e_filter = ev_get(c);
     CK(cudaEventRecord(e_filter, c->st));
   }
@@ -1253,10 +1306,20 @@ extern "C" cc_status cc_degrees_u32(cc_ctx* c, uint32_t* out, uint64_t cap, uint
   if (count) *count = n;
   if (!out || cap < n) return fail(c, CC_ERR_INVALID, "output buffer too small");
   CK(cudaSetDevice(c->cfg.device));
-  // the prediction stage's count (Alg. 2 line 2), same kernels and dispatch as cc_run
+  // the prediction stage's count (Alg. 2 line 2), same kernels and dispatch as cc_run in
+  // CC_MODE_AUTO (the speculative root level included on large lists: its prefix is counted
+  // by k_deg_sample)
   CK(cudaMemsetAsync(c->d_deg, 0, sizeof(uint32_t) * n, c->st));
+  const bool spec_want = m >= graph::spec_min_edges();
+  graph::SpecLevel spec{c->d_bm[1], c->d_bm[2], c->d_gctr};
+  if (spec_want) {
+    const uint64_t nw = (n + 31) / 32;
+    CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
+    CK(cudaMemsetAsync(spec.S, 0, sizeof(uint32_t) * 2 * nw, c->st));
+    CK(cudaMemsetAsync(spec.next, 0, sizeof(uint32_t) * nw, c->st));
+  }
   graph::launch_degree(c->d_edges, m, n, c->d_deg, c->st, c->d_tail, c->d_gctr + graph::G_NUM + 64,
-                       c->d_w[1], sizeof(uint64_t) * c->cap, c->d_garc);
+                       c->d_w[1], sizeof(uint64_t) * c->cap, c->d_garc, spec_want ? &spec : nullptr);
   CKL();
   c->ran = false;  // tuple buffer 1 was scratch: labels need a new cc_run
   if (n)

@@ -55,11 +55,17 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
              cudaStream_t st, bool excl = true, bool preset = false, const uint64_t* prevctr = nullptr,
-             int hot_shift = 0, const uint32_t* HW = nullptr);
+             int hot_shift = 0, const uint32_t* HW = nullptr, const uint64_t* hotcnt = nullptr,
+             int hot_mode = 0);
 // HW (pass B, row collapse): HW[r] = tuples folded into row r by collapse(); a row that leaves
 // adds them to ctr[C_HIDDEN_DEAD] (NULL before the first collapse of a run)
 // prevctr (device, the previous iteration's sv counters): the pass returns at once when it
-// left no live tuple, and is hot when |P_prev| << hot_shift < L (overrides `hot`)
+// left no live tuple, and is hot when |P_prev| << hot_shift < L (overrides `hot`).
+// hotcnt (device; overrides prevctr's count, and selects on the device in the first iteration
+// too): the number of distinct slots the pass updates, hot when count << hot_shift < L --
+// hot_mode 0: hotcnt[0] (pass A: |P_i|, the partition list's length); 1: hotcnt is this
+// iteration's sv counters after pstat1, count = |P_i| - changed + T_i (pass B's targets:
+// the unchanged partitions and the distinct p_min of the changed ones)
 // partition statistics after pass A (sets TB, clears PB); slot arrays padded to 4*ceil(n/4)
 // temps_all: a temporary for every partition, completed ones included (their tuples leave at
 // the end of the iteration or never)

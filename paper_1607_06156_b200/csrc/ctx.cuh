@@ -477,6 +477,11 @@ cc_status predict_gate(cc_ctx* c, cc_mode mode, bool want_hist, bool* run_bfs, u
 // world_size > 1 the partition slots are combined across ranks after each row pass.
 cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local);
 
+// Edge-streaming BFS peel over this rank's edges (cc_api.cu; replicated state, found bitmaps
+// OR-ed over ranks): remainder edges out, visited bitmap in d_bm[0], labels of VI written.
+cc_status bfs_stream(cc_ctx* c, uint64_t root, bool spec_ok, const uint2** rem, uint64_t* m_rem,
+                     cudaEvent_t* e_bfs);
+
 // cc_run for world_size > 1 (cc_dist.cu).
 cc_status run_dist(cc_ctx* c, cc_mode mode);
 

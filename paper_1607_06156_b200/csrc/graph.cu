@@ -105,7 +105,8 @@ __global__ void k_degree(const uint4* __restrict__ e2, uint64_t m, uint32_t* __r
   }
 }
 bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, void* scratch,
-                         uint64_t scratch_bytes, uint32_t* cursor, cudaStream_t st);
+                         uint64_t scratch_bytes, uint32_t* cursor, cudaStream_t st, const SpecLevel* spec,
+                         bool* spec_ran);
 // histogram of floor(log2(sample count)) over ids with count >= HUB_MIN (picks the threshold
 // that keeps the hubs within HUB_CAP: the largest ones)
 __global__ void k_hub_hist(const uint32_t* __restrict__ deg, uint64_t n, unsigned long long* bins) {
@@ -130,16 +131,17 @@ __global__ void k_hubs(const uint32_t* __restrict__ deg, uint64_t n, uint32_t t,
 }
 int launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
                   uint32_t* hub_scratch, uint64_t* hub_count, void* radix_scratch,
-                  uint64_t radix_bytes, uint32_t* radix_cursor) {
+                  uint64_t radix_bytes, uint32_t* radix_cursor, const SpecLevel* spec) {
   // hub_count[0]: hub count; hub_count[8 .. 40): log2 histogram of the sample counts
   if (!m) return 0;
   {
     // bucketed shared-memory count (default for n >= 2^20); CC_DEG_ALGO=radix|window forces one
     const char* e = getenv("CC_DEG_ALGO");
     const bool force_radix = e && e[0] == 'r', force_window = e && e[0] == 'w';
+    bool spec_ran = false;
     if (radix_scratch && !force_window && (force_radix || n >= (1ull << 20)) &&
-        launch_degree_radix(edges, m, n, deg, radix_scratch, radix_bytes, radix_cursor, st))
-      return 1;
+        launch_degree_radix(edges, m, n, deg, radix_scratch, radix_bytes, radix_cursor, st, spec, &spec_ran))
+      return 1 | (spec_ran ? 2 : 0);
   }
   static uint64_t window = 0;
   if (!window) {  // CC_DEG_WINDOW_LOG2: experiment hook for the counter window
@@ -179,6 +181,84 @@ int launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cud
           reinterpret_cast<const uint4*>(edges + m0), mr, deg, (uint32_t)lo, (uint32_t)hi, nullptr, nullptr);
   }
   return 0;
+}
+
+// ---------------------------------------------------------------- BFS state helpers
+// 2-bit vertex state of the BFS peel (see k_bfs_level): bit 0 visited, bit 1 frontier
+CC_DEVI uint32_t st2(const uint32_t* S, uint32_t v) { return (S[v >> 4] >> (2 * (v & 15))) & 3u; }
+// claim v (unvisited when its state was read) for the next frontier: the visited bit and the
+// next bit, both fire-and-forget reductions (idempotent: concurrent claims of one id are
+// harmless).  A level's found ids and their degree sum are counted afterwards from `next`
+// (k_farcs), so no thread waits on an atomic's result inside the level.
+CC_DEVI void mark2(uint32_t* S, uint32_t* next, uint32_t v) {
+  atomicOr(&S[v >> 4], 1u << (2 * (v & 15)));
+  atomicOr(&next[v >> 5], 1u << (v & 31));
+}
+
+// ---------------------------------------------------------------- speculative root level
+// The BFS root is the max-degree vertex, smallest id on ties (Alg. 2 line 7, PAPER.md:262;
+// SURVEY.md C13), so it is known only once every degree is; its level (frontier = {root})
+// would be one more stream over the edge list.  On large lists the root is guessed from the
+// counts of a prefix of the (randomly ordered) list -- counted straight into deg, so the
+// degree count stays exact -- and the bucketed degree pass claims the guess's neighbours
+// while it streams the rest (k_deg_part, SpecRoot).  cc_run keeps the claims only if the
+// guess equals the exact root; otherwise the state is cleared and level 1 runs as usual.
+// best key = max over the prefix of (count << 32 | ~v): largest count, smallest id
+__global__ void __launch_bounds__(BLOCK) k_deg_sample(const uint4* __restrict__ e2, uint64_t npair,
+                                                      uint32_t* __restrict__ deg,
+                                                      unsigned long long* best) {
+  unsigned long long key = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i < npair; i += (uint64_t)gridDim.x * BLOCK) {
+    const uint4 q = ldg_stream(e2 + i);
+    const uint32_t v[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      const uint32_t c = atomicAdd(&deg[v[h]], 1u) + 1u;
+      const unsigned long long k = ((unsigned long long)c << 32) | (0xFFFFFFFFu - v[h]);
+      key = k > key ? k : key;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, key, o);
+    key = x > key ? x : key;
+  }
+  if ((threadIdx.x & 31) == 0 && key) atomicMax(best, key);
+}
+template <bool ROOT, bool COMPACT>
+__global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e, uint64_t m, uint32_t root,
+                                                     const unsigned long long* root_key, uint32_t* S,
+                                                     uint32_t* next, uint2* __restrict__ out,
+                                                     unsigned long long* gctr);
+// the guess is visited (its level's frontier is itself)
+__global__ void k_spec_root(const unsigned long long* best, uint32_t* S) {
+  const unsigned long long k = *best;
+  if (k) {
+    const uint32_t r = 0xFFFFFFFFu - (uint32_t)k;
+    atomicOr(&S[r >> 4], 1u << (2 * (r & 15)));
+  }
+}
+// a level's found ids (*found += |next|) and their arcs (*farcs += sum of deg over next)
+__global__ void __launch_bounds__(BLOCK) k_farcs(const uint32_t* __restrict__ next, uint64_t nw,
+                                                 const uint32_t* __restrict__ deg,
+                                                 unsigned long long* found, unsigned long long* farcs) {
+  unsigned long long s = 0;
+  uint32_t c = 0;
+  for (uint64_t w = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * BLOCK) {
+    uint32_t x = next[w];
+    c += __popc(x);
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      s += __ldg(&deg[w * 32 + b]);
+    }
+  }
+  s = warp_sum(s);
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) {
+    atomicAdd(found, (unsigned long long)c);
+    atomicAdd(farcs, s);
+  }
 }
 
 // ---------------------------------------------------------------- degrees, bucketed
@@ -231,14 +311,32 @@ CC_DEVI uint64_t dr_addr(const DegRadix& R, uint32_t b, uint32_t pos) {
 // of b so that rows 64 bytes apart do not share banks) and one packed word
 // W[b] = (written-out << 16) | claimed, both renormalised to < 64 at every write-out.
 CC_DEVI uint32_t dr_phys(uint32_t b, uint32_t pos) { return (pos & 31u) ^ ((b << 2) & 24u); }
+// speculative root level carried by the degree pass (key == nullptr: off; see k_deg_sample)
+struct SpecRoot {
+  const unsigned long long* key;  // guess = ~(uint32_t)*key; 0: no guess
+  uint32_t* S;                    // 2-bit BFS state (the guess already visited)
+  uint32_t* next;                 // found bitmap
+};
 template <bool FULL>  // FULL: every id is in this super-window (lo = 0, n <= 2^26): no range test
 __global__ void __launch_bounds__(DR_THREADS, 1)
 k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo_arg, uint32_t nbk, DegRadix R,
-           uint32_t* __restrict__ deg) {
+           uint32_t* __restrict__ deg, SpecRoot sp) {
   extern __shared__ __align__(16) uint32_t dsm[];
   uint32_t* s_w = dsm;                                          // [DR_NB]
   uint16_t* s_row = reinterpret_cast<uint16_t*>(dsm + DR_NB);  // [DR_NB][DR_CAP]
   const uint32_t lo = FULL ? 0u : lo_arg;
+  bool spec = false;
+  uint32_t rg = 0;
+  if (sp.key) {
+    const unsigned long long k = *sp.key;
+    spec = k != 0;
+    rg = 0xFFFFFFFFu - (uint32_t)k;
+  }
+  // the guess's level: claim the other endpoint of every edge at the guess
+  auto spec_edge = [&](uint32_t a, uint32_t b) {
+    if (a == rg && b != rg) mark2(sp.S, sp.next, b);
+    if (b == rg && a != rg) mark2(sp.S, sp.next, a);
+  };
   for (uint32_t b = threadIdx.x; b < DR_NB; b += DR_THREADS) s_w[b] = 0;
   // this thread's buckets and the region position of their next 16-entry group
   const uint32_t ob[2] = {threadIdx.x, threadIdx.x + DR_THREADS};
@@ -270,6 +368,7 @@ k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo_arg, uint32_t n
     const uint2 t = reinterpret_cast<const uint2*>(e2)[m - 1];
     const uint32_t v[4] = {t.x - lo, t.y - lo, 0u, 0u};
     claim_store(v, 2);
+    if (spec) spec_edge(t.x, t.y);
   }
   auto load = [&](uint4 (&x)[DR_VEC], uint32_t r) {
     const uint4* p = e2 + (uint64_t)r * PER_ROUND + threadIdx.x;
@@ -288,6 +387,10 @@ k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo_arg, uint32_t n
       if (r >= full_rounds && (uint64_t)r * PER_ROUND + threadIdx.x + j * DR_THREADS >= npair) continue;
       const uint32_t v[4] = {x[j].x - lo, x[j].y - lo, x[j].z - lo, x[j].w - lo};
       claim_store(v, 4);
+      if (spec) {
+        spec_edge(x[j].x, x[j].y);
+        spec_edge(x[j].z, x[j].w);
+      }
     }
   };
   // one group of 16 entries of bucket b (in registers) to its reserved region position
@@ -437,8 +540,14 @@ uint64_t degree_radix_scratch(uint64_t m, uint64_t n) {
   const uint64_t mean = (2 * m + nb_all - 1) / nb_all;
   return 256 + sizeof(uint32_t) * 2 * DR_NB + nbk * sizeof(uint16_t) * (4 * mean + 16 * 160 * 2);
 }
+uint64_t spec_min_edges() {
+  const char* e = getenv("CC_SPEC_MIN_EDGES");  // test hook: exercise the guess on small lists
+  return e ? strtoull(e, nullptr, 10) : SPEC_MIN_EDGES;
+}
 bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, void* scratch,
-                         uint64_t scratch_bytes, uint32_t* /*cursor*/, cudaStream_t st) {
+                         uint64_t scratch_bytes, uint32_t* /*cursor*/, cudaStream_t st, const SpecLevel* spec,
+                         bool* spec_ran) {
+  *spec_ran = false;
   if (!m || !n) return true;
   uint64_t nbk, C;
   if (!deg_radix_plan(m, n, scratch_bytes, &nbk, &C)) return false;
@@ -459,15 +568,33 @@ bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* d
     attr = true;
   }
   const int G = sm_count();
+  // speculative root level: the prefix [0, m0) is counted by k_deg_sample (and its guess's
+  // edges claimed by a root-level pass over it), the degree pass counts [m0, m)
+  uint64_t m0 = 0;
+  SpecRoot sp{nullptr, nullptr, nullptr};
+  if (spec && m >= spec_min_edges()) {
+    const char* es = getenv("CC_SPEC_SAMPLE_EDGES");  // test hook
+    m0 = std::min<uint64_t>(es ? strtoull(es, nullptr, 10) : SPEC_SAMPLE_EDGES, m / 2) & ~1ull;
+    auto* gc = reinterpret_cast<unsigned long long*>(spec->gctr);
+    k_deg_sample<<<grid_for(m0 / 2, 148 * 4), BLOCK, 0, st>>>(reinterpret_cast<const uint4*>(edges), m0 / 2,
+                                                              deg, gc + G_GUESS);
+    k_spec_root<<<1, 1, 0, st>>>(gc + G_GUESS, spec->S);
+    k_bfs_level<true, false><<<grid_for((m0 + 1) / 2, 148 * 8), BLOCK, 0, st>>>(
+        edges, m0, 0u, gc + G_GUESS, spec->S, spec->next, nullptr, gc);
+    sp = SpecRoot{gc + G_GUESS, spec->S, spec->next};
+    *spec_ran = true;
+  }
+  const uint4* e2 = reinterpret_cast<const uint4*>(edges + m0);
+  const uint64_t mr = m - m0;
   for (uint64_t lo = 0; lo < n; lo += (uint64_t)DR_NB << DR_SPAN) {
     const uint32_t nb = (uint32_t)std::min<uint64_t>(DR_NB, (n - lo + (1u << DR_SPAN) - 1) >> DR_SPAN);
     R.nbk = nb;
     cudaMemsetAsync(R.cur, 0, sizeof(uint32_t) * DR_NB, st);
     if (lo == 0 && n <= ((uint64_t)DR_NB << DR_SPAN))
-      k_deg_part<true><<<G, DR_THREADS, smem_part, st>>>(reinterpret_cast<const uint4*>(edges), m, 0u, nb, R, deg);
+      k_deg_part<true><<<G, DR_THREADS, smem_part, st>>>(e2, mr, 0u, nb, R, deg, sp);
     else
-      k_deg_part<false><<<G, DR_THREADS, smem_part, st>>>(reinterpret_cast<const uint4*>(edges), m, (uint32_t)lo,
-                                                          nb, R, deg);
+      k_deg_part<false><<<G, DR_THREADS, smem_part, st>>>(e2, mr, (uint32_t)lo, nb, R, deg,
+                                                          lo == 0 ? sp : SpecRoot{nullptr, nullptr, nullptr});
     k_deg_order<<<1, 1024, 0, st>>>(R, nb);
     k_deg_count<<<nb, DR_THREADS, smem_count, st>>>(R, (uint32_t)lo, n, deg);
   }
@@ -569,20 +696,19 @@ void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* 
 // after the level (a frontier endpoint's neighbour is visited by then, by this or another
 // edge) -- staged per warp in shared memory and written in runs, so later levels and the
 // filter stream only those.  (edge-streaming bitmap BFS.)
-CC_DEVI uint32_t st2(const uint32_t* S, uint32_t v) { return (S[v >> 4] >> (2 * (v & 15))) & 3u; }
-CC_DEVI bool claim2(uint32_t* S, uint32_t* next, uint32_t v) {
-  const uint32_t m = 1u << (2 * (v & 15));
-  if (S[v >> 4] & m) return false;  // relaxed pre-check
-  if (atomicOr(&S[v >> 4], m) & m) return false;
-  atomicOr(&next[v >> 5], 1u << (v & 31));
-  return true;
-}
+// root_key (root level only): root = ~(uint32_t)*root_key, no level if 0 (the speculative
+// level)
 template <bool ROOT, bool COMPACT>
 __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e, uint64_t m,
-                                                     uint32_t root, uint32_t* S, uint32_t* next,
+                                                     uint32_t root, const unsigned long long* root_key,
+                                                     uint32_t* S, uint32_t* next,
                                                      uint2* __restrict__ out,
-                                                     unsigned long long* gctr,
-                                                     const uint32_t* __restrict__ deg) {
+                                                     unsigned long long* gctr) {
+  if (ROOT && root_key) {
+    const unsigned long long k = *root_key;
+    if (!k) return;
+    root = 0xFFFFFFFFu - (uint32_t)k;
+  }
   // compaction: survivors are staged per warp in shared memory and flushed in runs (one
   // global cursor atomic per run, coalesced stores)
   constexpr int WBUF = COMPACT ? 256 : 1;
@@ -598,8 +724,6 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
     __syncwarp();
     nbuf = 0;
   };
-  uint32_t found = 0;
-  unsigned long long farcs = 0;
   const uint64_t stride = (uint64_t)gridDim.x * BLOCK * 2;
   const uint64_t iters = (m + stride - 1) / stride;
   for (uint64_t it = 0; it < iters; it++) {
@@ -618,12 +742,12 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
       if (j >= cnt) continue;
       const uint32_t a = x[j].x, b = x[j].y;
       if (ROOT) {
-        if (a == root && claim2(S, next, b)) { found++; farcs += __ldg(&deg[b]); }
-        if (b == root && claim2(S, next, a)) { found++; farcs += __ldg(&deg[a]); }
+        if (a == root && b != root) mark2(S, next, b);
+        if (b == root && a != root) mark2(S, next, a);
       } else {
         const uint32_t sa = st2(S, a), sb = st2(S, b);
-        if ((sa & 2u) && !(sb & 1u) && claim2(S, next, b)) { found++; farcs += __ldg(&deg[b]); }
-        if ((sb & 2u) && !(sa & 1u) && claim2(S, next, a)) { found++; farcs += __ldg(&deg[a]); }
+        if ((sa & 2u) && !(sb & 1u)) mark2(S, next, b);
+        if ((sb & 2u) && !(sa & 1u)) mark2(S, next, a);
         // after this level a frontier endpoint's neighbour is visited (by this or another
         // edge): an edge whose endpoints are both visited then can no longer matter
         const bool va = (sa & 1u) || (sb & 2u), vb = (sb & 1u) || (sa & 2u);
@@ -642,15 +766,9 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
     }
   }
   if (COMPACT && nbuf) flush();
-  found = warp_sum(found);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) farcs += __shfl_xor_sync(0xffffffffu, farcs, o);
-  if ((threadIdx.x & 31) == 0 && found) {
-    atomicAdd(&gctr[G_NEWVIS], (unsigned long long)found);
-    atomicAdd(&gctr[G_FARCS], farcs);
-  }
 }
-// After a level: frontier bits <- next, visited bits already set by the claims.
+// After a level: frontier bits <- next, visited bits |= next (set by this rank's claims
+// already; with several ranks `next` also holds the other ranks' finds).
 __global__ void k_bfs_advance(uint32_t* S, const uint32_t* __restrict__ next, uint64_t nw2) {
   for (uint64_t w = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; w < nw2; w += (uint64_t)gridDim.x * BLOCK) {
     const uint32_t nb = (next[w >> 1] >> (16 * (w & 1))) & 0xFFFFu;
@@ -660,18 +778,24 @@ __global__ void k_bfs_advance(uint32_t* S, const uint32_t* __restrict__ next, ui
     x = (x | (x << 4)) & 0x0F0F0F0Fu;
     x = (x | (x << 2)) & 0x33333333u;
     x = (x | (x << 1)) & 0x55555555u;
-    S[w] = (S[w] & 0x55555555u) | (x << 1);
+    S[w] = (S[w] & 0x55555555u) | x | (x << 1);
   }
 }
 void launch_bfs_level(bool root_level, bool compact, const uint2* edges, uint64_t m, uint32_t root,
-                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, const uint32_t* deg,
-                      cudaStream_t st) {
+                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, cudaStream_t st) {
   if (!m) return;
   const unsigned g = grid_for((m + 1) / 2, 148 * 8);
   auto* c = reinterpret_cast<unsigned long long*>(gctr);
-  if (root_level) k_bfs_level<true, false><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c, deg);
-  else if (compact) k_bfs_level<false, true><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c, deg);
-  else k_bfs_level<false, false><<<g, BLOCK, 0, st>>>(edges, m, root, S, next, out, c, deg);
+  if (root_level) k_bfs_level<true, false><<<g, BLOCK, 0, st>>>(edges, m, root, nullptr, S, next, out, c);
+  else if (compact) k_bfs_level<false, true><<<g, BLOCK, 0, st>>>(edges, m, root, nullptr, S, next, out, c);
+  else k_bfs_level<false, false><<<g, BLOCK, 0, st>>>(edges, m, root, nullptr, S, next, out, c);
+}
+void launch_farcs(const uint32_t* next, uint64_t n, const uint32_t* deg, uint64_t* found, uint64_t* farcs,
+                  cudaStream_t st) {
+  const uint64_t nw = (n + 31) / 32;
+  if (nw)
+    k_farcs<<<grid_for(nw, 148 * 8), BLOCK, 0, st>>>(next, nw, deg, reinterpret_cast<unsigned long long*>(found),
+                                                      reinterpret_cast<unsigned long long*>(farcs));
 }
 void launch_bfs_advance(uint32_t* S, const uint32_t* next, uint64_t n, cudaStream_t st) {
   const uint64_t nw2 = (n + 15) / 16;

@@ -18,20 +18,34 @@ enum GCtr : int {
   G_MINVIS,        // min visited id
   G_ERR,           // input validation flags
   G_FARCS,         // BFS: arcs (full-graph degrees) of the vertices found in the current level
+  G_GUESS,         // speculative root: max over a prefix of (count<<32 | ~v)
   G_NUM
 };
 
+// speculative root level (graph.cu, k_deg_sample): on lists of >= SPEC_MIN_EDGES edges the
+// degree pass guesses the root from a prefix of SPEC_SAMPLE_EDGES edges and runs the guess's
+// level on the side.  S (2-bit state) and next are zeroed by the caller; the guess key lands
+// in gctr[G_GUESS], the ids found in the next bitmap.
+constexpr uint64_t SPEC_MIN_EDGES = 1ull << 26;
+constexpr uint64_t SPEC_SAMPLE_EDGES = 1ull << 21;
+uint64_t spec_min_edges();  // SPEC_MIN_EDGES, or $CC_SPEC_MIN_EDGES (test hook)
+struct SpecLevel {
+  uint32_t* S;
+  uint32_t* next;
+  uint64_t* gctr;
+};
 void launch_validate(const uint2* edges, uint64_t m, uint64_t n, uint64_t* gctr, cudaStream_t st);
 // deg[v] += arcs with source v (deg zeroed by the caller).  hub_scratch (>= 2048 u32) and
 // hub_count (40 device u64): per-block shared-memory counting of high-degree ids (NULL: off)
 // radix_scratch (>= degree_radix_scratch(m, n) bytes) and radix_cursor (2048 u32): the
 // bucketed shared-memory count (graph.cu), used when n >= 2^20 (CC_DEG_ALGO=radix|window
 // forces one); otherwise, or when the scratch is too small, L2 increments in id windows.
-// returns 1 if the bucketed count ran, 0 for the L2-window increments
+// returns bit 0: the bucketed count ran (else L2-window increments); bit 1: the speculative
+// root level ran (spec != nullptr, bucketed count, m >= SPEC_MIN_EDGES)
 int launch_degree(const uint2* edges, uint64_t m, uint64_t n, uint32_t* deg, cudaStream_t st,
                   uint32_t* hub_scratch = nullptr, uint64_t* hub_count = nullptr,
                   void* radix_scratch = nullptr, uint64_t radix_bytes = 0,
-                  uint32_t* radix_cursor = nullptr);
+                  uint32_t* radix_cursor = nullptr, const SpecLevel* spec = nullptr);
 uint64_t degree_radix_scratch(uint64_t m, uint64_t n);
 // deg[0, n) are the degrees of ids base .. base+n-1 (base > 0: a rank's vertex block)
 // the non-empty bins of hist[1, nb) as (degree, count) pairs into out, *cnt of them (unordered)
@@ -39,12 +53,14 @@ void launch_hist_pairs(const uint32_t* hist, uint64_t nb, uint2* out, uint64_t* 
 void launch_deg_hist(const uint32_t* deg, uint64_t n, uint32_t* hist, uint32_t* tail,
                      uint64_t* gctr, cudaStream_t st, uint64_t base = 0);
 // edge-streaming BFS level over 2-bit vertex state S (16 ids per word: bit0 visited, bit1
-// frontier); newly visited count in gctr[G_NEWVIS] and their degree sum (deg) in
-// gctr[G_FARCS]; with `compact`, the edges that can still matter (an endpoint unvisited after
-// the level) are appended to `out` (count in gctr[G_REMAIN]).
+// frontier): the ids found are set in `next` (and visited in S); with `compact`, the edges
+// that can still matter (an endpoint unvisited after the level) are appended to `out` (count
+// in gctr[G_REMAIN]).  The level's counts come from launch_farcs on `next` afterwards.
 void launch_bfs_level(bool root_level, bool compact, const uint2* edges, uint64_t m, uint32_t root,
-                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, const uint32_t* deg,
-                      cudaStream_t st);
+                      uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, cudaStream_t st);
+// *found += |next|, *farcs += sum of deg[v] over the ids set in next
+void launch_farcs(const uint32_t* next, uint64_t n, const uint32_t* deg, uint64_t* found, uint64_t* farcs,
+                  cudaStream_t st);
 void launch_bfs_advance(uint32_t* S, const uint32_t* next, uint64_t n, cudaStream_t st);
 void launch_filter(const uint2* edges, uint64_t m, const uint32_t* S, uint2* out,
                    uint64_t* gctr, cudaStream_t st);

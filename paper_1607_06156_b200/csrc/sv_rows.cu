@@ -177,11 +177,18 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     uint64_t L, uint32_t ntiles, const uint32_t* __restrict__ MAP,
     const uint32_t* __restrict__ NCPr, const uint32_t* __restrict__ TB, uint32_t* OUT,
     uint32_t* NCPw, uint32_t* __restrict__ label, unsigned long long* ctr, int preset, int excl,
-    const unsigned long long* __restrict__ prevctr, int hot_shift, const uint32_t* __restrict__ HW) {
-  // With prevctr both variants are launched and the previous iteration's counters pick one on
-  // the device (so the host can enqueue this pass before reading them): nothing left ->
-  // neither runs; few partitions per live tuple -> the HOT variant.
-  if (prevctr && (prevctr[sv::C_OUT] == 0 || ((prevctr[sv::C_PARTITIONS] << hot_shift) < L) != HOT)) return;
+    const unsigned long long* __restrict__ prevctr, int hot_shift, const uint32_t* __restrict__ HW,
+    const unsigned long long* __restrict__ hotcnt, int hot_mode) {
+  // With prevctr / hotcnt both variants are launched and device counters pick one (so the host
+  // can enqueue this pass before reading them): nothing left -> neither runs; few distinct
+  // slot targets per live tuple -> the HOT variant.
+  if (prevctr && prevctr[sv::C_OUT] == 0) return;
+  if (hotcnt || prevctr) {
+    const unsigned long long cnt =
+        hotcnt ? (hot_mode ? hotcnt[sv::C_PARTITIONS] - hotcnt[sv::C_CHANGED] + hotcnt[sv::C_TEMPS] : hotcnt[0])
+               : prevctr[sv::C_PARTITIONS];
+    if (((cnt << hot_shift) < L) != HOT) return;
+  }
   constexpr bool PRESET = A && X;
   constexpr int EXCL = (A || X) ? 1 : 0;  // (pass A's relabel ignores it)
   (void)preset;
@@ -852,25 +859,28 @@ template <bool A, bool HOT, bool REL, bool X>
 static void launch_rowpass_x(const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L, uint64_t nt,
                            const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
                            uint32_t* NCPw, uint32_t* label, unsigned long long* c, int preset, int excl,
-                           const uint64_t* prevctr, int hot_shift, cudaStream_t st, const uint32_t* HW) {
+                           const uint64_t* prevctr, int hot_shift, cudaStream_t st, const uint32_t* HW,
+                           const uint64_t* hotcnt, int hot_mode) {
   static unsigned grid = 0;
   if (!grid) grid = persistent_grid((const void*)k_rowpass<A, HOT, REL, X>);
   k_rowpass<A, HOT, REL, X><<<(unsigned)std::min<uint64_t>(nt, grid), PB, 0, st>>>(
       R, Pin, Pout, L, (uint32_t)nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
-      reinterpret_cast<const unsigned long long*>(prevctr), hot_shift, HW);
+      reinterpret_cast<const unsigned long long*>(prevctr), hot_shift, HW,
+      reinterpret_cast<const unsigned long long*>(hotcnt), hot_mode);
 }
 
 template <bool A, bool HOT, bool REL>
 static void launch_rowpass(const uint32_t* R, const uint32_t* Pin, uint32_t* Pout, uint64_t L, uint64_t nt,
                            const uint32_t* MAP, const uint32_t* NCPr, const uint32_t* TB, uint32_t* OUT,
                            uint32_t* NCPw, uint32_t* label, unsigned long long* c, int preset, int excl,
-                           const uint64_t* prevctr, int hot_shift, cudaStream_t st, const uint32_t* HW) {
+                           const uint64_t* prevctr, int hot_shift, cudaStream_t st, const uint32_t* HW,
+                           const uint64_t* hotcnt = nullptr, int hot_mode = 0) {
   if (A ? preset : excl)
     launch_rowpass_x<A, HOT, REL, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
-                                        prevctr, hot_shift, st, HW);
+                                        prevctr, hot_shift, st, HW, hotcnt, hot_mode);
   else
     launch_rowpass_x<A, HOT, REL, false>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, preset, excl,
-                                         prevctr, hot_shift, st, HW);
+                                         prevctr, hot_shift, st, HW, hotcnt, hot_mode);
 }
 
 uint64_t row_tiles(uint64_t L) { return (L + PTILE - 1) / PTILE; }
@@ -891,7 +901,7 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
              uint32_t* NCPw, uint32_t* label, uint64_t* UMIN, uint64_t* UMAX, uint32_t tag,
              const LongSeg* segs, const uint64_t* nsegs, bool have_long, bool hot, uint64_t* ctr,
              cudaStream_t st, bool excl, bool preset, const uint64_t* prevctr, int hot_shift,
-             const uint32_t* HW) {
+             const uint32_t* HW, const uint64_t* hotcnt, int hot_mode) {
   if (!L) return;
   const uint64_t nt = row_tiles(L);
   auto* umin = reinterpret_cast<unsigned long long*>(UMIN);
@@ -909,23 +919,25 @@ void rowpass(bool passA, const uint32_t* R, const uint32_t* Pin, uint32_t* Pout,
       k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
     }
   } else if (passA) {
-    if (prevctr || hot)
+    const bool sel = prevctr || hotcnt;
+    if (sel || hot)
       launch_rowpass<true, true, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                       hot_shift, st, passA ? nullptr : HW);
-    if (prevctr || !hot)
+                                       hot_shift, st, passA ? nullptr : HW, hotcnt, hot_mode);
+    if (sel || !hot)
       launch_rowpass<true, false, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                        hot_shift, st, passA ? nullptr : HW);
+                                        hot_shift, st, passA ? nullptr : HW, hotcnt, hot_mode);
     if (have_long) {
       k_long1<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<true><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);
     }
   } else {
-    if (prevctr || hot)
+    const bool sel = prevctr || hotcnt;
+    if (sel || hot)
       launch_rowpass<false, true, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                        hot_shift, st, passA ? nullptr : HW);
-    if (prevctr || !hot)
+                                        hot_shift, st, passA ? nullptr : HW, hotcnt, hot_mode);
+    if (sel || !hot)
       launch_rowpass<false, false, true>(R, Pin, Pout, L, nt, MAP, NCPr, TB, OUT, NCPw, label, c, pre, ex, prevctr,
-                                         hot_shift, st, passA ? nullptr : HW);
+                                         hot_shift, st, passA ? nullptr : HW, hotcnt, hot_mode);
     if (have_long) {
       k_long1<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, TB, umin, umax, tag);
       k_long2<false><<<148 * 4, RB, 0, st>>>(Pv, segs, ns, umin, umax, TB, OUT, NCPw, tag);

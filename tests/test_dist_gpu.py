@@ -344,3 +344,36 @@ def test_dist_failure_agreement():
     res = run_ranks(_rank_fail, 2, g.n, g.edges, 1, 1 << 16, timeout=120)
     assert res[1] == ("err", cc.CC_ERR_NOMEM)
     assert res[0] == ("err", cc.CC_ERR_COMM)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_dist_edge_partitioned_bfs(world):
+    """The BFS route over ranks (cc_dist.cu): degrees counted per rank and summed, each rank
+    streams its own edges with a replicated state (bfs_stream: level found bitmaps OR-ed, every
+    rank marks the others' finds visited, local compaction), only the remainder is regrouped.
+    Root, visited count, levels, remainder size and the remainder's SV trace equal the oracle's."""
+    from oracle import bfs as obfs
+    from oracle import degree as odeg
+    g = graphgen.rmat_scale_graph(16)
+    modes = ("auto", "bfs+sv")
+    res = run_ranks(_rank_run, world, g.n, g.edges, modes, 0)
+    _check(res, g.n, g.edges, modes, trace=False)
+    deg, _ = odeg.degree_distribution(g.n, g.edges)
+    root = obfs.bfs_root(deg)
+    vis, levels = obfs.bfs(g.n, g.edges, root)
+    rem = obfs.filter_edges(g.edges, vis)
+    _, tr = osv.sv_trace(g.n, rem)
+    want_tr = [tuple(int(d[k]) for k in ("A", "P", "T", "completed", "changed", "changed2")) for d in tr]
+    for mode in modes:
+        for r in res:
+            rep = r[mode][3]
+            assert rep["ran_bfs"] == 1
+            assert rep["bfs_root"] == root
+            assert rep["bfs_visited"] == int(vis.sum())
+            assert rep["bfs_levels"] == levels
+            assert rep["remainder_edges"] == rem.shape[0]
+            assert rep["max_degree"] == int(deg.max())
+            assert rep["n_present"] == int(np.count_nonzero(deg))
+            got = [(it["active_in"], it["partitions"], it["temps"], it["completed"], it["changed"],
+                    it["changed2"]) for it in rep["iters"]]
+            assert got == want_tr
