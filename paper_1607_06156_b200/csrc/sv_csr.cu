@@ -626,6 +626,11 @@ int group_shift(uint64_t n, uint64_t tuples) {
   int lg = 0;  // log2 G: about 2M tuples per group
   while (lg < 10 && (tuples >> (21 + lg)) > 0) lg++;
   int gs = kb - lg;
+  // at most 64 groups while a group can stay within 2^20 ids: k_bucket gives every group one
+  // run per 2048-edge tile, and with 1024 groups (C4 in mode sv) those runs were 4 arcs (one
+  // sector) long; 2^20 ids keep a k_bucket2 tile's subgroups within its 512 local counters
+  const int gs_min = std::min(20, kb - 6);
+  if (gs < gs_min) gs = gs_min;
   return gs < 12 ? 12 : gs;  // a k_rows tile (2^12 vertices) lies inside one group
 }
 
