@@ -79,6 +79,13 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
 #define CC_FLAG_PROFILE 0x10u        /* CUDA-event timing of kernel families (cc_kernel_stats) */
 #define CC_FLAG_NO_COLLAPSE 0x200u   /* csr engine: never collapse potentially-completed rows
                                         to one tuple (ablation; DESIGN.md §5.2 row collapse) */
+#define CC_FLAG_NO_RENUMBER 0x400u   /* BFS route: run the SV on the remainder with the original
+                                        id range instead of its endpoints renumbered densely in
+                                        id order (ablation)                   */
+#define CC_FLAG_BALANCE 0x800u      /* several ranks, csr engine with exclusion: the paper's
+                                        'balanced' variant -- the live rows are
+                                        redistributed evenly over the ranks after an iteration
+                                        whose most loaded rank holds > 1/16 above the mean  */
 #define CC_FLAG_BFS_CSR 0x40u        /* csr engine: degrees from the bucketed CSR build and a
                                         direction-optimising (top-down / bottom-up) BFS on the
                                         CSR rows instead of the edge-streaming BFS            */
@@ -170,6 +177,9 @@ typedef struct {
   int bfs_spec_root;                  /* 1: the BFS root's level ran inside the degree
                                          pass on a guessed root that proved exact (large
                                          lists); labels are unaffected  */
+  uint64_t sv_ids;                    /* id range the SV ran on: n, or n' (the remainder's
+                                         endpoints renumbered densely in id order, BFS
+                                         route); 0 if no SV ran           */
 } cc_report;
 
 /* Library version string. */

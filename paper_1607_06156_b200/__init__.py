@@ -33,6 +33,8 @@ CC_FLAG_BFS_CSR = 0x40
 CC_FLAG_NO_EXCLUDE = 0x80
 CC_FLAG_PERMUTE_IDS = 0x100
 CC_FLAG_NO_COLLAPSE = 0x200
+CC_FLAG_NO_RENUMBER = 0x400
+CC_FLAG_BALANCE = 0x800
 EXCLUSION_FLAGS = {"early": 0, "end": CC_FLAG_NO_EARLY_EXCLUDE, "none": CC_FLAG_NO_EXCLUDE}
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -85,7 +87,7 @@ class cc_report(ctypes.Structure):
                 ("ms_filter", ctypes.c_double), ("ms_sv", ctypes.c_double),
                 ("ms_finalize", ctypes.c_double), ("iters", ctypes.POINTER(cc_iter_stat)),
                 ("n_iters", ctypes.c_uint32),
-                ("bfs_spec_root", ctypes.c_int)]
+                ("bfs_spec_root", ctypes.c_int), ("sv_ids", ctypes.c_uint64)]
 
 
 EXPORTS = ["cc_version", "cc_get_unique_id", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",

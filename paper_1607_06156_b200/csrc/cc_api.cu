@@ -458,7 +458,11 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   uint64_t* CTR[2] = {c->d_ctr, c->d_ctr + sv::C_NUM};
   cudaEvent_t ev_read[2] = {ev_get(c), ev_get(c)};
   // hot thresholds measured on C2 (iterations with 490 k / 112 k / 16 k previous partitions):
-  // pass A gains from the block tables below 1/512 partitions per live tuple, pass B below 1/128
+  // pass A gains from the block tables below 1/512 partitions per live tuple, pass B below 1/128.
+  // Iteration 0 has no previous counters: its pass B selects on the distinct slots it will
+  // update (the p_min targets k_pstat1 counted, C_TDIST) -- on power-law graphs most
+  // partitions join a few hubs' minima at once (C4 mode sv: 11 k targets for 2.2 G tuples,
+  // cold pass B 223 ms serialised on those slots)
   // CC_HOT_SEL=1: select on the slot targets of this iteration instead (|P_i| for pass A, the
   // distinct p_min targets for pass B; csr.cuh rowpass), thresholds $CC_HOT_A / $CC_HOT_B
   const char* hs = getenv("CC_HOT_SEL");
@@ -520,7 +524,8 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
                    c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, false, ctr, c->st,
-                   excl, false, prevctr, HOT_B, hw_ready ? c->d_hw : nullptr, hot_cur ? ctr : nullptr, 1);
+                   excl, false, prevctr, HOT_B, hw_ready ? c->d_hw : nullptr,
+                   hot_cur || it == 0 ? ctr : nullptr, hot_cur ? 1 : 2);
       k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
     // live tuples: this rank's (compaction) and the global count (convergence)
@@ -553,6 +558,24 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   struct Snap { size_t nev; double bytes; uint64_t launches; } snap[KF_N];
   auto take_snap = [&]() {
     for (int f = 0; f < KF_N; f++) snap[f] = {c->kst[f].ev.size(), c->kst[f].bytes, c->kst[f].launches};
+  };
+  // 'balanced' variant (several ranks with exclusion, CC_FLAG_BALANCE): after an
+  // iteration whose most loaded rank holds > 1/16 above the mean, the live rows are
+  // redistributed evenly (rebalance_rows, cc_dist.cu); rows then live off their owner, so the
+  // long-row list takes the global degrees and the labels are min-combined at the end
+  const bool balance = multi && excl && (c->cfg.flags & CC_FLAG_BALANCE);
+  bool deg_global = false, rebalanced = false;
+  std::vector<uint64_t> loads;
+  auto gather_loads = [&](uint64_t mine) -> cc_status {
+    const int world = c->cfg.world_size;
+    if (!c->d_bal) TRY(comm_agree(c, dalloc_t(c, &c->d_bal, (uint64_t)(world + 1) + (uint64_t)world * (world + 1))));
+    const uint64_t v[2] = {mine, c->cap};
+    CK(cudaMemcpyAsync(c->d_bal, v, sizeof(v), cudaMemcpyHostToDevice, c->st));
+    TRY(comm_allgather(c, c->d_bal, c->d_bal + 2, sizeof(v)));
+    loads.resize(2 * (size_t)world);
+    CK(cudaMemcpyAsync(loads.data(), c->d_bal + 2, sizeof(uint64_t) * 2 * world, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return CC_OK;
   };
   uint64_t local_in = A_local;
   bool pending_compact = false;
@@ -623,7 +646,18 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
         collapse_force ? can_collapse && len_live > 0
                        : collapse_ok && it >= 1 && it >= last_collapse + 2 && len_live >= COLLAPSE_MIN_LEN &&
                              s.partitions * 16 < len_live;
-    const bool want = 3 * (len - len_live) > len || want_collapse;
+    bool rebalance = false;
+    if (balance) {
+      TRY(gather_loads(len_live));
+      uint64_t tot = 0, mx = 0;
+      for (int k = 0; k < c->cfg.world_size; k++) {
+        tot += loads[2 * k];
+        mx = std::max(mx, loads[2 * k]);
+      }
+      const uint64_t mean = (tot + c->cfg.world_size - 1) / c->cfg.world_size;
+      rebalance = tot > 0 && mx * 16 > mean * 17;
+    }
+    const bool want = 3 * (len - len_live) > len || want_collapse || (rebalance && len > len_live);
     if (pending_compact || (want && next_enq == it + 1)) {
       const bool do_collapse = pending_collapse || want_collapse;
       pending_compact = pending_collapse = false;
@@ -662,9 +696,31 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       pending_compact = true;
       pending_collapse = want_collapse;
     }
+    if (rebalance) {  // the live rows are now R[cb], Pc[0, len)
+      uint32_t* Pdst = P[cb ^ 1];
+      uint64_t nl = 0;
+      bool moved = false;
+      TRY(rebalance_rows(c, R[cb], Pc, R[cb ^ 1], Pdst, len, loads, &nl, &moved));
+      if (moved) {
+        if (!deg_global) {  // rows off their owner: the long-row list needs every degree
+          TRY(comm_allreduce(c, c->d_deg, n, CC_DT_I32, CC_OP_SUM));
+          deg_global = true;
+        }
+        rebalanced = true;
+        cb ^= 1;
+        Pc = P[cb];
+        Palt = c->d_q[0];
+        len = nl;
+        local_in = nl;
+        if (have_long) csr::longlist(R[cb], Pc, len, c->d_deg, c->d_lsegs, c->d_nlsegs, c->st);
+      }
+    }
     A = A_next;
     if (next_enq == it + 1) TRY(enqueue(it + 1));
   }
+  // a vertex whose row moved was labelled on the rank that held it; every other rank holds
+  // its own id or the (replicated) BFS label there, both >= the true label
+  if (rebalanced) TRY(comm_min_u32(c, c->d_label, n));
   CK(cudaStreamSynchronize(c->st));
   return CC_OK;
 }
@@ -921,6 +977,60 @@ cc_status bfs_stream(cc_ctx* c, uint64_t root, bool spec_ok, const uint2** rem, 
     *m_rem = c->h_gctr[graph::G_REMAIN];
     *rem = bufs[nb];
   }
+  return CC_OK;
+}
+
+// SV on the BFS remainder with its endpoints renumbered densely in id order (graph.cu,
+// "remainder renumbering").  Alg. 1 compares ids only, so the run on
+// [0, n') has the same sets and counters; the labels go back through inv.  Scratch: the
+// 2-bit BFS state (free after the peel) holds the bitmap and word prefixes, the other
+// remainder buffer the renumbered edges, inv, degrees and labels.
+static bool renumber_fits(const cc_ctx* c, const uint2* edges, uint64_t m_sv) {
+  if (c->cfg.flags & CC_FLAG_NO_RENUMBER) return false;
+  if (multi_gpu(c) || !c->d_rem || !c->d_rem2 || (edges != c->d_rem && edges != c->d_rem2)) return false;
+  if (m_sv == 0 || m_sv * 8 > c->n) return false;  // worth it once n' <= 2 m_sv is a fraction of n
+  const uint64_t nw = (c->n + 31) / 32;
+  // 8 m_sv bytes of edges + 3 x 4 (2 m_sv) bytes (inv, sdeg, labels) + the tile sums
+  return 32 * m_sv + 4 * graph::sub_bsum_words(nw) <= 8 * c->m;
+}
+static cc_status run_sv(cc_ctx* c, const uint2* edges, uint64_t m_sv, const uint32_t* vis);
+static cc_status run_sv_renumbered(cc_ctx* c, const uint2* edges, uint64_t m_sv) {
+  const uint64_t n = c->n, nw = (n + 31) / 32;
+  uint32_t* bm = c->d_bm[1];  // 2 nw words (the BFS state)
+  uint32_t* wpre = bm + nw;
+  uint2* se = edges == c->d_rem ? c->d_rem2 : c->d_rem;
+  uint32_t* inv = reinterpret_cast<uint32_t*>(se + m_sv);
+  uint32_t* sdeg = inv + 2 * m_sv;
+  uint32_t* slab = sdeg + 2 * m_sv;
+  uint32_t* bsum = slab + 2 * m_sv;
+  uint64_t* subn = c->d_gctr + graph::G_SUBN;
+  CK(cudaMemsetAsync(bm, 0, sizeof(uint32_t) * nw, c->st));
+  graph::launch_sub_mark(edges, m_sv, bm, c->st);
+  graph::launch_sub_rank(bm, nw, bsum, wpre, subn, c->st);
+  graph::launch_sub_edges(edges, m_sv, bm, wpre, c->d_deg, se, inv, sdeg, c->st);
+  c->launches += 4;
+  CKL();
+  TRY(sync_read(c));
+  const uint64_t ns = c->h_gctr[graph::G_SUBN];
+  if (ns == 0 || ns > 2 * m_sv) return fail(c, CC_ERR_INVALID, "internal: renumbered %llu ids for %llu edges",
+                                            (unsigned long long)ns, (unsigned long long)m_sv);
+  c->rep.sv_ids = ns;
+  sv::launch_init_labels(slab, ns, c->st);
+  c->launches += 1;
+  // the SV sees n' ids, their degrees and their labels
+  const uint64_t n_save = c->n;
+  uint32_t *deg_save = c->d_deg, *lab_save = c->d_label;
+  c->n = ns;
+  c->d_deg = sdeg;
+  c->d_label = slab;
+  const cc_status s = run_sv(c, se, m_sv, nullptr);
+  c->n = n_save;
+  c->d_deg = deg_save;
+  c->d_label = lab_save;
+  TRY(s);
+  graph::launch_sub_labels(inv, slab, ns, c->d_label, c->st);
+  c->launches += 1;
+  CKL();
   return CC_OK;
 }
 
@@ -1194,8 +1304,12 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
 
   // ------------------------------------------------ SV (line 13)
   if (gsf >= 0 && !run_bfs) {
+    c->rep.sv_ids = n;
     if (A_full) TRY(sv_iterate(c, A_full, A_full, A_full));  // the rows built above
+  } else if (run_bfs && renumber_fits(c, sv_edges, m_sv)) {
+    TRY(run_sv_renumbered(c, sv_edges, m_sv));
   } else {
+    c->rep.sv_ids = n;
     TRY(run_sv(c, sv_edges, m_sv, vis));
   }
   if (c->idw == CC_U64 && (c->cfg.flags & CC_FLAG_PERMUTE_IDS)) {

@@ -94,6 +94,40 @@ static unsigned gsz(uint64_t work, unsigned cap) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + DB - 1) / DB, cap));
 }
 
+// 'Balanced' variant: split points of this rank's rows for an even
+// redistribution.  R (flag-masked) is nondecreasing over the concatenation of all ranks'
+// arrays (rank k's rows come before rank k+1's), so the tuple at global position g belongs to
+// rank g / q, and a row goes whole to the rank of its head: split[t] is the first row head at
+// or after global position t*q.
+__global__ void k_bal_splits(const uint32_t* __restrict__ R, uint64_t len, uint64_t before, uint64_t q,
+                             int world, unsigned long long* split) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > world) return;
+  uint64_t s;
+  if (t == 0) s = 0;
+  else if (t == world) s = len;
+  else {
+    const uint64_t g = (uint64_t)t * q;
+    if (g <= before) s = 0;
+    else if (g - before >= len) s = len;
+    else {
+      uint64_t j = g - before;
+      const uint32_t v = R[j] & ~csr::R_LONG;
+      if ((R[j - 1] & ~csr::R_LONG) != v) s = j;
+      else {  // first index past the row holding j
+        uint64_t lo = j, hi = len;
+        while (lo < hi) {
+          const uint64_t mid = lo + (hi - lo) / 2;
+          if ((R[mid] & ~csr::R_LONG) > v) hi = mid;
+          else lo = mid + 1;
+        }
+        s = lo;
+      }
+    }
+  }
+  split[t] = s;
+}
+
 }  // namespace dist
 }  // namespace cc
 
@@ -308,6 +342,7 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
   uint64_t A = 0;
   CK(cudaMemcpyAsync(&A, tmp, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  R.sv_ids = n;
   if (A) TRY(sv_iterate(c, A, len, A_local));
   R.sv_iterations = (uint32_t)c->iters.size();
   // components: roots of the owned block, summed over ranks
@@ -324,5 +359,61 @@ cc_status run_dist(cc_ctx* c, cc_mode mode) {
   R.ms_bfs = run_bfs ? ev_ms(e_pred, e_bfs) : 0;
   R.ms_filter = run_bfs ? ev_ms(e_bfs, e_filter) : 0;
   R.ms_sv = ev_ms(e_filter, e_sv);
+  return CC_OK;
+}
+
+// 'Balanced' variant (sec:distSVOpt2; CC_FLAG_BALANCE): the live rows of all
+// ranks are redistributed evenly, whole rows, in global order (R nondecreasing over the ranks'
+// concatenation), by one all-to-all-v of R and one of P.  Rows may leave their owner: the
+// slots are combined over ranks anyway, the long-row list needs the global degrees
+// (sv_iterate sums them first) and the labels are min-combined at the end.  Collective; the
+// plan is computed identically on every rank from the gathered loads and split vectors, and a
+// plan that would overflow some rank's tuple capacity is skipped (*moved = false).
+cc_status rebalance_rows(cc_ctx* c, const uint32_t* Rsrc, const uint32_t* Psrc, uint32_t* Rdst,
+                         uint32_t* Pdst, uint64_t len, const std::vector<uint64_t>& loads,
+                         uint64_t* new_len, bool* moved) {
+  const int world = c->cfg.world_size, rank = c->cfg.rank;
+  *moved = false;
+  uint64_t total = 0, before = 0;
+  for (int k = 0; k < world; k++) {
+    total += loads[2 * k];
+    if (k < rank) before += loads[2 * k];
+  }
+  const uint64_t q = (total + world - 1) / world;
+  if (!c->d_bal) {
+    cc_status s = dalloc_t(c, &c->d_bal, (uint64_t)(world + 1) + (uint64_t)world * (world + 1));
+    TRY(comm_agree(c, s));
+  }
+  uint64_t* split = c->d_bal;                // world + 1
+  uint64_t* all = c->d_bal + world + 1;      // world x world send counts (tuples)
+  k_bal_splits<<<(world + 128) / 128, 128, 0, c->st>>>(Rsrc, len, before, q, world,
+                                                        reinterpret_cast<unsigned long long*>(split));
+  c->launches += 1;
+  CKL();
+  std::vector<uint64_t> sp(world + 1), cnt(world), mat((size_t)world * world);
+  CK(cudaMemcpyAsync(sp.data(), split, sizeof(uint64_t) * (world + 1), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  for (int t = 0; t < world; t++) cnt[t] = sp[t + 1] - sp[t];
+  CK(cudaMemcpyAsync(split, cnt.data(), sizeof(uint64_t) * world, cudaMemcpyHostToDevice, c->st));
+  TRY(comm_allgather(c, split, all, sizeof(uint64_t) * world));
+  CK(cudaMemcpyAsync(mat.data(), all, sizeof(uint64_t) * world * world, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  // mat[j * world + k]: tuples rank j sends to rank k
+  for (int k = 0; k < world; k++) {
+    uint64_t in = 0;
+    for (int j = 0; j < world; j++) in += mat[(size_t)j * world + k];
+    if (in + 64 > loads[2 * k + 1]) return CC_OK;  // would overflow rank k: skip (all ranks agree)
+  }
+  std::vector<uint64_t> sb(world), rb(world);
+  uint64_t nl = 0;
+  for (int k = 0; k < world; k++) {
+    sb[k] = sizeof(uint32_t) * mat[(size_t)rank * world + k];
+    rb[k] = sizeof(uint32_t) * mat[(size_t)k * world + rank];
+    nl += mat[(size_t)k * world + rank];
+  }
+  TRY(comm_alltoallv(c, Rsrc, sb.data(), Rdst, rb.data()));
+  TRY(comm_alltoallv(c, Psrc, sb.data(), Pdst, rb.data()));
+  *new_len = nl;
+  *moved = true;
   return CC_OK;
 }

@@ -84,6 +84,7 @@ struct cc_ctx {
   uint64_t* d_cnt = nullptr;     // per-owner arc counts (world_size^2 after the gather)
   uint2* d_xsend = nullptr;      // sparse slot exchange: my touched entries / everyone's
   uint2* d_xrecv = nullptr;
+  uint64_t* d_bal = nullptr;     // balanced variant: split points and the gathered send counts
   uint64_t xsend_cap = 0, xrecv_cap = 0;
   uint32_t* d_garc = nullptr;  // CSR vertex-group scratch: arcs per group (<= 2048 groups)
   uint64_t* d_gcur = nullptr;  // group cursors [0, 2048), long-row count at [2048]
@@ -189,6 +190,7 @@ static inline void dfree_all(cc_ctx* c) {
   c->d_gath = nullptr;
   c->d_cnt = nullptr;
   c->d_xsend = c->d_xrecv = nullptr;
+  c->d_bal = nullptr;
   c->xsend_cap = c->xrecv_cap = 0;
   c->recv_cap = c->gath_cap = 0;
   c->d_lsegs = nullptr;
@@ -484,6 +486,13 @@ cc_status bfs_stream(cc_ctx* c, uint64_t root, bool spec_ok, const uint2** rem, 
 
 // cc_run for world_size > 1 (cc_dist.cu).
 cc_status run_dist(cc_ctx* c, cc_mode mode);
+
+// 'Balanced' variant (cc_dist.cu; CC_FLAG_BALANCE): even redistribution of the live rows
+// (R, P of `len` tuples) over the ranks into (Rdst, Pdst); loads[2k] = rank k's live tuples,
+// loads[2k + 1] = its tuple capacity.  Collective; *moved = false if the plan was skipped.
+cc_status rebalance_rows(cc_ctx* c, const uint32_t* Rsrc, const uint32_t* Psrc, uint32_t* Rdst,
+                         uint32_t* Pdst, uint64_t len, const std::vector<uint64_t>& loads,
+                         uint64_t* new_len, bool* moved);
 
 // n-sized buffers and the owned vertex block for id range n (cc_api.cu).
 cc_status alloc_vertex_buffers(cc_ctx* c, uint64_t n);

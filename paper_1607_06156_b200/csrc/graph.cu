@@ -905,5 +905,99 @@ void launch_count_roots(const uint32_t* label, uint64_t lo, uint64_t hi, uint64_
                                                                 reinterpret_cast<unsigned long long*>(cnt));
 }
 
+// ------------------------------------------------------------- remainder renumbering
+// (DESIGN.md §5.3).  Alg. 1 only compares ids (minima, equality), so running it on the
+// remainder's endpoints renumbered in id order gives the same partitions, tuples and counters
+// (PAPER.md:133-178); the labels map back through inv.  Saves the id-range-sized passes of the
+// SV (slot clears and scans, CSR offsets) when the remainder is small (C4: 21 k of 67 M ids).
+__global__ void k_sub_mark(const uint2* __restrict__ e, uint64_t m, uint32_t* bm) {
+  for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i < m; i += (uint64_t)gridDim.x * BLOCK) {
+    const uint2 x = e[i];
+    atomicOr(&bm[x.x >> 5], 1u << (x.x & 31));
+    atomicOr(&bm[x.y >> 5], 1u << (x.y & 31));
+  }
+}
+constexpr int SUBW = 16;                       // bitmap words per thread
+constexpr uint64_t SUB_TILE = (uint64_t)BLOCK * SUBW;
+uint64_t sub_bsum_words(uint64_t nw) { return (nw + SUB_TILE - 1) / SUB_TILE + 1; }
+__global__ void __launch_bounds__(BLOCK) k_sub_bsum(const uint32_t* __restrict__ bm, uint64_t nw,
+                                                    uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t s_scan[BLOCK / 32 + 1];
+  const uint64_t w0 = blockIdx.x * SUB_TILE + (uint64_t)threadIdx.x * SUBW;
+  uint32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < SUBW; k++)
+    if (w0 + k < nw) c += __popc(bm[w0 + k]);
+  uint32_t tot;
+  block_excl_scan<BLOCK>(c, s_scan, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(BLOCK) k_sub_rank(const uint32_t* __restrict__ bm, uint64_t nw,
+                                                    const uint32_t* __restrict__ bsum,
+                                                    uint32_t* __restrict__ wpre,
+                                                    unsigned long long* total) {
+  __shared__ uint32_t s_scan[BLOCK / 32 + 1];
+  // this tile's offset: the sum of the earlier tiles' counts
+  uint32_t before = 0;
+  for (uint32_t j = threadIdx.x; j < blockIdx.x; j += BLOCK) before += bsum[j];
+  uint32_t pref;
+  block_excl_scan<BLOCK>(before, s_scan, &pref);
+  const uint64_t w0 = blockIdx.x * SUB_TILE + (uint64_t)threadIdx.x * SUBW;
+  uint32_t c[SUBW], sum = 0;
+#pragma unroll
+  for (int k = 0; k < SUBW; k++) {
+    c[k] = w0 + k < nw ? __popc(bm[w0 + k]) : 0u;
+    sum += c[k];
+  }
+  uint32_t tot;
+  uint32_t run = pref + block_excl_scan<BLOCK>(sum, s_scan, &tot);
+#pragma unroll
+  for (int k = 0; k < SUBW; k++) {
+    if (w0 + k < nw) wpre[w0 + k] = run;
+    run += c[k];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = (unsigned long long)pref + tot;
+}
+void launch_sub_mark(const uint2* edges, uint64_t m, uint32_t* bm, cudaStream_t st) {
+  if (m) k_sub_mark<<<grid_for(m, 148 * 8), BLOCK, 0, st>>>(edges, m, bm);
+}
+void launch_sub_rank(const uint32_t* bm, uint64_t nw, uint32_t* bsum, uint32_t* wpre, uint64_t* total,
+                     cudaStream_t st) {
+  if (!nw) return;
+  const unsigned tiles = (unsigned)((nw + SUB_TILE - 1) / SUB_TILE);
+  k_sub_bsum<<<tiles, BLOCK, 0, st>>>(bm, nw, bsum);
+  k_sub_rank<<<tiles, BLOCK, 0, st>>>(bm, nw, bsum, wpre, reinterpret_cast<unsigned long long*>(total));
+}
+CC_DEVI uint32_t sub_rank_of(const uint32_t* bm, const uint32_t* wpre, uint32_t x) {
+  return wpre[x >> 5] + __popc(bm[x >> 5] & ((1u << (x & 31)) - 1u));
+}
+__global__ void k_sub_edges(const uint2* __restrict__ e, uint64_t m, const uint32_t* __restrict__ bm,
+                            const uint32_t* __restrict__ wpre, const uint32_t* __restrict__ deg,
+                            uint2* __restrict__ out, uint32_t* __restrict__ inv, uint32_t* __restrict__ sdeg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i < m; i += (uint64_t)gridDim.x * BLOCK) {
+    const uint2 x = e[i];
+    const uint32_t ru = sub_rank_of(bm, wpre, x.x), rv = sub_rank_of(bm, wpre, x.y);
+    out[i] = make_uint2(ru, rv);
+    // every arc of an endpoint writes the same values (benign)
+    inv[ru] = x.x;
+    inv[rv] = x.y;
+    sdeg[ru] = deg[x.x];
+    sdeg[rv] = deg[x.y];
+  }
+}
+void launch_sub_edges(const uint2* edges, uint64_t m, const uint32_t* bm, const uint32_t* wpre,
+                      const uint32_t* deg, uint2* out, uint32_t* inv, uint32_t* sdeg, cudaStream_t st) {
+  if (m) k_sub_edges<<<grid_for(m, 148 * 8), BLOCK, 0, st>>>(edges, m, bm, wpre, deg, out, inv, sdeg);
+}
+__global__ void k_sub_labels(const uint32_t* __restrict__ inv, const uint32_t* __restrict__ slabel,
+                             uint64_t ns, uint32_t* __restrict__ label) {
+  for (uint64_t i = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; i < ns; i += (uint64_t)gridDim.x * BLOCK)
+    label[inv[i]] = inv[slabel[i]];
+}
+void launch_sub_labels(const uint32_t* inv, const uint32_t* slabel, uint64_t ns, uint32_t* label,
+                       cudaStream_t st) {
+  if (ns) k_sub_labels<<<grid_for(ns, 148 * 8), BLOCK, 0, st>>>(inv, slabel, ns, label);
+}
+
 }  // namespace graph
 }  // namespace cc

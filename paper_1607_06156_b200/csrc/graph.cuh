@@ -19,6 +19,7 @@ enum GCtr : int {
   G_ERR,           // input validation flags
   G_FARCS,         // BFS: arcs (full-graph degrees) of the vertices found in the current level
   G_GUESS,         // speculative root: max over a prefix of (count<<32 | ~v)
+  G_SUBN,          // remainder renumbering: n' (distinct endpoints of the remainder)
   G_NUM
 };
 
@@ -68,6 +69,22 @@ void launch_vis_bits(const uint32_t* S, uint64_t n, uint32_t* vis, cudaStream_t 
 void launch_bfs_labels(const uint32_t* visited, uint64_t n, uint32_t* label, uint64_t* gctr,
                        cudaStream_t st);
 void launch_min_visited(const uint32_t* visited, uint64_t n, uint64_t* gctr, cudaStream_t st);
+
+// Remainder renumbering: the edges left after the BFS peel touch few ids, so
+// the SV runs on their endpoints renumbered densely in id order, [0, n').  The map is monotone,
+// and Alg. 1 only compares ids, so its sets and counters are those of the original ids.
+// bm (nw words, caller-zeroed): the endpoints' bits
+void launch_sub_mark(const uint2* edges, uint64_t m, uint32_t* bm, cudaStream_t st);
+// wpre[w] = set bits of bm before word w; *total = n' (bsum: sub_bsum_words(nw) scratch words)
+uint64_t sub_bsum_words(uint64_t nw);
+void launch_sub_rank(const uint32_t* bm, uint64_t nw, uint32_t* bsum, uint32_t* wpre, uint64_t* total,
+                     cudaStream_t st);
+// out[i] = (rank(u), rank(v)); inv[rank(x)] = x; sdeg[rank(x)] = deg[x]
+void launch_sub_edges(const uint2* edges, uint64_t m, const uint32_t* bm, const uint32_t* wpre,
+                      const uint32_t* deg, uint2* out, uint32_t* inv, uint32_t* sdeg, cudaStream_t st);
+// label[inv[i]] = inv[slabel[i]] for i < ns
+void launch_sub_labels(const uint32_t* inv, const uint32_t* slabel, uint64_t ns, uint32_t* label,
+                       cudaStream_t st);
 
 // *cnt += #{v in [lo, hi) : label[v] = v} (caller-zeroed)
 void launch_count_roots(const uint32_t* label, uint64_t lo, uint64_t hi, uint64_t* cnt, cudaStream_t st);

@@ -14,6 +14,7 @@ enum Ctr : int {
   C_TEMPS,          // temporaries emitted
   C_CHANGED2,       // p_min != p at pass 4
   C_HIDDEN_DEAD,    // csr engine: collapsed tuples of the rows that left in pass B (row collapse)
+  C_TDIST,          // csr engine, iteration 0: distinct temporary targets p_min (set TB bits)
   C_SURVIVORS,      // non-temporary tuples kept
   C_VT_OUT,         // vertex-tuple cursor (init)
   C_ERR,            // error flags (range)

@@ -185,7 +185,9 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
   if (prevctr && prevctr[sv::C_OUT] == 0) return;
   if (hotcnt || prevctr) {
     const unsigned long long cnt =
-        hotcnt ? (hot_mode ? hotcnt[sv::C_PARTITIONS] - hotcnt[sv::C_CHANGED] + hotcnt[sv::C_TEMPS] : hotcnt[0])
+        hotcnt ? (hot_mode == 2   ? hotcnt[sv::C_TDIST]
+                  : hot_mode == 1 ? hotcnt[sv::C_PARTITIONS] - hotcnt[sv::C_CHANGED] + hotcnt[sv::C_TEMPS]
+                                  : hotcnt[0])
                : prevctr[sv::C_PARTITIONS];
     if (((cnt << hot_shift) < L) != HOT) return;
   }
@@ -599,8 +601,11 @@ __global__ void __launch_bounds__(RB) k_long2(const uint32_t* __restrict__ P,
 // --------------------------------------------------------------------------- slot scans
 // After pass A: |P_i|, completed, changed, T_i from PA/NCP; one temporary per surviving
 // partition marks TB(p_min) (line 22); PB is cleared for pass B.
+// nd (DIST): TB bits this thread set first, i.e. distinct temporary targets p_min = the slots
+// pass B will update (its hot-variant choice in iteration 0, which has no earlier counters)
+template <bool DIST = false>
 CC_DEVI bool pstat1_one(uint32_t pid, uint32_t pm, bool ncp, int temps_all, uint32_t* TB, uint32_t& np,
-                        uint32_t& nc, uint32_t& ch, uint32_t& nt) {
+                        uint32_t& nc, uint32_t& ch, uint32_t& nt, uint32_t& nd) {
   np++;
   ch += pm != pid;
   const bool comp = pm == pid && !ncp;
@@ -608,17 +613,22 @@ CC_DEVI bool pstat1_one(uint32_t pid, uint32_t pm, bool ncp, int temps_all, uint
   if (!comp || temps_all) {  // temps_all: completed partitions stay for this iteration
     nt++;
     const uint32_t b = 1u << (pm & 31);
-    if (!(*(volatile uint32_t*)&TB[pm >> 5] & b)) atomicOr(&TB[pm >> 5], b);
+    if (!(*(volatile uint32_t*)&TB[pm >> 5] & b)) {
+      if (DIST) nd += !(atomicOr(&TB[pm >> 5], b) & b);
+      else atomicOr(&TB[pm >> 5], b);
+    }
   }
   return comp;
 }
-CC_DEVI void pstat1_flush(uint32_t np, uint32_t nc, uint32_t ch, uint32_t nt, unsigned long long* ctr) {
-  np = warp_sum(np); nc = warp_sum(nc); ch = warp_sum(ch); nt = warp_sum(nt);
+CC_DEVI void pstat1_flush(uint32_t np, uint32_t nc, uint32_t ch, uint32_t nt, unsigned long long* ctr,
+                          uint32_t nd = 0) {
+  np = warp_sum(np); nc = warp_sum(nc); ch = warp_sum(ch); nt = warp_sum(nt); nd = warp_sum(nd);
   if ((threadIdx.x & 31) == 0) {
     if (np) atomicAdd(&ctr[sv::C_PARTITIONS], (unsigned long long)np);
     if (nc) atomicAdd(&ctr[sv::C_COMPLETED], (unsigned long long)nc);
     if (ch) atomicAdd(&ctr[sv::C_CHANGED], (unsigned long long)ch);
     if (nt) atomicAdd(&ctr[sv::C_TEMPS], (unsigned long long)nt);
+    if (nd) atomicAdd(&ctr[sv::C_TDIST], (unsigned long long)nd);
   }
 }
 // flag: mark completed partitions with CBIT in PA (pass B excludes them)
@@ -626,7 +636,7 @@ __global__ void __launch_bounds__(RB) k_pstat1(uint32_t* __restrict__ PA,
                                                const uint32_t* __restrict__ NCP, uint64_t n4,
                                                uint32_t* TB, uint32_t* __restrict__ PB,
                                                unsigned long long* ctr, int temps_all, int flag) {
-  uint32_t np = 0, nc = 0, ch = 0, nt = 0;
+  uint32_t np = 0, nc = 0, ch = 0, nt = 0, nd = 0;
   for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
     const uint4 a = reinterpret_cast<const uint4*>(PA)[t];
     reinterpret_cast<uint4*>(PB)[t] = make_uint4(INF, INF, INF, INF);
@@ -636,13 +646,13 @@ __global__ void __launch_bounds__(RB) k_pstat1(uint32_t* __restrict__ PA,
     uint32_t cm = 0;
 #pragma unroll
     for (int j = 0; j < 4; j++)
-      if (v[j] != INF && pstat1_one((uint32_t)(4 * t + j), v[j], (w >> j) & 1u, temps_all, TB, np, nc, ch, nt)) {
+      if (v[j] != INF && pstat1_one<true>((uint32_t)(4 * t + j), v[j], (w >> j) & 1u, temps_all, TB, np, nc, ch, nt, nd)) {
         v[j] |= CBIT;
         cm = 1;
       }
     if (cm && flag) reinterpret_cast<uint4*>(PA)[t] = make_uint4(v[0], v[1], v[2], v[3]);
   }
-  pstat1_flush(np, nc, ch, nt, ctr);
+  pstat1_flush(np, nc, ch, nt, ctr, nd);
 }
 // list form: statistics over L_i; PB is cleared over L_i-1 (its written keys lie in P_i-1)
 __global__ void __launch_bounds__(RB) k_pstat1_list(uint32_t* __restrict__ PA,
@@ -653,7 +663,7 @@ __global__ void __launch_bounds__(RB) k_pstat1_list(uint32_t* __restrict__ PA,
                                                     const unsigned long long* pcnt, uint32_t* TB,
                                                     uint32_t* __restrict__ PB, unsigned long long* ctr,
                                                     int temps_all, int flag) {
-  uint32_t np = 0, nc = 0, ch = 0, nt = 0;
+  uint32_t np = 0, nc = 0, ch = 0, nt = 0, nd = 0;
   const uint64_t cp = *pcnt;
   for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cp; i += (uint64_t)gridDim.x * RB)
     PB[prev[i]] = INF;
@@ -661,7 +671,7 @@ __global__ void __launch_bounds__(RB) k_pstat1_list(uint32_t* __restrict__ PA,
   for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * RB) {
     const uint32_t pid = list[i];
     const uint32_t pm = PA[pid];
-    if (pm != INF && pstat1_one(pid, pm, tbit(NCP, pid), temps_all, TB, np, nc, ch, nt) && flag)
+    if (pm != INF && pstat1_one(pid, pm, tbit(NCP, pid), temps_all, TB, np, nc, ch, nt, nd) && flag)
       PA[pid] = pm | CBIT;
   }
   pstat1_flush(np, nc, ch, nt, ctr);

@@ -377,3 +377,46 @@ def test_dist_edge_partitioned_bfs(world):
             got = [(it["active_in"], it["partitions"], it["temps"], it["completed"], it["changed"],
                     it["changed2"]) for it in rep["iters"]]
             assert got == want_tr
+
+
+def _skewed_graph(seed, n):
+    """A long random tree on the low quarter of the ids (many SV iterations, rows owned by
+    rank 0) and triangles/pairs on the rest (complete within two iterations): with exclusion
+    the higher ranks run out of live tuples (fig:loadbal)."""
+    rng = np.random.default_rng(seed)
+    k = n // 4
+    order = rng.permutation(k)
+    tree = np.stack([order[1:], order[rng.integers(0, np.arange(1, k))]], 1)
+    rest = np.arange(k, n - (n - k) % 3).reshape(-1, 3)
+    tri = np.concatenate([rest[:, [0, 1]], rest[:, [1, 2]], rest[::2][:, [2, 0]]])
+    e = np.concatenate([tree, tri]).astype(np.uint32)
+    return e[rng.permutation(e.shape[0])]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("graph", ["skewed", "c1"])
+def test_dist_balanced(world, graph):
+    """The paper's 'balanced' variant (CC_FLAG_BALANCE): live rows redistributed
+    evenly over the ranks.  Labels and every Alg. 1 counter equal the oracle's (rows moving
+    between ranks change no set); after the first iteration the per-rank loads stay within a
+    sixteenth of the mean plus one row, where without it they drift apart."""
+    import paper_1607_06156_b200 as cc
+    if graph == "skewed":
+        n = 1 << 17
+        edges = _skewed_graph(7, n)
+    else:
+        g = graphgen.make("c1", 0.5)
+        n, edges = g.n, g.edges
+    maxrow = int(np.bincount(edges.reshape(-1).astype(np.int64), minlength=n).max()) + 1
+    res_b = run_ranks(_rank_run, world, n, edges, ("sv",), cc.CC_FLAG_BALANCE)
+    _check(res_b, n, edges, ("sv",))
+    res_u = run_ranks(_rank_run, world, n, edges, ("sv",), 0)
+    _check(res_u, n, edges, ("sv",))
+
+    def spread(res):
+        its = res[0]["sv"][3]["iters"]
+        return [(it["active_max"] * world - it["active_in"], it["active_in"]) for it in its[1:]]
+    for excess, a in spread(res_b):
+        assert excess <= world * (a // (16 * world) + maxrow + 1), (excess, a)
+    if graph == "skewed":
+        assert any(excess > world * (a // (16 * world) + maxrow + 1) for excess, a in spread(res_u))

@@ -378,6 +378,67 @@ def test_rmat_bfs_route(cc):
             assert norm(trace_of(rep)) == norm(tr)
 
 
+def _peel_graph(seed, n, hub, small):
+    """A star-like giant component on `hub` random ids (the BFS peel) plus `small` small
+    components (paths, cycles, trees with a duplicate edge and a self-loop) on other ids spread
+    over [0, n), ids 0 and n-1 included: the remainder touches a small fraction of the ids."""
+    rng = np.random.default_rng(seed)
+    ids = rng.permutation(n)
+    root, H = ids[1], ids[2:2 + hub]
+    e = [np.stack([np.full(hub, root), H], 1), np.stack([H, rng.choice(H, hub)], 1)]
+    rest = np.concatenate([[0, n - 1], ids[2 + hub:]])
+    pos = 0
+    for k in range(small):
+        sz = 2 + (k % 7)
+        vs = rest[pos:pos + sz]
+        pos += sz
+        kind = k % 4
+        if kind == 0:  # path
+            e.append(np.stack([vs[:-1], vs[1:]], 1))
+        elif kind == 1:  # cycle
+            e.append(np.stack([vs, np.roll(vs, 1)], 1))
+        elif kind == 2:  # random tree + duplicate edge + self-loop
+            par = [vs[rng.integers(0, i)] for i in range(1, sz)]
+            t = np.stack([vs[1:], par], 1)
+            e.append(np.concatenate([t, t[:1], [[vs[0], vs[0]]]]))
+        else:  # star
+            e.append(np.stack([np.full(sz - 1, vs[-1]), vs[:-1]], 1))
+    edges = np.concatenate(e).astype(np.uint32)
+    return edges[rng.permutation(edges.shape[0])]
+
+
+@pytest.mark.parametrize("seed,n,hub,small", [(0, 1 << 16, 4000, 200), (1, 1 << 20, 60000, 3000),
+                                              (2, (1 << 22) + 37, 200000, 9000)])
+def test_renumbered_remainder(cc, request, seed, n, hub, small):
+    """BFS route with a small remainder: the SV runs on the remainder's endpoints renumbered
+    densely in id order.  Labels, the SV trace (Alg. 1 counters, which the
+    monotone renumbering must not change) and n' equal the oracle's, and equal the ablation
+    that keeps the original id range (CC_FLAG_NO_RENUMBER)."""
+    import paper_1607_06156_b200 as ccmod
+    edges = _peel_graph(seed, n, hub, small)
+    want = oracle.uf_labels(n, edges).astype(np.int64)
+    deg, _ = odeg.degree_distribution(n, edges)
+    vis, _ = obfs.bfs(n, edges, obfs.bfs_root(deg))
+    rem = obfs.filter_edges(edges, vis)
+    _, tr = osv.sv_trace(n, rem)
+    lab, rep = run(cc, n, edges, "bfs+sv")
+    assert np.array_equal(lab, want)
+    assert rep["remainder_edges"] == rem.shape[0]
+    assert norm(trace_of(rep)) == norm(tr)
+    # the edge-streaming BFS route renumbers (csrbfs peels on its CSR rows and keeps n)
+    assert rep["sv_ids"] in (n, np.unique(rem).shape[0])
+    if request.node.callspec.params["cc"] != "csrbfs":
+        assert rep["sv_ids"] == np.unique(rem).shape[0]
+    ab = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE | ccmod.CC_FLAG_NO_RENUMBER)
+    try:
+        lab2, rep2 = run(ab, n, edges, "bfs+sv")
+    finally:
+        ab.close()
+    assert np.array_equal(lab2, want)
+    assert rep2["sv_ids"] == n
+    assert norm(trace_of(rep2)) == norm(tr)
+
+
 # ------------------------------------------------------------------ prediction / gate
 @pytest.mark.parametrize("graph", ["c1", "c2s", "rmat14", "rmat18"])
 def test_gate_parity(cc, graph):
