@@ -644,8 +644,11 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     // at most every other iteration, and not again after one that folded little
     const bool want_collapse =
         collapse_force ? can_collapse && len_live > 0
-                       : collapse_ok && it >= 1 && it >= last_collapse + 2 && len_live >= COLLAPSE_MIN_LEN &&
-                             s.partitions * 16 < len_live;
+                       : collapse_ok && it >= 1 && len_live >= COLLAPSE_MIN_LEN && s.partitions * 16 < len_live &&
+                             (it >= last_collapse + 2 ||
+                              // already after iteration 1 when a few partitions hold everything
+                              // (C4 mode sv: 11 k partitions for 2.2 G tuples)
+                              (last_collapse == 0 && s.partitions * 1024 < len_live));
     bool rebalance = false;
     if (balance) {
       TRY(gather_loads(len_live));
@@ -1204,7 +1207,6 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   uint2* bucketed = reinterpret_cast<uint2*>(c->d_w[1]);  // 2m arcs fit: cap >= 2m + 2n
   CK(cudaMemsetAsync(c->d_gctr, 0, sizeof(uint64_t) * graph::G_NUM, c->st));
   CK(cudaMemsetAsync(c->d_gctr + graph::G_MINVIS, 0xFF, sizeof(uint64_t), c->st));
-  sv::launch_init_labels(c->d_label, n, c->st);
   // speculative root level (graph.cu k_deg_sample): on large lists the degree pass also runs
   // the BFS level of a root guessed from a prefix; kept below if the guess is the root
   bool spec_ran = false;
@@ -1249,6 +1251,11 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   bool run_bfs = false;
   uint64_t root = 0;
   TRY(predict_gate(c, mode, want_hist, &run_bfs, &root));
+  // every id starts as its own label; on the BFS route k_bfs_labels writes them with L_bfs
+  if (!run_bfs) {
+    sv::launch_init_labels(c->d_label, n, c->st);
+    c->launches += 1;
+  }
   e_pred = ev_get(c);
   CK(cudaEventRecord(e_pred, c->st));
 

@@ -634,8 +634,17 @@ __global__ void __launch_bounds__(BLOCK) k_deg_hist(const uint32_t* __restrict__
       if (pos < TAIL_CAP) tail[pos] = d;
     }
   };
-  const uint64_t n4 = n >> 2;  // 16-byte loads (deg is 16-byte aligned)
-  for (uint64_t q = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; q < n4; q += (uint64_t)gridDim.x * BLOCK) {
+  const uint64_t n4 = n >> 2;  // 16-byte loads (deg is 16-byte aligned), two in flight
+  const uint64_t stride = (uint64_t)gridDim.x * BLOCK;
+  uint64_t q = blockIdx.x * (uint64_t)BLOCK + threadIdx.x;
+  for (; q + stride < n4; q += 2 * stride) {
+    const uint4 d = reinterpret_cast<const uint4*>(deg)[q];
+    const uint4 e = reinterpret_cast<const uint4*>(deg)[q + stride];
+    add(d.x, 4 * q); add(d.y, 4 * q + 1); add(d.z, 4 * q + 2); add(d.w, 4 * q + 3);
+    const uint64_t r = q + stride;
+    add(e.x, 4 * r); add(e.y, 4 * r + 1); add(e.z, 4 * r + 2); add(e.w, 4 * r + 3);
+  }
+  if (q < n4) {
     const uint4 d = reinterpret_cast<const uint4*>(deg)[q];
     add(d.x, 4 * q); add(d.y, 4 * q + 1); add(d.z, 4 * q + 2); add(d.w, 4 * q + 3);
   }
@@ -856,17 +865,26 @@ void launch_vis_bits(const uint32_t* S, uint64_t n, uint32_t* vis, cudaStream_t 
 
 CC_DEVI bool bit(const uint32_t* bm, uint32_t v) { return (__ldg(&bm[v >> 5]) >> (v & 31)) & 1u; }
 
-// L_bfs = min id in VI: first set bit of the visited bitmap.
+// L_bfs = min id in VI: first set bit of the visited bitmap.  Each thread's
+// first set bit (its words are visited in increasing order), min over the warp, one atomic
+// per warp (one per thread serialised ~150 k atomics on one address: 98 us on C4).
 __global__ void k_min_visited(const uint32_t* __restrict__ vis, uint64_t nwords,
                               unsigned long long* gctr) {
+  unsigned long long mn = ~0ull;
   for (uint64_t w = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; w < nwords;
        w += (uint64_t)gridDim.x * BLOCK) {
-    uint32_t x = vis[w];
+    const uint32_t x = vis[w];
     if (x) {
-      atomicMin(&gctr[G_MINVIS], (unsigned long long)(w * 32 + (__ffs(x) - 1)));
-      return;
+      mn = w * 32 + (__ffs(x) - 1);
+      break;
     }
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, mn, o);
+    mn = y < mn ? y : mn;
+  }
+  if ((threadIdx.x & 31) == 0 && mn != ~0ull) atomicMin(&gctr[G_MINVIS], mn);
 }
 void launch_min_visited(const uint32_t* visited, uint64_t n, uint64_t* gctr, cudaStream_t st) {
   uint64_t nw = (n + 31) / 32;
@@ -875,34 +893,63 @@ void launch_min_visited(const uint32_t* visited, uint64_t n, uint64_t* gctr, cud
                                                            reinterpret_cast<unsigned long long*>(gctr));
 }
 
+// label[v] = L_bfs for v in VI, v otherwise (the initial label of every other id, written here
+// so the BFS route needs no separate initialisation pass): 4 ids per thread, 16-byte stores
 __global__ void k_bfs_labels(const uint32_t* __restrict__ vis, uint64_t n,
                              uint32_t* __restrict__ label, const unsigned long long* gctr) {
   const uint32_t L = (uint32_t)gctr[G_MINVIS];
-  for (uint64_t v = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; v < n;
-       v += (uint64_t)gridDim.x * BLOCK)
-    if (bit(vis, (uint32_t)v)) label[v] = L;
+  const uint64_t n4 = n >> 2;
+  for (uint64_t q = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; q < n4; q += (uint64_t)gridDim.x * BLOCK) {
+    const uint32_t b = (__ldg(&vis[q >> 3]) >> (4 * (q & 7))) & 15u;
+    const uint32_t v = (uint32_t)(4 * q);
+    reinterpret_cast<uint4*>(label)[q] =
+        make_uint4(b & 1u ? L : v, b & 2u ? L : v + 1, b & 4u ? L : v + 2, b & 8u ? L : v + 3);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const uint32_t v = (uint32_t)(4 * n4 + threadIdx.x);
+    label[v] = bit(vis, v) ? L : v;
+  }
 }
 void launch_bfs_labels(const uint32_t* visited, uint64_t n, uint32_t* label, uint64_t* gctr,
                        cudaStream_t st) {
   if (!n) return;
-  k_bfs_labels<<<grid_for(n, 148 * 16), BLOCK, 0, st>>>(
+  k_bfs_labels<<<grid_for((n + 3) / 4, 148 * 16), BLOCK, 0, st>>>(
       visited, n, label, reinterpret_cast<const unsigned long long*>(gctr));
 }
 
 // components = #{v : label[v] = v} over [lo, hi) (every component has exactly one root,
 // its minimum id); added to *cnt
+__global__ void k_count_roots_small(const uint32_t* __restrict__ label, uint64_t lo, uint64_t hi,
+                                    unsigned long long* cnt) {
+  const uint64_t v = lo + threadIdx.x;
+  const uint32_t c = warp_sum(v < hi && label[v] == (uint32_t)v ? 1u : 0u);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, (unsigned long long)c);
+}
 __global__ void k_count_roots(const uint32_t* __restrict__ label, uint64_t lo, uint64_t hi,
                               unsigned long long* cnt) {
   uint32_t c = 0;
-  for (uint64_t v = lo + blockIdx.x * (uint64_t)BLOCK + threadIdx.x; v < hi; v += (uint64_t)gridDim.x * BLOCK)
-    c += label[v] == (uint32_t)v;
+  // 16-byte loads over the aligned middle [a, b), single ids at the ends (hi - lo >= 8: a < b)
+  const uint64_t a = (lo + 3) & ~3ull, b = hi & ~3ull;
+  for (uint64_t q = a / 4 + blockIdx.x * (uint64_t)BLOCK + threadIdx.x; q < b / 4; q += (uint64_t)gridDim.x * BLOCK) {
+    const uint4 x = reinterpret_cast<const uint4*>(label)[q];
+    const uint32_t v = (uint32_t)(4 * q);
+    c += (x.x == v) + (x.y == v + 1) + (x.z == v + 2) + (x.w == v + 3);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 8) {
+    const uint64_t v = threadIdx.x < 4 ? lo + threadIdx.x : b + (threadIdx.x - 4);
+    if (threadIdx.x < 4 ? v < a : v < hi) c += label[v] == (uint32_t)v;
+  }
   c = warp_sum(c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, (unsigned long long)c);
 }
 void launch_count_roots(const uint32_t* label, uint64_t lo, uint64_t hi, uint64_t* cnt, cudaStream_t st) {
-  if (hi > lo)
-    k_count_roots<<<grid_for(hi - lo, 148 * 8), BLOCK, 0, st>>>(label, lo, hi,
-                                                                reinterpret_cast<unsigned long long*>(cnt));
+  if (hi <= lo) return;
+  if (hi - lo < 8) {  // tiny ranges: one thread per id
+    k_count_roots_small<<<1, BLOCK, 0, st>>>(label, lo, hi, reinterpret_cast<unsigned long long*>(cnt));
+    return;
+  }
+  k_count_roots<<<grid_for((hi - lo + 3) / 4, 148 * 8), BLOCK, 0, st>>>(label, lo, hi,
+                                                                      reinterpret_cast<unsigned long long*>(cnt));
 }
 
 // ------------------------------------------------------------- remainder renumbering
