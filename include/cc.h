@@ -86,6 +86,10 @@ typedef enum { CC_U32 = 0, CC_U64 = 1 } cc_idw;
                                         'balanced' variant -- the live rows are
                                         redistributed evenly over the ranks after an iteration
                                         whose most loaded rank holds > 1/16 above the mean  */
+#define CC_FLAG_DENSE_EXCHANGE 0x1000u /* several ranks: combine the partition slots by dense
+                                        n-slot all-reduces (and a sparse all-gather late)
+                                        instead of the owner-computes exchange (
+                                        ablation)                                            */
 #define CC_FLAG_BFS_CSR 0x40u        /* csr engine: degrees from the bucketed CSR build and a
                                         direction-optimising (top-down / bottom-up) BFS on the
                                         CSR rows instead of the edge-streaming BFS            */

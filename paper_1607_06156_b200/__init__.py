@@ -35,6 +35,7 @@ CC_FLAG_PERMUTE_IDS = 0x100
 CC_FLAG_NO_COLLAPSE = 0x200
 CC_FLAG_NO_RENUMBER = 0x400
 CC_FLAG_BALANCE = 0x800
+CC_FLAG_DENSE_EXCHANGE = 0x1000
 EXCLUSION_FLAGS = {"early": 0, "end": CC_FLAG_NO_EARLY_EXCLUDE, "none": CC_FLAG_NO_EXCLUDE}
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)

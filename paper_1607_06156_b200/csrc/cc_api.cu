@@ -455,6 +455,12 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   // counters on the device; counters alternate between two blocks.  Compaction (rare) is a
   // synchronisation point.  Several ranks, or no exclusion, run step by step.
   const bool ahead = !multi && excl;
+  // several ranks: the owner-computes slot exchange (NEXT-1, ctx.cuh oc_push / oc_reply) unless
+  // the dense all-reduce is asked for (CC_FLAG_DENSE_EXCHANGE), or completed partitions keep
+  // temporaries, or rows leave their owner (balanced variant: TB(r) must reach the row holder)
+  const bool oc = multi && excl && !temps_all && !(c->cfg.flags & (CC_FLAG_DENSE_EXCHANGE | CC_FLAG_BALANCE));
+  if (oc) TRY(oc_ensure(c));
+  const uint64_t nwl = c->lo / 32, nwh = (c->hi + 31) / 32;  // own words of the slot bitmaps
   uint64_t* CTR[2] = {c->d_ctr, c->d_ctr + sv::C_NUM};
   cudaEvent_t ev_read[2] = {ev_get(c), ev_get(c)};
   // hot thresholds measured on C2 (iterations with 490 k / 112 k / 16 k previous partitions):
@@ -503,10 +509,27 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
                    hot_cur && lcur ? LC + lb : nullptr, 0);
       k.end(8.0 * len + (it ? 4.0 * len : 0.0), 1 + (have_long ? 2 : 0)); }
     if (it) std::swap(Pc, Palt);
+    if (oc) {
+      // ---- owner-computes (NEXT-1): the relabel read PB; clear the other owners' replies,
+      // send the partials of foreign slots to their owners, statistics of the own block
+      if (it) csr::oc_put(c->ocB.send, c->ocB.nsend, nullptr, PB, c->st);
+      TRY(oc_push(c, PA, NCP, c->ocA));
+      { Prof k(c, KF_SLOTS);
+        csr::pstat1_block(PA, NCP, c->lo, c->hi, TB, PB, ctr, c->st);
+        k.end(8.0 * (double)(c->hi - c->lo), 1); }
+      CK(cudaMemsetAsync(NCP, 0, sizeof(uint32_t) * nwp, c->st));
+      TRY(comm_allreduce(c, ctr + sv::C_PARTITIONS, 4, CC_DT_I64, CC_OP_SUM));
+      // p_min (with the completed flag) back to the ranks holding those partitions; the
+      // temporaries' targets to the owners of their rows
+      TRY(oc_reply(c, PA, c->ocA));
+      TRY(oc_push(c, nullptr, TB, c->ocT));
+      if (nwl) CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nwl, c->st));
+      if (nwp > nwh) CK(cudaMemsetAsync(TB + nwh, 0, sizeof(uint32_t) * (nwp - nwh), c->st));
+    }
     // sparse exchange once few partitions remain: the entries all ranks touched (at most
     // |P_i-1| per rank) cost less than the dense n-slot reduction
-    const bool sparse = multi && it > 0 && prevp * (uint64_t)c->cfg.world_size * 2 < n4;
-    if (multi) {  // partition minima and 'not completed' flags over all ranks
+    const bool sparse = multi && !oc && it > 0 && prevp * (uint64_t)c->cfg.world_size * 2 < n4;
+    if (multi && !oc) {  // partition minima and 'not completed' flags over all ranks
       if (sparse) {
         TRY(comm_sparse_slots(c, PA, NCP, n4));
       } else {
@@ -515,16 +538,18 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
       }
     }
     // ---- line 22 bookkeeping: |P_i|, completed, changed, temporaries
-    { Prof k(c, KF_SLOTS);
+    if (!oc) {
+      Prof k(c, KF_SLOTS);
       if (lcur) csr::pstat1(PA, NCP, n, TB, PB, ctr, c->st, temps_all, excl, L[lb], LC + lb,
                             lprev ? L[lb ^ 1] : nullptr, lprev ? LC + (lb ^ 1) : nullptr);
       else csr::pstat1(PA, NCP, n, TB, PB, ctr, c->st, temps_all, excl);
-      k.end(lcur ? 12.0 * (double)prevp : 8.0 * n4, 1); }
+      k.end(lcur ? 12.0 * (double)prevp : 8.0 * n4, 1);
+    }
     // ---- lines 17-21 (exclusion, p <- p_min), line 24 (+ temporaries), line 25 minima
     { Prof k(c, KF_ROWB);
       csr::rowpass(false, Rc, Pc, Palt, len, PA, NCP, TB, PB, nullptr, c->d_label, c->d_umin,
                    c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs, have_long, false, ctr, c->st,
-                   excl, false, prevctr, HOT_B, hw_ready ? c->d_hw : nullptr,
+                   excl, /*B: write q = p too (owner exchange)*/ oc, prevctr, HOT_B, hw_ready ? c->d_hw : nullptr,
                    hot_cur || it == 0 ? ctr : nullptr, hot_cur ? 1 : 2);
       k.end(12.0 * len, 1 + (have_long ? 2 : 0)); }
     std::swap(Pc, Palt);
@@ -532,15 +557,31 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     if (multi) {
       CK(cudaMemcpyAsync(ctr + sv::C_SURVIVORS, ctr + sv::C_OUT, sizeof(uint64_t), cudaMemcpyDeviceToDevice,
                          c->st));
-      if (sparse) TRY(comm_sparse_slots(c, PB, nullptr, n4));
-      else TRY(comm_min_u32(c, PB, n4));
+      if (oc) {
+        // the partials of foreign slots to their owners; the pass read PA: clear the replies
+        TRY(oc_push(c, PB, nullptr, c->ocB));
+        csr::oc_put(c->ocA.send, c->ocA.nsend, nullptr, PA, c->st);
+      } else if (sparse) {
+        TRY(comm_sparse_slots(c, PB, nullptr, n4));
+      } else {
+        TRY(comm_min_u32(c, PB, n4));
+      }
       TRY(comm_allreduce(c, ctr + sv::C_OUT, 1, CC_DT_I64, CC_OP_SUM));
     }
-    { Prof k(c, KF_SLOTS);
+    if (oc) {
+      { Prof k(c, KF_SLOTS);
+        csr::pstat2_block(PB, c->lo, c->hi, PA, TB, ctr, c->st);
+        k.end(8.0 * (double)(c->hi - c->lo), 1); }
+      CK(cudaMemsetAsync(TB, 0, sizeof(uint32_t) * nwp, c->st));
+      TRY(comm_allreduce(c, ctr + sv::C_CHANGED2, 1, CC_DT_I64, CC_OP_SUM));
+      TRY(oc_reply(c, PB, c->ocB));  // the next relabel's p -> PB[p]
+    } else {
+      Prof k(c, KF_SLOTS);
       csr::pstat2(PB, n, PA, TB, ctr, c->st, NX, lcur ? L[lb] : nullptr, lcur ? LC + lb : nullptr);
       csr::list_from_bits(NX, n, L[lb ^ 1], LC + (lb ^ 1), NCP, TB, exact_next ? PA : nullptr, c->st);
-      k.end(lcur ? 12.0 * (double)prevp + n / 4.0 : 8.0 * n4 + n / 4.0, 2); }
-    lexact = exact_next;
+      k.end(lcur ? 12.0 * (double)prevp + n / 4.0 : 8.0 * n4 + n / 4.0, 2);
+    }
+    lexact = exact_next && !oc;
     lprev = lcur;
     lcur = true;
     lb ^= 1;
@@ -644,11 +685,12 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     // at most every other iteration, and not again after one that folded little
     const bool want_collapse =
         collapse_force ? can_collapse && len_live > 0
-                       : collapse_ok && it >= 1 && len_live >= COLLAPSE_MIN_LEN && s.partitions * 16 < len_live &&
-                             (it >= last_collapse + 2 ||
-                              // already after iteration 1 when a few partitions hold everything
-                              // (C4 mode sv: 11 k partitions for 2.2 G tuples)
-                              (last_collapse == 0 && s.partitions * 1024 < len_live));
+                       : collapse_ok && len_live >= COLLAPSE_MIN_LEN &&
+                             ((it >= 1 && it >= last_collapse + 2 && s.partitions * 16 < len_live) ||
+                              // after iteration 1 (decided now: iteration 1 is already in flight)
+                              // when iteration 0 sent everything to a few p_min targets
+                              // (C4 mode sv: 11 k targets = |P_1| for 2.2 G tuples)
+                              (it == 0 && h[sv::C_TDIST] > 0 && h[sv::C_TDIST] * 1024 < len_live));
     bool rebalance = false;
     if (balance) {
       TRY(gather_loads(len_live));

@@ -93,6 +93,24 @@ void list_from_bits(uint32_t* NX, uint64_t n, uint32_t* list, uint64_t* lcnt, ui
 void extract_slots(const uint32_t* S, const uint32_t* BM, uint64_t n, uint2* out, uint64_t* cnt,
                    cudaStream_t st);
 void apply_slots(const uint2* in, uint64_t count, uint32_t* S, uint32_t* BM, cudaStream_t st);
+// multi-GPU owner-computes exchange (NEXT-1; cc_api.cu sv_iterate).  pstat1/pstat2 over one
+// owner block [lo, hi) (lo a multiple of 32; TB absolute in pstat1, ids offset by lo; no list)
+void pstat1_block(uint32_t* PA, const uint32_t* NCP, uint64_t lo, uint64_t hi, uint32_t* TB, uint32_t* PB,
+                  uint64_t* ctr, cudaStream_t st);
+void pstat2_block(uint32_t* PB, uint64_t lo, uint64_t hi, uint32_t* PA, const uint32_t* TB, uint64_t* ctr,
+                  cudaStream_t st);
+// entries (p, value | flag << 31) of the touched slots outside [lo, hi), grouped by owner p / blk:
+// S != NULL: S[p] != INF (flag: the BM bit); S == NULL: set bits of BM.  oc_count adds the
+// per-owner counts to cnt[world]; oc_scatter writes them at cursor[owner]++ (exclusive offsets)
+void oc_count(const uint32_t* S, const uint32_t* BM, uint64_t n, uint64_t lo, uint64_t hi, uint64_t blk, int world,
+              uint64_t* cnt, cudaStream_t st);
+void oc_scatter(const uint32_t* S, const uint32_t* BM, uint64_t n, uint64_t lo, uint64_t hi, uint64_t blk,
+                uint64_t* cursor, uint2* out, cudaStream_t st);
+// owner: S[p] = min(S[p], value) (S may be NULL), BM bit |= flag; out[i] = S[in[i].p]
+void oc_apply(const uint2* in, uint64_t count, uint32_t* S, uint32_t* BM, cudaStream_t st);
+void oc_gather(const uint2* in, uint64_t count, const uint32_t* S, uint32_t* out, cudaStream_t st);
+// requester: S[sent[i].p] = vals[i] (vals NULL: INF)
+void oc_put(const uint2* sent, uint64_t count, const uint32_t* vals, uint32_t* S, cudaStream_t st);
 // multi-GPU slot exchange helpers: a[i] ^= 0x80000000; out[i] = OR_k parts[k*words + i]
 void flip_sign(uint32_t* a, uint64_t n, cudaStream_t st);
 void or_parts(const uint32_t* parts, uint64_t words, int world, uint32_t* out, cudaStream_t st);

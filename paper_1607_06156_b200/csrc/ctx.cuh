@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -85,6 +86,16 @@ struct cc_ctx {
   uint2* d_xsend = nullptr;      // sparse slot exchange: my touched entries / everyone's
   uint2* d_xrecv = nullptr;
   uint64_t* d_bal = nullptr;     // balanced variant: split points and the gathered send counts
+  // owner-computes slot exchange (NEXT-1): entries sent (kept for the reply and the clears)
+  struct OcSide {
+    uint2* send = nullptr;
+    uint64_t nsend = 0, nrecv = 0;
+    std::vector<uint64_t> sc, rc;  // entries per destination / per source rank
+  } ocA, ocB, ocT;
+  uint2* d_ocrecv = nullptr;     // entries received for this rank's slot block
+  uint32_t* d_ocval[2] = {nullptr, nullptr};  // reply values (sent / received)
+  uint64_t* d_occnt = nullptr;   // counts [world], cursors [world], gathered counts [world^2]
+  uint64_t oc_cap = 0;           // entries each buffer holds
   uint64_t xsend_cap = 0, xrecv_cap = 0;
   uint32_t* d_garc = nullptr;  // CSR vertex-group scratch: arcs per group (<= 2048 groups)
   uint64_t* d_gcur = nullptr;  // group cursors [0, 2048), long-row count at [2048]
@@ -191,6 +202,11 @@ static inline void dfree_all(cc_ctx* c) {
   c->d_cnt = nullptr;
   c->d_xsend = c->d_xrecv = nullptr;
   c->d_bal = nullptr;
+  c->ocA.send = c->ocB.send = c->ocT.send = nullptr;
+  c->d_ocrecv = nullptr;
+  c->d_ocval[0] = c->d_ocval[1] = nullptr;
+  c->d_occnt = nullptr;
+  c->oc_cap = 0;
   c->xsend_cap = c->xrecv_cap = 0;
   c->recv_cap = c->gath_cap = 0;
   c->d_lsegs = nullptr;
@@ -450,6 +466,75 @@ static inline cc_status comm_sparse_slots(cc_ctx* c, uint32_t* S, uint32_t* BM, 
   }
   TRY(comm_allgather(c, c->d_xsend, c->d_xrecv, pad * sizeof(uint2)));
   csr::apply_slots(c->d_xrecv, world * pad, S, BM, c->st);
+  c->launches += 2;
+  return CC_OK;
+}
+
+// ------------------------------------------------------------ owner-computes exchange (NEXT-1)
+// rank k owns the partition slots [lo, hi) (the same block as its rows).
+// After a row pass every rank holds partials for the slots its tuples touched; oc_push sends
+// those outside its block to their owner as (slot, value | flag) entries (one all-to-all-v,
+// entry counts exchanged first) and the owner min-combines them (and ORs the flag bitmap);
+// the owner computes the block's statistics, and oc_reply sends the final value of every
+// received slot back to the rank that sent it, in the order sent.  Volume per rank: the
+// distinct slots its tuples touch, not n.
+static inline cc_status oc_ensure(cc_ctx* c) {
+  const uint64_t world = (uint64_t)c->cfg.world_size;
+  const uint64_t need = std::max<uint64_t>(c->n, world * c->blk) + 1;
+  if (c->oc_cap >= need) return CC_OK;
+  cc_status s = CC_OK;
+  for (auto* p : {&c->ocA.send, &c->ocB.send, &c->ocT.send, &c->d_ocrecv})
+    if (s == CC_OK) s = dalloc_t(c, p, need);
+  for (int i = 0; i < 2 && s == CC_OK; i++) s = dalloc_t(c, &c->d_ocval[i], need);
+  if (s == CC_OK && !c->d_occnt) s = dalloc_t(c, &c->d_occnt, 2 * world + world * world);
+  TRY(comm_agree(c, s));
+  c->oc_cap = need;
+  return CC_OK;
+}
+static inline cc_status oc_push(cc_ctx* c, uint32_t* S, uint32_t* BM, cc_ctx::OcSide& side) {
+  const int world = c->cfg.world_size, rank = c->cfg.rank;
+  uint64_t* cnt = c->d_occnt;
+  CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * world, c->st));
+  csr::oc_count(S, BM, c->n, c->lo, c->hi, c->blk, world, cnt, c->st);
+  side.sc.assign(world, 0);
+  CK(cudaMemcpyAsync(side.sc.data(), cnt, sizeof(uint64_t) * world, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  std::vector<uint64_t> cur(world);
+  uint64_t o = 0;
+  for (int k = 0; k < world; k++) { cur[k] = o; o += side.sc[k]; }
+  side.nsend = o;
+  CK(cudaMemcpyAsync(cnt + world, cur.data(), sizeof(uint64_t) * world, cudaMemcpyHostToDevice, c->st));
+  csr::oc_scatter(S, BM, c->n, c->lo, c->hi, c->blk, cnt + world, side.send, c->st);
+  c->launches += 2;
+  // every rank's counts -> the counts this rank receives
+  CK(cudaMemcpyAsync(cnt, side.sc.data(), sizeof(uint64_t) * world, cudaMemcpyHostToDevice, c->st));
+  TRY(comm_allgather(c, cnt, cnt + 2 * world, sizeof(uint64_t) * world));
+  std::vector<uint64_t> mat((size_t)world * world);
+  CK(cudaMemcpyAsync(mat.data(), cnt + 2 * world, sizeof(uint64_t) * world * world, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  side.rc.assign(world, 0);
+  side.nrecv = 0;
+  for (int k = 0; k < world; k++) {
+    side.rc[k] = mat[(size_t)k * world + rank];
+    side.nrecv += side.rc[k];
+  }
+  if (side.nrecv > c->oc_cap || side.nsend > c->oc_cap)
+    return fail(c, CC_ERR_INVALID, "internal: owner exchange of %llu / %llu entries", (unsigned long long)side.nsend,
+                (unsigned long long)side.nrecv);
+  std::vector<uint64_t> sb(world), rb(world);
+  for (int k = 0; k < world; k++) { sb[k] = sizeof(uint2) * side.sc[k]; rb[k] = sizeof(uint2) * side.rc[k]; }
+  TRY(comm_alltoallv(c, side.send, sb.data(), c->d_ocrecv, rb.data()));
+  csr::oc_apply(c->d_ocrecv, side.nrecv, S, BM, c->st);
+  c->launches += 1;
+  return CC_OK;
+}
+static inline cc_status oc_reply(cc_ctx* c, uint32_t* S, const cc_ctx::OcSide& side) {
+  const int world = c->cfg.world_size;
+  csr::oc_gather(c->d_ocrecv, side.nrecv, S, c->d_ocval[1], c->st);
+  std::vector<uint64_t> sb(world), rb(world);
+  for (int k = 0; k < world; k++) { sb[k] = sizeof(uint32_t) * side.rc[k]; rb[k] = sizeof(uint32_t) * side.sc[k]; }
+  TRY(comm_alltoallv(c, c->d_ocval[1], sb.data(), c->d_ocval[0], rb.data()));
+  csr::oc_put(side.send, side.nsend, c->d_ocval[0], S, c->st);
   c->launches += 2;
   return CC_OK;
 }

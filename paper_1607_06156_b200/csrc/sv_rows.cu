@@ -193,7 +193,6 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
   }
   constexpr bool PRESET = A && X;
   constexpr int EXCL = (A || X) ? 1 : 0;  // (pass A's relabel ignores it)
-  (void)preset;
   (void)excl;
   constexpr int NW = PB / 32;
   // double-buffered tile staging: TMA brings tile i+2 while tile i is processed
@@ -451,7 +450,9 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       if (k[j] == k[RITEMS - 1] && cout_k == k[RITEMS - 1]) { q = min(q, cout_m); if (A) x = max(x, cout_x); }
       if (k[j] == INF || k[j] == kfirst) continue;
       if (j == RITEMS - 1) qlast = q;
-      if ((!A || PRESET) && q == p[j]) {
+      // (several ranks, owner-computes exchange: pass B writes every value it holds, q = p
+      // too, so the slot is requested from its owner -- preset = 1 there)
+      if ((A ? PRESET : !preset) && q == p[j]) {
         // A: PA[p] was preset to p (p is a partition of this iteration).  B: every live value
         // p is p_min of a surviving partition, so TB(p) holds and k_pstat2 applies the
         // temporary's own min(PB[p], p).  Either way min(slot, p) changes nothing.
@@ -488,7 +489,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
       const uint32_t klast = s_wh[NW].key;
       const uint64_t pos = t0 + tlen;
       const bool in0 = xr == klast;
-      if (in0 && (q != xm || (A && !PRESET))) atomicMin(&OUT[xm], q);  // q = p: see above
+      if (in0 && (q != xm || (A ? !PRESET : preset))) atomicMin(&OUT[xm], q);  // q = p: see above
       if (!__ballot_sync(FULL, !in0)) {
         for (uint64_t base = pos + 32; base < pos + LONG; base += 32) {
           const uint64_t i = base + lane;
@@ -632,10 +633,12 @@ CC_DEVI void pstat1_flush(uint32_t np, uint32_t nc, uint32_t ch, uint32_t nt, un
   }
 }
 // flag: mark completed partitions with CBIT in PA (pass B excludes them)
+// base (multiple of 32): PA, NCP, PB start at slot base (an owner block); TB is absolute
 __global__ void __launch_bounds__(RB) k_pstat1(uint32_t* __restrict__ PA,
                                                const uint32_t* __restrict__ NCP, uint64_t n4,
                                                uint32_t* TB, uint32_t* __restrict__ PB,
-                                               unsigned long long* ctr, int temps_all, int flag) {
+                                               unsigned long long* ctr, int temps_all, int flag,
+                                               uint32_t base) {
   uint32_t np = 0, nc = 0, ch = 0, nt = 0, nd = 0;
   for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
     const uint4 a = reinterpret_cast<const uint4*>(PA)[t];
@@ -646,7 +649,7 @@ __global__ void __launch_bounds__(RB) k_pstat1(uint32_t* __restrict__ PA,
     uint32_t cm = 0;
 #pragma unroll
     for (int j = 0; j < 4; j++)
-      if (v[j] != INF && pstat1_one<true>((uint32_t)(4 * t + j), v[j], (w >> j) & 1u, temps_all, TB, np, nc, ch, nt, nd)) {
+      if (v[j] != INF && pstat1_one<true>(base + (uint32_t)(4 * t + j), v[j], (w >> j) & 1u, temps_all, TB, np, nc, ch, nt, nd)) {
         v[j] |= CBIT;
         cm = 1;
       }
@@ -689,25 +692,26 @@ CC_DEVI void mark(uint32_t* NX, uint32_t v) {
   const uint32_t b = 1u << (v & 31);
   if (!(*(volatile uint32_t*)&NX[v >> 5] & b)) atomicOr(&NX[v >> 5], b);
 }
+// base (multiple of 32): PB, PA and TB start at slot base (an owner block); NX NULL: no list
 __global__ void __launch_bounds__(RB) k_pstat2(uint32_t* __restrict__ PB, uint64_t n4,
                                                uint32_t* __restrict__ PA, const uint32_t* __restrict__ TB,
-                                               unsigned long long* ctr, uint32_t* NX) {
+                                               unsigned long long* ctr, uint32_t* NX, uint32_t base) {
   uint32_t ch = 0;
   for (uint64_t t = blockIdx.x * (uint64_t)RB + threadIdx.x; t < n4; t += (uint64_t)gridDim.x * RB) {
     uint4 b = reinterpret_cast<const uint4*>(PB)[t];
     reinterpret_cast<uint4*>(PA)[t] = make_uint4(INF, INF, INF, INF);
     const uint32_t tw = (TB[t >> 3] >> (4 * (t & 7))) & 15u;
+    const uint32_t u0 = base + (uint32_t)(4 * t);
     if (tw) {
-      const uint32_t u0 = (uint32_t)(4 * t);
-      if (tw & 1u) { b.x = min(b.x, u0); mark(NX, b.x); }
-      if (tw & 2u) { b.y = min(b.y, u0 + 1); mark(NX, b.y); }
-      if (tw & 4u) { b.z = min(b.z, u0 + 2); mark(NX, b.z); }
-      if (tw & 8u) { b.w = min(b.w, u0 + 3); mark(NX, b.w); }
+      if (tw & 1u) { b.x = min(b.x, u0); if (NX) mark(NX, b.x); }
+      if (tw & 2u) { b.y = min(b.y, u0 + 1); if (NX) mark(NX, b.y); }
+      if (tw & 4u) { b.z = min(b.z, u0 + 2); if (NX) mark(NX, b.z); }
+      if (tw & 8u) { b.w = min(b.w, u0 + 3); if (NX) mark(NX, b.w); }
       reinterpret_cast<uint4*>(PB)[t] = b;
     }
     const uint32_t v[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int j = 0; j < 4; j++) ch += v[j] != INF && v[j] != (uint32_t)(4 * t + j);
+    for (int j = 0; j < 4; j++) ch += v[j] != INF && v[j] != u0 + j;
   }
   ch = warp_sum(ch);
   if ((threadIdx.x & 31) == 0 && ch) atomicAdd(&ctr[sv::C_CHANGED2], (unsigned long long)ch);
@@ -970,7 +974,7 @@ void pstat1(uint32_t* PA, const uint32_t* NCP, uint64_t n, uint32_t* TB, uint32_
   const uint64_t n4 = (n + 3) / 4;
   if (!n4) return;
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
-  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, c, temps_all ? 1 : 0, flag ? 1 : 0);
+  k_pstat1<<<g, RB, 0, st>>>(PA, NCP, n4, TB, PB, c, temps_all ? 1 : 0, flag ? 1 : 0, 0u);
 }
 void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t* ctr, cudaStream_t st,
             uint32_t* NX, const uint32_t* list, const uint64_t* lcnt) {
@@ -983,8 +987,115 @@ void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t
   const uint64_t n4 = (n + 3) / 4;
   if (!n4) return;
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
-  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, TB, c, NX);
+  k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, TB, c, NX, 0u);
 }
+void pstat1_block(uint32_t* PA, const uint32_t* NCP, uint64_t lo, uint64_t hi, uint32_t* TB, uint32_t* PB,
+                  uint64_t* ctr, cudaStream_t st) {
+  const uint64_t n4 = (hi - lo + 3) / 4;
+  if (!n4) return;
+  const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
+  k_pstat1<<<g, RB, 0, st>>>(PA + lo, NCP + lo / 32, n4, TB, PB + lo, reinterpret_cast<unsigned long long*>(ctr),
+                             0, 1, (uint32_t)lo);
+}
+void pstat2_block(uint32_t* PB, uint64_t lo, uint64_t hi, uint32_t* PA, const uint32_t* TB, uint64_t* ctr,
+                  cudaStream_t st) {
+  const uint64_t n4 = (hi - lo + 3) / 4;
+  if (!n4) return;
+  const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
+  k_pstat2<<<g, RB, 0, st>>>(PB + lo, n4, PA + lo, TB + lo / 32, reinterpret_cast<unsigned long long*>(ctr),
+                             nullptr, (uint32_t)lo);
+}
+
+// ------------------------------------------------------- owner-computes slot exchange (NEXT-1)
+// Entries (slot, value | flag << 31) of the slots this rank touched outside its own block,
+// grouped by the owner of the slot (owner k holds [k*blk, (k+1)*blk)).  S != NULL: slots
+// with S[p] != INF, flag = BM bit (NCP); S == NULL: the set bits of BM, value 0, flag 1 (TB).
+CC_DEVI bool oc_take(const uint32_t* S, const uint32_t* BM, uint64_t p, uint64_t n, uint64_t lo, uint64_t hi,
+                     uint32_t* v) {
+  if (p >= n || (p >= lo && p < hi)) return false;
+  if (S) {
+    *v = S[p];
+    if (*v == INF) return false;
+    if (BM) *v |= ((BM[p >> 5] >> (p & 31)) & 1u) << 31;
+    return true;
+  }
+  *v = 0x80000000u;
+  return (BM[p >> 5] >> (p & 31)) & 1u;
+}
+__global__ void k_oc_count(const uint32_t* __restrict__ S, const uint32_t* __restrict__ BM, uint64_t n,
+                           uint64_t lo, uint64_t hi, uint64_t blk, int world, unsigned long long* cnt) {
+  __shared__ uint32_t s[256];
+  for (int i = threadIdx.x; i < world; i += RB) s[i] = 0;
+  __syncthreads();
+  for (uint64_t p = blockIdx.x * (uint64_t)RB + threadIdx.x; p < n; p += (uint64_t)gridDim.x * RB) {
+    uint32_t v;
+    if (oc_take(S, BM, p, n, lo, hi, &v)) atomicAdd(&s[p / blk], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < world; i += RB)
+    if (s[i]) atomicAdd(&cnt[i], (unsigned long long)s[i]);
+}
+__global__ void k_oc_scatter(const uint32_t* __restrict__ S, const uint32_t* __restrict__ BM, uint64_t n,
+                             uint64_t lo, uint64_t hi, uint64_t blk, unsigned long long* cursor,
+                             uint2* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t p0 = blockIdx.x * (uint64_t)RB; p0 < n; p0 += (uint64_t)gridDim.x * RB) {
+    const uint64_t p = p0 + threadIdx.x;
+    uint32_t v = 0;
+    const bool take = oc_take(S, BM, p, n, lo, hi, &v);
+    const uint32_t own = take ? (uint32_t)(p / blk) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(FULL, own);
+    if (take) {
+      const int leader = __ffs(peers) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(&cursor[own], (unsigned long long)__popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      out[base + __popc(peers & ((1u << lane) - 1u))] = make_uint2((uint32_t)p, v);
+    }
+  }
+}
+// owner side: S[p] = min(S[p], value), BM bit p |= flag
+__global__ void k_oc_apply(const uint2* __restrict__ in, uint64_t count, uint32_t* S, uint32_t* BM) {
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < count; i += (uint64_t)gridDim.x * RB) {
+    const uint2 e = in[i];
+    if (S) {
+      const uint32_t v = e.y & 0x7FFFFFFFu;
+      if (v < S[e.x]) atomicMin(&S[e.x], v);
+    }
+    if ((e.y >> 31) && BM) set_bit(BM, e.x);
+  }
+}
+// owner side: the final value of every received slot, in receive order
+__global__ void k_oc_gather(const uint2* __restrict__ in, uint64_t count, const uint32_t* __restrict__ S,
+                            uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < count; i += (uint64_t)gridDim.x * RB)
+    out[i] = S[in[i].x];
+}
+// requester side: S[sent[i].slot] = vals[i] (vals == NULL: INF, the clear)
+__global__ void k_oc_put(const uint2* __restrict__ sent, uint64_t count, const uint32_t* __restrict__ vals,
+                         uint32_t* S) {
+  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < count; i += (uint64_t)gridDim.x * RB)
+    S[sent[i].x] = vals ? vals[i] : INF;
+}
+static unsigned oc_grid(uint64_t work) { return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + RB - 1) / RB, 148 * 8)); }
+void oc_count(const uint32_t* S, const uint32_t* BM, uint64_t n, uint64_t lo, uint64_t hi, uint64_t blk, int world,
+              uint64_t* cnt, cudaStream_t st) {
+  if (n) k_oc_count<<<oc_grid(n), RB, 0, st>>>(S, BM, n, lo, hi, blk, world, reinterpret_cast<unsigned long long*>(cnt));
+}
+void oc_scatter(const uint32_t* S, const uint32_t* BM, uint64_t n, uint64_t lo, uint64_t hi, uint64_t blk,
+                uint64_t* cursor, uint2* out, cudaStream_t st) {
+  if (n) k_oc_scatter<<<oc_grid(n), RB, 0, st>>>(S, BM, n, lo, hi, blk, reinterpret_cast<unsigned long long*>(cursor), out);
+}
+void oc_apply(const uint2* in, uint64_t count, uint32_t* S, uint32_t* BM, cudaStream_t st) {
+  if (count) k_oc_apply<<<oc_grid(count), RB, 0, st>>>(in, count, S, BM);
+}
+void oc_gather(const uint2* in, uint64_t count, const uint32_t* S, uint32_t* out, cudaStream_t st) {
+  if (count) k_oc_gather<<<oc_grid(count), RB, 0, st>>>(in, count, S, out);
+}
+void oc_put(const uint2* sent, uint64_t count, const uint32_t* vals, uint32_t* S, cudaStream_t st) {
+  if (count) k_oc_put<<<oc_grid(count), RB, 0, st>>>(sent, count, vals, S);
+}
+
 void list_from_bits(uint32_t* NX, uint64_t n, uint32_t* list, uint64_t* lcnt, uint32_t* NCP, uint32_t* TB,
                     uint32_t* PA, cudaStream_t st) {
   cudaMemsetAsync(lcnt, 0, sizeof(uint64_t), st);

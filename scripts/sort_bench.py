@@ -2,7 +2,9 @@
 random 64-bit keys with a u32 payload against torch.sort (CUB DeviceRadixSort) on one B200.
 PAPER.md:389 benchmarks its samplesort on 2 billion random 64-bit integers.
 
-    python scripts/sort_bench.py [--log2n 31] [--reps 3]
+    python scripts/sort_bench.py [--log2n 30 | --n 2000000000] [--reps 3]
+
+--n 2000000000 is the paper's size; it stays below INT_MAX, which torch.sort needs.
 """
 import argparse
 import json
@@ -32,9 +34,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--log2n", type=int, default=30,
                     help="torch.sort takes at most INT_MAX elements: 30 for the comparison")
+    ap.add_argument("--n", type=int, default=0, help="key count (overrides --log2n)")
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
-    n = 1 << args.log2n
+    n = args.n or (1 << args.log2n)
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev)
     g.manual_seed(1607)

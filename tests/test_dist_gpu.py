@@ -420,3 +420,21 @@ def test_dist_balanced(world, graph):
         assert excess <= world * (a // (16 * world) + maxrow + 1), (excess, a)
     if graph == "skewed":
         assert any(excess > world * (a // (16 * world) + maxrow + 1) for excess, a in spread(res_u))
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("dense", [False, True])
+def test_dist_exchange_modes(world, dense):
+    """Both slot exchanges of the sharded SV: owner-computes (default; SURVEY NEXT-1 -- foreign
+    slot partials to their owner, statistics per owner block, p_min / PB replied to the
+    senders, temporaries routed to their rows' owner) and the dense all-reduce ablation
+    (CC_FLAG_DENSE_EXCHANGE).  Labels and every Alg. 1 counter equal the oracle's."""
+    import paper_1607_06156_b200 as cc
+    flags = cc.CC_FLAG_DENSE_EXCHANGE if dense else 0
+    g = graphgen.make("c1", 0.5)
+    modes = ("sv", "auto")
+    _check(run_ranks(_rank_run, world, g.n, g.edges, modes, flags), g.n, g.edges, modes)
+    s = graphgen.make("c2", 0.01)
+    _check(run_ranks(_rank_run, world, s.n, s.edges, ("sv",), flags), s.n, s.edges, ("sv",))
+    r = graphgen.rmat_scale_graph(12)
+    _check(run_ranks(_rank_run, world, r.n, r.edges, ("sv", "bfs+sv"), flags), r.n, r.edges, ("sv", "bfs+sv"))
