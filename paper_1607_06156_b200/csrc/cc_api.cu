@@ -685,12 +685,8 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     // at most every other iteration, and not again after one that folded little
     const bool want_collapse =
         collapse_force ? can_collapse && len_live > 0
-                       : collapse_ok && len_live >= COLLAPSE_MIN_LEN &&
-                             ((it >= 1 && it >= last_collapse + 2 && s.partitions * 16 < len_live) ||
-                              // after iteration 1 (decided now: iteration 1 is already in flight)
-                              // when iteration 0 sent everything to a few p_min targets
-                              // (C4 mode sv: 11 k targets = |P_1| for 2.2 G tuples)
-                              (it == 0 && h[sv::C_TDIST] > 0 && h[sv::C_TDIST] * 1024 < len_live));
+                       : collapse_ok && it >= 1 && it >= last_collapse + 2 && len_live >= COLLAPSE_MIN_LEN &&
+                             s.partitions * 16 < len_live;
     bool rebalance = false;
     if (balance) {
       TRY(gather_loads(len_live));
