@@ -950,6 +950,7 @@ cc_status bfs_stream(cc_ctx* c, uint64_t root, bool spec_ok, const uint2** rem, 
     c->h_word[0] = 1u << (2 * (root & 15));
     CK(cudaMemcpyAsync(S + root / 16, c->h_word, 4, cudaMemcpyHostToDevice, c->st));
   }
+  if (!spec_ok) CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));  // then cleared per level
   const uint2* cur = c->d_edges;
   uint64_t mcur = m;
   int nb = 0;  // next scratch buffer
@@ -960,7 +961,6 @@ cc_status bfs_stream(cc_ctx* c, uint64_t root, bool spec_ok, const uint2** rem, 
     const bool root_level = levels == 0;
     bool compact = false;
     if (!spec_pending) {
-      CK(cudaMemsetAsync(X, 0, sizeof(uint32_t) * nw, c->st));
       // compact (keep only edges that can still matter) once most present vertices are
       // visited, or when the frontier's arcs are a fifth of the current edge list: every edge
       // at the frontier leaves, so the next level reads that much less (a local decision:
@@ -978,7 +978,8 @@ cc_status bfs_stream(cc_ctx* c, uint64_t root, bool spec_ok, const uint2** rem, 
     TRY(comm_or_bits(c, X, nw));
     CK(cudaMemsetAsync(c->d_gctr + graph::G_NEWVIS, 0, sizeof(uint64_t), c->st));
     CK(cudaMemsetAsync(c->d_gctr + graph::G_FARCS, 0, sizeof(uint64_t), c->st));
-    graph::launch_farcs(X, n, c->d_deg, c->d_gctr + graph::G_NEWVIS, c->d_gctr + graph::G_FARCS, c->st);
+    // counts, S advanced (frontier <- X, visited |= X; a no-op past the last level), X cleared
+    graph::launch_farcs_advance(X, S, n, c->d_deg, c->d_gctr + graph::G_NEWVIS, c->d_gctr + graph::G_FARCS, c->st);
     c->launches += 1;
     CKL();
     TRY(sync_read(c));
@@ -993,8 +994,6 @@ cc_status bfs_stream(cc_ctx* c, uint64_t root, bool spec_ok, const uint2** rem, 
     visited += nv;
     front_arcs = c->h_gctr[graph::G_FARCS];
     levels++;
-    graph::launch_bfs_advance(S, X, n, c->st);
-    c->launches += 1;
   }
   R.bfs_visited = visited;
   R.bfs_levels = levels;

@@ -460,12 +460,15 @@ k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo_arg, uint32_t n
     put_group(b, opos[i], r0, r1);
   }
 }
-// order[rank] = bucket, by decreasing entry count (ties: smaller bucket first); one block
-__global__ void __launch_bounds__(1024) k_deg_order(DegRadix R, uint32_t nbk) {
+// order[rank] = bucket, by decreasing entry count (ties: smaller bucket first); each block
+// ranks DR_ORDER_PER buckets against all of them (one block ranking all 2048 took 120 us)
+constexpr uint32_t DR_ORDER_PER = 128;
+__global__ void __launch_bounds__(DR_ORDER_PER) k_deg_order(DegRadix R, uint32_t nbk) {
   __shared__ uint32_t s_size[DR_NB];
   for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) s_size[b] = min(R.cur[b], R.C);
   __syncthreads();
-  for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) {
+  for (uint32_t b = blockIdx.x * DR_ORDER_PER + threadIdx.x; b < nbk && b < (blockIdx.x + 1) * DR_ORDER_PER;
+       b += blockDim.x) {
     const uint32_t sb = s_size[b];
     uint32_t rank = 0;
     for (uint32_t o = 0; o < nbk; o++) {
@@ -595,7 +598,7 @@ bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* d
     else
       k_deg_part<false><<<G, DR_THREADS, smem_part, st>>>(e2, mr, (uint32_t)lo, nb, R, deg,
                                                           lo == 0 ? sp : SpecRoot{nullptr, nullptr, nullptr});
-    k_deg_order<<<1, 1024, 0, st>>>(R, nb);
+    k_deg_order<<<(nb + DR_ORDER_PER - 1) / DR_ORDER_PER, DR_ORDER_PER, 0, st>>>(R, nb);
     k_deg_count<<<nb, DR_THREADS, smem_count, st>>>(R, (uint32_t)lo, n, deg);
   }
   return true;
@@ -805,6 +808,49 @@ void launch_farcs(const uint32_t* next, uint64_t n, const uint32_t* deg, uint64_
   if (nw)
     k_farcs<<<grid_for(nw, 148 * 8), BLOCK, 0, st>>>(next, nw, deg, reinterpret_cast<unsigned long long*>(found),
                                                       reinterpret_cast<unsigned long long*>(farcs));
+}
+// One pass after a level: the level's found ids (*found += |next|) and their arcs (*farcs),
+// S advanced (frontier <- next, visited |= next) and next cleared for the following level
+// (replaces k_farcs + k_bfs_advance + a memset of next: one pass over the state instead of three)
+__global__ void __launch_bounds__(BLOCK) k_farcs_advance(uint32_t* __restrict__ next, uint32_t* __restrict__ S,
+                                                         uint64_t nw, const uint32_t* __restrict__ deg,
+                                                         unsigned long long* found, unsigned long long* farcs) {
+  unsigned long long s = 0;
+  uint32_t c = 0;
+  auto spread = [](uint32_t x) {  // 16 bits to the odd positions of 32
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+  };
+  for (uint64_t w = blockIdx.x * (uint64_t)BLOCK + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * BLOCK) {
+    uint32_t x = next[w];
+    if (x) next[w] = 0;
+    const uint2 sv = reinterpret_cast<const uint2*>(S)[w];
+    const uint32_t lo = spread(x & 0xFFFFu), hi = spread(x >> 16);
+    const uint2 nv = make_uint2((sv.x & 0x55555555u) | lo | (lo << 1), (sv.y & 0x55555555u) | hi | (hi << 1));
+    if (nv.x != sv.x || nv.y != sv.y) reinterpret_cast<uint2*>(S)[w] = nv;
+    c += __popc(x);
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      s += __ldg(&deg[w * 32 + b]);
+    }
+  }
+  s = warp_sum(s);
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) {
+    atomicAdd(found, (unsigned long long)c);
+    atomicAdd(farcs, s);
+  }
+}
+void launch_farcs_advance(uint32_t* next, uint32_t* S, uint64_t n, const uint32_t* deg, uint64_t* found,
+                          uint64_t* farcs, cudaStream_t st) {
+  const uint64_t nw = (n + 31) / 32;
+  if (nw)
+    k_farcs_advance<<<grid_for(nw, 148 * 8), BLOCK, 0, st>>>(next, S, nw, deg, reinterpret_cast<unsigned long long*>(found),
+                                                             reinterpret_cast<unsigned long long*>(farcs));
 }
 void launch_bfs_advance(uint32_t* S, const uint32_t* next, uint64_t n, cudaStream_t st) {
   const uint64_t nw2 = (n + 15) / 16;

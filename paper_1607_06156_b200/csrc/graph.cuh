@@ -63,6 +63,9 @@ void launch_bfs_level(bool root_level, bool compact, const uint2* edges, uint64_
 void launch_farcs(const uint32_t* next, uint64_t n, const uint32_t* deg, uint64_t* found, uint64_t* farcs,
                   cudaStream_t st);
 void launch_bfs_advance(uint32_t* S, const uint32_t* next, uint64_t n, cudaStream_t st);
+// both of the above in one pass, and next cleared (S: 2n bits, 16-byte aligned words)
+void launch_farcs_advance(uint32_t* next, uint32_t* S, uint64_t n, const uint32_t* deg, uint64_t* found,
+                          uint64_t* farcs, cudaStream_t st);
 void launch_filter(const uint2* edges, uint64_t m, const uint32_t* S, uint2* out,
                    uint64_t* gctr, cudaStream_t st);
 void launch_vis_bits(const uint32_t* S, uint64_t n, uint32_t* vis, cudaStream_t st);

@@ -179,7 +179,7 @@ constexpr int MAXG = 2048;
 // DIRECTED: the input is already arcs (r, p) (multi-GPU: arcs received by their owner),
 // one tuple each; otherwise undirected edges, two tuples each.
 template <bool DIRECTED>
-__global__ void __launch_bounds__(B) k_bucket(const uint2* __restrict__ e, uint64_t m, int gshift,
+__global__ void __launch_bounds__(B, 4) k_bucket(const uint2* __restrict__ e, uint64_t m, int gshift,
                                               int G, unsigned long long* gcur,
                                               uint2* __restrict__ out) {
   constexpr int PER = DIRECTED ? 1 : 2;
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(B) k_collapse(const uint32_t* __restrict__ R,
   for (int k = 0; k < CITEMS; k++) {
     const uint32_t x = x0 + k;
     if (hh[k] == x + 1 && s_cnt[x]) {
-      HW[r[k]] += s_cnt[x];
+      atomicAdd(&HW[r[k]], s_cnt[x]);  // result unused: a fire-and-forget reduction, no dependent load
       hid += s_cnt[x];
     }
   }
