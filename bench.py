@@ -248,13 +248,13 @@ def cpu_baseline(g, budget_s=12.0):
                       f"{t_used:.1f} s, single thread", "host": host}
 
 
-def traffic_for(config, regroup):
+def traffic_for(config, regroup, mode="auto"):
     """ncu DRAM bytes per cc_run by kernel family (profiles/traffic.json, scripts/traffic.py)."""
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(tp):
         return {}, None
     d = json.load(open(tp))
-    return d.get(f"{config}/{regroup}", {}), d.get("_source")
+    return d.get(f"{config}/{regroup}" + ("" if mode == "auto" else "/" + mode), {}), d.get("_source")
 
 
 def main():
@@ -417,7 +417,7 @@ def main():
     if rk == 0:
         peak, peak_src = peaks()
         mp = micro_peaks()
-        traffic, traffic_src = traffic_for(args.config, args.regroup)
+        traffic, traffic_src = traffic_for(args.config, args.regroup, args.mode)
         K = args.steps
         # dominant kernel: the single-kernel family with the largest device time in the timed
         # region (family 1 is the whole-iteration aggregate, excluded)

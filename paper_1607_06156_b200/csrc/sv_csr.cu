@@ -156,6 +156,10 @@ __global__ void __launch_bounds__(B) k_fill_long(const uint32_t* __restrict__ of
   }
 }
 
+// Group cursor slot: with few groups (G <= 64, the large graphs) each cursor gets its own
+// 256-byte line, so the per-block cursor atomics (C4 mode sv: 524 k blocks x 64 groups)
+// spread over L2 slices instead of queueing on the two lines 64 packed counters share
+__host__ __device__ inline uint32_t gslot(int g, int G) { return G <= 64 ? (uint32_t)g * 32u : (uint32_t)g; }
 // Group start offsets of the bucketed arc list (exclusive scan of per-group arc counts).
 __global__ void k_gscan(const uint32_t* __restrict__ garc, int G, unsigned long long* gcur) {
   __shared__ uint32_t s_scan[B / 32 + 1];
@@ -165,7 +169,7 @@ __global__ void k_gscan(const uint32_t* __restrict__ garc, int G, unsigned long 
     const uint32_t x = g < G ? garc[g] : 0u;
     uint32_t tot;
     const uint32_t e = block_excl_scan<B>(x, s_scan, &tot);
-    if (g < G) gcur[g] = carry + e;
+    if (g < G) gcur[gslot(g, G)] = carry + e;
     carry += tot;
   }
 }
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(B, 4) k_bucket(const uint2* __restrict__ e, ui
   }
   __syncthreads();
   for (int g = threadIdx.x; g < G; g += B)
-    s_base[g] = s_cnt[g] ? atomicAdd(&gcur[g], (unsigned long long)s_cnt[g]) : 0ull;
+    s_base[g] = s_cnt[g] ? atomicAdd(&gcur[gslot(g, G)], (unsigned long long)s_cnt[g]) : 0ull;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < BITEMS; k++) {
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(1024) k_group_degree(const uint2* __restrict__
   const uint32_t cnt = (uint32_t)min((uint64_t)1 << gshift, n - base);
   for (uint32_t v = threadIdx.x; v < cnt; v += blockDim.x) s_deg[v] = 0;
   __syncthreads();
-  const uint64_t a = g ? gend[g - 1] : 0, b = gend[g];
+  const uint64_t a = g ? gend[gslot((int)g - 1, (int)gridDim.x)] : 0, b = gend[gslot((int)g, (int)gridDim.x)];
   const uint32_t lt = lanemask_lt();
   for (uint64_t i0 = a; i0 < b; i0 += blockDim.x) {
     const uint64_t i = i0 + threadIdx.x;

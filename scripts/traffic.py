@@ -46,20 +46,23 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
     ap.add_argument("--regroup", default="csr")
+    ap.add_argument("--mode", default="auto")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "traffic.json"))
     ap.add_argument("--from-csv", default=None, help="recompute from a CSV an earlier run saved")
     args = ap.parse_args()
-    csv_path = os.path.join(ROOT, "gpurun_out", f"traffic_{args.config}.csv")
+    tag = args.config + ("" if args.mode == "auto" else "_" + args.mode)
+    csv_path = os.path.join(ROOT, "gpurun_out", f"traffic_{tag}.csv")
     if args.from_csv:
         return summarize(open(args.from_csv).read(), args)
-    tl = os.path.join(ROOT, "gpurun_out", f"traffic_tl_{args.config}.json")
-    subprocess.check_call([sys.executable, os.path.join(ROOT, "scripts", "timeline.py"), "--config", args.config,
-                           "--out", tl], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    tl = os.path.join(ROOT, "gpurun_out", f"traffic_tl_{tag}.json")
+    tl_args = ["--config", args.config, "--mode", args.mode, "--out", tl]
+    subprocess.check_call([sys.executable, os.path.join(ROOT, "scripts", "timeline.py"), *tl_args],
+                          stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
     per_run = sum(1 for o in json.load(open(tl))["ops"] if not o[2].startswith(("Memset", "Memcpy")))
     out = subprocess.check_output(
         ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
          "--clock-control", "none", "--csv", "-s", str(3 * per_run), "-c", str(per_run),
-         sys.executable, os.path.join(ROOT, "scripts", "timeline.py"), "--config", args.config, "--out", tl],
+         sys.executable, os.path.join(ROOT, "scripts", "timeline.py"), *tl_args],
         text=True, stderr=subprocess.DEVNULL)
     os.makedirs(os.path.dirname(csv_path), exist_ok=True)
     with open(csv_path, "w") as f:
@@ -85,7 +88,7 @@ def summarize(out, args):
         f = family(name)
         fams[f] = fams.get(f, 0.0) + by
     data = json.load(open(args.out)) if os.path.exists(args.out) else {}
-    data[f"{args.config}/{args.regroup}"] = fams
+    data[f"{args.config}/{args.regroup}" + ("" if args.mode == "auto" else "/" + args.mode)] = fams
     data["_source"] = ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every kernel of one "
                        "cc_run after three warm-up runs (scripts/traffic.py): bytes per cc_run by kernel family")
     json.dump(data, open(args.out, "w"), indent=1)
