@@ -59,11 +59,17 @@ __global__ void __launch_bounds__(DB) k_owner_scatter(const uint2* __restrict__ 
   const uint64_t e0 = blockIdx.x * (uint64_t)DB * SITEMS + threadIdx.x;
   uint2 arc[2 * SITEMS];
   uint32_t slot[2 * SITEMS];
+  uint2 ld[SITEMS];  // all loads in flight before the first (ordering) shared atomic
+#pragma unroll
+  for (int k = 0; k < SITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * DB;
+    ld[k] = i < m ? e[i] : make_uint2(0, 0);
+  }
 #pragma unroll
   for (int k = 0; k < SITEMS; k++) {
     const uint64_t i = e0 + (uint64_t)k * DB;
     if (i < m) {
-      const uint2 xy = e[i];
+      const uint2 xy = ld[k];
       arc[2 * k] = make_uint2(xy.y, xy.x);      // <x,_,y>: r = y, p = x
       arc[2 * k + 1] = make_uint2(xy.x, xy.y);  // <y,_,x>: r = x, p = y
       slot[2 * k] = atomicAdd(&s_cnt[xy.y / blk], 1u);

@@ -159,7 +159,9 @@ __global__ void __launch_bounds__(B) k_fill_long(const uint32_t* __restrict__ of
 // Group cursor slot: with few groups (G <= 64, the large graphs) each cursor gets its own
 // 256-byte line, so the per-block cursor atomics (C4 mode sv: 524 k blocks x 64 groups)
 // spread over L2 slices instead of queueing on the two lines 64 packed counters share
-__host__ __device__ inline uint32_t gslot(int g, int G) { return G <= 64 ? (uint32_t)g * 32u : (uint32_t)g; }
+__host__ __device__ inline uint32_t gslot(int g, int G) {
+  return G <= 64 ? (uint32_t)g * 32u : G <= 256 ? (uint32_t)g * 8u : (uint32_t)g;
+}
 // Group start offsets of the bucketed arc list (exclusive scan of per-group arc counts).
 __global__ void k_gscan(const uint32_t* __restrict__ garc, int G, unsigned long long* gcur) {
   __shared__ uint32_t s_scan[B / 32 + 1];
@@ -194,11 +196,19 @@ __global__ void __launch_bounds__(B, 4) k_bucket(const uint2* __restrict__ e, ui
   const uint64_t e0 = (blockIdx.x * (uint64_t)B * BITEMS) + threadIdx.x;
   uint2 arc[PER * BITEMS];
   uint32_t slot[PER * BITEMS];
+  // every load in flight before the first shared atomic: the atomics order memory, so loads
+  // interleaved with them were issued one at a time (C4 mode sv: IPC 0.21, 32 ms)
+  uint2 ld[BITEMS];
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * B;
+    ld[k] = i < m ? e[i] : make_uint2(0, 0);
+  }
 #pragma unroll
   for (int k = 0; k < BITEMS; k++) {
     const uint64_t i = e0 + (uint64_t)k * B;
     if (i < m) {
-      const uint2 xy = e[i];
+      const uint2 xy = ld[k];
       if (DIRECTED) {
         arc[k] = xy;
         slot[k] = atomicAdd(&s_cnt[xy.x >> gshift], 1u);
@@ -223,6 +233,81 @@ __global__ void __launch_bounds__(B, 4) k_bucket(const uint2* __restrict__ e, ui
         out[s_base[arc[PER * k + t].x >> gshift] + slot[PER * k + t]] = arc[PER * k + t];
     }
   }
+}
+
+// The same pass with the block's arcs staged in shared memory in group order, for G <= 256
+// groups (the large graphs): each group's run then leaves as consecutive 8-byte stores.
+// Scattered from registers, a warp's 32 stores went to ~27 different sectors (each lane to
+// another group's run), and on C4 in mode sv the pass was bound by 1.8 G partial-sector
+// writes into L2 (32 ms for 26 GB of DRAM traffic).
+constexpr int GST = 256;
+template <bool DIRECTED>
+__global__ void __launch_bounds__(B) k_bucket_st(const uint2* __restrict__ e, uint64_t m, int gshift, int G,
+                                                 unsigned long long* gcur, uint2* __restrict__ out) {
+  constexpr int PER = DIRECTED ? 1 : 2;
+  static_assert(B == GST, "one thread per group counter in the scan");
+  __shared__ uint32_t s_scan[B / 32 + 1];
+  __shared__ uint32_t s_cnt[GST], s_off[GST];
+  __shared__ unsigned long long s_base[GST];
+  __shared__ uint2 s_arc[B * BITEMS * PER];
+  s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t e0 = (blockIdx.x * (uint64_t)B * BITEMS) + threadIdx.x;
+  uint2 ld[BITEMS];
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * B;
+    ld[k] = i < m ? e[i] : make_uint2(0, 0);
+  }
+  uint2 arc[PER * BITEMS];
+  uint32_t slot[PER * BITEMS];
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * B;
+    if (i < m) {
+      const uint2 xy = ld[k];
+      if (DIRECTED) {
+        arc[k] = xy;
+        slot[k] = atomicAdd(&s_cnt[xy.x >> gshift], 1u);
+      } else {
+        arc[PER * k] = make_uint2(xy.y, xy.x);            // <x,_,y>: r = y, p = x
+        arc[PER * k + PER - 1] = make_uint2(xy.x, xy.y);  // <y,_,x>: r = x, p = y
+        slot[PER * k] = atomicAdd(&s_cnt[xy.y >> gshift], 1u);
+        slot[PER * k + PER - 1] = atomicAdd(&s_cnt[xy.x >> gshift], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t c = threadIdx.x < (uint32_t)G ? s_cnt[threadIdx.x] : 0u;
+  uint32_t tot;
+  s_off[threadIdx.x] = block_excl_scan<B>(c, s_scan, &tot);
+  if (c) s_base[threadIdx.x] = atomicAdd(&gcur[gslot(threadIdx.x, G)], (unsigned long long)c);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < BITEMS; k++) {
+    const uint64_t i = e0 + (uint64_t)k * B;
+    if (i < m) {
+#pragma unroll
+      for (int t = 0; t < PER; t++) {
+        const uint2 a = arc[PER * k + t];
+        s_arc[s_off[a.x >> gshift] + slot[PER * k + t]] = a;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t q = threadIdx.x; q < tot; q += B) {
+    const uint2 a = s_arc[q];
+    const uint32_t g = a.x >> gshift;
+    out[s_base[g] + (q - s_off[g])] = a;
+  }
+}
+template <bool DIRECTED>
+static void launch_bucket(const uint2* edges, uint64_t m, int gshift, int G, unsigned long long* gc, uint2* out,
+                          cudaStream_t st) {
+  if (!m) return;
+  const unsigned gb = (unsigned)((m + B * BITEMS - 1) / (B * BITEMS));
+  if (G <= GST) k_bucket_st<DIRECTED><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, out);
+  else k_bucket<DIRECTED><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, out);
 }
 
 // ---- degrees without global atomics (prediction of the csr engine, n <= 2^26)
@@ -280,6 +365,9 @@ __global__ void __launch_bounds__(B) k_bucket2(const uint2* __restrict__ in, uin
                                                uint32_t* scur, uint2* __restrict__ out) {
   __shared__ uint32_t s_cnt[MAXS2];
   __shared__ uint32_t s_base[MAXS2];
+  __shared__ uint32_t s_off[MAXS2];
+  __shared__ uint32_t s_scan[B / 32 + 1];
+  __shared__ uint2 s_arc[B * BITEMS];
   __shared__ uint32_t s_lo, s_hi;
   if (threadIdx.x == 0) {
     s_lo = 0xFFFFFFFFu;
@@ -317,6 +405,31 @@ __global__ void __launch_bounds__(B) k_bucket2(const uint2* __restrict__ in, uin
     if (arc[k].x == 0xFFFFFFFFu) continue;
     const uint32_t sg = arc[k].x >> SUBG;
     slot[k] = local ? atomicAdd(&s_cnt[sg - slo], 1u) : atomicAdd(&scur[sg], 1u);
+  }
+  if (local && s_hi - slo < 128) {
+    // few subgroups in the tile (>= 16 arcs per subgroup on average): staged in subgroup
+    // order, then written as runs (scattered from registers, a warp's 32 stores touched ~31
+    // sectors); with more subgroups the runs are too short to pay for the staging
+    __syncthreads();
+    static_assert(MAXS2 == 2 * B, "two counters per thread in the scan");
+    const uint32_t c0 = s_cnt[2 * threadIdx.x], c1 = s_cnt[2 * threadIdx.x + 1];
+    uint32_t tot;
+    const uint32_t o = block_excl_scan<B>(c0 + c1, s_scan, &tot);
+    s_off[2 * threadIdx.x] = o;
+    s_off[2 * threadIdx.x + 1] = o + c0;
+    if (c0) s_base[2 * threadIdx.x] = atomicAdd(&scur[slo + 2 * threadIdx.x], c0);
+    if (c1) s_base[2 * threadIdx.x + 1] = atomicAdd(&scur[slo + 2 * threadIdx.x + 1], c1);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BITEMS; k++)
+      if (arc[k].x != 0xFFFFFFFFu) s_arc[s_off[(arc[k].x >> SUBG) - slo] + slot[k]] = arc[k];
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < tot; q += B) {
+      const uint2 a = s_arc[q];
+      const uint32_t l = (a.x >> SUBG) - slo;
+      out[s_base[l] + (q - s_off[l])] = a;
+    }
+    return;
   }
   if (local) {
     __syncthreads();
@@ -627,13 +740,14 @@ __global__ void __launch_bounds__(B) k_collapse(const uint32_t* __restrict__ R,
 int group_shift(uint64_t n, uint64_t tuples) {
   int kb = 0;
   while ((1ull << kb) < n) kb++;
-  int lg = 0;  // log2 G: about 2M tuples per group
-  while (lg < 10 && (tuples >> (21 + lg)) > 0) lg++;
+  int lg = 0;  // log2 G: about 256 k tuples per group (up to 256 groups, below)
+  while (lg < 10 && (tuples >> (18 + lg)) > 0) lg++;
   int gs = kb - lg;
-  // at most 64 groups while a group can stay within 2^20 ids: k_bucket gives every group one
-  // run per 2048-edge tile, and with 1024 groups (C4 in mode sv) those runs were 4 arcs (one
-  // sector) long; 2^20 ids keep a k_bucket2 tile's subgroups within its 512 local counters
-  const int gs_min = std::min(20, kb - 6);
+  // at most 256 groups while a group can stay within 2^18 ids: k_bucket gives every group one
+  // run per 2048-edge tile (16 arcs at 256 groups, staged in shared memory: k_bucket_st;
+  // with 1024 groups those runs were 4 arcs, one sector), and 2^18 ids are 128 subgroups, so
+  // a k_bucket2 tile's subgroups fit its local counters and its runs are long enough to stage
+  const int gs_min = std::min(18, kb - 8);
   if (gs < gs_min) gs = gs_min;
   return gs < 12 ? 12 : gs;  // a k_rows tile (2^12 vertices) lies inside one group
 }
@@ -667,9 +781,7 @@ void bucket_degrees(const uint2* edges, uint64_t m, uint64_t n, int gshift, uint
   cudaMemsetAsync(garc, 0, sizeof(uint32_t) * G, st);
   if (m) k_group_hist<<<grid(m, B, 148 * 4), B, 0, st>>>(edges, m, gshift, G, garc);
   k_gscan<<<1, B, 0, st>>>(garc, G, gc);
-  if (m)
-    k_bucket<false><<<(unsigned)((m + B * BITEMS - 1) / (B * BITEMS)), B, 0, st>>>(edges, m, gshift, G,
-                                                                                  gc, tmp);
+  launch_bucket<false>(edges, m, gshift, G, gc, tmp, st);
   // k_bucket advanced every group cursor to its group's end
   const int smem = (int)(sizeof(uint32_t) << gshift);
   static int attr_set = 0;
@@ -702,9 +814,8 @@ void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, ui
     auto* gc = reinterpret_cast<unsigned long long*>(gcur);
     uint2* tmp1 = reinterpret_cast<uint2*>(R);
     k_gscan<<<1, B, 0, st>>>(garc, G, gc);
-    const unsigned gb = (unsigned)((m + B * BITEMS - 1) / (B * BITEMS));
-    if (directed) k_bucket<true><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp1);
-    else k_bucket<false><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp1);
+    if (directed) launch_bucket<true>(edges, m, gshift, G, gc, tmp1, st);
+    else launch_bucket<false>(edges, m, gshift, G, gc, tmp1, st);
     const uint64_t na = directed ? m : 2 * m;
     const uint64_t ns = ((n - 1) >> SUBG) + 1;
     uint32_t* scur = longlist;  // n-sized scratch, ns entries used
@@ -725,9 +836,8 @@ void fill(const uint2* edges, uint64_t m, const uint32_t* off, uint32_t* cur, ui
   if (!m) return;
   auto* gc = reinterpret_cast<unsigned long long*>(gcur);
   k_gscan<<<1, B, 0, st>>>(garc, G, gc);
-  const unsigned gb = (unsigned)((m + B * BITEMS - 1) / (B * BITEMS));
-  if (directed) k_bucket<true><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp);
-  else k_bucket<false><<<gb, B, 0, st>>>(edges, m, gshift, G, gc, tmp);
+  if (directed) launch_bucket<true>(edges, m, gshift, G, gc, tmp, st);
+  else launch_bucket<false>(edges, m, gshift, G, gc, tmp, st);
   const uint64_t na = directed ? m : 2 * m;
   k_scatter<<<grid((na + XITEMS - 1) / XITEMS, B, 148 * 8), B, 0, st>>>(tmp, na, cur, P);
 }
