@@ -473,6 +473,17 @@ def main():
             if "dram_GBps" in kr:
                 roof["dram_GBps_live"] = kr["dram_GBps"]
                 roof["dram_frac"] = kr["dram_frac"]
+        # north star: DRAM bytes the SV iterations move (ncu, per run) over the
+        # iterations' device time (family 1, CUDA events around each iteration)
+        sv_dram = None
+        if 1 in fam and fam[1]["ms"] > 0 and traffic:
+            sv_fams = [k for k in traffic if k.startswith(("k_rowpass", "k_pstat", "k_compact"))]
+            b = sum(traffic[k] for k in sv_fams)
+            if b > 0:
+                gbps = b / (fam[1]["ms"] / K / 1e3) / 1e9
+                sv_dram = {"ncu_bytes_per_step": b, "ms_per_step": fam[1]["ms"] / K, "GBps": gbps,
+                           "frac": gbps / peak, "families": sv_fams,
+                           "target": "north star: >= 0.5 of HBM per SV iteration"}
         path_bytes = alg_bytes(rep, n if not u64 else rep["n_present"], m)
         step_s = ms_max / 1e3 / K
         dram_step = sum(v for k, v in traffic.items()) if traffic else None
@@ -502,6 +513,7 @@ def main():
             "dram_path": ({"ncu_bytes_per_step": dram_step, "GBps": dram_step / step_s / 1e9,
                            "frac": dram_step / step_s / 1e9 / peak, "source": traffic_src}
                           if dram_step else None),
+            "sv_iteration_dram": sv_dram,
             "stages_ms": {k: rep[k] for k in ("ms_relabel", "ms_prediction", "ms_bfs", "ms_filter", "ms_sv",
                                               "ms_finalize")},
             "sv_iters": [{"A": it["active_in"], "P": it["partitions"], "ms": round(it["ms"], 4)}

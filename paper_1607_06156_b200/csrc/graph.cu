@@ -396,9 +396,7 @@ k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo_arg, uint32_t n
   // one group of 16 entries of bucket b (in registers) to its reserved region position
   auto put_group = [&](uint32_t b, uint32_t pos, const uint4& r0, const uint4& r1) {
     if (pos < R.C) {  // C and pos are multiples of 16
-      uint4* dst = reinterpret_cast<uint4*>(R.reg + dr_addr(R, b, pos));
-      dst[0] = r0;
-      dst[1] = r1;
+      st_v8(R.reg + dr_addr(R, b, pos), r0, r1);  // one 32-byte sector per group
     } else {  // region full: count directly
       const uint32_t wv[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
       const uint32_t bs = lo + (b << DR_SPAN);

@@ -28,7 +28,7 @@ FAMILIES = [
     (("k_pstat", "k_list_from_bits"), "k_pstat1/k_pstat2/k_list_from_bits (partition slot scans)"),
     (("k_rows", "k_fill", "k_bucket", "k_scatter", "k_place", "k_gscan"),
      "CSR build (k_rows, k_fill_*, k_bucket, k_scatter)"),
-    (("k_compact",), "k_compact (ordered exclusion of completed rows)"),
+    (("k_compact", "k_collapse"), "k_compact (ordered exclusion of completed rows)"),
     (("k_onesweep", "k_hist<", "radix::k_hist"), "k_hist+k_onesweep (radix regroup)"),
 ]
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
