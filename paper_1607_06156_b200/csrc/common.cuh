@@ -47,6 +47,12 @@ CC_DEVI uint4 ldg_stream(const uint4* p) {
   return v;
 }
 
+// 256-bit streaming load (sm_100: LDG.E.256): two uint4 from 32 bytes (p 32-byte aligned)
+CC_DEVI void ldg_stream_v8(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.cs.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
 // 256-bit store (sm_100: STG.E.256): 32 bytes, one full sector per request (p 32-byte aligned)
 CC_DEVI void st_v8(void* p, const uint4& a, const uint4& b) {
   asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),

@@ -370,21 +370,22 @@ k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo_arg, uint32_t n
     claim_store(v, 2);
     if (spec) spec_edge(t.x, t.y);
   }
+  // a thread's DR_VEC = 2 uint4 of a round are adjacent: one 256-bit load
+  static_assert(DR_VEC == 2, "one 32-byte load per thread per round");
   auto load = [&](uint4 (&x)[DR_VEC], uint32_t r) {
-    const uint4* p = e2 + (uint64_t)r * PER_ROUND + threadIdx.x;
+    const uint4* p = e2 + (uint64_t)r * PER_ROUND + DR_VEC * threadIdx.x;
     if (r < full_rounds) {
-#pragma unroll
-      for (int j = 0; j < DR_VEC; j++) x[j] = ldg_stream(p + j * DR_THREADS);
+      ldg_stream_v8(p, x[0], x[1]);
     } else if (r < rounds) {
 #pragma unroll
       for (int j = 0; j < DR_VEC; j++)
-        if ((uint64_t)r * PER_ROUND + threadIdx.x + j * DR_THREADS < npair) x[j] = ldg_stream(p + j * DR_THREADS);
+        if ((uint64_t)r * PER_ROUND + DR_VEC * threadIdx.x + j < npair) x[j] = ldg_stream(p + j);
     }
   };
   auto insert_round = [&](const uint4 (&x)[DR_VEC], uint32_t r) {
 #pragma unroll
     for (int j = 0; j < DR_VEC; j++) {
-      if (r >= full_rounds && (uint64_t)r * PER_ROUND + threadIdx.x + j * DR_THREADS >= npair) continue;
+      if (r >= full_rounds && (uint64_t)r * PER_ROUND + DR_VEC * threadIdx.x + j >= npair) continue;
       const uint32_t v[4] = {x[j].x - lo, x[j].y - lo, x[j].z - lo, x[j].w - lo};
       claim_store(v, 4);
       if (spec) {
@@ -575,7 +576,8 @@ bool launch_degree_radix(const uint2* edges, uint64_t m, uint64_t n, uint32_t* d
   SpecRoot sp{nullptr, nullptr, nullptr};
   if (spec && m >= spec_min_edges()) {
     const char* es = getenv("CC_SPEC_SAMPLE_EDGES");  // test hook
-    m0 = std::min<uint64_t>(es ? strtoull(es, nullptr, 10) : SPEC_SAMPLE_EDGES, m / 2) & ~1ull;
+    // a multiple of 4 edges: the degree pass reads the rest with 32-byte loads
+    m0 = std::min<uint64_t>(es ? strtoull(es, nullptr, 10) : SPEC_SAMPLE_EDGES, m / 2) & ~3ull;
     auto* gc = reinterpret_cast<unsigned long long*>(spec->gctr);
     k_deg_sample<<<grid_for(m0 / 2, 148 * 4), BLOCK, 0, st>>>(reinterpret_cast<const uint4*>(edges), m0 / 2,
                                                               deg, gc + G_GUESS);
@@ -734,21 +736,29 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
     __syncwarp();
     nbuf = 0;
   };
-  const uint64_t stride = (uint64_t)gridDim.x * BLOCK * 2;
+  // EPT edges per thread per step, one 256-bit load (the list is 32-byte aligned): 2 EPT
+  // state reads in flight per thread
+  constexpr int EPT = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * BLOCK * EPT;
   const uint64_t iters = (m + stride - 1) / stride;
   for (uint64_t it = 0; it < iters; it++) {
-    const uint64_t i0 = it * stride + (blockIdx.x * (uint64_t)BLOCK + threadIdx.x) * 2;
-    uint2 x[2];
-    bool keep[2] = {false, false};
+    const uint64_t i0 = it * stride + (blockIdx.x * (uint64_t)BLOCK + threadIdx.x) * EPT;
+    uint2 x[EPT];
+    bool keep[EPT] = {false, false, false, false};
     int cnt = 0;
-    if (i0 + 1 < m) {
-      const uint4 q = ldg_stream(reinterpret_cast<const uint4*>(e + i0));
-      x[0] = make_uint2(q.x, q.y); x[1] = make_uint2(q.z, q.w); cnt = 2;
-    } else if (i0 < m) {
-      x[0] = e[i0]; cnt = 1;
+    if (i0 + EPT <= m) {
+      uint4 q0, q1;
+      ldg_stream_v8(e + i0, q0, q1);
+      x[0] = make_uint2(q0.x, q0.y); x[1] = make_uint2(q0.z, q0.w);
+      x[2] = make_uint2(q1.x, q1.y); x[3] = make_uint2(q1.z, q1.w);
+      cnt = EPT;
+    } else {
+#pragma unroll
+      for (int j = 0; j < EPT; j++)
+        if (i0 + j < m) { x[j] = e[i0 + j]; cnt = j + 1; }
     }
 #pragma unroll
-    for (int j = 0; j < 2; j++) {
+    for (int j = 0; j < EPT; j++) {
       if (j >= cnt) continue;
       const uint32_t a = x[j].x, b = x[j].y;
       if (ROOT) {
@@ -767,12 +777,12 @@ __global__ void __launch_bounds__(BLOCK) k_bfs_level(const uint2* __restrict__ e
     if (COMPACT) {
       const uint32_t lt = lanemask_lt();
 #pragma unroll
-      for (int j = 0; j < 2; j++) {
+      for (int j = 0; j < EPT; j++) {
         const uint32_t mk = __ballot_sync(0xffffffffu, keep[j]);
         if (keep[j]) s_buf[wid][nbuf + __popc(mk & lt)] = x[j];
         nbuf += __popc(mk);
       }
-      if (nbuf > (uint32_t)(COMPACT ? WBUF - 64 : 0)) flush();
+      if (nbuf > (uint32_t)(COMPACT ? WBUF - 32 * EPT : 0)) flush();
     }
   }
   if (COMPACT && nbuf) flush();
@@ -794,7 +804,7 @@ __global__ void k_bfs_advance(uint32_t* S, const uint32_t* __restrict__ next, ui
 void launch_bfs_level(bool root_level, bool compact, const uint2* edges, uint64_t m, uint32_t root,
                       uint32_t* S, uint32_t* next, uint2* out, uint64_t* gctr, cudaStream_t st) {
   if (!m) return;
-  const unsigned g = grid_for((m + 1) / 2, 148 * 8);
+  const unsigned g = grid_for((m + 3) / 4, 148 * 8);
   auto* c = reinterpret_cast<unsigned long long*>(gctr);
   if (root_level) k_bfs_level<true, false><<<g, BLOCK, 0, st>>>(edges, m, root, nullptr, S, next, out, c);
   else if (compact) k_bfs_level<false, true><<<g, BLOCK, 0, st>>>(edges, m, root, nullptr, S, next, out, c);
