@@ -455,6 +455,11 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   // counters on the device; counters alternate between two blocks.  Compaction (rare) is a
   // synchronisation point.  Several ranks, or no exclusion, run step by step.
   const bool ahead = !multi && excl;
+  // iteration 0's pass A by pull (csr::rowpass_a0_pull; one GPU: the pull reads the u_min of
+  // rows other ranks own).  The CSR offsets are still in d_q[0] then.  CC_PULL0=1: the pull
+  // (default: the push, until the pull is measured)
+  const char* p0 = getenv("CC_PULL0");
+  const bool pull0 = !multi && (p0 && p0[0] == '1');
   // several ranks: the owner-computes slot exchange (NEXT-1, ctx.cuh oc_push / oc_reply) unless
   // the dense all-reduce is asked for (CC_FLAG_DENSE_EXCHANGE), or completed partitions keep
   // temporaries, or rows leave their owner (balanced variant: TB(r) must reach the row holder)
@@ -503,10 +508,14 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
     CK(cudaMemsetAsync(ctr, 0, sizeof(uint64_t) * (sv::C_SURVIVORS + 1), c->st));
     // ---- lines 8-16 (+ line 25 relabel of the previous iteration)
     { Prof k(c, KF_ROWA);
-      csr::rowpass(true, Rc, Pc, it ? Palt : nullptr, len, it ? PB : nullptr, nullptr, nullptr, PA,
-                   NCP, c->d_label, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs,
-                   have_long, false, ctr, c->st, true, /*preset=*/lexact, prevctr, HOT_A, nullptr,
-                   hot_cur && lcur ? LC + lb : nullptr, 0);
+      if (it == 0 && pull0)
+        csr::rowpass_a0_pull(c->d_q[0], Pc, n, PB, PA, NCP, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs,
+                             c->d_nlsegs, have_long, c->st);
+      else
+        csr::rowpass(true, Rc, Pc, it ? Palt : nullptr, len, it ? PB : nullptr, nullptr, nullptr, PA,
+                     NCP, c->d_label, c->d_umin, c->d_umax, ++c->row_tag, c->d_lsegs, c->d_nlsegs,
+                     have_long, false, ctr, c->st, true, /*preset=*/lexact, prevctr, HOT_A, nullptr,
+                     hot_cur && lcur ? LC + lb : nullptr, 0);
       k.end(8.0 * len + (it ? 4.0 * len : 0.0), 1 + (have_long ? 2 : 0)); }
     if (it) std::swap(Pc, Palt);
     if (oc) {

@@ -93,6 +93,12 @@ void list_from_bits(uint32_t* NX, uint64_t n, uint32_t* list, uint64_t* lcnt, ui
 void extract_slots(const uint32_t* S, const uint32_t* BM, uint64_t n, uint2* out, uint64_t* cnt,
                    cudaStream_t st);
 void apply_slots(const uint2* in, uint64_t count, uint32_t* S, uint32_t* BM, cudaStream_t st);
+// Iteration 0's pass A by pull (one GPU, the tuple array still in CSR order with offsets
+// off[0..n]): U[r] = u_min(r), NCP(u_min) of non-PC rows, PA[p] = min over row p's values x
+// of U[x]; U is n-sized scratch (PB: k_pstat1 clears it next), tag the long-row epoch
+void rowpass_a0_pull(const uint32_t* off, const uint32_t* P, uint64_t n, uint32_t* U, uint32_t* PA, uint32_t* NCP,
+                     uint64_t* UMIN, uint64_t* UMAX, uint32_t tag, const LongSeg* segs, const uint64_t* nsegs,
+                     bool have_long, cudaStream_t st);
 // multi-GPU owner-computes exchange (NEXT-1; cc_api.cu sv_iterate).  pstat1/pstat2 over one
 // owner block [lo, hi) (lo a multiple of 32; TB absolute in pstat1, ids offset by lo; no list)
 void pstat1_block(uint32_t* PA, const uint32_t* NCP, uint64_t lo, uint64_t hi, uint32_t* TB, uint32_t* PB,

@@ -989,6 +989,81 @@ void pstat2(uint32_t* PB, uint64_t n, uint32_t* PA, const uint32_t* TB, uint64_t
   const unsigned g = (unsigned)std::min<uint64_t>((n4 + RB - 1) / RB, 148 * 8);
   k_pstat2<<<g, RB, 0, st>>>(PB, n4, PA, TB, c, NX, 0u);
 }
+// ------------------------------------------------- iteration 0, pass A by pull (one GPU)
+// Pass A pushes u_min(r) to PA[p] for every tuple p of every row r.  In iteration 0 the rows
+// are the CSR rows of Alg. 1 line 3 (row r holds r and N(r)), and p is in row r iff r is in
+// row p (both arcs of an edge are tuples), so PA[p] = min over the values x of row p of
+// u_min(x): the same minima gathered by the row that owns the slot -- random reads of a
+// u_min array instead of random reductions into PA (C2: 79 M reductions at the L2 reduction
+// rate; C4 in mode sv: 2.2 G reductions into a 268 MB array).  Short rows by a thread each
+// (rows are adjacent, so a warp reads one span), long rows by the segment kernels.
+__global__ void k_u0(const uint32_t* __restrict__ off, const uint32_t* __restrict__ P, uint64_t n,
+                     uint32_t* __restrict__ U, uint32_t* NCP) {
+  for (uint64_t r = blockIdx.x * (uint64_t)RB + threadIdx.x; r < n; r += (uint64_t)gridDim.x * RB) {
+    const uint32_t a = off[r], b = off[r + 1];
+    if (a == b || b - a > LONG) continue;
+    uint32_t mn = INF, mx = 0;
+    for (uint32_t i = a; i < b; i++) {
+      const uint32_t v = P[i];
+      mn = min(mn, v);
+      mx = max(mx, v);
+    }
+    U[r] = mn;
+    if (mn != mx) set_bit(NCP, mn);  // not PC: 'not potentially completed' at its minimum (R18)
+  }
+}
+// long rows: u_min and the max from k_long1<true>'s segment partials (the row's first segment)
+__global__ void k_u0_long(const LongSeg* __restrict__ segs, const unsigned long long* nsegs,
+                          const uint32_t* __restrict__ off, const unsigned long long* __restrict__ UMIN,
+                          const unsigned long long* __restrict__ UMAX, uint32_t* __restrict__ U, uint32_t* NCP) {
+  const uint64_t cnt = *nsegs;
+  for (uint64_t s = blockIdx.x * (uint64_t)RB + threadIdx.x; s < cnt; s += (uint64_t)gridDim.x * RB) {
+    const LongSeg sg = segs[s];
+    if (sg.start != off[sg.u]) continue;
+    const uint32_t mn = (uint32_t)UMIN[sg.u], mx = (uint32_t)UMAX[sg.u];
+    U[sg.u] = mn;
+    if (mn != mx) set_bit(NCP, mn);
+  }
+}
+__global__ void k_pull0(const uint32_t* __restrict__ off, const uint32_t* __restrict__ P, uint64_t n,
+                        const uint32_t* __restrict__ U, uint32_t* __restrict__ PA) {
+  for (uint64_t p = blockIdx.x * (uint64_t)RB + threadIdx.x; p < n; p += (uint64_t)gridDim.x * RB) {
+    const uint32_t a = off[p], b = off[p + 1];
+    if (a == b || b - a > LONG) continue;
+    uint32_t mn = INF;
+    for (uint32_t i = a; i < b; i++) mn = min(mn, __ldg(&U[P[i]]));
+    PA[p] = mn;  // the slot's only writer
+  }
+}
+__global__ void k_pull0_long(const uint32_t* __restrict__ P, const LongSeg* __restrict__ segs,
+                             const unsigned long long* nsegs, const uint32_t* __restrict__ U, uint32_t* PA) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t cnt = *nsegs;
+  for (uint64_t s = (blockIdx.x * (uint64_t)RB + threadIdx.x) >> 5; s < cnt; s += ((uint64_t)gridDim.x * RB) >> 5) {
+    const LongSeg sg = segs[s];
+    uint32_t mn = INF;
+    for (uint32_t i = lane; i < sg.len; i += 32) mn = min(mn, __ldg(&U[P[sg.start + i]]));
+    mn = __reduce_min_sync(FULL, mn);
+    if (lane == 0) atomicMin(&PA[sg.u], mn);
+  }
+}
+void rowpass_a0_pull(const uint32_t* off, const uint32_t* P, uint64_t n, uint32_t* U, uint32_t* PA, uint32_t* NCP,
+                     uint64_t* UMIN, uint64_t* UMAX, uint32_t tag, const LongSeg* segs, const uint64_t* nsegs,
+                     bool have_long, cudaStream_t st) {
+  if (!n) return;
+  auto* umin = reinterpret_cast<unsigned long long*>(UMIN);
+  auto* umax = reinterpret_cast<unsigned long long*>(UMAX);
+  auto* ns = reinterpret_cast<const unsigned long long*>(nsegs);
+  const unsigned g = (unsigned)std::min<uint64_t>((n + RB - 1) / RB, 148 * 8);
+  k_u0<<<g, RB, 0, st>>>(off, P, n, U, NCP);
+  if (have_long) {
+    k_long1<true><<<148 * 4, RB, 0, st>>>(P, segs, ns, nullptr, umin, umax, tag);
+    k_u0_long<<<148 * 2, RB, 0, st>>>(segs, ns, off, umin, umax, U, NCP);
+  }
+  k_pull0<<<g, RB, 0, st>>>(off, P, n, U, PA);
+  if (have_long) k_pull0_long<<<148 * 4, RB, 0, st>>>(P, segs, ns, U, PA);
+}
+
 void pstat1_block(uint32_t* PA, const uint32_t* NCP, uint64_t lo, uint64_t hi, uint32_t* TB, uint32_t* PB,
                   uint64_t* ctr, cudaStream_t st) {
   const uint64_t n4 = (hi - lo + 3) / 4;

@@ -237,6 +237,49 @@ def test_row_collapse_forced(graph, monkeypatch):
         ref.close()
 
 
+@pytest.mark.parametrize("graph", ["stars", "rmat14", "c1", "c2s"])
+def test_pass_a0_pull_vs_push(graph, monkeypatch):
+    """Iteration 0's pass A by pull (PA[p] = min over row p's values x of
+    u_min(x)) against the push form (CC_PULL0=0) and the oracle: labels and every counter of
+    every iteration, on hubs longer than one long-row segment (stars of 300 / 1024 / 1025 /
+    5000 leaves with cross links), an R-MAT in mode sv, C1 and a C2 sample."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_06156_b200 as ccmod
+    if graph == "stars":
+        rng = np.random.default_rng(3)
+        n, parts, nxt = 20000, [], 0
+        perm = rng.permutation(n).astype(np.uint32)
+        for k in (300, 1024, 1025, 5000, 2, 1):
+            parts.append(np.stack([np.full(k, perm[nxt], np.uint32), perm[nxt + 1:nxt + 1 + k]], 1))
+            nxt += k + 1
+        parts.append(rng.choice(perm[:nxt], size=(400, 2)).astype(np.uint32))
+        e = np.concatenate(parts).astype(np.uint32)
+    elif graph == "rmat14":
+        g = graphgen.rmat_scale_graph(14)
+        n, e = g.n, g.edges
+    elif graph == "c1":
+        g = graphgen.make("c1")
+        n, e = g.n, g.edges
+    else:
+        g = graphgen.make("c2", 0.02)
+        n, e = g.n, g.edges
+    want = oracle.uf_labels(n, e).astype(np.int64)
+    _, tr = osv.sv_trace(n, e)
+    got = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("CC_PULL0", env)
+        ctx = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE)
+        try:
+            lab, rep = run(ctx, n, e, "sv")
+        finally:
+            ctx.close()
+        assert np.array_equal(lab, want), env
+        got[env] = norm(trace_of(rep))
+        assert got[env] == norm(tr), env
+
+
 @pytest.mark.parametrize("exclusion", ["end", "none"])
 def test_exclusion_variants_trace(exclusion):
     """The paper's exclusion timings (SURVEY C4, sec:distSVOpt1 P:220-225) and the
