@@ -456,10 +456,10 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   // synchronisation point.  Several ranks, or no exclusion, run step by step.
   const bool ahead = !multi && excl;
   // iteration 0's pass A by pull (csr::rowpass_a0_pull; one GPU: the pull reads the u_min of
-  // rows other ranks own).  The CSR offsets are still in d_q[0] then.  CC_PULL0=1: the pull
-  // (default: the push, until the pull is measured)
+  // rows other ranks own).  The CSR offsets are still in d_q[0] then.  CC_PULL0=0: the push
+  // (C2 5.61 -> 5.53 ms, C3 6.03 -> 5.92 ms, C4 mode sv 225 -> 205 ms with the pull)
   const char* p0 = getenv("CC_PULL0");
-  const bool pull0 = !multi && (p0 && p0[0] == '1');
+  const bool pull0 = !multi && !(p0 && p0[0] == '0');
   // several ranks: the owner-computes slot exchange (NEXT-1, ctx.cuh oc_push / oc_reply) unless
   // the dense all-reduce is asked for (CC_FLAG_DENSE_EXCHANGE), or completed partitions keep
   // temporaries, or rows leave their owner (balanced variant: TB(r) must reach the row holder)
