@@ -382,7 +382,47 @@ k_deg_part(const uint4* __restrict__ e2, uint64_t m, uint32_t lo_arg, uint32_t n
         if ((uint64_t)r * PER_ROUND + DR_VEC * threadIdx.x + j < npair) x[j] = ldg_stream(p + j);
     }
   };
+  // a full round of a FULL window: every endpoint is valid and in range, so there is no
+  // sentinel; the ring store and the (rare) direct count are predicated rather than branched
+  // (PTX predicates: ptxas had wrapped each in a BSSY/BRA pair), and the guess test is one
+  // predicate per two edges.  k_deg_part on C4 5.78 -> 5.50 ms (profiles/r02/bench_c4_s6_pred*)
+  const uint32_t row_base = (uint32_t)__cvta_generic_to_shared(s_row);
+  auto insert_full = [&](const uint4 (&x)[DR_VEC]) {
+#pragma unroll
+    for (int j = 0; j < DR_VEC; j++) {
+      const uint32_t v[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
+      uint32_t old[4];
+#pragma unroll
+      for (int h = 0; h < 4; h++) old[h] = atomicAdd(&s_w[v[h] >> DR_SPAN], 1u);
+#pragma unroll
+      for (int h = 0; h < 4; h++) {
+        const uint32_t b = v[h] >> DR_SPAN, w = old[h] & 0xFFFFu;
+        const uint32_t sa = row_base + 2u * (b * DR_CAP + dr_phys(b, w));
+        // ring slot free: the u16 store; ring full this round: the direct count
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.lt.u32 p, %0, %4;\n\t"
+            "@p st.shared.u16 [%1], %2;\n\t"
+            "@!p red.global.add.u32 [%3], 1;\n\t}"
+            :: "r"(w - (old[h] >> 16)), "r"(sa), "h"((unsigned short)(v[h] & LOWMASK)), "l"(deg + v[h]),
+               "n"(DR_CAP) : "memory");
+      }
+    }
+    if (spec) {
+#pragma unroll
+      for (int j = 0; j < DR_VEC; j++) {
+        if (((x[j].x == rg) | (x[j].y == rg) | (x[j].z == rg) | (x[j].w == rg)) != 0) {
+          spec_edge(x[j].x, x[j].y);
+          spec_edge(x[j].z, x[j].w);
+        }
+      }
+    }
+  };
   auto insert_round = [&](const uint4 (&x)[DR_VEC], uint32_t r) {
+    if (FULL && r < full_rounds) {
+      insert_full(x);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < DR_VEC; j++) {
       if (r >= full_rounds && (uint64_t)r * PER_ROUND + DR_VEC * threadIdx.x + j >= npair) continue;

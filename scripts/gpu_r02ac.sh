@@ -15,3 +15,6 @@ import json;d=json.load(open('gpurun_out/${TAG}_c4_l${lg}_$rep.json'));print('c4
 done
 CC_DEG_LEGACY=0 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "c4 or gate or degree" > gpurun_out/${TAG}_pytest2.log 2>&1; echo "pytest2 rc=$?"
 tail -2 gpurun_out/${TAG}_pytest2.log
+timeout 300 python bench.py --config c2 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_c2.json 2> gpurun_out/${TAG}_c2.err; echo "c2 rc=$?"
+timeout 600 python scripts/timeline.py --config c4 --mode sv --out gpurun_out/${TAG}_tl_c4sv.json > /dev/null 2> gpurun_out/${TAG}_tl_c4sv.err; echo "tl c4sv rc=$?"
+timeout 300 python scripts/timeline.py --config c4 --out gpurun_out/${TAG}_tl_c4.json > /dev/null 2>&1; echo "tl c4 rc=$?"
