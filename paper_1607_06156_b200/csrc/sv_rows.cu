@@ -55,6 +55,9 @@ constexpr int RITEMS = 8;
 constexpr int PB = 256;               // row-pass block: 8 warps, tiles of PB * RITEMS tuples (128: slower)
 constexpr int PTILE = PB * RITEMS;
 constexpr int RCACHE = 512;
+// long-row segment kernels: LU loads of a lane in flight (a warp walks a 1024-tuple segment;
+// one dependent load per step left them latency-bound: k_long2 5.5 ms on C4 mode sv)
+constexpr int LU = 8;
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr uint32_t DEAD = 0xFFFFFFFFu;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
@@ -523,18 +526,37 @@ __global__ void __launch_bounds__(RB) k_longlist(const uint32_t* __restrict__ R,
                                                  const uint32_t* __restrict__ deg,
                                                  LongSeg* __restrict__ segs,
                                                  unsigned long long* nsegs, uint64_t cap) {
-  for (uint64_t i = blockIdx.x * (uint64_t)RB + threadIdx.x; i < L; i += (uint64_t)gridDim.x * RB) {
-    const uint32_t ru = R[i];
-    if (!(ru & R_LONG) || (i > 0 && R[i - 1] == ru) || P[i] == DEAD) continue;
-    const uint32_t u = ru & ~R_LONG;
-    const uint64_t len = (uint64_t)deg[u] + 1, ns = (len + LSEG - 1) / LSEG;
-    const uint64_t b = atomicAdd(nsegs, (unsigned long long)ns);
-    for (uint64_t s = 0; s < ns && b + s < cap; s++) {
-      LongSeg sg;
-      sg.u = u;
-      sg.start = i + s * LSEG;
-      sg.len = (uint32_t)(len - s * LSEG < LSEG ? len - s * LSEG : LSEG);
-      segs[b + s] = sg;
+  // four tuples per thread: one 16-byte load of R when the array is 16-byte aligned
+  const bool vec = (reinterpret_cast<uintptr_t>(R) & 15) == 0;
+  const uint64_t nq = (L + 3) / 4;
+  for (uint64_t q = blockIdx.x * (uint64_t)RB + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * RB) {
+    const uint64_t i0 = 4 * q;
+    uint32_t r[4];
+    if (vec && i0 + 4 <= L) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(R) + q);
+      r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; j++) r[j] = i0 + j < L ? R[i0 + j] : 0u;
+    }
+    if (!((r[0] | r[1] | r[2] | r[3]) & R_LONG)) continue;  // no long-row tuple here
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint64_t i = i0 + j;
+      const uint32_t ru = r[j];
+      if (i >= L || !(ru & R_LONG)) continue;
+      const uint32_t prev = j ? r[j - 1] : (i > 0 ? R[i - 1] : ~ru);
+      if (prev == ru || P[i] == DEAD) continue;
+      const uint32_t u = ru & ~R_LONG;
+      const uint64_t len = (uint64_t)deg[u] + 1, ns = (len + LSEG - 1) / LSEG;
+      const uint64_t b = atomicAdd(nsegs, (unsigned long long)ns);
+      for (uint64_t s = 0; s < ns && b + s < cap; s++) {
+        LongSeg sg;
+        sg.u = u;
+        sg.start = i + s * LSEG;
+        sg.len = (uint32_t)(len - s * LSEG < LSEG ? len - s * LSEG : LSEG);
+        segs[b + s] = sg;
+      }
     }
   }
 }
@@ -553,10 +575,15 @@ __global__ void __launch_bounds__(RB) k_long1(const uint32_t* __restrict__ P,
        s += ((uint64_t)gridDim.x * RB) >> 5) {
     const LongSeg sg = segs[s];
     uint32_t mn = INF, mx = 0;
-    for (uint32_t i = lane; i < sg.len; i += 32) {
-      const uint32_t v = P[sg.start + i];
-      mn = min(mn, v);
-      if (v != DEAD) mx = max(mx, v);
+    for (uint32_t i0 = lane; i0 < sg.len; i0 += 32 * LU) {
+      uint32_t pv[LU];
+#pragma unroll
+      for (int u = 0; u < LU; u++) pv[u] = i0 + 32u * u < sg.len ? P[sg.start + i0 + 32u * u] : INF;
+#pragma unroll
+      for (int u = 0; u < LU; u++) {
+        mn = min(mn, pv[u]);
+        if (pv[u] != DEAD) mx = max(mx, pv[u]);
+      }
     }
     mn = __reduce_min_sync(FULL, mn);
     mx = __reduce_max_sync(FULL, mx);
@@ -588,7 +615,15 @@ __global__ void __launch_bounds__(RB) k_long2(const uint32_t* __restrict__ P,
     const unsigned long long um = UMIN[sg.u];
     if ((uint32_t)(um >> 32) != 0xFFFFFFFFu - tag) continue;  // row left (completed)
     const uint32_t q = (uint32_t)um;
-    for (uint32_t i = lane; i < sg.len; i += 32) push_min(OUT, s_pc, P[sg.start + i], q);
+    for (uint32_t i0 = lane; i0 < sg.len; i0 += 32 * LU) {
+      uint32_t pv[LU];
+#pragma unroll
+      for (int u = 0; u < LU; u++)
+        if (i0 + 32u * u < sg.len) pv[u] = P[sg.start + i0 + 32u * u];
+#pragma unroll
+      for (int u = 0; u < LU; u++)
+        if (i0 + 32u * u < sg.len) push_min(OUT, s_pc, pv[u], q);
+    }
     if (lane == 0) {
       if (A) {
         if (q != (uint32_t)UMAX[sg.u]) set_bit(NCPw, q);
@@ -1030,8 +1065,13 @@ __global__ void k_pull0(const uint32_t* __restrict__ off, const uint32_t* __rest
   for (uint64_t p = blockIdx.x * (uint64_t)RB + threadIdx.x; p < n; p += (uint64_t)gridDim.x * RB) {
     const uint32_t a = off[p], b = off[p + 1];
     if (a == b || b - a > LONG) continue;
-    uint32_t mn = INF;
-    for (uint32_t i = a; i < b; i++) mn = min(mn, __ldg(&U[P[i]]));
+    uint32_t mn = INF, i = a;
+    for (; i + 4 <= b; i += 4) {  // four gathers in flight
+      const uint32_t p0 = P[i], p1 = P[i + 1], p2 = P[i + 2], p3 = P[i + 3];
+      const uint32_t u0 = __ldg(&U[p0]), u1 = __ldg(&U[p1]), u2 = __ldg(&U[p2]), u3 = __ldg(&U[p3]);
+      mn = min(mn, min(min(u0, u1), min(u2, u3)));
+    }
+    for (; i < b; i++) mn = min(mn, __ldg(&U[P[i]]));
     PA[p] = mn;  // the slot's only writer
   }
 }
@@ -1042,7 +1082,15 @@ __global__ void k_pull0_long(const uint32_t* __restrict__ P, const LongSeg* __re
   for (uint64_t s = (blockIdx.x * (uint64_t)RB + threadIdx.x) >> 5; s < cnt; s += ((uint64_t)gridDim.x * RB) >> 5) {
     const LongSeg sg = segs[s];
     uint32_t mn = INF;
-    for (uint32_t i = lane; i < sg.len; i += 32) mn = min(mn, __ldg(&U[P[sg.start + i]]));
+    for (uint32_t i0 = lane; i0 < sg.len; i0 += 32 * LU) {
+      uint32_t pv[LU], uv[LU];
+#pragma unroll
+      for (int u = 0; u < LU; u++) pv[u] = i0 + 32u * u < sg.len ? P[sg.start + i0 + 32u * u] : INF;
+#pragma unroll
+      for (int u = 0; u < LU; u++) uv[u] = pv[u] != INF ? __ldg(&U[pv[u]]) : INF;
+#pragma unroll
+      for (int u = 0; u < LU; u++) mn = min(mn, uv[u]);
+    }
     mn = __reduce_min_sync(FULL, mn);
     if (lane == 0) atomicMin(&PA[sg.u], mn);
   }
