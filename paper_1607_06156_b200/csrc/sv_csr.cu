@@ -355,6 +355,9 @@ __global__ void __launch_bounds__(1024) k_group_degree(const uint2* __restrict__
 // (subgroup s's arcs land in [off[v0], ...), inside the P range its rows will occupy), then
 // one block per subgroup places its arcs with shared-memory row cursors and writes R and the
 // vertex tuples of its rows: every global write stays inside the subgroup's own P window.
+// 2^11 ids: smaller subgroups (2^7, so that a C4 subgroup's 4 k tuples would stage in
+// k_place) spread a k_bucket2 tile over more subgroups than its counters hold, and the
+// pass fell back to global cursor atomics (C4 in mode sv: k_bucket2 12 -> 115 ms).
 constexpr int SUBG = 11;
 constexpr int MAXS2 = 512;
 __global__ void k_sub_init(const uint32_t* __restrict__ off, uint64_t ns, uint32_t* __restrict__ scur) {
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(B) k_place(const uint32_t* __restrict__ off, u
     } else {
       P[base0 + a] = v;
       if (b - a <= LONG_ROW) {
-        for (uint32_t i = a; i < b; i++) R[base0 + i] = v;
+        // R of short rows: written below by a warp per row (coalesced runs)
       } else {
         const uint32_t j = atomicAdd(&s_nlong, 1u);
         if (j < PLACE_LONG_CAP) {
@@ -493,6 +496,14 @@ __global__ void __launch_bounds__(B) k_place(const uint32_t* __restrict__ off, u
     }
   }
   __syncthreads();
+  if (!staged) {  // R of the short rows, a warp per row: one store request per 32 tuples
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t l = threadIdx.x >> 5; l < cnt; l += B / 32) {
+      const uint32_t a = s_off[l], b = s_off[l + 1];
+      if (b - a > LONG_ROW) continue;
+      for (uint32_t i = a + lane; i < b; i += 32) R[base0 + i] = (uint32_t)(v0 + l);
+    }
+  }
   // arcs of the subgroup: shared-memory row cursors
   const uint32_t a1 = scur_end[s];
   constexpr int PI = 8;  // arcs per thread in flight
