@@ -264,6 +264,12 @@ cc_status cc_block_range(const cc_ctx* ctx, uint64_t* lo, uint64_t* hi);
  * an earlier cc_run (CC_ERR_STATE from cc_labels_* until the next cc_run). */
 cc_status cc_bfs_eccentricity(cc_ctx* ctx, const uint64_t* seeds, uint32_t count, uint64_t* ecc);
 
+/* The paper's approximate diameter (approximated "by executing a total of 100
+ * BFS runs from a set of random seed vertices"; read as the largest depth found): the maximum of cc_bfs_eccentricity over the `count` seeds the caller drew (host
+ * array; the draw is the caller's so that a test passes the same seeds to its oracle) into
+ * *diameter (0 with no seed).  Same limits, errors and side effects as cc_bfs_eccentricity. */
+cc_status cc_approx_diameter(cc_ctx* ctx, const uint64_t* seeds, uint32_t count, uint64_t* diameter);
+
 /* Stable LSD radix sort (the onesweep regroup primitive of the sort engine, PAPER.md:207
  * "the bulk step of the algorithm is the sorting of tuples") of n 64-bit keys by their bits
  * [0, key_bits), key_bits in 1..64 (keys must be < 2^key_bits), carrying a u32 payload.  keys/vals: device arrays of n,

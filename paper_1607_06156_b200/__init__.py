@@ -92,7 +92,7 @@ class cc_report(ctypes.Structure):
 
 
 EXPORTS = ["cc_version", "cc_get_unique_id", "cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
-           "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_radix_sort_pairs",
+           "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_approx_diameter", "cc_radix_sort_pairs",
            "cc_degree_histogram", "cc_degrees_u32",
            "cc_set_profiling", "cc_last_launch_count",
            "cc_kernel_stats", "cc_kernel_ops",
@@ -121,6 +121,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_degree_histogram.argtypes = [P, P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
     lib.cc_degrees_u32.argtypes = [P, P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     lib.cc_bfs_eccentricity.argtypes = [P, P, ctypes.c_uint32, P]
+    lib.cc_approx_diameter.argtypes = [P, P, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64)]
     lib.cc_radix_sort_pairs.argtypes = [P, P, P, P, ctypes.c_uint64, ctypes.c_int, P]
     lib.cc_radix_sort_pairs.restype = ctypes.c_int
     lib.cc_set_profiling.argtypes = [P, ctypes.c_int]
@@ -135,8 +136,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.cc_kernel_name.restype = ctypes.c_char_p
     lib.cc_kernel_name.argtypes = [ctypes.c_int]
     for f in ("cc_init", "cc_load_edges", "cc_run", "cc_labels_u32", "cc_labels_u64",
-              "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_kernel_stats",
-              "cc_destroy", "cc_degree_histogram", "cc_degrees_u32"):
+              "cc_labels_device", "cc_block_range", "cc_bfs_eccentricity", "cc_approx_diameter",
+              "cc_kernel_stats", "cc_destroy", "cc_degree_histogram", "cc_degrees_u32"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -449,7 +450,15 @@ def approx_diameter(ctx, n, runs=100, seed=0, present=None):
     rng = np.random.default_rng(seed)
     pool = np.arange(n) if present is None else np.flatnonzero(present)
     seeds = rng.choice(pool, size=min(runs, pool.shape[0]), replace=False)
-    return int(cc_bfs_eccentricity(ctx, seeds).max()) if seeds.size else 0
+    return cc_approx_diameter(ctx, seeds)
+
+
+def cc_approx_diameter(ctx, seeds):
+    """Maximum BFS eccentricity over the given seeds, taken in the library."""
+    s = np.ascontiguousarray(seeds, dtype=np.uint64)
+    d = ctypes.c_uint64()
+    _check(ctx, lib().cc_approx_diameter(ctx, s.ctypes.data_as(ctypes.c_void_p), s.shape[0], ctypes.byref(d)))
+    return int(d.value)
 
 
 def cc_radix_sort_pairs(keys, vals, tmp_keys, tmp_vals, key_bits=64, stream=None):

@@ -234,6 +234,7 @@ static cc_status load_buffers(cc_ctx* c, cc_idw w, uint64_t m, uint64_t n, bool 
 extern "C" {
 
 cc_status cc_load_edges(cc_ctx* c, cc_idw w, const void* pairs, uint64_t m, uint64_t n, int on_dev) {
+  NvtxRange nv_load("cc_load_edges");
   if (!c) return CC_ERR_INVALID;
   if (m && !pairs) return fail(c, CC_ERR_INVALID, "pairs is NULL");
   if (w != CC_U32 && w != CC_U64) return fail(c, CC_ERR_INVALID, "bad id width %d", (int)w);
@@ -494,6 +495,7 @@ cc_status sv_iterate(cc_ctx* c, uint64_t A, uint64_t len, uint64_t A_local) {
   const bool collapse_force = cf && cf[0] == '1';
   const uint64_t COLLAPSE_MIN_LEN = collapse_force ? 0 : (1ull << 16);
   auto enqueue = [&](uint32_t it) -> cc_status {
+    NvtxRange nv_it("SV iteration (Alg. 1 lines 8-25)");
     cudaEvent_t ev_it = ev_get(c);
     CK(cudaEventRecord(ev_it, c->st));
     c->it_ev.push_back(ev_it);
@@ -1217,6 +1219,9 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
 
   cudaEvent_t e0 = ev_get(c), e_rel, e_pred, e_bfs, e_filter, e_sv, e_end;
   CK(cudaEventRecord(e0, c->st));
+  NvtxRange nv_run("cc_run");
+  NvtxStages nv;  // the stages of cc_report.ms_*
+  nv.next("relabel (Alg. 2 line 4)");
   // ------------------------------------------------ relabel (Alg. 2 line 4; u64 ids only)
   // ids are made dense first: every later stage addresses buckets by id (R18)
   if (c->idw == CC_U64) {
@@ -1249,6 +1254,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   const uint64_t n = c->n;
   e_rel = ev_get(c);
   CK(cudaEventRecord(e_rel, c->st));
+  nv.next("prediction (Alg. 2 lines 2-3)");
   // ------------------------------------------------ prediction (Alg. 2 lines 2-3)
   // csr engine, n <= 2^26: the arcs are bucketed by vertex group (the CSR build needs this
   // pass anyway) and degrees are counted per group in shared memory; otherwise counting
@@ -1312,6 +1318,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   }
   e_pred = ev_get(c);
   CK(cudaEventRecord(e_pred, c->st));
+  nv.next(run_bfs ? "BFS peel + filter (Alg. 2 lines 7-11)" : "SV (Alg. 1)");
 
   // ------------------------------------------------ full CSR rows (csr engine, both routes)
   uint64_t A_full = 0;
@@ -1364,6 +1371,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   }
 
   // ------------------------------------------------ SV (line 13)
+  if (run_bfs) nv.next("SV on the remainder (Alg. 2 line 13)");
   if (gsf >= 0 && !run_bfs) {
     c->rep.sv_ids = n;
     if (A_full) TRY(sv_iterate(c, A_full, A_full, A_full));  // the rows built above
@@ -1383,6 +1391,7 @@ extern "C" cc_status cc_run(cc_ctx* c, cc_mode mode, cc_report* out) {
   R.sv_iterations = (uint32_t)c->iters.size();
   e_sv = ev_get(c);
   CK(cudaEventRecord(e_sv, c->st));
+  nv.next("finalise");
   // components, isolated ids included (each has exactly one root: its minimum id)
   uint64_t* roots = c->d_gctr + graph::G_TAIL;
   CK(cudaMemsetAsync(roots, 0, sizeof(uint64_t), c->st));
@@ -1564,6 +1573,15 @@ extern "C" cc_status cc_bfs_eccentricity(cc_ctx* c, const uint64_t* seeds, uint3
     ecc[i] = lev;
   }
   CK(cudaStreamSynchronize(c->st));
+  return CC_OK;
+}
+
+extern "C" cc_status cc_approx_diameter(cc_ctx* c, const uint64_t* seeds, uint32_t count, uint64_t* diameter) {
+  if (!c || !diameter || (count && !seeds)) return CC_ERR_INVALID;
+  std::vector<uint64_t> ecc(count);
+  *diameter = 0;
+  TRY(cc_bfs_eccentricity(c, seeds, count, ecc.data()));
+  for (uint32_t i = 0; i < count; i++) *diameter = std::max(*diameter, ecc[i]);
   return CC_OK;
 }
 

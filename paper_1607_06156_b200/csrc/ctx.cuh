@@ -2,6 +2,7 @@
 // the single-GPU driver (cc_api.cu) and the multi-GPU driver (cc_dist.cu).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -252,13 +253,41 @@ static const char* const kKfOps[KF_N] = {
     "", "", "random 4-byte L2 reads (2 per edge of the level)", "", "", "", "",
     "shared-memory atomics (2 per arc: bucket claim + count)", "", ""};
 
+// NVTX ranges (header-only nvtx3; a no-op pointer call unless a tool such as Nsight Systems is
+// attached): cc_load_edges / cc_run, the stages of a run, every SV iteration and every kernel
+// family below, so a timeline reads in the paper's terms.  Ranges nest per host thread.
+struct NvtxRange {
+  explicit NvtxRange(const char* s) { nvtxRangePushA(s); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+// consecutive stages of one call: next() closes the open stage and opens the named one
+struct NvtxStages {
+  bool open = false;
+  void next(const char* s) {
+    if (open) nvtxRangePop();
+    nvtxRangePushA(s);
+    open = true;
+  }
+  void close() {
+    if (open) nvtxRangePop();
+    open = false;
+  }
+  ~NvtxStages() { close(); }
+};
+
 struct Prof {
   cc_ctx* c;
   int f;
   cudaEvent_t a = nullptr;
   Prof(cc_ctx* c_, int f_) : c(c_), f(f_) {
+    nvtxRangePushA(kKfNames[f]);
     if (profiling(c)) { a = ev_get(c); cudaEventRecord(a, c->st); }
   }
+  ~Prof() { nvtxRangePop(); }
+  Prof(const Prof&) = delete;
+  Prof& operator=(const Prof&) = delete;
   void end(double bytes, uint64_t nl, double ops = 0) {
     if (!profiling(c)) return;
     cudaEvent_t b = ev_get(c);

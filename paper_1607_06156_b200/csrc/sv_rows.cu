@@ -40,6 +40,7 @@
 // iteration's counters (prevctr) both hot variants are launched and the device runs one,
 // which lets the host enqueue the next iteration before reading the counters.
 #include <algorithm>
+#include <cstdlib>
 
 #include "csr.cuh"
 #include "sv.cuh"
@@ -325,7 +326,20 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     if (lane == 31) s_last[wid] = k[RITEMS - 1];
     // the leading run belongs to the previous tile when the tile starts inside a row
     if (threadIdx.x == 0) s_kfirst = (t0 > 0 && k[0] != INF && rprev == k[0]) ? k[0] : INF;
-    __syncthreads();
+    bool anyk = false;
+#pragma unroll
+    for (int j = 0; j < RITEMS; j++) anyk |= k[j] != INF;
+    if (!__syncthreads_or(anyk)) {
+      // a tile of nothing but long-row tuples (a hub row spans many tiles: 3/4 of C4's tuples
+      // in mode sv) and dead tuples: relabelled, counted and stored above, no run to reduce.
+      // One barrier instead of two: the next tile's first barrier still separates the reuse
+      // of the aggregate buffers.
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(tile + 2 * gridDim.x, buf);
+      }
+      continue;
+    }
     const uint32_t kfirst = s_kfirst;
     if (lane == 0) prevk = wid ? s_last[wid - 1] : kfirst;
     if (threadIdx.x == 0) {  // every thread has its items: refill this buffer
@@ -1060,23 +1074,43 @@ __global__ void k_u0_long(const LongSeg* __restrict__ segs, const unsigned long 
     if (mn != mx) set_bit(NCP, mn);
   }
 }
+// WIN: one id window [lo, lo + span) of U per launch (n-sized U beyond the L2: the gathers of a
+// window hit the L2 while P streams past it with evict-first loads; PA[p] accumulates the
+// windows' minima -- still the slot's only writer)
+template <bool WIN>
 __global__ void k_pull0(const uint32_t* __restrict__ off, const uint32_t* __restrict__ P, uint64_t n,
-                        const uint32_t* __restrict__ U, uint32_t* __restrict__ PA) {
+                        const uint32_t* __restrict__ U, uint32_t* __restrict__ PA, uint32_t lo, uint32_t span) {
   for (uint64_t p = blockIdx.x * (uint64_t)RB + threadIdx.x; p < n; p += (uint64_t)gridDim.x * RB) {
     const uint32_t a = off[p], b = off[p + 1];
     if (a == b || b - a > LONG) continue;
     uint32_t mn = INF, i = a;
-    for (; i + 4 <= b; i += 4) {  // four gathers in flight
-      const uint32_t p0 = P[i], p1 = P[i + 1], p2 = P[i + 2], p3 = P[i + 3];
-      const uint32_t u0 = __ldg(&U[p0]), u1 = __ldg(&U[p1]), u2 = __ldg(&U[p2]), u3 = __ldg(&U[p3]);
-      mn = min(mn, min(min(u0, u1), min(u2, u3)));
+    if (WIN) {
+      for (; i + 4 <= b; i += 4) {
+        const uint32_t p0 = __ldcs(&P[i]), p1 = __ldcs(&P[i + 1]), p2 = __ldcs(&P[i + 2]), p3 = __ldcs(&P[i + 3]);
+        const uint32_t u0 = p0 - lo < span ? __ldg(&U[p0]) : INF, u1 = p1 - lo < span ? __ldg(&U[p1]) : INF;
+        const uint32_t u2 = p2 - lo < span ? __ldg(&U[p2]) : INF, u3 = p3 - lo < span ? __ldg(&U[p3]) : INF;
+        mn = min(mn, min(min(u0, u1), min(u2, u3)));
+      }
+      for (; i < b; i++) {
+        const uint32_t p0 = __ldcs(&P[i]);
+        if (p0 - lo < span) mn = min(mn, __ldg(&U[p0]));
+      }
+      if (mn != INF) PA[p] = min(PA[p], mn);
+    } else {
+      for (; i + 4 <= b; i += 4) {  // four gathers in flight
+        const uint32_t p0 = P[i], p1 = P[i + 1], p2 = P[i + 2], p3 = P[i + 3];
+        const uint32_t u0 = __ldg(&U[p0]), u1 = __ldg(&U[p1]), u2 = __ldg(&U[p2]), u3 = __ldg(&U[p3]);
+        mn = min(mn, min(min(u0, u1), min(u2, u3)));
+      }
+      for (; i < b; i++) mn = min(mn, __ldg(&U[P[i]]));
+      PA[p] = mn;  // the slot's only writer
     }
-    for (; i < b; i++) mn = min(mn, __ldg(&U[P[i]]));
-    PA[p] = mn;  // the slot's only writer
   }
 }
+template <bool WIN>
 __global__ void k_pull0_long(const uint32_t* __restrict__ P, const LongSeg* __restrict__ segs,
-                             const unsigned long long* nsegs, const uint32_t* __restrict__ U, uint32_t* PA) {
+                             const unsigned long long* nsegs, const uint32_t* __restrict__ U, uint32_t* PA,
+                             uint32_t lo, uint32_t span) {
   const int lane = threadIdx.x & 31;
   const uint64_t cnt = *nsegs;
   for (uint64_t s = (blockIdx.x * (uint64_t)RB + threadIdx.x) >> 5; s < cnt; s += ((uint64_t)gridDim.x * RB) >> 5) {
@@ -1085,15 +1119,23 @@ __global__ void k_pull0_long(const uint32_t* __restrict__ P, const LongSeg* __re
     for (uint32_t i0 = lane; i0 < sg.len; i0 += 32 * LU) {
       uint32_t pv[LU], uv[LU];
 #pragma unroll
-      for (int u = 0; u < LU; u++) pv[u] = i0 + 32u * u < sg.len ? P[sg.start + i0 + 32u * u] : INF;
+      for (int u = 0; u < LU; u++)
+        pv[u] = i0 + 32u * u < sg.len ? (WIN ? __ldcs(&P[sg.start + i0 + 32u * u]) : P[sg.start + i0 + 32u * u]) : INF;
 #pragma unroll
-      for (int u = 0; u < LU; u++) uv[u] = pv[u] != INF ? __ldg(&U[pv[u]]) : INF;
+      for (int u = 0; u < LU; u++)
+        uv[u] = (WIN ? pv[u] - lo < span : pv[u] != INF) ? __ldg(&U[pv[u]]) : INF;
 #pragma unroll
       for (int u = 0; u < LU; u++) mn = min(mn, uv[u]);
     }
     mn = __reduce_min_sync(FULL, mn);
-    if (lane == 0) atomicMin(&PA[sg.u], mn);
+    if (lane == 0 && mn != INF) atomicMin(&PA[sg.u], mn);
   }
+}
+// CC_PULLW: log2 of the window's id count (0: no windows); default 2^24 ids = 64 MB of U
+static int pull_window_log2() {
+  const char* e = getenv("CC_PULLW");  // read per run, so a test can switch it
+  const int x = e && *e ? atoi(e) : 24;
+  return x < 0 || x > 31 ? 0 : x;
 }
 void rowpass_a0_pull(const uint32_t* off, const uint32_t* P, uint64_t n, uint32_t* U, uint32_t* PA, uint32_t* NCP,
                      uint64_t* UMIN, uint64_t* UMAX, uint32_t tag, const LongSeg* segs, const uint64_t* nsegs,
@@ -1108,8 +1150,18 @@ void rowpass_a0_pull(const uint32_t* off, const uint32_t* P, uint64_t n, uint32_
     k_long1<true><<<148 * 4, RB, 0, st>>>(P, segs, ns, nullptr, umin, umax, tag);
     k_u0_long<<<148 * 2, RB, 0, st>>>(segs, ns, off, umin, umax, U, NCP);
   }
-  k_pull0<<<g, RB, 0, st>>>(off, P, n, U, PA);
-  if (have_long) k_pull0_long<<<148 * 4, RB, 0, st>>>(P, segs, ns, U, PA);
+  // U beyond the L2 (C4 in mode sv: 268 MB): the gathers by windows of 2^pull_window_log2 ids
+  const int wl = pull_window_log2();
+  if (wl > 0 && n > (3ull << wl) / 2) {
+    const uint32_t span = 1u << wl;
+    for (uint64_t lo = 0; lo < n; lo += span) {
+      k_pull0<true><<<g, RB, 0, st>>>(off, P, n, U, PA, (uint32_t)lo, span);
+      if (have_long) k_pull0_long<true><<<148 * 4, RB, 0, st>>>(P, segs, ns, U, PA, (uint32_t)lo, span);
+    }
+    return;
+  }
+  k_pull0<false><<<g, RB, 0, st>>>(off, P, n, U, PA, 0u, 0u);
+  if (have_long) k_pull0_long<false><<<148 * 4, RB, 0, st>>>(P, segs, ns, U, PA, 0u, 0u);
 }
 
 void pstat1_block(uint32_t* PA, const uint32_t* NCP, uint64_t lo, uint64_t hi, uint32_t* TB, uint32_t* PB,

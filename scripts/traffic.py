@@ -21,7 +21,8 @@ FAMILIES = [
      "degree count (k_deg_part, k_deg_order, k_deg_count)"),
     (("k_deg_hist", "k_hist_pairs"), "degree distribution (k_deg_hist, k_hist_pairs)"),
     (("k_bfs_level",), "k_bfs_level"),
-    (("k_rowpass<true", "k_rowpass<1", "k_long1<true", "k_long2<true", "k_long1<1", "k_long2<1"),
+    # k_u0 / k_pull0: iteration 0's pass A by pull (timed in the same family by the library)
+    (("k_rowpass<true", "k_rowpass<1", "k_long1<true", "k_long2<true", "k_long1<1", "k_long2<1", "k_u0", "k_pull0"),
      "k_rowpass<A> +k_long1/2 (Alg.1 lines 8-16)"),
     (("k_rowpass<false", "k_rowpass<0", "k_long1<false", "k_long2<false", "k_long1<0", "k_long2<0"),
      "k_rowpass<B> +k_long1/2 (Alg.1 lines 17-25)"),

@@ -268,8 +268,15 @@ def test_pass_a0_pull_vs_push(graph, monkeypatch):
     want = oracle.uf_labels(n, e).astype(np.int64)
     _, tr = osv.sv_trace(n, e)
     got = {}
-    for env in ("1", "0"):
+    # "w": the pull by id windows of U (CC_PULLW = log2 of the window's ids; 2^9 and 2^11 ids
+    # give these graphs 8 to 128 windows, the default 2^24 gives them none)
+    for env, win in (("1", None), ("0", None), ("1", "9"), ("1", "11")):
         monkeypatch.setenv("CC_PULL0", env)
+        if win is None:
+            monkeypatch.delenv("CC_PULLW", raising=False)
+        else:
+            monkeypatch.setenv("CC_PULLW", win)
+            env = "w" + win
         ctx = ccmod.CC(device=0, flags=ccmod.CC_FLAG_TRACE)
         try:
             lab, rep = run(ctx, n, e, "sv")
@@ -706,13 +713,19 @@ def test_bfs_eccentricity():
             seeds = rng.integers(0, g.n, size=6).astype(np.uint64)
             ctx.load(g.edges, g.n)
             got = ctx.eccentricity(seeds)
+            wants = []
             for s, lev in zip(seeds, got):
                 _, want = obfs.bfs(g.n, g.edges, int(s))
                 assert int(lev) == want
+                wants.append(want)
+            # the approximate diameter over the same seeds (taken in the library)
+            assert ccmod.cc_approx_diameter(ctx.ctx, seeds) == max(wants)
         path = np.stack([np.arange(999), np.arange(1, 1000)], 1).astype(np.uint32)
         ctx.load(path, 1000)
         assert ctx.eccentricity(np.array([0, 500, 999], np.uint64)).tolist() == [999, 500, 999]
-        assert ccmod.approx_diameter(ctx.ctx, 1000, runs=20, seed=1) <= 999
+        assert ccmod.cc_approx_diameter(ctx.ctx, np.array([3, 500], np.uint64)) == 996
+        assert ccmod.cc_approx_diameter(ctx.ctx, np.zeros(0, np.uint64)) == 0
+        assert 500 <= ccmod.approx_diameter(ctx.ctx, 1000, runs=20, seed=1) <= 999
     finally:
         ctx.close()
 
