@@ -326,20 +326,12 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     if (lane == 31) s_last[wid] = k[RITEMS - 1];
     // the leading run belongs to the previous tile when the tile starts inside a row
     if (threadIdx.x == 0) s_kfirst = (t0 > 0 && k[0] != INF && rprev == k[0]) ? k[0] : INF;
-    bool anyk = false;
-#pragma unroll
-    for (int j = 0; j < RITEMS; j++) anyk |= k[j] != INF;
-    if (!__syncthreads_or(anyk)) {
-      // a tile of nothing but long-row tuples (a hub row spans many tiles: 3/4 of C4's tuples
-      // in mode sv) and dead tuples: relabelled, counted and stored above, no run to reduce.
-      // One barrier instead of two: the next tile's first barrier still separates the reuse
-      // of the aggregate buffers.
-      if (threadIdx.x == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(tile + 2 * gridDim.x, buf);
-      }
-      continue;
-    }
+    // (Tried: skipping the scans of a tile that holds nothing but long-row and dead tuples --
+    // 3/4 of C4's tiles in mode sv.  Iteration 2's pass B 9.0 -> 4.9 ms, but iteration 1's
+    // passes 9.5 -> 15.8 and 9.8 -> 14.9 ms -- presumably the relabel gathers of consecutive
+    // tiles, no longer spaced by the scans, pile onto the few L2 lines of the giant partitions' slots.
+    // profiles/r02/timeline_c4sv_s7_tileskip_rejected.json)
+    __syncthreads();
     const uint32_t kfirst = s_kfirst;
     if (lane == 0) prevk = wid ? s_last[wid - 1] : kfirst;
     if (threadIdx.x == 0) {  // every thread has its items: refill this buffer
@@ -1154,8 +1146,14 @@ void rowpass_a0_pull(const uint32_t* off, const uint32_t* P, uint64_t n, uint32_
   const int wl = pull_window_log2();
   if (wl > 0 && n > (3ull << wl) / 2) {
     const uint32_t span = 1u << wl;
+    // Short rows in one pass unless CC_PULLW_SHORT=1: a thread walks its row, so each window
+    // costs the whole latency-bound walk again (C4 mode sv: 4 x 4.5 ms against 8.3 ms),
+    // while the long rows' warps stream P at full rate (4 x 1.9 ms against 16.6 ms).
+    const char* ws = getenv("CC_PULLW_SHORT");
+    const bool win_short = ws && ws[0] == '1';
+    if (!win_short) k_pull0<false><<<g, RB, 0, st>>>(off, P, n, U, PA, 0u, 0u);
     for (uint64_t lo = 0; lo < n; lo += span) {
-      k_pull0<true><<<g, RB, 0, st>>>(off, P, n, U, PA, (uint32_t)lo, span);
+      if (win_short) k_pull0<true><<<g, RB, 0, st>>>(off, P, n, U, PA, (uint32_t)lo, span);
       if (have_long) k_pull0_long<true><<<148 * 4, RB, 0, st>>>(P, segs, ns, U, PA, (uint32_t)lo, span);
     }
     return;

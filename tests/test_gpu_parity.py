@@ -270,8 +270,10 @@ def test_pass_a0_pull_vs_push(graph, monkeypatch):
     got = {}
     # "w": the pull by id windows of U (CC_PULLW = log2 of the window's ids; 2^9 and 2^11 ids
     # give these graphs 8 to 128 windows, the default 2^24 gives them none)
-    for env, win in (("1", None), ("0", None), ("1", "9"), ("1", "11")):
+    # (windows are for the long rows' warps; CC_PULLW_SHORT=1 also windows the short rows' pull)
+    for env, win, short in (("1", None, "0"), ("0", None, "0"), ("1", "9", "0"), ("1", "11", "1")):
         monkeypatch.setenv("CC_PULL0", env)
+        monkeypatch.setenv("CC_PULLW_SHORT", short)
         if win is None:
             monkeypatch.delenv("CC_PULLW", raising=False)
         else:
