@@ -279,7 +279,21 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
         if (s0 + j >= tlen) { r[j] = INF; p[j] = DEAD; }
     }
     // ---- relabel (A: line 25 of the previous iteration) / exclusion + line 19 (B)
-    {
+    // Pass A: a relabelled live tuple stays live (its partition has a slot), so the keys below
+    // need only the input; the gathers are issued here and first used after the tile's first
+    // barrier, so their latency overlaps the barrier wait instead of preceding it (ncu, C4 mode
+    // sv iteration 1: 29 % of the stall samples sat at that barrier and 19 % at the first use,
+    // profiles/r02/ncu_rowpassA1_c4sv_s7.txt).  C2 5.54 -> 5.49 ms, C3 5.93 -> 5.89 ms (pass A
+    // 1.03 -> 0.99 ms per C2 step), C4 mode sv unchanged.
+    constexpr bool LATE = A && REL;
+    uint32_t gl[LATE ? RITEMS : 1];
+    if (LATE) {
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) {
+        const bool fresh = p[j] != DEAD && (j == 0 || p[j] != p[j - 1]);
+        gl[LATE ? j : 0] = fresh ? __ldg(&MAP[p[j]]) : p[j];
+      }
+    } else {
       // one gather per run of equal p in the thread's slice: once a few partitions hold most
       // tuples, thousands of threads would otherwise hit the same L2 line at once
       uint32_t m[RITEMS], cpl = 0;
@@ -317,7 +331,7 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) p[j] = m[j];
     }
-    if (!A || REL) store8(Pout, i0, L, p);
+    if (!LATE && (!A || REL)) store8(Pout, i0, L, p);
     // keys: dead tuples and long rows (k_long1/k_long2) take no part
     uint32_t k[RITEMS];
 #pragma unroll
@@ -328,15 +342,24 @@ __global__ void __launch_bounds__(PB, 2048 / PB / 2) k_rowpass(
     if (threadIdx.x == 0) s_kfirst = (t0 > 0 && k[0] != INF && rprev == k[0]) ? k[0] : INF;
     // (Tried: skipping the scans of a tile that holds nothing but long-row and dead tuples --
     // 3/4 of C4's tiles in mode sv.  Iteration 2's pass B 9.0 -> 4.9 ms, but iteration 1's
-    // passes 9.5 -> 15.8 and 9.8 -> 14.9 ms -- presumably the relabel gathers of consecutive
-    // tiles, no longer spaced by the scans, pile onto the few L2 lines of the giant partitions' slots.
-    // profiles/r02/timeline_c4sv_s7_tileskip_rejected.json)
+    // pass B 9.8 -> 14.9 ms, pass A unchanged, C2 5.53 -> 5.62 ms: no net gain, removed.
+    // profiles/r02/timeline_c4sv_s7_tileskip_rejected.json against timeline_c4sv_s7_final.json)
     __syncthreads();
     const uint32_t kfirst = s_kfirst;
     if (lane == 0) prevk = wid ? s_last[wid - 1] : kfirst;
     if (threadIdx.x == 0) {  // every thread has its items: refill this buffer
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(tile + 2 * gridDim.x, buf);
+    }
+    if (LATE) {  // the gathered labels: one per run of equal p in the thread's slice
+      uint32_t m[RITEMS];
+      m[0] = gl[0];
+#pragma unroll
+      for (int j = 1; j < RITEMS; j++)
+        m[j] = (p[j] != DEAD && p[j] == p[j - 1]) ? m[j - 1] : gl[LATE ? j : 0];
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) p[j] = m[j];
+      store8(Pout, i0, L, p);
     }
     // ---- thread-local scans; the temporary <r,_,r> of line 22 joins VB(r) at the row head
     uint32_t v[RITEMS];
